@@ -1,0 +1,244 @@
+/*
+ * sparcml.h — C ABI of the B200-native SparCML hot path (arXiv 1802.08021).
+ *
+ * libsparcml.so (paper_1802_08021_b200/libsparcml.so) exports exactly the
+ * functions declared here.  Signatures carry only plain pointers and sizes.
+ * Citations: "P:n" = PAPER.md line n (section in brackets).
+ *
+ * Conventions (apply to every call unless stated):
+ *  - Pointers are DEVICE pointers unless the name ends in _host.
+ *  - `stream` is a cudaStream_t passed as void*; NULL means the legacy default
+ *    stream.  Every device call is stream-ordered and returns as soon as the
+ *    work is enqueued; outputs are valid once `stream` reaches that point.
+ *  - Return value is a sparcml_status; the library never throws, never
+ *    aborts and never synchronises the device except where stated.
+ *    Argument errors are reported before anything is enqueued.
+ *    Device-detected errors (unsorted input, non-finite values) are written
+ *    to the result header's `status` field (sparcml_header.status).
+ *  - Sparse streams are struct-of-arrays: idx[n] (uint32, strictly
+ *    increasing, every index < N) and val[n] (float32,
+ *    P:470-471).  Inputs are read-only and must stay valid until `stream`
+ *    passes the call; outputs must not alias inputs unless stated.
+ *  - There is no CPU fallback: a call that cannot run on the GPU fails.
+ */
+#ifndef SPARCML_H
+#define SPARCML_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPARCML_MAX_RANKS 16          /* one 8-GPU box; 16 for loopback worlds */
+#define SPARCML_HEADER_BYTES 64       /* result header at out[0]              */
+#define SPARCML_IPC_HANDLE_BYTES 64   /* cudaIpcMemHandle_t                    */
+#define SPARCML_HEADER_MAGIC 0x4D435053u /* "SPCM" little-endian              */
+
+typedef enum {
+  SPARCML_OK = 0,
+  SPARCML_ERR_INVALID_ARG = 1,  /* bad size, null pointer, unsupported option */
+  SPARCML_ERR_UNSORTED = 2,     /* input indices not strictly increasing or >= N */
+  SPARCML_ERR_NONFINITE = 3,    /* NaN/Inf value where the method needs finite */
+  SPARCML_ERR_MISMATCH = 4,     /* ranks disagree on a collective argument     */
+  SPARCML_ERR_CUDA = 5,         /* a CUDA runtime call failed (see last_error) */
+  SPARCML_ERR_OOM = 7,          /* device allocation failed                    */
+  SPARCML_ERR_STATE = 8         /* communicator not connected / wrong mode     */
+} sparcml_status;
+
+/* Coordinate-wise reduction with a neutral element.  SUM only on
+ * the hot path (neutral 0). */
+typedef enum { SPARCML_OP_SUM = 0 } sparcml_op;
+
+/* Allreduce algorithms (§5.3).  AUTO: recursive doubling for the
+ * small-data case, split-allgather otherwise; inside split-
+ * allgather SSAR vs DSAR follows the dense-switch rule (R-5). */
+typedef enum {
+  SPARCML_ALGO_AUTO = 0,
+  SPARCML_SSAR_RECURSIVE_DOUBLE = 1,   /* §5.3.1                 */
+  SPARCML_SSAR_SPLIT_ALLGATHER = 2,    /* §5.3.2                 */
+  SPARCML_DSAR_SPLIT_ALLGATHER = 3     /* §5.3.3 P:782-832 (+ §6 QSGD)     */
+} sparcml_algo;
+
+/* Representation flag "at the beginning of each vector". */
+typedef enum { SPARCML_REPR_SPARSE = 0, SPARCML_REPR_DENSE = 1 } sparcml_repr;
+
+typedef struct {
+  sparcml_algo algo;      /* default AUTO                                          */
+  float switch_scale;     /* delta multiplier, default 1 ("should be even smaller") */
+  int index_bytes;        /* c in delta = N*isize/(c+isize); must be 4 (u32) */
+  int quant_bits;         /* 0 = off; 2, 4 or 8: QSGD in DSAR phase 2 only (§6) */
+  uint32_t quant_bucket;  /* B, default 1024; multiple of 4, <= 1024, divides 1024 */
+  uint64_t seed;          /* Philox key for QSGD                                    */
+  uint64_t k_sum_hint;    /* 0 = unknown; else the exact sum of all ranks' nnz: lets
+                             the host pick SSAR/DSAR without launching both paths   */
+  int validate;           /* 1: check sorted/unique/< N and finiteness on device    */
+} sparcml_opts;
+
+/* Result header, 64 bytes at out[0] (device).  The payload follows it:
+ *   dense:  val[N] float at byte SPARCML_HEADER_BYTES
+ *   sparse: idx[nnz] uint32 at byte SPARCML_HEADER_BYTES and val[nnz] float at
+ *           byte val_offset (fixed for a given N: the buffer is laid out for
+ *           the largest sparse result, delta = N/2 pairs).        */
+typedef struct {
+  uint32_t magic;        /* SPARCML_HEADER_MAGIC                                */
+  uint32_t repr;         /* sparcml_repr                                        */
+  uint64_t nnz;          /* sparse: K = |union H_i| exactly; dense: N           */
+  uint64_t N;
+  uint64_t k_sum;        /* sum over ranks of the input nnz                     */
+  uint64_t bytes_sent;   /* payload bytes this rank put on NVLink               */
+  uint64_t bytes_recv;   /* payload bytes this rank received                    */
+  uint32_t algo_used;    /* sparcml_algo actually run                           */
+  uint32_t status;       /* 0, or a sparcml_status detected on the device       */
+  uint64_t val_offset;   /* byte offset of val[] from the start of out          */
+} sparcml_header;
+
+/* ----------------------------- utilities ------------------------------- */
+
+const char* sparcml_version(void);
+const char* sparcml_status_string(sparcml_status s);
+void sparcml_opts_default(sparcml_opts* opts_host);
+
+/* delta = floor(scale * N*isize/(c+isize)) (§5.1).  Sparse is kept
+ * while nnz <= delta. */
+uint64_t sparcml_switch_threshold(uint64_t N, int isize, int c, float scale);
+
+/* E[K] = N(1-(1-k/N)^P) for uniform supports (App. B). */
+double sparcml_expected_nnz(uint64_t k, uint64_t N, int P);
+
+/* Bytes `out` must provide for an allreduce over dimension N:
+ * 64 + max(4N, 8*H) + 32 with H = ceil4(floor(N/2)). */
+size_t sparcml_result_bytes(uint64_t N);
+
+/* Byte offset of val[] for a sparse result of dimension N. */
+size_t sparcml_result_val_offset(uint64_t N);
+
+/* ---------------------------- communicator ----------------------------- */
+
+typedef struct sparcml_comm sparcml_comm;
+
+/* One rank per process (the production mode).  Allocates the rank's
+ * symmetric workspace on `cuda_device`, sized for dimensions <= max_N and
+ * per-rank nnz <= max_nnz.  Then every rank exports its handle, the caller
+ * gathers the nranks handles in rank order (any host transport; the Python
+ * binding uses torch.distributed) and passes them to sparcml_comm_connect,
+ * which maps the peers' workspaces over NVLink (CUDA IPC). */
+sparcml_status sparcml_comm_create(sparcml_comm** comm_out_host, int nranks, int rank,
+                                   int cuda_device, uint64_t max_N, uint64_t max_nnz);
+sparcml_status sparcml_comm_export_handle(sparcml_comm* comm, uint8_t* handle_host /* 64 B */);
+sparcml_status sparcml_comm_connect(sparcml_comm* comm,
+                                    const uint8_t* all_handles_host /* nranks*64 B, rank order */);
+
+/* Loopback world: all nranks ranks live in this process on one device and
+ * run the same kernels and exchanges through local memory.  Used for tests
+ * and single-GPU emulation.  Collectives are issued with the *_local calls. */
+sparcml_status sparcml_comm_create_local(sparcml_comm** comm_out_host, int nranks,
+                                         int cuda_device, uint64_t max_N, uint64_t max_nnz);
+
+sparcml_status sparcml_comm_destroy(sparcml_comm* comm);
+int sparcml_comm_nranks(const sparcml_comm* comm);
+int sparcml_comm_rank(const sparcml_comm* comm);   /* -1 for a loopback world */
+const char* sparcml_last_error(const sparcml_comm* comm);  /* NULL comm: global */
+
+/* ---------------------------- allreduce -------------------------------- */
+
+/* Sparse allreduce (§5.3 problem statement P:576-579): every rank passes its
+ * stream (idx, val, nnz) over dimension N; after the call `out` on every rank
+ * holds x = sum_i x_i with index set exactly the union of the H_i (explicit
+ * zeros kept), sparse or dense per the dense-switch rule
+ * (P:501-527).  Collective: all ranks call with the same N, op and opts in
+ * the same order.  `out` (out_bytes >= sparcml_result_bytes(N)) must not
+ * alias the inputs; it is fully written (header + payload).  Never
+ * synchronises the host; read the header after the stream passes.
+ * Errors: N == 0, N > max_N, nnz > max_nnz, null pointers with nnz > 0,
+ * unsupported opts -> SPARCML_ERR_INVALID_ARG; loopback comm ->
+ * SPARCML_ERR_STATE. */
+sparcml_status sparcml_sparse_allreduce(sparcml_comm* comm, const uint32_t* idx, const float* val,
+                                        uint64_t nnz, uint64_t N, sparcml_op op,
+                                        const sparcml_opts* opts_host /* NULL = defaults */,
+                                        void* out, size_t out_bytes, void* stream);
+
+/* Loopback-world allreduce: arrays of nranks per-rank inputs/outputs (host
+ * arrays of device pointers).  Same semantics as above for every rank. */
+sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* comm,
+                                              const uint32_t* const* idx_host,
+                                              const float* const* val_host,
+                                              const uint64_t* nnz_host, uint64_t N, sparcml_op op,
+                                              const sparcml_opts* opts_host,
+                                              void* const* out_host, size_t out_bytes, void* stream);
+
+/* Synchronous helper: copies the 64-byte header at out[0] to the host
+ * (cudaMemcpyAsync on `stream` + stream synchronize). */
+sparcml_status sparcml_read_header(const void* out, sparcml_header* hdr_host, void* stream);
+
+/* ------------------------------ stream ops ----------------------------- */
+
+/* Workspace for the stand-alone stream ops below: size, and one-time zero
+ * initialisation of a fresh allocation (stream-ordered memset). */
+size_t sparcml_ops_workspace_bytes(uint64_t max_elems);
+sparcml_status sparcml_ops_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* Union-merge-with-sum of two sparse streams (§5.1 "Efficient Summation",
+ * both sparse, overlapping indices; no dense switch).  io/vo hold
+ * na+nb pairs; *n_out_dev receives the output count (device uint64). */
+sparcml_status sparcml_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
+                                 const uint32_t* ib, const float* vb, uint64_t nb,
+                                 uint32_t* io, float* vo, uint64_t* n_out_dev,
+                                 void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------- top-k --------------------------------- */
+
+/* Top-k by magnitude (§2.2): the m = min(k, N) coordinates with the
+ * largest |x_j|, ties to the lower index; written sorted by index to
+ * idx_out[m], val_out[m] (= x_j).  residual (nullable, may alias x) receives
+ * x with the selected coordinates zeroed (acc - TopK(acc)).
+ * bucket must be 0 (global top-k).  Requires finite x (NaN/Inf are
+ * reported through sparcml_topk_status).  ws from sparcml_topk_workspace_bytes,
+ * zero-initialised once with sparcml_ops_workspace_init. */
+size_t sparcml_topk_workspace_bytes(uint64_t N, uint64_t k);
+sparcml_status sparcml_topk_sparsify(const float* x, uint64_t N, uint64_t k, uint64_t bucket,
+                                     uint32_t* idx_out, float* val_out, float* residual,
+                                     void* ws, size_t ws_bytes, void* stream);
+
+/* Error-feedback top-k, Algorithm 1: acc = fmaf(alpha, grad, eps)
+ * (one rounding), (idx, val) = TopK(acc), eps <- acc - TopK(acc), in place. */
+sparcml_status sparcml_ef_topk(float* eps, const float* grad, float alpha, uint64_t N,
+                               uint64_t k, uint64_t bucket, uint32_t* idx_out, float* val_out,
+                               void* ws, size_t ws_bytes, void* stream);
+
+/* Synchronous: device status of the last top-k run on `ws` (0 or
+ * SPARCML_ERR_NONFINITE) and how many filter passes it needed. */
+sparcml_status sparcml_topk_status(const void* ws, uint32_t* status_host, uint32_t* passes_host,
+                                   void* stream);
+
+/* -------------------------------- QSGD --------------------------------- */
+
+/* Sizes of a QSGD encoding of n values (§6): ceil(n*bits/8) code
+ * bytes and ceil(n/bucket) fp32 scales. */
+sparcml_status sparcml_quantized_size(uint64_t n, int bits, uint32_t bucket,
+                                      size_t* code_bytes_host, size_t* n_scales_host);
+
+/* Stochastic bucketed quantization (§6, R-16): per bucket
+ * of `bucket` consecutive values scale = max|v|; level = min(s, floor(fl(
+ * fl(fl(|v|/scale)*s) + u))) with s = 2^(bits-1)-1 and u from Philox4x32-10
+ * (key = seed, counter = ctr_base + element index); code = sign<<(bits-1) |
+ * level packed little-endian.  bits in {2,4,8}; bucket multiple of 4. */
+sparcml_status sparcml_quantize(const float* x, uint64_t n, int bits, uint32_t bucket,
+                                uint64_t seed, uint64_t ctr_base, uint8_t* codes, float* scales,
+                                void* stream);
+
+/* v = +-fl(fl(level/s) * scale). */
+sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uint64_t n, int bits,
+                                  uint32_t bucket, float* out, void* stream);
+
+/* ------------------------------ telemetry ------------------------------ */
+
+/* Number of kernels this process has enqueued through the library since
+ * load (the bench's gpu_launches count). */
+uint64_t sparcml_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARCML_H */
