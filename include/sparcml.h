@@ -31,6 +31,10 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
 #define SPARCML_MAX_RANKS 16          /* one 8-GPU box; 16 for loopback worlds */
 #define SPARCML_HEADER_BYTES 64       /* result header at out[0]              */
 #define SPARCML_IPC_HANDLE_BYTES 64   /* cudaIpcMemHandle_t                    */
@@ -69,7 +73,7 @@ typedef struct {
   float switch_scale;     /* delta multiplier, default 1 ("should be even smaller") */
   int index_bytes;        /* c in delta = N*isize/(c+isize); must be 4 (u32) */
   int quant_bits;         /* 0 = off; 2, 4 or 8: QSGD in DSAR phase 2 only (§6) */
-  uint32_t quant_bucket;  /* B, default 1024; multiple of 4, <= 1024, divides 1024 */
+  uint32_t quant_bucket;  /* B, default 1024; a power of two in [8, 1024]     */
   uint64_t seed;          /* Philox key for QSGD                                    */
   uint64_t k_sum_hint;    /* 0 = unknown; else the exact sum of all ranks' nnz: lets
                              the host pick SSAR/DSAR without launching both paths   */
@@ -223,7 +227,8 @@ sparcml_status sparcml_quantized_size(uint64_t n, int bits, uint32_t bucket,
  * of `bucket` consecutive values scale = max|v|; level = min(s, floor(fl(
  * fl(fl(|v|/scale)*s) + u))) with s = 2^(bits-1)-1 and u from Philox4x32-10
  * (key = seed, counter = ctr_base + element index); code = sign<<(bits-1) |
- * level packed little-endian.  bits in {2,4,8}; bucket multiple of 4. */
+ * level packed little-endian.  bits in {2,4,8}; bucket a power of two in
+ * [8, 1024]; codes 4-byte aligned. */
 sparcml_status sparcml_quantize(const float* x, uint64_t n, int bits, uint32_t bucket,
                                 uint64_t seed, uint64_t ctr_base, uint8_t* codes, float* scales,
                                 void* stream);
@@ -237,6 +242,10 @@ sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uin
 /* Number of kernels this process has enqueued through the library since
  * load (the bench's gpu_launches count). */
 uint64_t sparcml_kernel_launches(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 }

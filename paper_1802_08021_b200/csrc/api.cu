@@ -1,0 +1,876 @@
+// api.cu — the C ABI of include/sparcml.h: argument checks, the symmetric
+// workspace and its CUDA-IPC mapping, and the host-side schedule of each
+// collective (which kernels, barriers and buffers, in which order).  Every
+// step of the method runs in the kernels; this file only enqueues them.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace sparcml;
+
+namespace sparcml {
+cudaError_t topk_read_status(const void* ws, uint32_t* status, uint32_t* passes, cudaStream_t s);
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+uint64_t half_cap(uint64_t N) {   // H = ceil4(floor(N/2)): sparse slots in a result
+  return align_up(N / 2, 4);
+}
+
+// ---------------------------------------------------------------------------
+// canonical tree over ranks (reading R-8): tree(lo,hi) = tree(lo,mid) + tree(mid,hi)
+// ---------------------------------------------------------------------------
+struct TreeNode {
+  int lo, mid, hi, height, id;   // id: index of internal node (post-order)
+  int left, right;               // child node ids, -1 for leaves (then leaf = lo / mid)
+};
+
+int build_tree(int lo, int hi, std::vector<TreeNode>& nodes) {   // returns node id or -1 (leaf)
+  if (hi - lo == 1) return -1;
+  const int mid = lo + (hi - lo) / 2;
+  const int l = build_tree(lo, mid, nodes), r = build_tree(mid, hi, nodes);
+  TreeNode n;
+  n.lo = lo;
+  n.mid = mid;
+  n.hi = hi;
+  n.left = l;
+  n.right = r;
+  n.height = 1 + std::max(l < 0 ? 0 : nodes[l].height, r < 0 ? 0 : nodes[r].height);
+  n.id = (int)nodes.size();
+  nodes.push_back(n);
+  return n.id;
+}
+
+TreeSched make_sched(int P) {
+  std::vector<TreeNode> nodes;
+  build_tree(0, P, nodes);
+  TreeSched ts = {};
+  ts.n = (int)nodes.size();
+  for (size_t i = 0; i < nodes.size(); ++i) {   // post-order: children before parents
+    ts.dst[i] = (uint8_t)nodes[i].lo;
+    ts.src[i] = (uint8_t)nodes[i].mid;
+  }
+  return ts;
+}
+
+// ---------------------------------------------------------------------------
+// symmetric workspace layout (identical on every rank)
+// ---------------------------------------------------------------------------
+struct Layout {
+  int P;
+  uint64_t max_N, max_nnz;
+  uint64_t part_cap;     // largest partition
+  uint64_t cap_s;        // pairs per receive region (one per source)
+  size_t status_off, n_status;
+  size_t recv_off, region_bytes;
+  size_t part_off, part_bytes, scales_off;
+  std::vector<size_t> node_off;     // tree internal nodes (non-root)
+  std::vector<uint64_t> node_cap;
+  size_t rd_off, rd_bytes, rd_val_off;   // 5 stream buffers: cur0 cur1 recv0 recv1 recv_init
+  size_t total;
+};
+
+Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
+  Layout L;
+  L.P = P;
+  L.max_N = max_N;
+  L.max_nnz = max_nnz;
+  L.part_cap = max_N / P + P;
+  L.cap_s = std::min<uint64_t>(max_nnz, L.part_cap);
+  size_t off = align_up(sizeof(Ctrl), 256);
+  L.status_off = off;
+  L.n_status = max_N / 1024 + 2 * max_nnz / kMergeTile + 256;
+  off = align_up(off + L.n_status * sizeof(TileStatus), 256);
+  L.recv_off = off;
+  L.region_bytes = align_up(8 * L.cap_s, 256);
+  off += (size_t)P * L.region_bytes;
+  L.part_off = off;
+  L.part_bytes = align_up(8 * L.part_cap + 256, 256);
+  L.scales_off = off + align_up(L.part_cap + 16, 256);   // codes <= part_cap bytes (8 bits)
+  off += L.part_bytes;
+  std::vector<TreeNode> nodes;
+  build_tree(0, P, nodes);
+  L.node_off.assign(nodes.size(), 0);
+  L.node_cap.assign(nodes.size(), 0);
+  for (size_t i = 0; i + 1 < nodes.size(); ++i) {   // the root (last) writes the partition result
+    const uint64_t cap = std::min<uint64_t>((uint64_t)(nodes[i].hi - nodes[i].lo) * L.cap_s, L.part_cap);
+    L.node_off[i] = off;
+    L.node_cap[i] = cap;
+    off = align_up(off + 8 * cap, 256);
+  }
+  L.rd_off = off;
+  L.rd_val_off = align_up(4 * half_cap(max_N) + 64, 256);
+  L.rd_bytes = align_up(std::max<size_t>(2 * L.rd_val_off, 4 * max_N) + 256, 256);
+  const bool pow2 = (P & (P - 1)) == 0;
+  if (pow2 && P > 1) off += 5 * L.rd_bytes;
+  L.total = align_up(off, 1 << 20);
+  return L;
+}
+
+}  // namespace
+
+struct sparcml_comm {
+  int P = 1, rank = 0, device = 0;
+  bool local = false, connected = false;
+  Layout L;
+  std::vector<char*> own;    // workspaces allocated here (local: P, ipc: 1)
+  std::vector<char*> peer;   // every rank's workspace as seen from this process
+  std::vector<bool> opened;  // peer[p] came from cudaIpcOpenMemHandle
+  cudaIpcMemHandle_t handle;
+  std::string err;
+};
+
+namespace {
+
+sparcml_status fail(sparcml_comm* c, sparcml_status s, const std::string& msg) {
+  g_last_error = msg;
+  if (c) c->err = msg;
+  return s;
+}
+
+sparcml_status cuda_fail(sparcml_comm* c, cudaError_t e, const char* what) {
+  return fail(c, SPARCML_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(c, x)                                   \
+  do {                                             \
+    cudaError_t e_ = (x);                          \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, #x); \
+  } while (0)
+
+inline Ctrl* ctrl_of(char* base) { return reinterpret_cast<Ctrl*>(base); }
+inline TileStatus* status_of(const Layout& L, char* base) {
+  return reinterpret_cast<TileStatus*>(base + L.status_off);
+}
+inline uint32_t* recv_idx(const Layout& L, char* base, int src) {
+  return reinterpret_cast<uint32_t*>(base + L.recv_off + (size_t)src * L.region_bytes);
+}
+inline float* recv_val(const Layout& L, char* base, int src) {
+  return reinterpret_cast<float*>(base + L.recv_off + (size_t)src * L.region_bytes + 4 * L.cap_s);
+}
+inline StreamBuf rd_buf(const Layout& L, char* base, int which) {   // 0,1 cur; 2,3 recv; 4 recv_init
+  StreamBuf b;
+  b.base = base + L.rd_off + (size_t)which * L.rd_bytes;
+  b.val_off = L.rd_val_off;
+  return b;
+}
+
+uint64_t effective_delta(uint64_t N, const sparcml_opts& o) {
+  // delta = floor(scale * N*4/(c+4)), c = 4 -> N/2; never above the result capacity
+  const uint64_t d = (uint64_t)std::floor((double)o.switch_scale * (double)N * 4.0 / (double)(o.index_bytes + 4));
+  return std::min<uint64_t>(d, N / 2);
+}
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+sparcml_status check_opts(sparcml_comm* c, const sparcml_opts& o) {
+  if (o.index_bytes != 4) return fail(c, SPARCML_ERR_INVALID_ARG, "index_bytes must be 4 (u32 indices, P:931)");
+  if (!(o.switch_scale > 0.0f) || o.switch_scale > 1.0f)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "switch_scale must be in (0, 1]");
+  if (o.quant_bits != 0 && o.quant_bits != 2 && o.quant_bits != 4 && o.quant_bits != 8)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "quant_bits must be 0, 2, 4 or 8");
+  if (o.quant_bits && (o.quant_bucket < 8 || o.quant_bucket > 1024 || (o.quant_bucket & (o.quant_bucket - 1))))
+    return fail(c, SPARCML_ERR_INVALID_ARG, "quant_bucket must be a power of two in [8, 1024]");
+  if (o.algo < SPARCML_ALGO_AUTO || o.algo > SPARCML_DSAR_SPLIT_ALLGATHER)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "unknown algorithm");
+  return SPARCML_OK;
+}
+
+// per-call parameters shared by all local ranks
+struct CallCtx {
+  uint64_t N, delta, val_offset;
+  sparcml_opts o;
+  int algo;            // resolved: RD, SPLIT (SSAR/DSAR/AUTO decided below)
+  int host_dsar;       // -1 unknown (device decides), 0/1 known
+  cudaStream_t s;
+};
+
+BarrierArgs barrier_args(sparcml_comm* c, int r, int first) {
+  BarrierArgs b = {};
+  b.my = ctrl_of(c->peer[r]);
+  b.P = c->P;
+  b.rank = r;
+  b.first_in_call = first;
+  b.loopback = c->local ? 1 : 0;
+  for (int p = 0; p < c->P; ++p) b.peer_flags[p] = &ctrl_of(c->peer[p])->flags[r];
+  return b;
+}
+
+// ------------------------------------------------------------ RD schedule ---
+sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
+                      const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
+  const Layout& L = c->L;
+  const int P = c->P;
+  int Lg = 0;
+  while ((1 << Lg) < P) ++Lg;
+  if (P == 2)   // one stage: protect recv_init from the next call (graph-replay safe)
+    for (int r : R) CK(c, launch_barrier(barrier_args(c, r, 1), cc.s));
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int r = R[i], q = r ^ 1;
+    RdPushArgs a = {};
+    a.idx = idx[i];
+    a.val = val[i];
+    a.n = nnz[i];
+    a.dst = rd_buf(L, c->peer[q], 4);
+    a.dst_n = &ctrl_of(c->peer[q])->rd_n[2];
+    a.dst_dense = &ctrl_of(c->peer[q])->rd_dense[2];
+    a.dst_ksum = &ctrl_of(c->peer[q])->rd_ksum[2];
+    a.ctl = ctrl_of(c->peer[r]);
+    a.N = cc.N;
+    a.validate = cc.o.validate;
+    CK(c, launch_rd_push(a, cc.s));
+  }
+  for (int t = 1; t <= Lg; ++t) {
+    for (int r : R) CK(c, launch_barrier(barrier_args(c, r, t == 1 && P != 2), cc.s));
+    for (size_t i = 0; i < R.size(); ++i) {
+      const int r = R[i];
+      Ctrl* my = ctrl_of(c->peer[r]);
+      RdStageArgs a = {};
+      if (t == 1) {
+        a.a_idx = idx[i];
+        a.a_val = val[i];
+        a.a_n = nnz[i];
+      } else {
+        StreamBuf cur = rd_buf(L, c->peer[r], (t - 1) % 2);
+        a.a_idx = reinterpret_cast<const uint32_t*>(cur.base);
+        a.a_val = reinterpret_cast<const float*>(cur.base + cur.val_off);
+        a.a_n_dev = &my->own_n[(t - 1) % 2];
+        a.a_dense_dev = &my->own_dense[(t - 1) % 2];
+        a.a_ksum_dev = &my->own_ksum[(t - 1) % 2];
+      }
+      const int rb = t == 1 ? 4 : 2 + (t % 2);
+      const int ci = t == 1 ? 2 : t % 2;   // ctrl slot of that recv buffer
+      a.b = rd_buf(L, c->peer[r], rb);
+      a.b_n_dev = &my->rd_n[ci];
+      a.b_dense_dev = &my->rd_dense[ci];
+      a.b_ksum_dev = &my->rd_ksum[ci];
+      a.N = cc.N;
+      a.delta = cc.delta;
+      if (t == Lg) {
+        a.o.base = out[i] + SPARCML_HEADER_BYTES;
+        a.o.val_off = cc.val_offset - SPARCML_HEADER_BYTES;
+        a.o_n_dev = &my->own_n[t % 2];   // scratch copies of the final counts
+        a.o_dense_dev = &my->own_dense[t % 2];
+        a.o_ksum_dev = &my->own_ksum[t % 2];
+        a.hdr = reinterpret_cast<sparcml_header*>(out[i]);
+        a.last = 1;
+      } else {
+        a.o = rd_buf(L, c->peer[r], t % 2);
+        a.o_n_dev = &my->own_n[t % 2];
+        a.o_dense_dev = &my->own_dense[t % 2];
+        a.o_ksum_dev = &my->own_ksum[t % 2];
+        const int q = r ^ (1 << t);   // next stage's partner
+        Ctrl* qc = ctrl_of(c->peer[q]);
+        const int qslot = (t + 1) % 2;
+        a.m = rd_buf(L, c->peer[q], 2 + qslot);
+        a.m_n_dev = &qc->rd_n[qslot];
+        a.m_dense_dev = &qc->rd_dense[qslot];
+        a.m_ksum_dev = &qc->rd_ksum[qslot];
+      }
+      a.ctl = my;
+      a.stage = t;
+      a.ctr = &my->scan[0];
+      a.status = status_of(L, c->peer[r]);
+      CK(c, launch_rd_stage(a, cc.s));
+    }
+  }
+  return SPARCML_OK;
+}
+
+// --------------------------------------------------------- split schedule ---
+sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
+                         const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
+  const Layout& L = c->L;
+  const int P = c->P;
+  const uint64_t part = cc.N / P;
+  uint64_t bnd[kMaxRanks + 1];
+  for (int j = 0; j < P; ++j) bnd[j] = (uint64_t)j * part;
+  bnd[P] = cc.N;
+  // phase 1: split + push to owners
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int r = R[i];
+    PushArgs a = {};
+    a.idx = idx[i];
+    a.val = val[i];
+    a.n = nnz[i];
+    a.N = cc.N;
+    a.P = P;
+    a.rank = r;
+    for (int j = 0; j <= P; ++j) a.bnd[j] = bnd[j];
+    for (int j = 0; j < P; ++j) {
+      a.dst_idx[j] = recv_idx(L, c->peer[j], r);
+      a.dst_val[j] = recv_val(L, c->peer[j], r);
+      a.dst_cnt[j] = &ctrl_of(c->peer[j])->slice_cnt[r];
+      a.dst_k[j] = &ctrl_of(c->peer[j])->k_in[r];
+    }
+    a.ctl = ctrl_of(c->peer[r]);
+    a.validate = cc.o.validate;
+    CK(c, launch_split_push(a, cc.s));
+  }
+  for (int r : R) {
+    Ctrl* my = ctrl_of(c->peer[r]);
+    DecideArgs d;
+    d.k_in = my->k_in;
+    d.P = P;
+    d.algo = cc.o.algo == SPARCML_SSAR_RECURSIVE_DOUBLE ? SPARCML_ALGO_AUTO : cc.o.algo;
+    d.delta = (uint64_t)std::floor((double)cc.delta);
+    d.dsar_out = &my->dsar;
+    d.k_sum_out = &my->k_sum;
+    CK(c, launch_barrier_decide(barrier_args(c, r, 1), d, cc.s));
+  }
+  const bool run_ssar = cc.host_dsar != 1, run_dsar = cc.host_dsar != 0;
+  std::vector<TreeNode> nodes;
+  build_tree(0, P, nodes);
+  int H = 0;
+  for (auto& n : nodes) H = std::max(H, n.height);
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int r = R[i];
+    char* base = c->peer[r];
+    Ctrl* my = ctrl_of(base);
+    if (run_ssar) {
+      // owner reduction: canonical tree of union-merges, one batched launch per height
+      for (int h = 1; h <= H; ++h) {
+        MergeJobsArgs m = {};
+        for (size_t ni = 0; ni < nodes.size(); ++ni) {
+          const TreeNode& nd = nodes[ni];
+          if (nd.height != h) continue;
+          MergeJob& jb = m.job[m.njobs++];
+          auto src = [&](int child, int leaf, const uint32_t** ix, const float** vx, const uint64_t** nx) {
+            if (child < 0) {
+              *ix = recv_idx(L, base, leaf);
+              *vx = recv_val(L, base, leaf);
+              *nx = &my->slice_cnt[leaf];
+            } else {
+              *ix = reinterpret_cast<const uint32_t*>(base + L.node_off[child]);
+              *vx = reinterpret_cast<const float*>(base + L.node_off[child] + 4 * L.node_cap[child]);
+              *nx = &my->node_n[child];
+            }
+          };
+          src(nd.left, nd.lo, &jb.a_idx, &jb.a_val, &jb.a_n_dev);
+          src(nd.right, nd.mid, &jb.b_idx, &jb.b_val, &jb.b_n_dev);
+          if ((size_t)nd.id + 1 == nodes.size()) {   // root -> partition result
+            jb.out.idx = reinterpret_cast<uint32_t*>(base + L.part_off);
+            jb.out.val = reinterpret_cast<float*>(base + L.part_off + 4 * L.part_cap);
+            jb.out.n = &my->owner_K;
+          } else {
+            jb.out.idx = reinterpret_cast<uint32_t*>(base + L.node_off[nd.id]);
+            jb.out.val = reinterpret_cast<float*>(base + L.node_off[nd.id] + 4 * L.node_cap[nd.id]);
+            jb.out.n = &my->node_n[nd.id];
+          }
+        }
+        m.ctr = &my->scan[0];
+        m.status = status_of(L, base);
+        if (cc.host_dsar < 0) m.gate = Gate{&my->dsar, 0u};
+        CK(c, launch_merge_jobs(m, 1 << 30, cc.s));
+      }
+    }
+    if (run_dsar) {
+      // DSAR owner: P sparse slices -> dense partition (+ QSGD), one fused window pass
+      WindowArgs w = {};
+      w.nsrc = P;
+      for (int s = 0; s < P; ++s) {
+        w.src[s].idx = recv_idx(L, base, s);
+        w.src[s].val = recv_val(L, base, s);
+        w.src[s].n_dev = &my->slice_cnt[s];
+      }
+      w.sched = make_sched(P);
+      w.lo = bnd[r];
+      w.hi = bnd[r + 1];
+      if (cc.o.quant_bits) {
+        w.out.mode = WIN_QUANT;
+        w.out.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
+        w.out.scales = reinterpret_cast<float*>(base + L.scales_off);
+        w.out.qbase = bnd[r];
+        w.out.bits = cc.o.quant_bits;
+        w.out.bucket = cc.o.quant_bucket;
+        w.out.seed_lo = (uint32_t)cc.o.seed;
+        w.out.seed_hi = (uint32_t)(cc.o.seed >> 32);
+      } else {
+        w.out.mode = WIN_DENSE;
+        w.out.dense = reinterpret_cast<float*>(base + L.part_off);
+        w.out.dense_base = bnd[r];
+      }
+      w.ctr = &my->scan[0];
+      w.status = status_of(L, base);
+      if (cc.host_dsar < 0) w.gate = Gate{&my->dsar, 1u};
+      CK(c, launch_window(w, cc.s));
+    }
+  }
+  for (int r : R) CK(c, launch_barrier(barrier_args(c, r, 0), cc.s));
+  // phase 2: pull every partition result into out
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int r = R[i];
+    ConcatArgs a = {};
+    a.P = P;
+    a.rank = r;
+    a.N = cc.N;
+    a.delta = cc.delta;
+    for (int j = 0; j <= P; ++j) a.bnd[j] = bnd[j];
+    for (int j = 0; j < P; ++j) {
+      char* pb = c->peer[j];
+      a.r_idx[j] = reinterpret_cast<const uint32_t*>(pb + L.part_off);
+      a.r_val[j] = reinterpret_cast<const float*>(pb + L.part_off + 4 * L.part_cap);
+      a.r_n[j] = &ctrl_of(pb)->owner_K;
+      a.r_codes[j] = reinterpret_cast<const uint8_t*>(pb + L.part_off);
+      a.r_scales[j] = reinterpret_cast<const float*>(pb + L.scales_off);
+      a.r_dense[j] = reinterpret_cast<const float*>(pb + L.part_off);
+    }
+    a.ctl = ctrl_of(c->peer[r]);
+    a.bits = cc.o.quant_bits;
+    a.bucket = cc.o.quant_bucket ? cc.o.quant_bucket : 1024;
+    a.out = out[i];
+    a.val_offset = cc.val_offset;
+    a.algo = SPARCML_SSAR_SPLIT_ALLGATHER;
+    a.ctr = &ctrl_of(c->peer[r])->scan[0];
+    a.status = status_of(L, c->peer[r]);
+    CK(c, launch_concat(a, cc.s));
+  }
+  return SPARCML_OK;
+}
+
+// ------------------------------------------------------------- P == 1 ---
+sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, uint64_t n, char* out,
+                      const CallCtx& cc) {
+  const Layout& L = c->L;
+  char* base = c->peer[0];
+  Ctrl* my = ctrl_of(base);
+  P1PrepArgs p = {};
+  p.idx = idx;
+  p.val = val;
+  p.n = n;
+  p.N = cc.N;
+  p.delta = cc.delta;
+  p.algo = cc.o.algo;
+  p.ctl = my;
+  p.validate = cc.o.validate;
+  CK(c, launch_p1_prep(p, cc.s));
+  const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER ||
+                    (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
+  ConcatArgs a = {};
+  a.P = 1;
+  a.rank = 0;
+  a.N = cc.N;
+  a.delta = cc.delta;
+  a.bnd[0] = 0;
+  a.bnd[1] = cc.N;
+  a.r_idx[0] = idx;
+  a.r_val[0] = val;
+  a.r_n[0] = &my->owner_K;
+  if (dsar) {
+    WindowArgs w = {};
+    w.nsrc = 1;
+    w.src[0].idx = idx;
+    w.src[0].val = val;
+    w.src[0].n = n;
+    w.sched.n = 0;
+    w.lo = 0;
+    w.hi = cc.N;
+    if (cc.o.quant_bits) {
+      w.out.mode = WIN_QUANT;
+      w.out.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
+      w.out.scales = reinterpret_cast<float*>(base + L.scales_off);
+      w.out.qbase = 0;
+      w.out.bits = cc.o.quant_bits;
+      w.out.bucket = cc.o.quant_bucket;
+      w.out.seed_lo = (uint32_t)cc.o.seed;
+      w.out.seed_hi = (uint32_t)(cc.o.seed >> 32);
+    } else {
+      w.out.mode = WIN_DENSE;
+      w.out.dense = reinterpret_cast<float*>(base + L.part_off);
+      w.out.dense_base = 0;
+    }
+    w.ctr = &my->scan[0];
+    w.status = status_of(L, base);
+    CK(c, launch_window(w, cc.s));
+    a.r_codes[0] = reinterpret_cast<const uint8_t*>(base + L.part_off);
+    a.r_scales[0] = reinterpret_cast<const float*>(base + L.scales_off);
+    a.r_dense[0] = reinterpret_cast<const float*>(base + L.part_off);
+  }
+  a.ctl = my;
+  a.bits = cc.o.quant_bits;
+  a.bucket = cc.o.quant_bucket ? cc.o.quant_bucket : 1024;
+  a.out = out;
+  a.val_offset = cc.val_offset;
+  a.algo = cc.o.algo == SPARCML_ALGO_AUTO ? SPARCML_SSAR_SPLIT_ALLGATHER : cc.o.algo;
+  a.ctr = &my->scan[0];
+  a.status = status_of(L, base);
+  CK(c, launch_concat(a, cc.s));
+  return SPARCML_OK;
+}
+
+sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
+                              const uint64_t* nnz, uint64_t N, sparcml_op op, const sparcml_opts* opts,
+                              void* const* out, size_t out_bytes, void* stream) {
+  if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
+  if (!c->connected) return fail(c, SPARCML_ERR_STATE, "communicator not connected");
+  if (op != SPARCML_OP_SUM) return fail(c, SPARCML_ERR_INVALID_ARG, "only SPARCML_OP_SUM is supported");
+  if (N == 0 || N > c->L.max_N) return fail(c, SPARCML_ERR_INVALID_ARG, "N must be in [1, max_N]");
+  if (N > 0xFFFFFFFFull) return fail(c, SPARCML_ERR_INVALID_ARG, "N must fit u32 indices");
+  if ((uint64_t)c->P > N) return fail(c, SPARCML_ERR_INVALID_ARG, "N must be >= nranks");
+  sparcml_opts o;
+  sparcml_opts_default(&o);
+  if (opts) o = *opts;
+  sparcml_status st = check_opts(c, o);
+  if (st != SPARCML_OK) return st;
+  if (out_bytes < sparcml_result_bytes(N)) return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N)");
+  const int nl = c->local ? c->P : 1;
+  uint64_t ksum_host = 0;
+  for (int i = 0; i < nl; ++i) {
+    if (nnz[i] > c->L.max_nnz) return fail(c, SPARCML_ERR_INVALID_ARG, "nnz > max_nnz");
+    if (nnz[i] > N) return fail(c, SPARCML_ERR_INVALID_ARG, "nnz > N");
+    if (nnz[i] > 0 && (!idx[i] || !val[i])) return fail(c, SPARCML_ERR_INVALID_ARG, "null input with nnz > 0");
+    if (!out[i]) return fail(c, SPARCML_ERR_INVALID_ARG, "null out");
+    if ((reinterpret_cast<uintptr_t>(out[i]) & 15u) != 0) return fail(c, SPARCML_ERR_INVALID_ARG, "out must be 16-byte aligned");
+    ksum_host += nnz[i];
+  }
+  CallCtx cc;
+  cc.N = N;
+  cc.o = o;
+  cc.delta = effective_delta(N, o);
+  cc.val_offset = sparcml_result_val_offset(N);
+  cc.s = static_cast<cudaStream_t>(stream);
+  CK(c, cudaSetDevice(c->device));
+  // algorithm: AUTO -> recursive doubling for small data (latency-bound,
+  // P:635-650), split-allgather otherwise; RD needs P = 2^m
+  int algo = o.algo;
+  if (algo == SPARCML_ALGO_AUTO && c->P > 1)
+    algo = (is_pow2(c->P) && 4 * N <= (256u << 10)) ? SPARCML_SSAR_RECURSIVE_DOUBLE : SPARCML_ALGO_AUTO;
+  if (algo == SPARCML_SSAR_RECURSIVE_DOUBLE && !is_pow2(c->P))
+    return fail(c, SPARCML_ERR_INVALID_ARG, "recursive doubling needs a power-of-two world");
+  cc.algo = algo;
+  // SSAR/DSAR for split-allgather: forced, or AUTO by sum k_i > delta (R-5)
+  if (algo == SPARCML_SSAR_SPLIT_ALLGATHER) cc.host_dsar = 0;
+  else if (algo == SPARCML_DSAR_SPLIT_ALLGATHER) cc.host_dsar = 1;
+  else if (c->local) cc.host_dsar = ksum_host > cc.delta ? 1 : 0;
+  else if (o.k_sum_hint) cc.host_dsar = o.k_sum_hint > cc.delta ? 1 : 0;
+  else cc.host_dsar = -1;
+  if (c->P == 1) return run_p1(c, idx[0], val[0], nnz[0], static_cast<char*>(out[0]), cc);
+  std::vector<int> R;
+  if (c->local)
+    for (int r = 0; r < c->P; ++r) R.push_back(r);
+  else
+    R.push_back(c->rank);
+  char* const* outs = reinterpret_cast<char* const*>(out);
+  if (algo == SPARCML_SSAR_RECURSIVE_DOUBLE) return run_rd(c, R, idx, val, nnz, outs, cc);
+  return run_split(c, R, idx, val, nnz, outs, cc);
+}
+
+sparcml_status alloc_ws(sparcml_comm* c, char** p) {
+  cudaError_t e = cudaMalloc(p, c->L.total);
+  if (e == cudaErrorMemoryAllocation) return fail(c, SPARCML_ERR_OOM, "workspace allocation failed");
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc");
+  e = cudaMemset(*p, 0, c->L.total);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset");
+  return SPARCML_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* sparcml_version(void) { return "sparcml-b200 0.1 (sm_100a)"; }
+
+const char* sparcml_status_string(sparcml_status s) {
+  switch (s) {
+    case SPARCML_OK: return "ok";
+    case SPARCML_ERR_INVALID_ARG: return "invalid argument";
+    case SPARCML_ERR_UNSORTED: return "input indices not strictly increasing or out of range";
+    case SPARCML_ERR_NONFINITE: return "non-finite value";
+    case SPARCML_ERR_MISMATCH: return "ranks disagree on a collective argument";
+    case SPARCML_ERR_CUDA: return "CUDA error";
+    case SPARCML_ERR_OOM: return "out of device memory";
+    case SPARCML_ERR_STATE: return "communicator in the wrong state";
+  }
+  return "unknown status";
+}
+
+void sparcml_opts_default(sparcml_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->algo = SPARCML_ALGO_AUTO;
+  o->switch_scale = 1.0f;
+  o->index_bytes = 4;
+  o->quant_bits = 0;
+  o->quant_bucket = 1024;
+  o->seed = 0;
+  o->k_sum_hint = 0;
+  o->validate = 0;
+}
+
+uint64_t sparcml_switch_threshold(uint64_t N, int isize, int c, float scale) {
+  if (N == 0 || isize <= 0 || c <= 0 || !(scale > 0.0f)) return 0;
+  return (uint64_t)std::floor((double)scale * (double)N * (double)isize / (double)(c + isize));
+}
+
+double sparcml_expected_nnz(uint64_t k, uint64_t N, int P) {
+  if (N == 0 || P <= 0) return 0.0;
+  const double d = std::min(1.0, (double)k / (double)N);
+  if (d >= 1.0) return (double)N;
+  return (double)N * -std::expm1((double)P * std::log1p(-d));   // N(1-(1-d)^P)
+}
+
+size_t sparcml_result_val_offset(uint64_t N) { return SPARCML_HEADER_BYTES + 4 * half_cap(N); }
+
+size_t sparcml_result_bytes(uint64_t N) {
+  return SPARCML_HEADER_BYTES + std::max<size_t>(4 * N, 8 * half_cap(N)) + 32;
+}
+
+sparcml_status sparcml_comm_create(sparcml_comm** out, int nranks, int rank, int dev, uint64_t max_N,
+                                   uint64_t max_nnz) {
+  if (!out) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  if (nranks < 1 || nranks > SPARCML_MAX_RANKS || rank < 0 || rank >= nranks)
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bad nranks/rank");
+  if (max_N == 0 || max_N > 0xFFFFFFFFull || max_nnz == 0)
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bad max_N / max_nnz");
+  if (nranks > 8) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "IPC worlds span one 8-GPU box");
+  sparcml_comm* c = new sparcml_comm();
+  c->P = nranks;
+  c->rank = rank;
+  c->device = dev;
+  c->L = make_layout(nranks, max_N, max_nnz);
+  cudaError_t e = cudaSetDevice(dev);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(nullptr, e, "cudaSetDevice");
+  }
+  char* p = nullptr;
+  sparcml_status st = alloc_ws(c, &p);
+  if (st != SPARCML_OK) {
+    delete c;
+    return st;
+  }
+  c->own.push_back(p);
+  c->peer.assign(nranks, nullptr);
+  c->opened.assign(nranks, false);
+  c->peer[rank] = p;
+  if (nranks > 1) {
+    e = cudaIpcGetMemHandle(&c->handle, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      delete c;
+      return cuda_fail(nullptr, e, "cudaIpcGetMemHandle");
+    }
+  } else {
+    c->connected = true;
+  }
+  *out = c;
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_comm_export_handle(sparcml_comm* c, uint8_t* h) {
+  if (!c || !h) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
+  if (c->local) return fail(c, SPARCML_ERR_STATE, "loopback worlds have no handle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == SPARCML_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(h, &c->handle, SPARCML_IPC_HANDLE_BYTES);
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_comm_connect(sparcml_comm* c, const uint8_t* all) {
+  if (!c || !all) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
+  if (c->local) return fail(c, SPARCML_ERR_STATE, "loopback worlds are connected at creation");
+  if (c->connected) return SPARCML_OK;
+  CK(c, cudaSetDevice(c->device));
+  for (int p = 0; p < c->P; ++p) {
+    if (p == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, all + (size_t)p * SPARCML_IPC_HANDLE_BYTES, SPARCML_IPC_HANDLE_BYTES);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaIpcOpenMemHandle");
+    c->peer[p] = static_cast<char*>(ptr);
+    c->opened[p] = true;
+  }
+  c->connected = true;
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_comm_create_local(sparcml_comm** out, int nranks, int dev, uint64_t max_N,
+                                         uint64_t max_nnz) {
+  if (!out) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null out");
+  *out = nullptr;
+  if (nranks < 1 || nranks > SPARCML_MAX_RANKS) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bad nranks");
+  if (max_N == 0 || max_N > 0xFFFFFFFFull || max_nnz == 0)
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bad max_N / max_nnz");
+  sparcml_comm* c = new sparcml_comm();
+  c->P = nranks;
+  c->rank = -1;
+  c->device = dev;
+  c->local = true;
+  c->L = make_layout(nranks, max_N, max_nnz);
+  cudaError_t e = cudaSetDevice(dev);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(nullptr, e, "cudaSetDevice");
+  }
+  for (int r = 0; r < nranks; ++r) {
+    char* p = nullptr;
+    sparcml_status st = alloc_ws(c, &p);
+    if (st != SPARCML_OK) {
+      for (char* q : c->own) cudaFree(q);
+      delete c;
+      return st;
+    }
+    c->own.push_back(p);
+  }
+  c->peer = c->own;
+  c->opened.assign(nranks, false);
+  c->connected = true;
+  *out = c;
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_comm_destroy(sparcml_comm* c) {
+  if (!c) return SPARCML_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int p = 0; p < (int)c->peer.size(); ++p)
+    if (c->opened[p]) cudaIpcCloseMemHandle(c->peer[p]);
+  for (char* q : c->own) cudaFree(q);
+  delete c;
+  return SPARCML_OK;
+}
+
+int sparcml_comm_nranks(const sparcml_comm* c) { return c ? c->P : 0; }
+int sparcml_comm_rank(const sparcml_comm* c) { return c ? c->rank : -1; }
+const char* sparcml_last_error(const sparcml_comm* c) {
+  return c ? c->err.c_str() : g_last_error.c_str();
+}
+
+sparcml_status sparcml_sparse_allreduce(sparcml_comm* c, const uint32_t* idx, const float* val, uint64_t nnz,
+                                        uint64_t N, sparcml_op op, const sparcml_opts* opts, void* out,
+                                        size_t out_bytes, void* stream) {
+  if (c && c->local) return fail(c, SPARCML_ERR_STATE, "use sparcml_sparse_allreduce_local on a loopback world");
+  return allreduce_impl(c, &idx, &val, &nnz, N, op, opts, &out, out_bytes, stream);
+}
+
+sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
+                                              const uint64_t* nnz, uint64_t N, sparcml_op op,
+                                              const sparcml_opts* opts, void* const* out, size_t out_bytes,
+                                              void* stream) {
+  if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
+  if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
+  return allreduce_impl(c, idx, val, nnz, N, op, opts, out, out_bytes, stream);
+}
+
+sparcml_status sparcml_read_header(const void* out, sparcml_header* h, void* stream) {
+  if (!out || !h) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(nullptr, cudaMemcpyAsync(h, out, sizeof(sparcml_header), cudaMemcpyDeviceToHost, s));
+  CK(nullptr, cudaStreamSynchronize(s));
+  return SPARCML_OK;
+}
+
+size_t sparcml_ops_workspace_bytes(uint64_t max_elems) {
+  return 256 + (max_elems / kMergeTile + 4) * sizeof(TileStatus);
+}
+
+sparcml_status sparcml_ops_workspace_init(void* ws, size_t bytes, void* stream) {
+  if (!ws) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null workspace");
+  CK(nullptr, cudaMemsetAsync(ws, 0, bytes, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_merge_sum(const uint32_t* ia, const float* va, uint64_t na, const uint32_t* ib,
+                                 const float* vb, uint64_t nb, uint32_t* io, float* vo, uint64_t* n_out,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  if (!n_out || !ws) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  if ((na && (!ia || !va)) || (nb && (!ib || !vb)) || ((na + nb) && (!io || !vo)))
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null stream with nonzero length");
+  if (ws_bytes < sparcml_ops_workspace_bytes(na + nb)) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "workspace too small");
+  MergeJobsArgs m = {};
+  m.njobs = 1;
+  m.job[0].a_idx = ia;
+  m.job[0].a_val = va;
+  m.job[0].a_n = na;
+  m.job[0].b_idx = ib;
+  m.job[0].b_val = vb;
+  m.job[0].b_n = nb;
+  m.job[0].out.idx = io;
+  m.job[0].out.val = vo;
+  m.job[0].out.n = n_out;
+  m.ctr = static_cast<ScanCounters*>(ws);
+  m.status = reinterpret_cast<TileStatus*>(static_cast<char*>(ws) + 256);
+  const int tiles = (int)std::min<uint64_t>((na + nb + kMergeTile - 1) / kMergeTile, 1u << 20);
+  CK(nullptr, launch_merge_jobs(m, std::max(1, tiles), static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+size_t sparcml_topk_workspace_bytes(uint64_t N, uint64_t k) { return topk_workspace_bytes(N, k); }
+
+static sparcml_status topk_common(const float* x, const float* grad, float alpha, int ef, float* xout, uint64_t N,
+                                  uint64_t k, uint64_t bucket, uint32_t* io, float* vo, float* resid, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  if (N == 0 || k == 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "N and k must be positive");
+  if (N > 0xFFFFFFFFull) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "N must fit u32 indices");
+  if (bucket != 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bucketed top-k is not implemented (bucket must be 0)");
+  if (!x || !io || !vo || (ef && !grad)) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; };
+  if (mis(x) || (grad && mis(grad)) || (resid && mis(resid)))
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "vectors must be 16-byte aligned");
+  if (k < N && (!ws || ws_bytes < topk_workspace_bytes(N, k)))
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "workspace too small");
+  CK(nullptr, launch_topk(x, grad, alpha, ef, xout, N, k, io, vo, resid, ws, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_topk_sparsify(const float* x, uint64_t N, uint64_t k, uint64_t bucket, uint32_t* io,
+                                     float* vo, float* resid, void* ws, size_t ws_bytes, void* stream) {
+  return topk_common(x, nullptr, 0.0f, 0, nullptr, N, k, bucket, io, vo, resid, ws, ws_bytes, stream);
+}
+
+sparcml_status sparcml_ef_topk(float* eps, const float* grad, float alpha, uint64_t N, uint64_t k, uint64_t bucket,
+                               uint32_t* io, float* vo, void* ws, size_t ws_bytes, void* stream) {
+  return topk_common(eps, grad, alpha, 1, eps, N, k, bucket, io, vo, nullptr, ws, ws_bytes, stream);
+}
+
+sparcml_status sparcml_topk_status(const void* ws, uint32_t* status, uint32_t* passes, void* stream) {
+  if (!ws || !status || !passes) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  CK(nullptr, topk_read_status(ws, status, passes, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_quantized_size(uint64_t n, int bits, uint32_t bucket, size_t* cb, size_t* ns) {
+  if (!cb || !ns || (bits != 2 && bits != 4 && bits != 8) || bucket == 0)
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bad quantizer arguments");
+  *cb = (size_t)((n * (uint64_t)bits + 7) / 8);
+  *ns = (size_t)((n + bucket - 1) / bucket);
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_quantize(const float* x, uint64_t n, int bits, uint32_t bucket, uint64_t seed,
+                                uint64_t ctr_base, uint8_t* codes, float* scales, void* stream) {
+  if ((bits != 2 && bits != 4 && bits != 8) || bucket < 8 || bucket > 1024 || (bucket & (bucket - 1)))
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bits in {2,4,8}, bucket a power of two in [8,1024]");
+  if (n == 0) return SPARCML_OK;
+  if (!x || !codes || !scales) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(codes) & 3u) != 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "codes must be 4-byte aligned");
+  CK(nullptr, launch_quantize(x, n, bits, bucket, seed, ctr_base, codes, scales, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uint64_t n, int bits, uint32_t bucket,
+                                  float* out, void* stream) {
+  if ((bits != 2 && bits != 4 && bits != 8) || bucket < 8 || (bucket & 7))
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bits in {2,4,8}, bucket a multiple of 8");
+  if (n == 0) return SPARCML_OK;
+  if (!codes || !scales || !out) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  if ((reinterpret_cast<uintptr_t>(codes) & 7u) != 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "codes must be 8-byte aligned");
+  CK(nullptr, launch_dequantize(codes, scales, n, bits, bucket, out, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+uint64_t sparcml_kernel_launches(void) { return (uint64_t)g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,287 @@
+// common.cuh — device helpers and shared layouts of libsparcml (sm_100a).
+//
+// Nothing here is shared with oracle/ (which is plain C); this header is
+// product code only.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sparcml.h"
+
+namespace sparcml {
+
+constexpr int kMaxRanks = SPARCML_MAX_RANKS;
+constexpr int kThreads = 256;            // every tile kernel: 8 warps
+constexpr int kWarps = kThreads / 32;
+constexpr int kMergeItems = 8;           // merge-path items per thread
+constexpr int kMergeTile = kThreads * kMergeItems;   // 2048 merged inputs per tile
+constexpr int kWin = 1024;               // window kernel: index positions per window
+constexpr int kWinPerThread = kWin / kThreads;       // 4
+constexpr int kMaxJobs = kMaxRanks / 2;  // batched merges per launch
+
+// ---------------------------------------------------------------------------
+// memory-model helpers (PTX)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// streaming (read-once) vector load, no L1 allocation
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// warp / block scans (256 threads)
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_sum(T x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Exclusive block sum of `x` over kThreads threads; returns the prefix and
+// writes the block total to *total.  `scratch` holds kWarps+1 elements.
+template <typename T>
+__device__ __forceinline__ T block_exclusive_sum(T x, T* scratch, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = warp_inclusive_sum(x);
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T w = lane < kWarps ? scratch[lane] : T(0);
+    T wi = warp_inclusive_sum(w);
+    if (lane < kWarps) scratch[lane] = wi - w;
+    if (lane == kWarps - 1) scratch[kWarps] = wi;
+  }
+  __syncthreads();
+  T r = scratch[warp] + inc - x;
+  *total = scratch[kWarps];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// ordered tile scan: dynamic tickets + decoupled look-back (single pass)
+// ---------------------------------------------------------------------------
+struct ScanCounters {
+  uint32_t ticket;   // next tile ticket
+  uint32_t done;     // blocks finished
+  uint32_t gen;      // launch generation (tags TileStatus entries)
+  uint32_t pad;
+};
+
+struct alignas(32) TileStatus {
+  uint32_t flag;     // (gen << 2) | state ; state 1 = aggregate, 2 = inclusive
+  uint32_t pad;
+  uint64_t agg;
+  uint64_t incl;
+  uint64_t pad2;
+};
+
+// Called by ONE thread.  Publishes this tile's aggregate, walks back to the
+// nearest inclusive predecessor within [first, tile) and returns the exclusive
+// prefix.  `first` is the job's first global tile (look-back never crosses it).
+__device__ __forceinline__ uint64_t tile_lookback(TileStatus* st, uint32_t tile, uint32_t first,
+                                                  uint64_t agg, uint32_t gen) {
+  const uint32_t tag = gen << 2;
+  if (tile == first) {
+    st[tile].incl = agg;
+    __threadfence();
+    st_release_gpu(&st[tile].flag, tag | 2u);
+    return 0;
+  }
+  st[tile].agg = agg;
+  __threadfence();
+  st_release_gpu(&st[tile].flag, tag | 1u);
+  uint64_t excl = 0;
+  uint32_t t = tile - 1;
+  while (true) {
+    uint32_t f;
+    do {
+      f = ld_acquire_gpu(&st[t].flag);
+    } while ((f & ~3u) != tag || (f & 3u) == 0);
+    if ((f & 3u) == 2u) {
+      excl += ld_relaxed_gpu(&st[t].incl);
+      break;
+    }
+    excl += ld_relaxed_gpu(&st[t].agg);
+    if (t == first) break;   // cannot happen: the first tile publishes inclusive
+    --t;
+  }
+  st[tile].incl = excl + agg;
+  __threadfence();
+  st_release_gpu(&st[tile].flag, tag | 2u);
+  return excl;
+}
+
+// End-of-kernel protocol for ticketed kernels: the last block to finish
+// resets the ticket/done counters and bumps the generation.
+__device__ __forceinline__ void scan_block_exit(ScanCounters* c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t d = atomicAdd(&c->done, 1u);
+    if (d == gridDim.x - 1) {
+      c->ticket = 0;
+      c->done = 0;
+      c->gen = c->gen + 1;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. SC'11).  Independent implementation from the
+// oracle's; equality is checked by the parity tests.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ uint32_t u4_get(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// QSGD level for |v| with bucket scale `scale`, s levels, uniform word w
+// (reading R-16): level = min(s, floor(fl(fl(fl(|v|/scale)*s) + u))).
+__device__ __forceinline__ uint32_t qsgd_code(float v, float scale, uint32_t s, int bits, uint32_t w) {
+  uint32_t level = 0;
+  if (scale != 0.0f) {
+    const float u = __fmul_rn(__uint2float_rn(w >> 8), 5.9604644775390625e-8f);  // 2^-24
+    const float r = __fdiv_rn(fabsf(v), scale);
+    const float t = __fmul_rn(r, __uint2float_rn(s));
+    const float f = floorf(__fadd_rn(t, u));
+    level = (uint32_t)f;
+    if (level > s) level = s;
+  }
+  const uint32_t neg = (v < 0.0f && level > 0) ? 1u : 0u;
+  return (neg << (bits - 1)) | level;
+}
+
+__device__ __forceinline__ float qsgd_decode(uint32_t code, float scale, uint32_t s, int bits) {
+  const uint32_t level = code & s;
+  const float mag = __fmul_rn(__fdiv_rn(__uint2float_rn(level), __uint2float_rn(s)), scale);
+  return (code >> (bits - 1)) ? -mag : mag;
+}
+
+// ---------------------------------------------------------------------------
+// warp-cooperative searches (32 probes per step)
+// ---------------------------------------------------------------------------
+// first position p in a[0..n) with a[p] >= key (all lanes return it)
+__device__ __forceinline__ uint64_t warp_lower_bound(const uint32_t* __restrict__ a, uint64_t n,
+                                                     uint64_t key) {
+  const int lane = threadIdx.x & 31;
+  uint64_t lo = 0, hi = n;
+  while (hi - lo > 32) {
+    const uint64_t span = hi - lo;
+    const uint64_t p = lo + (span * (uint64_t)(lane + 1)) / 33;
+    const bool pred = (uint64_t)a[p] < key;
+    const uint32_t b = __ballot_sync(0xffffffffu, pred);
+    const int c = __popc(b);
+    const uint64_t plo = lo + (span * (uint64_t)c) / 33;          // probe c-1 (+1)
+    const uint64_t phi = lo + (span * (uint64_t)(c + 1)) / 33;    // probe c
+    const uint64_t nlo = c > 0 ? plo + 1 : lo;
+    const uint64_t nhi = c < 32 ? phi : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const bool pred = (lo + lane < hi) && ((uint64_t)a[lo + lane] < key);
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+
+// merge-path split of diagonal d for A-first ties: the number of A elements
+// among the first d elements of merge(A, B) where A[i] precedes B[j] iff
+// A[i] <= B[j].
+__device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__ A, uint64_t na,
+                                                    const uint32_t* __restrict__ B, uint64_t nb,
+                                                    uint64_t d) {
+  const int lane = threadIdx.x & 31;
+  uint64_t lo = d > nb ? d - nb : 0;
+  uint64_t hi = d < na ? d : na;
+  while (hi - lo > 32) {
+    const uint64_t span = hi - lo;
+    const uint64_t p = lo + (span * (uint64_t)(lane + 1)) / 33;
+    const bool pred = A[p] <= B[d - 1 - p];
+    const uint32_t b = __ballot_sync(0xffffffffu, pred);
+    const int c = __popc(b);
+    const uint64_t plo = lo + (span * (uint64_t)c) / 33;
+    const uint64_t phi = lo + (span * (uint64_t)(c + 1)) / 33;
+    const uint64_t nlo = c > 0 ? plo + 1 : lo;
+    const uint64_t nhi = c < 32 ? phi : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const uint64_t p = lo + lane;
+  const bool pred = (p < hi) && (A[p] <= B[d - 1 - p]);
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+
+// ---------------------------------------------------------------------------
+// per-rank control block at offset 0 of the symmetric workspace
+// ---------------------------------------------------------------------------
+struct alignas(128) Ctrl {
+  uint32_t flags[kMaxRanks];      // barrier arrivals; slot p written by rank p
+  uint32_t epoch;                 // this rank's barrier epoch
+  uint32_t call_count;            // collectives started (bumped by the first barrier)
+  uint32_t dsar;                  // split-allgather decision of the current call
+  uint32_t status;                // device-detected sparcml_status bits
+  uint32_t pad0[12];
+  // split-allgather
+  uint64_t k_in[kMaxRanks];       // nnz of rank i (written by rank i)
+  uint64_t slice_cnt[kMaxRanks];  // pairs rank i pushed into my receive region i
+  uint64_t slice_out[kMaxRanks];  // pairs I pushed to owner j
+  uint64_t owner_K;               // my partition's reduced pair count
+  uint64_t k_sum;                 // sum of k_i (owner stage)
+  uint64_t node_n[2 * kMaxRanks]; // tree-merge internal node counts
+  // recursive doubling (double-buffered by stage parity)
+  uint64_t rd_n[2];               // pairs (or N) of the stream in my recv[b]
+  uint64_t rd_ksum[2];            // k-sum of the group that stream covers
+  uint32_t rd_dense[2];
+  uint32_t own_dense[2];
+  uint64_t own_n[2];              // my own stream in cur[b]
+  uint64_t own_ksum[2];
+  uint64_t rd_sent[8];            // bytes I pushed before stage t (t = 1..log2 P)
+  uint64_t rd_recv[8];            // bytes I received for stage t
+  ScanCounters scan[4];           // ticket counters of the tile kernels
+};
+
+}  // namespace sparcml

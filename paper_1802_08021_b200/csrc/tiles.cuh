@@ -1,0 +1,377 @@
+// tiles.cuh — the two reduction tiles every collective is built from.
+//
+//  merge tile  : union-merge-with-sum of two sorted sparse streams over one
+//                merge-path tile (§5.1 "Efficient Summation", both sparse,
+//                overlapping indices).
+//  window tile : coordinate window [wlo, whi) of a P-way reduction whose
+//                sources are sparse or dense (§5.1 sparse+dense / dense+dense,
+//                P:528-530; the DSAR owner's sparse->dense switch),
+//                combined in the canonical rank-order tree (R-8),
+//                emitted dense, compacted sparse, or QSGD-encoded (§6).
+#pragma once
+
+#include "common.cuh"
+
+namespace sparcml {
+
+// ---------------------------------------------------------------------------
+// merge tile
+// ---------------------------------------------------------------------------
+struct MergeSmem {
+  uint32_t ak[kMergeTile + 1];   // ak[0] = A[a0-1] (look-behind), ak[1+i] = A[a0+i]
+  float av[kMergeTile + 1];
+  uint32_t bk[kMergeTile + 1];   // bk[i] = B[b0+i], bk[lb] = B[b1] (look-ahead)
+  float bv[kMergeTile + 1];
+  uint64_t split[2];
+  uint32_t scan[kWarps + 1];
+  uint64_t excl;
+  int has_prev_a, has_next_b;
+};
+
+struct MergeOutput {
+  uint32_t* idx;
+  float* val;
+  uint64_t* n;          // receives the output count (written by the last tile)
+  uint32_t* idx2;       // optional mirror (a peer's receive buffer over NVLink)
+  float* val2;
+  uint64_t* n2;
+};
+
+// Merges diagonal range [d0, d0 + kMergeTile) of merge(A, B).  Returns nothing;
+// writes its outputs at the exclusive prefix found by look-back.  Must be
+// called by all kThreads threads.  gtile/gfirst: global tile ids for the
+// look-back chain of this job.
+__device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
+                                           const float* __restrict__ Av, uint64_t na,
+                                           const uint32_t* __restrict__ B,
+                                           const float* __restrict__ Bv, uint64_t nb,
+                                           uint64_t d0, MergeSmem& sm, TileStatus* st,
+                                           uint32_t gtile, uint32_t gfirst, uint32_t gen,
+                                           const MergeOutput& out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t total_in = na + nb;
+  const uint64_t d1 = (d0 + kMergeTile < total_in) ? d0 + kMergeTile : total_in;
+  if (warp == 0) {
+    const uint64_t s = warp_merge_path(A, na, B, nb, d0);
+    if (lane == 0) sm.split[0] = s;
+  } else if (warp == 1) {
+    const uint64_t s = warp_merge_path(A, na, B, nb, d1);
+    if (lane == 0) sm.split[1] = s;
+  }
+  __syncthreads();
+  const uint64_t a0 = sm.split[0], a1 = sm.split[1];
+  const uint64_t b0 = d0 - a0, b1 = d1 - a1;
+  const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
+  for (int i = tid; i < la; i += kThreads) {
+    sm.ak[i + 1] = A[a0 + i];
+    sm.av[i + 1] = Av[a0 + i];
+  }
+  for (int i = tid; i < lb; i += kThreads) {
+    sm.bk[i] = B[b0 + i];
+    sm.bv[i] = Bv[b0 + i];
+  }
+  if (tid == 0) {
+    sm.has_prev_a = a0 > 0;
+    if (a0 > 0) sm.ak[0] = A[a0 - 1];
+    sm.has_next_b = b1 < nb;
+    if (b1 < nb) {
+      sm.bk[lb] = B[b1];
+      sm.bv[lb] = Bv[b1];
+    }
+  }
+  __syncthreads();
+  const int L = la + lb;
+  const int dt = min(tid * kMergeItems, L);
+  int lo = max(0, dt - lb), hi = min(dt, la);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sm.ak[mid + 1] <= sm.bk[dt - 1 - mid]) lo = mid + 1; else hi = mid;
+  }
+  int ia = lo, ib = dt - lo;
+  const bool has_prev_a = sm.has_prev_a, has_next_b = sm.has_next_b;
+  uint32_t ok[kMergeItems];
+  float ov[kMergeItems];
+  uint32_t emit = 0;
+#pragma unroll
+  for (int s = 0; s < kMergeItems; ++s) {
+    ok[s] = 0;
+    ov[s] = 0.0f;
+    if (dt + s < L) {
+      const bool takeA = ib >= lb || (ia < la && sm.ak[ia + 1] <= sm.bk[ib]);
+      if (takeA) {
+        const uint32_t key = sm.ak[ia + 1];
+        float v = sm.av[ia + 1];
+        // the element following A[ia] in merged order is B[ib] (or the look-ahead)
+        if ((ib < lb || has_next_b) && sm.bk[ib] == key) v = __fadd_rn(v, sm.bv[ib]);
+        ok[s] = key;
+        ov[s] = v;
+        emit |= 1u << s;
+        ++ia;
+      } else {
+        const uint32_t key = sm.bk[ib];
+        // a B element equal to the preceding A element was already summed into it
+        const bool dup = (ia > 0 || has_prev_a) && sm.ak[ia] == key;
+        if (!dup) {
+          ok[s] = key;
+          ov[s] = sm.bv[ib];
+          emit |= 1u << s;
+        }
+        ++ib;
+      }
+    }
+  }
+  uint32_t tile_total;
+  const uint32_t my_off = block_exclusive_sum<uint32_t>(__popc(emit), sm.scan, &tile_total);
+  // block_exclusive_sum ended with __syncthreads: ak/av are free for staging
+  if (tid == 0) sm.excl = tile_lookback(st, gtile, gfirst, tile_total, gen);
+#pragma unroll
+  for (int s = 0; s < kMergeItems; ++s) {
+    if (emit & (1u << s)) {
+      const uint32_t pos = my_off + __popc(emit & ((1u << s) - 1u));
+      sm.ak[pos] = ok[s];
+      sm.av[pos] = ov[s];
+    }
+  }
+  __syncthreads();
+  const uint64_t base = sm.excl;
+  for (uint32_t i = tid; i < tile_total; i += kThreads) {
+    out.idx[base + i] = sm.ak[i];
+    out.val[base + i] = sm.av[i];
+    if (out.idx2) {
+      out.idx2[base + i] = sm.ak[i];
+      out.val2[base + i] = sm.av[i];
+    }
+  }
+  if (tid == 0 && d1 == total_in) {
+    if (out.n) *out.n = base + tile_total;
+    if (out.n2) *out.n2 = base + tile_total;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// window tile
+// ---------------------------------------------------------------------------
+struct WinSource {
+  const uint32_t* idx;   // sparse: global indices
+  const float* val;      // sparse values, or dense values indexed by (g - dense_base)
+  uint64_t n;            // sparse count
+  uint64_t dense_base;   // dense: global index of val[0]
+  int dense;
+};
+
+enum WinMode : int { WIN_DENSE = 0, WIN_SPARSE = 1, WIN_QUANT = 2 };
+
+struct WinOutput {
+  int mode;
+  // WIN_DENSE: out[g - dense_base] (and mirror)
+  float* dense;
+  float* dense2;
+  uint64_t dense_base;
+  // WIN_SPARSE: compacted (g, v); count to *n (and mirrors)
+  uint32_t* idx;
+  float* val;
+  uint64_t* n;
+  uint32_t* idx2;
+  float* val2;
+  uint64_t* n2;
+  // WIN_QUANT: QSGD of the window, positions relative to qbase (= partition start)
+  uint8_t* codes;
+  float* scales;
+  uint64_t qbase;
+  int bits;
+  uint32_t bucket;
+  uint32_t seed_lo, seed_hi;
+};
+
+// Dynamic shared memory: pres[kWin] | vals[nsrc][kWin] | misc
+struct WinMisc {
+  uint64_t rng[kMaxRanks][2];
+  uint32_t scan[kWarps + 1];
+  uint64_t excl;
+  uint32_t bmax[kWin / 8];
+};
+
+__host__ __device__ constexpr size_t win_smem_bytes(int nsrc) {
+  return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)nsrc + sizeof(WinMisc);
+}
+
+// Canonical tree schedule (reading R-8): post-order list of (dst, src) slot
+// pairs for tree(lo, hi) with mid = lo + (hi - lo)/2, result in slot lo.
+struct TreeSched {
+  uint8_t dst[kMaxRanks];
+  uint8_t src[kMaxRanks];
+  int n;
+};
+
+// QSGD-encode 4 consecutive values v[0..3] at partition-relative position e
+// (e % 4 == 0), global counter c0 = qbase + e, valid = how many of the 4 exist.
+__device__ __forceinline__ void qsgd_encode4(const float v[4], float scale, uint64_t e, uint64_t c0,
+                                             int valid, int bits, uint32_t k0, uint32_t k1,
+                                             uint8_t* __restrict__ codes) {
+  const uint32_t s = (1u << (bits - 1)) - 1u;
+  uint32_t packed = 0;
+  uint4 blk = philox4x32_10(make_uint4((uint32_t)(c0 >> 2), (uint32_t)(c0 >> 34), 0u, 0u), k0, k1);
+  uint4 blk2 = blk;
+  if ((c0 & 3) != 0) {
+    const uint64_t nb = (c0 >> 2) + 1;
+    blk2 = philox4x32_10(make_uint4((uint32_t)nb, (uint32_t)(nb >> 32), 0u, 0u), k0, k1);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t c = c0 + i;
+    const uint32_t w = ((c >> 2) == (c0 >> 2)) ? u4_get(blk, (int)(c & 3)) : u4_get(blk2, (int)(c & 3));
+    const uint32_t code = i < valid ? qsgd_code(v[i], scale, s, bits, w) : 0u;
+    packed |= code << (i * bits);
+  }
+  if (valid == 4) {
+    if (bits == 2) codes[e / 4] = (uint8_t)packed;
+    else if (bits == 4) *reinterpret_cast<uint16_t*>(codes + e / 2) = (uint16_t)packed;
+    else *reinterpret_cast<uint32_t*>(codes + e) = packed;
+  } else if (valid > 0) {
+    const int nbytes = (valid * bits + 7) / 8;
+    uint8_t* dst = codes + (e * (uint64_t)bits) / 8;
+    for (int b = 0; b < nbytes; ++b) dst[b] = (uint8_t)(packed >> (8 * b));
+  }
+}
+
+// Whole block (kThreads): QSGD-encode one window of kThreads*4 consecutive
+// values, thread t holding positions [e, e+4) (e % 4 == 0, partition-relative)
+// with global Philox counter c0 = ctr_base + e.  Buckets of B positions (a
+// power of two, 8 <= B <= 1024) start at multiples of B: scale = max |v|
+// (P:845-849), one thread per bucket stores it.  bmax: kWin/8 smem words.
+__device__ __forceinline__ void qsgd_block_encode(const float r[4], int valid, uint64_t e, uint64_t c0, int bits,
+                                                  uint32_t B, uint32_t k0, uint32_t k1, uint8_t* __restrict__ codes,
+                                                  float* __restrict__ scales, uint32_t* bmax) {
+  const int tid = threadIdx.x;
+  const uint32_t tpb = B / 4;             // threads per bucket (>= 2)
+  float m = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m = fmaxf(m, i < valid ? fabsf(r[i]) : 0.0f);
+  const uint32_t seg = tpb < 32 ? tpb : 32;
+  for (uint32_t o = 1; o < seg; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int nb_win = (kThreads * 4) / (int)B;
+  for (int b = tid; b < nb_win; b += kThreads) bmax[b] = 0u;
+  __syncthreads();
+  if ((tid % seg) == 0) atomicMax(&bmax[tid / tpb], __float_as_uint(m));
+  __syncthreads();
+  const float scale = __uint_as_float(bmax[tid / tpb]);
+  if (valid > 0) {
+    qsgd_encode4(r, scale, e, c0, valid, bits, k0, k1, codes);
+    if ((e % B) == 0) scales[e / B] = scale;
+  }
+}
+
+// Processes window w of [lo, hi): positions [lo + w*kWin, min(lo+(w+1)*kWin, hi)).
+// ticket order == window order (required for WIN_SPARSE's look-back).
+__device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, const TreeSched& ts,
+                                            uint64_t lo, uint64_t hi, uint32_t w,
+                                            unsigned char* smem, TileStatus* st, uint32_t gen,
+                                            uint32_t nwin, const WinOutput& out) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
+  float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
+  WinMisc& mc = *reinterpret_cast<WinMisc*>(smem + sizeof(uint32_t) * kWin + sizeof(float) * kWin * nsrc);
+  const uint64_t wlo = lo + (uint64_t)w * kWin;
+  const uint64_t whi = (wlo + kWin < hi) ? wlo + kWin : hi;
+  const int wn = (int)(whi - wlo);
+
+  for (int s = warp; s < nsrc; s += kWarps) {
+    if (!src[s].dense) {
+      const uint64_t p0 = warp_lower_bound(src[s].idx, src[s].n, wlo);
+      const uint64_t p1 = p0 + warp_lower_bound(src[s].idx + p0, src[s].n - p0, whi);
+      if ((tid & 31) == 0) {
+        mc.rng[s][0] = p0;
+        mc.rng[s][1] = p1;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kWinPerThread; ++i) pres[tid + i * kThreads] = 0u;
+  __syncthreads();
+  for (int s = 0; s < nsrc; ++s) {
+    if (src[s].dense) {
+      const float* dv = src[s].val + (wlo - src[s].dense_base);
+      for (int p = tid; p < wn; p += kThreads) vals[s * kWin + p] = dv[p];
+      for (int p = tid; p < wn; p += kThreads) atomicOr(&pres[p], 1u << s);
+    } else {
+      const uint64_t p0 = mc.rng[s][0], p1 = mc.rng[s][1];
+      for (uint64_t e = p0 + tid; e < p1; e += kThreads) {
+        const uint32_t pos = src[s].idx[e] - (uint32_t)wlo;
+        vals[s * kWin + pos] = src[s].val[e];
+        atomicOr(&pres[pos], 1u << s);
+      }
+    }
+  }
+  __syncthreads();
+
+  // each thread: 4 consecutive positions
+  const int p0 = tid * kWinPerThread;
+  float r[kWinPerThread];
+  uint32_t present = 0;
+#pragma unroll
+  for (int i = 0; i < kWinPerThread; ++i) {
+    const int p = p0 + i;
+    uint32_t m = (p < wn) ? pres[p] : 0u;
+    for (int q = 0; q < ts.n; ++q) {
+      const int d = ts.dst[q], s = ts.src[q];
+      if (m & (1u << s)) {
+        if (m & (1u << d)) {
+          vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[s * kWin + p]);
+        } else {
+          vals[d * kWin + p] = vals[s * kWin + p];
+          m |= 1u << d;
+        }
+      }
+    }
+    r[i] = (m & 1u) ? vals[p] : 0.0f;
+    if (m & 1u) present |= 1u << i;
+  }
+
+  if (out.mode == WIN_DENSE) {
+    const uint64_t g0 = wlo + p0;
+    if (p0 < wn) {
+      float* d = out.dense + (g0 - out.dense_base);
+      if (p0 + 4 <= wn && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
+        *reinterpret_cast<float4*>(d) = make_float4(r[0], r[1], r[2], r[3]);
+        if (out.dense2) *reinterpret_cast<float4*>(out.dense2 + (g0 - out.dense_base)) = make_float4(r[0], r[1], r[2], r[3]);
+      } else {
+        for (int i = 0; i < kWinPerThread && p0 + i < wn; ++i) {
+          d[i] = r[i];
+          if (out.dense2) out.dense2[g0 - out.dense_base + i] = r[i];
+        }
+      }
+    }
+  } else if (out.mode == WIN_SPARSE) {
+    uint32_t total;
+    const uint32_t off = block_exclusive_sum<uint32_t>(__popc(present), mc.scan, &total);
+    if (tid == 0) mc.excl = tile_lookback(st, w, 0, total, gen);
+    __syncthreads();
+    const uint64_t base = mc.excl + off;
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < kWinPerThread; ++i) {
+      if (present & (1u << i)) {
+        out.idx[base + c] = (uint32_t)(wlo + p0 + i);
+        out.val[base + c] = r[i];
+        if (out.idx2) {
+          out.idx2[base + c] = (uint32_t)(wlo + p0 + i);
+          out.val2[base + c] = r[i];
+        }
+        ++c;
+      }
+    }
+    if (tid == 0 && w == nwin - 1) {
+      if (out.n) *out.n = mc.excl + total;
+      if (out.n2) *out.n2 = mc.excl + total;
+    }
+  } else {
+    const uint64_t e = (wlo - out.qbase) + p0;   // partition-relative position
+    const int valid = max(0, min(kWinPerThread, wn - p0));
+    qsgd_block_encode(r, valid, e, wlo + p0, out.bits, out.bucket, out.seed_lo, out.seed_hi, out.codes,
+                      out.scales, mc.bmax);
+  }
+  __syncthreads();
+}
+
+}  // namespace sparcml

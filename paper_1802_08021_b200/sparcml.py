@@ -1,0 +1,370 @@
+"""Thin ctypes binding of libsparcml.so (include/sparcml.h).
+
+Argument marshalling only: every step of the method runs in the library's
+CUDA kernels.  torch supplies device memory, the current stream and (for
+multi-process worlds) the process group used to exchange CUDA-IPC handles.
+There is no CPU fallback: if the library is missing, importing this module
+raises.
+
+Index tensors are torch.int32 reinterpreted as uint32; values are
+torch.float32.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparcml.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(nvcc, sm_100a). There is no CPU fallback.")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- constants --
+OK, ERR_INVALID_ARG, ERR_UNSORTED, ERR_NONFINITE, ERR_MISMATCH, ERR_CUDA, ERR_OOM, ERR_STATE = 0, 1, 2, 3, 4, 5, 7, 8
+ALGO_AUTO, SSAR_RECURSIVE_DOUBLE, SSAR_SPLIT_ALLGATHER, DSAR_SPLIT_ALLGATHER = 0, 1, 2, 3
+REPR_SPARSE, REPR_DENSE = 0, 1
+HEADER_BYTES = 64
+IPC_HANDLE_BYTES = 64
+MAX_RANKS = 16
+HEADER_MAGIC = 0x4D435053
+
+EXPORTED = [
+    "sparcml_version", "sparcml_status_string", "sparcml_opts_default", "sparcml_switch_threshold",
+    "sparcml_expected_nnz", "sparcml_result_bytes", "sparcml_result_val_offset", "sparcml_comm_create",
+    "sparcml_comm_export_handle", "sparcml_comm_connect", "sparcml_comm_create_local", "sparcml_comm_destroy",
+    "sparcml_comm_nranks", "sparcml_comm_rank", "sparcml_last_error", "sparcml_sparse_allreduce",
+    "sparcml_sparse_allreduce_local", "sparcml_read_header", "sparcml_ops_workspace_bytes",
+    "sparcml_ops_workspace_init", "sparcml_merge_sum", "sparcml_topk_workspace_bytes", "sparcml_topk_sparsify",
+    "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
+    "sparcml_kernel_launches",
+]
+
+
+class Opts(C.Structure):
+    _fields_ = [("algo", C.c_int), ("switch_scale", C.c_float), ("index_bytes", C.c_int),
+                ("quant_bits", C.c_int), ("quant_bucket", C.c_uint32), ("seed", C.c_uint64),
+                ("k_sum_hint", C.c_uint64), ("validate", C.c_int)]
+
+
+class Header(C.Structure):
+    _fields_ = [("magic", C.c_uint32), ("repr", C.c_uint32), ("nnz", C.c_uint64), ("N", C.c_uint64),
+                ("k_sum", C.c_uint64), ("bytes_sent", C.c_uint64), ("bytes_recv", C.c_uint64),
+                ("algo_used", C.c_uint32), ("status", C.c_uint32), ("val_offset", C.c_uint64)]
+
+
+assert C.sizeof(Header) == HEADER_BYTES
+
+_p, _u64, _i32, _f32, _sz = C.c_void_p, C.c_uint64, C.c_int, C.c_float, C.c_size_t
+_sig = {
+    "sparcml_version": (C.c_char_p, []),
+    "sparcml_status_string": (C.c_char_p, [_i32]),
+    "sparcml_opts_default": (None, [C.POINTER(Opts)]),
+    "sparcml_switch_threshold": (_u64, [_u64, _i32, _i32, _f32]),
+    "sparcml_expected_nnz": (C.c_double, [_u64, _u64, _i32]),
+    "sparcml_result_bytes": (_sz, [_u64]),
+    "sparcml_result_val_offset": (_sz, [_u64]),
+    "sparcml_comm_create": (_i32, [C.POINTER(_p), _i32, _i32, _i32, _u64, _u64]),
+    "sparcml_comm_export_handle": (_i32, [_p, _p]),
+    "sparcml_comm_connect": (_i32, [_p, _p]),
+    "sparcml_comm_create_local": (_i32, [C.POINTER(_p), _i32, _i32, _u64, _u64]),
+    "sparcml_comm_destroy": (_i32, [_p]),
+    "sparcml_comm_nranks": (_i32, [_p]),
+    "sparcml_comm_rank": (_i32, [_p]),
+    "sparcml_last_error": (C.c_char_p, [_p]),
+    "sparcml_sparse_allreduce": (_i32, [_p, _p, _p, _u64, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_sparse_allreduce_local": (_i32, [_p, _p, _p, _p, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_read_header": (_i32, [_p, C.POINTER(Header), _p]),
+    "sparcml_ops_workspace_bytes": (_sz, [_u64]),
+    "sparcml_ops_workspace_init": (_i32, [_p, _sz, _p]),
+    "sparcml_merge_sum": (_i32, [_p, _p, _u64, _p, _p, _u64, _p, _p, _p, _p, _sz, _p]),
+    "sparcml_topk_workspace_bytes": (_sz, [_u64, _u64]),
+    "sparcml_topk_sparsify": (_i32, [_p, _u64, _u64, _u64, _p, _p, _p, _p, _sz, _p]),
+    "sparcml_ef_topk": (_i32, [_p, _p, _f32, _u64, _u64, _u64, _p, _p, _p, _sz, _p]),
+    "sparcml_topk_status": (_i32, [_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), _p]),
+    "sparcml_quantized_size": (_i32, [_u64, _i32, C.c_uint32, C.POINTER(_sz), C.POINTER(_sz)]),
+    "sparcml_quantize": (_i32, [_p, _u64, _i32, C.c_uint32, _u64, _u64, _p, _p, _p]),
+    "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
+    "sparcml_kernel_launches": (_u64, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+class SparcmlError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"sparcml status {status} ({status_string(status)}): {msg}")
+        self.status = status
+
+
+def status_string(s: int) -> str:
+    return _lib.sparcml_status_string(s).decode()
+
+
+def _check(rc: int, comm=None):
+    if rc != OK:
+        raise SparcmlError(rc, _lib.sparcml_last_error(comm).decode())
+
+
+def version() -> str:
+    return _lib.sparcml_version().decode()
+
+
+def kernel_launches() -> int:
+    return int(_lib.sparcml_kernel_launches())
+
+
+def switch_threshold(N: int, isize: int = 4, c: int = 4, scale: float = 1.0) -> int:
+    return int(_lib.sparcml_switch_threshold(N, isize, c, scale))
+
+
+def expected_nnz(k: int, N: int, P: int) -> float:
+    return float(_lib.sparcml_expected_nnz(k, N, P))
+
+
+def result_bytes(N: int) -> int:
+    return int(_lib.sparcml_result_bytes(N))
+
+
+def result_val_offset(N: int) -> int:
+    return int(_lib.sparcml_result_val_offset(N))
+
+
+def make_opts(algo: int = ALGO_AUTO, switch_scale: float = 1.0, quant_bits: int = 0, quant_bucket: int = 1024,
+              seed: int = 0, k_sum_hint: int = 0, validate: bool = False) -> Opts:
+    o = Opts()
+    _lib.sparcml_opts_default(C.byref(o))
+    o.algo, o.switch_scale, o.quant_bits, o.quant_bucket = algo, switch_scale, quant_bits, quant_bucket
+    o.seed, o.k_sum_hint, o.validate = seed, k_sum_hint, int(validate)
+    return o
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype, name):
+    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous CUDA {dtype} tensor")
+
+
+# ------------------------------------------------------------------ results --
+@dataclass
+class Result:
+    """Decoded allreduce output (views into the `out` buffer)."""
+    header: Header
+    dense: bool
+    idx: Optional[torch.Tensor]   # int32 [nnz] (sparse) or None
+    val: torch.Tensor             # float32 [nnz] or [N]
+
+
+def new_out(N: int, device=None) -> torch.Tensor:
+    return torch.empty(result_bytes(N), dtype=torch.uint8, device=device or "cuda")
+
+
+def read_result(out: torch.Tensor, stream=None) -> Result:
+    """Synchronises `stream`, reads the header and returns views of the payload."""
+    h = Header()
+    _check(_lib.sparcml_read_header(out.data_ptr(), C.byref(h), _stream(stream)))
+    if h.magic != HEADER_MAGIC:
+        raise SparcmlError(ERR_STATE, "output header not written")
+    N = int(h.N)
+    if h.repr == REPR_DENSE:
+        val = out[HEADER_BYTES:HEADER_BYTES + 4 * N].view(torch.float32)
+        return Result(h, True, None, val)
+    n = int(h.nnz)
+    idx = out[HEADER_BYTES:HEADER_BYTES + 4 * n].view(torch.int32)
+    val = out[h.val_offset:h.val_offset + 4 * n].view(torch.float32)
+    return Result(h, False, idx, val)
+
+
+# -------------------------------------------------------------- communicators --
+class LocalWorld:
+    """All P ranks in this process on one GPU (loopback exchanges)."""
+
+    def __init__(self, P: int, max_N: int, max_nnz: int, device: Optional[int] = None):
+        dev = torch.cuda.current_device() if device is None else device
+        h = C.c_void_p()
+        _check(_lib.sparcml_comm_create_local(C.byref(h), P, dev, max_N, max_nnz))
+        self._h, self.P, self.max_N, self.max_nnz, self.device = h, P, max_N, max_nnz, dev
+
+    def allreduce(self, streams: Sequence, N: int, outs: Optional[Sequence[torch.Tensor]] = None,
+                  opts: Optional[Opts] = None, stream=None):
+        """streams: P pairs (idx int32 cuda, val float32 cuda).  Returns the P out buffers."""
+        P = self.P
+        assert len(streams) == P
+        for i, v in streams:
+            _need(i, torch.int32, "idx")
+            _need(v, torch.float32, "val")
+        if outs is None:
+            outs = [new_out(N, i.device) for i, _ in streams]
+        ia = (C.c_void_p * P)(*[_ptr(i) for i, _ in streams])
+        va = (C.c_void_p * P)(*[_ptr(v) for _, v in streams])
+        na = (C.c_uint64 * P)(*[int(i.numel()) for i, _ in streams])
+        oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
+        o = opts if opts is not None else make_opts()
+        _check(_lib.sparcml_sparse_allreduce_local(self._h, ia, va, na, N, 0, C.byref(o), oa,
+                                                   int(outs[0].numel()), _stream(stream)), self._h)
+        return list(outs)
+
+    def close(self):
+        if self._h:
+            _lib.sparcml_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Comm:
+    """One rank per process; peers' workspaces mapped over NVLink (CUDA IPC).
+    Handles are exchanged with torch.distributed (any backend)."""
+
+    def __init__(self, max_N: int, max_nnz: int, group=None, device: Optional[int] = None):
+        import torch.distributed as dist
+        rank = dist.get_rank(group)
+        P = dist.get_world_size(group)
+        dev = torch.cuda.current_device() if device is None else device
+        h = C.c_void_p()
+        _check(_lib.sparcml_comm_create(C.byref(h), P, rank, dev, max_N, max_nnz))
+        self._h, self.P, self.rank, self.device = h, P, rank, dev
+        if P > 1:
+            buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
+            _check(_lib.sparcml_comm_export_handle(h, buf), h)
+            mine = bytes(buf)
+            allh = [None] * P
+            dist.all_gather_object(allh, mine, group=group)
+            blob = b"".join(allh)
+            arr = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+            _check(_lib.sparcml_comm_connect(h, arr), h)
+
+    def allreduce(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,
+                  opts: Optional[Opts] = None, stream=None) -> torch.Tensor:
+        _need(idx, torch.int32, "idx")
+        _need(val, torch.float32, "val")
+        if out is None:
+            out = new_out(N, idx.device)
+        o = opts if opts is not None else make_opts()
+        _check(_lib.sparcml_sparse_allreduce(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, 0, C.byref(o),
+                                             out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
+        return out
+
+    def allreduce_host(self, idx_host, val_host, N: int, out_host=None, opts: Optional[Opts] = None, stream=None):
+        """End-to-end path through the C ABI with HOST buffers: H2D of the input,
+        the collective, D2H of the result payload.  Returns (header, out_host)."""
+        dev_idx = idx_host.to(f"cuda:{self.device}", non_blocking=True)
+        dev_val = val_host.to(f"cuda:{self.device}", non_blocking=True)
+        out = self.allreduce(dev_idx, dev_val, N, opts=opts, stream=stream)
+        if out_host is None:
+            out_host = torch.empty(out.numel(), dtype=torch.uint8, pin_memory=True)
+        out_host.copy_(out, non_blocking=True)
+        return out_host
+
+    def close(self):
+        if self._h:
+            _lib.sparcml_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------ stream ops ----
+def merge_sum(ia: torch.Tensor, va: torch.Tensor, ib: torch.Tensor, vb: torch.Tensor, stream=None):
+    """Union-merge-with-sum of two sorted sparse streams.  Syncs to read the count."""
+    n = ia.numel() + ib.numel()
+    dev = ia.device
+    io = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    vo = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    wsb = int(_lib.sparcml_ops_workspace_bytes(n))
+    ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)
+    _check(_lib.sparcml_merge_sum(_ptr(ia), _ptr(va), ia.numel(), _ptr(ib), _ptr(vb), ib.numel(), _ptr(io),
+                                  _ptr(vo), cnt.data_ptr(), ws.data_ptr(), wsb, _stream(stream)))
+    m = int(cnt.item())
+    return io[:m], vo[:m]
+
+
+class TopkWorkspace:
+    def __init__(self, N: int, k: int, device=None):
+        self.bytes = int(_lib.sparcml_topk_workspace_bytes(N, k))
+        self.buf = torch.zeros(self.bytes, dtype=torch.uint8, device=device or "cuda")
+        self.N, self.k = N, k
+
+    def status(self, stream=None):
+        st, ps = C.c_uint32(), C.c_uint32()
+        _check(_lib.sparcml_topk_status(self.buf.data_ptr(), C.byref(st), C.byref(ps), _stream(stream)))
+        return int(st.value), int(ps.value)
+
+
+def topk_sparsify(x: torch.Tensor, k: int, residual: Optional[torch.Tensor] = None, ws: Optional[TopkWorkspace] = None,
+                  idx_out=None, val_out=None, stream=None):
+    """Top-k by magnitude, ties to the lower index; returns (idx int32, val float32) sorted by index."""
+    _need(x, torch.float32, "x")
+    N = x.numel()
+    m = min(k, N)
+    ws = ws or TopkWorkspace(N, k, x.device)
+    io = idx_out if idx_out is not None else torch.empty(m, dtype=torch.int32, device=x.device)
+    vo = val_out if val_out is not None else torch.empty(m, dtype=torch.float32, device=x.device)
+    _check(_lib.sparcml_topk_sparsify(x.data_ptr(), N, k, 0, io.data_ptr(), vo.data_ptr(), _ptr(residual),
+                                      ws.buf.data_ptr(), ws.bytes, _stream(stream)))
+    return io, vo
+
+
+def ef_topk(eps: torch.Tensor, grad: torch.Tensor, alpha: float, k: int, ws: Optional[TopkWorkspace] = None,
+            idx_out=None, val_out=None, stream=None):
+    """Algorithm 1: acc = eps + alpha*grad (one fma), select TopK(acc), eps <- acc - TopK(acc)."""
+    _need(eps, torch.float32, "eps")
+    _need(grad, torch.float32, "grad")
+    N = eps.numel()
+    m = min(k, N)
+    ws = ws or TopkWorkspace(N, k, eps.device)
+    io = idx_out if idx_out is not None else torch.empty(m, dtype=torch.int32, device=eps.device)
+    vo = val_out if val_out is not None else torch.empty(m, dtype=torch.float32, device=eps.device)
+    _check(_lib.sparcml_ef_topk(eps.data_ptr(), grad.data_ptr(), alpha, N, k, 0, io.data_ptr(), vo.data_ptr(),
+                                ws.buf.data_ptr(), ws.bytes, _stream(stream)))
+    return io, vo
+
+
+def quantized_size(n: int, bits: int, bucket: int = 1024):
+    cb, ns = C.c_size_t(), C.c_size_t()
+    _check(_lib.sparcml_quantized_size(n, bits, bucket, C.byref(cb), C.byref(ns)))
+    return int(cb.value), int(ns.value)
+
+
+def quantize(x: torch.Tensor, bits: int, bucket: int = 1024, seed: int = 0, ctr_base: int = 0, stream=None):
+    _need(x, torch.float32, "x")
+    n = x.numel()
+    cb, ns = quantized_size(n, bits, bucket)
+    codes = torch.empty(max(cb, 8), dtype=torch.uint8, device=x.device)
+    scales = torch.empty(max(ns, 1), dtype=torch.float32, device=x.device)
+    _check(_lib.sparcml_quantize(x.data_ptr(), n, bits, bucket, seed, ctr_base, codes.data_ptr(),
+                                 scales.data_ptr(), _stream(stream)))
+    return codes[:cb], scales[:ns]
+
+
+def dequantize(codes: torch.Tensor, scales: torch.Tensor, n: int, bits: int, bucket: int = 1024, stream=None):
+    out = torch.empty(n, dtype=torch.float32, device=codes.device)
+    _check(_lib.sparcml_dequantize(codes.data_ptr(), scales.data_ptr(), n, bits, bucket, out.data_ptr(),
+                                   _stream(stream)))
+    return out

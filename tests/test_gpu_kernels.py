@@ -1,0 +1,133 @@
+"""GPU parity of the stream kernels against the oracle, element by element,
+through the C ABI: union-merge-with-sum, top-k (+EF) and the QSGD codec.
+Sizes span several tiles plus ragged tails; integer/index outputs must be
+bit-exact, and so must float values here (same operations, same order)."""
+import numpy as np
+import pytest
+
+from paper_1802_08021_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1802_08021_b200 import sparcml as S  # noqa: E402
+
+
+def cu(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dtype=dtype, device="cuda")
+
+
+def cu_idx(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
+
+
+def host_idx(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+MERGE_CASES = [
+    (0, 0, 100), (0, 5, 100), (7, 0, 100), (1, 1, 2), (2047, 1, 5000), (2048, 2048, 10_000),
+    (3000, 5000, 9000), (10_000, 10_000, 10_000), (100_000, 30_000, 1 << 20), (70_001, 70_003, 1 << 18),
+]
+
+
+@pytest.mark.parametrize("na,nb,N", MERGE_CASES)
+def test_merge_sum_parity(orc, na, nb, N):
+    (ia, va), (ib, vb) = synth.uniform_streams(2, N, [na, nb], seed=na + nb, kind="normal")
+    io, vo = S.merge_sum(cu_idx(ia), cu(va, torch.float32), cu_idx(ib), cu(vb, torch.float32))
+    eo, ev = orc.merge_sum(ia, va, ib, vb)
+    np.testing.assert_array_equal(host_idx(io), eo)
+    np.testing.assert_array_equal(vo.cpu().numpy().view(np.uint32), ev.view(np.uint32))
+
+
+def test_merge_identical_and_disjoint(orc):
+    N = 1 << 16
+    for streams in (synth.identical_streams(2, N, 20_000, seed=1), synth.disjoint_streams(2, N, 20_000, seed=1)):
+        (ia, va), (ib, vb) = streams
+        io, vo = S.merge_sum(cu_idx(ia), cu(va, torch.float32), cu_idx(ib), cu(vb, torch.float32))
+        eo, ev = orc.merge_sum(ia, va, ib, vb)
+        np.testing.assert_array_equal(host_idx(io), eo)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+
+
+TOPK_CASES = [
+    (1, 1), (10, 3), (1000, 1), (4095, 17), (4097, 4096), (65_535, 100), (65_536, 655),
+    (1 << 20, 1), (1 << 20, 1048), (1 << 20, 10_485), (3_000_001, 3000), (1 << 22, 41_943),
+]
+
+
+@pytest.mark.parametrize("N,k", TOPK_CASES)
+def test_topk_parity(orc, N, k):
+    x = synth.gaussian_vector(N, seed=N % 97 + k)
+    xt = cu(x, torch.float32)
+    res = torch.empty_like(xt)
+    ws = S.TopkWorkspace(N, k)
+    io, vo = S.topk_sparsify(xt, k, residual=res, ws=ws)
+    ei, ev, er = orc.topk(x, k, residual=True)
+    np.testing.assert_array_equal(host_idx(io), ei)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    np.testing.assert_array_equal(res.cpu().numpy(), er)
+    st, passes = ws.status()
+    assert st == 0 and passes in (1, 2)
+
+
+def test_topk_ties_lower_index_wins(orc):
+    rng = np.random.default_rng(3)
+    for N, k in [(5000, 123), (300_000, 4_000), (1 << 20, 77_777)]:
+        x = (rng.integers(-8, 9, size=N) * 0.5).astype(np.float32)   # massive ties
+        io, vo = S.topk_sparsify(cu(x, torch.float32), k)
+        ei, ev = orc.topk(x, k)
+        np.testing.assert_array_equal(host_idx(io), ei)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+
+
+def test_topk_sparse_input_and_in_place_residual(orc):
+    N, k = 1 << 20, 5000
+    x = np.zeros(N, np.float32)
+    sel = np.random.default_rng(1).choice(N, 3000, replace=False)
+    x[sel] = 1.0 + np.arange(3000, dtype=np.float32)   # fewer non-zeros than k: zeros fill in index order
+    xt = cu(x, torch.float32)
+    io, vo = S.topk_sparsify(xt, k, residual=xt)        # residual aliases x
+    ei, ev, er = orc.topk(x, k, residual=True)
+    np.testing.assert_array_equal(host_idx(io), ei)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    np.testing.assert_array_equal(xt.cpu().numpy(), er)
+
+
+def test_topk_k_ge_n(orc):
+    x = synth.gaussian_vector(1000, seed=2)
+    io, vo = S.topk_sparsify(cu(x, torch.float32), 5000)
+    np.testing.assert_array_equal(host_idx(io), np.arange(1000))
+    np.testing.assert_array_equal(vo.cpu().numpy(), x)
+
+
+@pytest.mark.parametrize("N,k", [(100_000, 100), (1 << 21, 2097), (25_557_032 // 8, 3194)])
+def test_ef_topk_parity(orc, N, k):
+    eps = synth.gaussian_vector(N, seed=5) * np.float32(0.1)
+    g = synth.gaussian_vector(N, seed=6)
+    et = cu(eps, torch.float32)
+    gt = cu(g, torch.float32)
+    ws = S.TopkWorkspace(N, k)
+    for step in range(3):   # error feedback carries over steps
+        io, vo = S.ef_topk(et, gt, 0.05, k, ws=ws)
+        ei, ev, eps = orc.ef_topk(eps, g, 0.05, k)
+        np.testing.assert_array_equal(host_idx(io), ei)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+        np.testing.assert_array_equal(et.cpu().numpy(), eps)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 1000, 1024, 4099, 1 << 20, 1_000_003])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("B", [8, 256, 1024])
+def test_qsgd_parity(orc, n, bits, B):
+    x = synth.gaussian_vector(n, seed=n + bits)
+    seed, base = 1234 + bits, 3 * n + 5
+    c, s = S.quantize(cu(x, torch.float32), bits, bucket=B, seed=seed, ctr_base=base)
+    ec, es = orc.qsgd_quantize(x, bits, bucket=B, seed=seed, ctr_base=base)
+    np.testing.assert_array_equal(c.cpu().numpy(), ec)
+    np.testing.assert_array_equal(s.cpu().numpy(), es)
+    d = S.dequantize(c.clone(), s, n, bits, bucket=B)
+    np.testing.assert_array_equal(d.cpu().numpy(), orc.qsgd_dequantize(ec, es, n, bits, B))
