@@ -109,7 +109,8 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
     off = align_up(off + 8 * cap, 256);
   }
   L.rd_off = off;
-  L.rd_val_off = align_up(4 * half_cap(max_N) + 64, 256);
+  // sparse slots: stage outputs hold <= delta <= N/2 pairs, the stage-1 push a whole input
+  L.rd_val_off = align_up(4 * std::max<uint64_t>(half_cap(max_N), max_nnz) + 64, 256);
   L.rd_bytes = align_up(std::max<size_t>(2 * L.rd_val_off, 4 * max_N) + 256, 256);
   const bool pow2 = (P & (P - 1)) == 0;
   if (pow2 && P > 1) off += 5 * L.rd_bytes;

@@ -272,10 +272,10 @@ struct alignas(128) Ctrl {
   uint64_t owner_K;               // my partition's reduced pair count
   uint64_t k_sum;                 // sum of k_i (owner stage)
   uint64_t node_n[2 * kMaxRanks]; // tree-merge internal node counts
-  // recursive doubling (double-buffered by stage parity)
-  uint64_t rd_n[2];               // pairs (or N) of the stream in my recv[b]
-  uint64_t rd_ksum[2];            // k-sum of the group that stream covers
-  uint32_t rd_dense[2];
+  // recursive doubling: recv[0], recv[1] (stage parity) and recv_init [2]
+  uint64_t rd_n[3];               // pairs (or N) of the stream in my recv buffer
+  uint64_t rd_ksum[3];            // k-sum of the group that stream covers
+  uint32_t rd_dense[3];
   uint32_t own_dense[2];
   uint64_t own_n[2];              // my own stream in cur[b]
   uint64_t own_ksum[2];

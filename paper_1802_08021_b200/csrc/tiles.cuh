@@ -298,8 +298,10 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
       const uint64_t p0 = mc.rng[s][0], p1 = mc.rng[s][1];
       for (uint64_t e = p0 + tid; e < p1; e += kThreads) {
         const uint32_t pos = src[s].idx[e] - (uint32_t)wlo;
-        vals[s * kWin + pos] = src[s].val[e];
-        atomicOr(&pres[pos], 1u << s);
+        if (pos < (uint32_t)wn) {   // guards against unsorted (invalid) input only
+          vals[s * kWin + pos] = src[s].val[e];
+          atomicOr(&pres[pos], 1u << s);
+        }
       }
     }
   }

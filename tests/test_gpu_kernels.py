@@ -71,7 +71,7 @@ def test_topk_parity(orc, N, k):
     np.testing.assert_array_equal(vo.cpu().numpy(), ev)
     np.testing.assert_array_equal(res.cpu().numpy(), er)
     st, passes = ws.status()
-    assert st == 0 and passes in (1, 2)
+    assert st == 0 and passes in ((0, 1, 2) if k >= N else (1, 2))
 
 
 def test_topk_ties_lower_index_wins(orc):
