@@ -243,6 +243,17 @@ sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uin
  * load (the bench's gpu_launches count). */
 uint64_t sparcml_kernel_launches(void);
 
+/* Per-kernel timing for the bench's roofline.  While enabled, every launch of
+ * a kernel class ("topk_filter", "merge", "window", "concat", "split_push",
+ * "barrier", "rd_stage", ...) is bracketed by CUDA events on its stream.
+ * sparcml_profile_read synchronises those events and returns the launch
+ * count and the summed duration in milliseconds. */
+void sparcml_profile_enable(int on);
+void sparcml_profile_only(const char* kernel_name /* NULL: every class */);
+void sparcml_profile_reset(void);
+sparcml_status sparcml_profile_read(const char* kernel_name, uint64_t* launches_host,
+                                    double* total_ms_host);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -181,6 +181,19 @@ struct P1PrepArgs {                 // P == 1: validate and fill the control blo
 // ----------------------------------------------------------- launchers -----
 extern unsigned long long g_launches;   // kernels enqueued by this library
 
+// RAII event bracket around one launch (no-op unless profiling is enabled)
+class ProfScope {
+ public:
+  ProfScope(const char* name, cudaStream_t s);
+  ~ProfScope();
+
+ private:
+  const char* name_;
+  cudaStream_t s_;
+  void* a_;
+};
+#define SPARCML_PROF(name, s) ::sparcml::ProfScope prof_scope_##__LINE__(name, s)
+
 int device_sm_count();
 cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t s);
 cudaError_t launch_window(const WindowArgs& a, cudaStream_t s);

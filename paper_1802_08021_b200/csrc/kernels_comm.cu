@@ -98,6 +98,7 @@ cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t
     attr = true;
   }
   const int grid = std::max(1, std::min(grid_cap, device_sm_count() * 4));
+  SPARCML_PROF("merge", s);
   merge_jobs_kernel<<<grid, kThreads, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -149,6 +150,7 @@ cudaError_t launch_window(const WindowArgs& a, cudaStream_t s) {
   }
   const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)device_sm_count() * 4));
+  SPARCML_PROF("window", s);
   window_kernel<<<grid, kThreads, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
 cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s) {
   const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads,
                                                                     (uint64_t)device_sm_count() * 8));
+  SPARCML_PROF("rd_push", s);
   rd_push_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -313,6 +316,7 @@ cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int grid = device_sm_count() * 4;
+  SPARCML_PROF("rd_stage", s);
   rd_stage_kernel<<<grid, kThreads, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -365,6 +369,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s) {
   const uint64_t per = (uint64_t)kThreads * kPushItems;
   const uint64_t blocks = std::max<uint64_t>(1, (a.n + per - 1) / per);
+  SPARCML_PROF("split_push", s);
   split_push_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -409,6 +414,7 @@ __global__ void barrier_kernel(BarrierArgs a, BarrierDecide dec) {
 
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
   BarrierDecide d = {};
+  SPARCML_PROF("barrier", s);
   barrier_kernel<<<1, 32, 0, s>>>(a, d);
   ++g_launches;
   return cudaGetLastError();
@@ -418,6 +424,7 @@ cudaError_t launch_barrier_decide(const BarrierArgs& a, const DecideArgs& da, cu
   BarrierDecide d;
   d.enabled = 1;
   d.d = da;
+  SPARCML_PROF("barrier", s);
   barrier_kernel<<<1, 32, 0, s>>>(a, d);
   ++g_launches;
   return cudaGetLastError();
@@ -449,6 +456,7 @@ __global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
 
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
   const uint64_t blocks = a.validate ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 1024)) : 1;
+  SPARCML_PROF("p1_prep", s);
   p1_prep_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
@@ -587,6 +595,7 @@ cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int grid = device_sm_count() * 4;
+  SPARCML_PROF("concat", s);
   concat_kernel<<<grid, kThreads, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();

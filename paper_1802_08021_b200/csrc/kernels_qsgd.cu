@@ -64,6 +64,7 @@ cudaError_t launch_quantize(const float* x, uint64_t n, int bits, uint32_t bucke
                             uint8_t* codes, float* scales, cudaStream_t s) {
   const uint64_t nwin = (n + kWin - 1) / kWin;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)device_sm_count() * 8));
+  SPARCML_PROF("quantize", s);
   quantize_kernel<<<grid, kThreads, 0, s>>>(x, n, bits, bucket, (uint32_t)seed, (uint32_t)(seed >> 32), ctr_base,
                                             codes, scales);
   ++g_launches;
@@ -75,6 +76,7 @@ cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, uint64_
   const uint64_t groups = (n + 7) / 8;
   const unsigned grid =
       (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + kThreads - 1) / kThreads, (uint64_t)device_sm_count() * 8));
+  SPARCML_PROF("dequantize", s);
   dequantize_kernel<<<grid, kThreads, 0, s>>>(codes, scales, n, bits, bucket, out);
   ++g_launches;
   return cudaGetLastError();

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kThreads) topk_sample_kernel(const float* __re
                                                                uint64_t N, uint64_t k, TopkLayout L) {
   __shared__ uint32_t sh[kBins];
   TopkCtl* c = L.ctl;
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->status = 0;   // per-call device status
   if (N < kSampleMinN) {
     if (blockIdx.x == 0 && threadIdx.x == 0) c->tau_key = 0;
     return;
@@ -481,6 +482,7 @@ cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, 
   const int sms = device_sm_count();
   if (k >= N) {
     const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((N + 255) / 256, (uint64_t)sms * 8));
+    SPARCML_PROF("topk_all", s);
     if (ef) topk_all_kernel<true><<<blocks, 256, 0, s>>>(x, grad, alpha, x_out, nullptr, N, idx_out, val_out);
     else topk_all_kernel<false><<<blocks, 256, 0, s>>>(x, nullptr, 0.0f, nullptr, residual, N, idx_out, val_out);
     ++g_launches;
@@ -491,21 +493,32 @@ cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, 
   const unsigned fgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(L.ntiles, (uint64_t)sms * 4));
   const unsigned rgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((L.ntiles + kWarps - 1) / kWarps, (uint64_t)sms * 2));
   const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(L.ntiles, (uint64_t)sms * 4));
-  if (ef) {
-    topk_sample_kernel<true><<<sgrid, kThreads, 0, s>>>(x, grad, alpha, N, k, L);
-    topk_filter_kernel<true, false><<<fgrid, kThreads, 0, s>>>(x, grad, alpha, x_out, nullptr, N, k, L);
-  } else if (residual && residual != x) {
-    topk_sample_kernel<false><<<sgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, N, k, L);
-    topk_filter_kernel<false, true><<<fgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, residual, N, k, L);
-  } else {
-    topk_sample_kernel<false><<<sgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, N, k, L);
-    topk_filter_kernel<false, false><<<fgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, nullptr, N, k, L);
+  {
+    SPARCML_PROF("topk_sample", s);
+    if (ef) topk_sample_kernel<true><<<sgrid, kThreads, 0, s>>>(x, grad, alpha, N, k, L);
+    else topk_sample_kernel<false><<<sgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, N, k, L);
   }
-  topk_refine_kernel<2><<<rgrid, kThreads, 0, s>>>(k, L);
-  topk_refine_kernel<3><<<rgrid, kThreads, 0, s>>>(k, L);
+  {
+    SPARCML_PROF("topk_filter", s);
+    if (ef) topk_filter_kernel<true, false><<<fgrid, kThreads, 0, s>>>(x, grad, alpha, x_out, nullptr, N, k, L);
+    else if (residual && residual != x)
+      topk_filter_kernel<false, true><<<fgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, residual, N, k, L);
+    else topk_filter_kernel<false, false><<<fgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, nullptr, N, k, L);
+  }
+  {
+    SPARCML_PROF("topk_refine", s);
+    topk_refine_kernel<2><<<rgrid, kThreads, 0, s>>>(k, L);
+  }
+  {
+    SPARCML_PROF("topk_refine", s);
+    topk_refine_kernel<3><<<rgrid, kThreads, 0, s>>>(k, L);
+  }
   float* zero_at = ef ? x_out : residual;
-  if (zero_at) topk_compact_kernel<true><<<cgrid, kThreads, 0, s>>>(idx_out, val_out, zero_at, L);
-  else topk_compact_kernel<false><<<cgrid, kThreads, 0, s>>>(idx_out, val_out, nullptr, L);
+  {
+    SPARCML_PROF("topk_compact", s);
+    if (zero_at) topk_compact_kernel<true><<<cgrid, kThreads, 0, s>>>(idx_out, val_out, zero_at, L);
+    else topk_compact_kernel<false><<<cgrid, kThreads, 0, s>>>(idx_out, val_out, nullptr, L);
+  }
   g_launches += 5;
   return cudaGetLastError();
 }

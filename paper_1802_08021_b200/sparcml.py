@@ -44,7 +44,8 @@ EXPORTED = [
     "sparcml_sparse_allreduce_local", "sparcml_read_header", "sparcml_ops_workspace_bytes",
     "sparcml_ops_workspace_init", "sparcml_merge_sum", "sparcml_topk_workspace_bytes", "sparcml_topk_sparsify",
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
-    "sparcml_kernel_launches",
+    "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
+    "sparcml_profile_read",
 ]
 
 
@@ -93,6 +94,10 @@ _sig = {
     "sparcml_quantize": (_i32, [_p, _u64, _i32, C.c_uint32, _u64, _u64, _p, _p, _p]),
     "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
     "sparcml_kernel_launches": (_u64, []),
+    "sparcml_profile_enable": (None, [_i32]),
+    "sparcml_profile_reset": (None, []),
+    "sparcml_profile_only": (None, [C.c_char_p]),
+    "sparcml_profile_read": (_i32, [C.c_char_p, C.POINTER(_u64), C.POINTER(C.c_double)]),
 }
 for _name, (_res, _args) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -121,6 +126,30 @@ def version() -> str:
 
 def kernel_launches() -> int:
     return int(_lib.sparcml_kernel_launches())
+
+
+def profile_enable(on: bool = True):
+    _lib.sparcml_profile_enable(int(on))
+
+
+def profile_only(name: Optional[str]):
+    _lib.sparcml_profile_only(None if name is None else name.encode())
+
+
+def profile_reset():
+    _lib.sparcml_profile_reset()
+
+
+def profile_read(name: str):
+    """(launches, total_ms) recorded for kernel class `name` (syncs its events)."""
+    n, ms = C.c_uint64(), C.c_double()
+    _check(_lib.sparcml_profile_read(name.encode(), C.byref(n), C.byref(ms)))
+    return int(n.value), float(ms.value)
+
+
+PROFILED_KERNELS = ["topk_sample", "topk_filter", "topk_refine", "topk_compact", "topk_all", "split_push",
+                    "barrier", "merge", "window", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
+                    "dequantize"]
 
 
 def switch_threshold(N: int, isize: int = 4, c: int = 4, scale: float = 1.0) -> int:
@@ -193,6 +222,20 @@ def read_result(out: torch.Tensor, stream=None) -> Result:
 
 
 # -------------------------------------------------------------- communicators --
+def exchange_handles(mine: bytes, group=None) -> bytes:
+    """All-gather every rank's 64-byte workspace handle over the process group
+    (host-side bootstrap; any backend) and return them concatenated in rank order."""
+    import torch.distributed as dist
+    if len(mine) != IPC_HANDLE_BYTES:
+        raise ValueError("handle must be 64 bytes")
+    P = dist.get_world_size(group)
+    allh = [None] * P
+    dist.all_gather_object(allh, mine, group=group)
+    if any(h is None or len(h) != IPC_HANDLE_BYTES for h in allh):
+        raise SparcmlError(ERR_MISMATCH, "a rank sent a malformed handle")
+    return b"".join(allh)
+
+
 class LocalWorld:
     """All P ranks in this process on one GPU (loopback exchanges)."""
 
@@ -248,10 +291,7 @@ class Comm:
         if P > 1:
             buf = (C.c_uint8 * IPC_HANDLE_BYTES)()
             _check(_lib.sparcml_comm_export_handle(h, buf), h)
-            mine = bytes(buf)
-            allh = [None] * P
-            dist.all_gather_object(allh, mine, group=group)
-            blob = b"".join(allh)
+            blob = exchange_handles(bytes(buf), group)
             arr = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
             _check(_lib.sparcml_comm_connect(h, arr), h)
 

@@ -1,0 +1,75 @@
+"""torchrun worker for tests/test_multigpu.py: one rank per GPU, CUDA-IPC
+world, every algorithm checked against the oracle on every rank."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_1802_08021_b200 import sparcml as S  # noqa: E402
+from paper_1802_08021_b200 import synth  # noqa: E402
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, P = dist.get_rank(), dist.get_world_size()
+    lr = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(lr)
+    cases = [
+        ("rd", 200_003, 3000, S.SSAR_RECURSIVE_DOUBLE, 0),
+        ("rd-dense", 50_000, 20_000, S.SSAR_RECURSIVE_DOUBLE, 0),
+        ("ssar", 1 << 20, 10_000, S.SSAR_SPLIT_ALLGATHER, 0),
+        ("dsar", 1 << 20, 200_000, S.DSAR_SPLIT_ALLGATHER, 0),
+        ("dsar4", 1 << 20, 200_000, S.DSAR_SPLIT_ALLGATHER, 4),
+        ("auto", 1 << 20, 300_000, S.ALGO_AUTO, 2),
+        ("ssar-big", 1 << 24, 167_772, S.SSAR_SPLIT_ALLGATHER, 0),
+    ]
+    max_N = max(c[1] for c in cases)
+    max_k = max(c[2] for c in cases)
+    comm = S.Comm(max_N, max_k)
+    fails = 0
+    for rep in range(2):
+        for name, N, k, algo, bits in cases:
+            if algo == S.SSAR_RECURSIVE_DOUBLE and (P & (P - 1)):
+                continue
+            streams = synth.uniform_streams(P, N, k, seed=rep * 10 + len(name), kind="normal")
+            i, v = streams[rank]
+            it = torch.from_numpy(i.view(np.int32)).cuda()
+            vt = torch.from_numpy(v).cuda()
+            opts = S.make_opts(algo=algo, quant_bits=bits, seed=3)
+            out = comm.allreduce(it, vt, N, opts=opts)
+            res = S.read_result(out)
+            if algo == S.SSAR_RECURSIVE_DOUBLE:
+                ref, st = oracle.ssar_recursive_double(N, streams)
+            else:
+                oa = {S.SSAR_SPLIT_ALLGATHER: oracle.ALGO_SSAR_SPLIT, S.DSAR_SPLIT_ALLGATHER: oracle.ALGO_DSAR_SPLIT,
+                      S.ALGO_AUTO: oracle.ALGO_AUTO}[algo]
+                ref, st, _ = oracle.split_allgather(N, streams, algo=oa, quant_bits=bits, seed=3)
+            d, ei, ev = ref[rank]
+            ok = res.header.status == 0 and res.dense == d and res.header.k_sum == P * k
+            if ok and d:
+                ok = np.array_equal(res.val.cpu().numpy(), ev)
+            elif ok:
+                ok = (np.array_equal(res.idx.cpu().numpy().view(np.uint32), ei)
+                      and np.array_equal(res.val.cpu().numpy(), ev))
+            ok = ok and res.header.bytes_recv == st[rank]["bytes_recv"] and res.header.bytes_sent == st[rank]["bytes_sent"]
+            if not ok:
+                fails += 1
+                print(f"rank {rank}: case {name} rep {rep} MISMATCH (dense {res.dense} vs {d}, "
+                      f"nnz {res.header.nnz}, status {res.header.status})", flush=True)
+    t = torch.tensor([fails])
+    dist.all_reduce(t)
+    comm.close()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"multigpu P={P}: {'OK' if t.item() == 0 else 'FAILED'} ({int(t.item())} mismatches)", flush=True)
+    sys.exit(0 if t.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
