@@ -105,7 +105,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.ok:
@@ -252,7 +252,8 @@ def main():
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
             flush.zero_()
-            torch.cuda.synchronize()
+            barrier()
+            comm.barrier()     # device-side alignment of the ranks before the events
             a = torch.cuda.Event(enable_timing=True)
             mid = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -273,6 +274,9 @@ def main():
     for _ in range(args.steps):
         flush.zero_()
         barrier()
+        S.profile_enable(False)
+        comm.barrier()
+        S.profile_enable(True)
         step()
     barrier()
     S.profile_enable(False)

@@ -172,6 +172,11 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* comm,
                                               const sparcml_opts* opts_host,
                                               void* const* out_host, size_t out_bytes, void* stream);
 
+/* Device-side barrier of all ranks (one warp per rank spinning on flags its
+ * peers store over NVLink).  Stream-ordered, no host synchronisation;
+ * collective like the allreduce.  On a loopback world it only orders. */
+sparcml_status sparcml_barrier(sparcml_comm* comm, void* stream);
+
 /* Synchronous helper: copies the 64-byte header at out[0] to the host
  * (cudaMemcpyAsync on `stream` + stream synchronize). */
 sparcml_status sparcml_read_header(const void* out, sparcml_header* hdr_host, void* stream);

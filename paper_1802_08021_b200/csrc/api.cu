@@ -765,6 +765,19 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* c, const uint32_t* c
   return allreduce_impl(c, idx, val, nnz, N, op, opts, out, out_bytes, stream);
 }
 
+sparcml_status sparcml_barrier(sparcml_comm* c, void* stream) {
+  if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
+  if (!c->connected) return fail(c, SPARCML_ERR_STATE, "communicator not connected");
+  CK(c, cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->local) {
+    for (int r = 0; r < c->P; ++r) CK(c, launch_barrier(barrier_args(c, r, 0), s));
+  } else if (c->P > 1) {
+    CK(c, launch_barrier(barrier_args(c, c->rank, 0), s));
+  }
+  return SPARCML_OK;
+}
+
 sparcml_status sparcml_read_header(const void* out, sparcml_header* h, void* stream) {
   if (!out || !h) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -109,39 +109,62 @@ struct alignas(32) TileStatus {
   uint64_t pad2;
 };
 
-// Called by ONE thread.  Publishes this tile's aggregate, walks back to the
-// nearest inclusive predecessor within [first, tile) and returns the exclusive
-// prefix.  `first` is the job's first global tile (look-back never crosses it).
-__device__ __forceinline__ uint64_t tile_lookback(TileStatus* st, uint32_t tile, uint32_t first,
-                                                  uint64_t agg, uint32_t gen) {
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Called by ONE full warp.  Publishes this tile's aggregate, then looks back
+// 32 predecessors at a time (within [first, tile)) until it meets an
+// inclusive prefix; publishes its own inclusive prefix and returns the
+// exclusive one (to every lane).  `first` is the job's first global tile.
+__device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t tile, uint32_t first,
+                                                       uint64_t agg, uint32_t gen) {
+  const int lane = threadIdx.x & 31;
   const uint32_t tag = gen << 2;
   if (tile == first) {
-    st[tile].incl = agg;
-    __threadfence();
-    st_release_gpu(&st[tile].flag, tag | 2u);
+    if (lane == 0) {
+      st[tile].incl = agg;
+      __threadfence();
+      st_release_gpu(&st[tile].flag, tag | 2u);
+    }
     return 0;
   }
-  st[tile].agg = agg;
-  __threadfence();
-  st_release_gpu(&st[tile].flag, tag | 1u);
+  if (lane == 0) {
+    st[tile].agg = agg;
+    __threadfence();
+    st_release_gpu(&st[tile].flag, tag | 1u);
+  }
   uint64_t excl = 0;
-  uint32_t t = tile - 1;
+  int64_t base = (int64_t)tile - 1;
   while (true) {
-    uint32_t f;
-    do {
-      f = ld_acquire_gpu(&st[t].flag);
-    } while ((f & ~3u) != tag || (f & 3u) == 0);
-    if ((f & 3u) == 2u) {
-      excl += ld_relaxed_gpu(&st[t].incl);
+    const int64_t t = base - lane;
+    uint32_t state = 2;
+    uint64_t v = 0;
+    if (t >= (int64_t)first) {
+      uint32_t f;
+      do {
+        f = ld_acquire_gpu(&st[t].flag);
+      } while ((f & ~3u) != tag || (f & 3u) == 0);
+      state = f & 3u;
+      v = state == 2u ? ld_relaxed_gpu(&st[t].incl) : ld_relaxed_gpu(&st[t].agg);
+    }
+    const uint32_t im = __ballot_sync(0xffffffffu, state == 2u);
+    if (im) {
+      const int j = __ffs(im) - 1;   // nearest predecessor holding an inclusive prefix
+      excl += warp_sum<uint64_t>(lane <= j ? v : 0ull);
       break;
     }
-    excl += ld_relaxed_gpu(&st[t].agg);
-    if (t == first) break;   // cannot happen: the first tile publishes inclusive
-    --t;
+    excl += warp_sum<uint64_t>(v);
+    base -= 32;
   }
-  st[tile].incl = excl + agg;
-  __threadfence();
-  st_release_gpu(&st[tile].flag, tag | 2u);
+  if (lane == 0) {
+    st[tile].incl = excl + agg;
+    __threadfence();
+    st_release_gpu(&st[tile].flag, tag | 2u);
+  }
   return excl;
 }
 

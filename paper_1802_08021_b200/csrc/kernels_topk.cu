@@ -385,66 +385,101 @@ __global__ void __launch_bounds__(kThreads) topk_refine_kernel(uint64_t k, TopkL
 }
 
 // ------------------------------------------------------------- compact -----
+// One ticket = a chunk of kCompactTiles filter tiles, processed warp-per-tile.
+// Selected = |x| > kth, or |x| == kth among the first `need` in index order
+// (ties to the lower index, R-18).  Chunk prefixes (gt count in the low 32
+// bits, eq count in the high 32) come from a warp-parallel decoupled look-back.
+constexpr int kCompactTiles = 16;
+
+__device__ __forceinline__ void count_tile(const float* cv, uint32_t n, uint32_t kth, uint32_t* gt, uint32_t* eq) {
+  const int lane = threadIdx.x & 31;
+  uint32_t g = 0, e = 0;
+  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t key = i < n ? abs_key(cv[i]) : 0u;
+    g += __popc(__ballot_sync(0xffffffffu, i < n && key > kth));
+    e += __popc(__ballot_sync(0xffffffffu, i < n && key == kth));
+  }
+  *gt = g;
+  *eq = e;
+}
+
 template <bool ZERO>
 __global__ void __launch_bounds__(kThreads) topk_compact_kernel(uint32_t* __restrict__ idx_out,
                                                                 float* __restrict__ val_out,
                                                                 float* __restrict__ zero_at, TopkLayout L) {
-  __shared__ uint64_t s_scan[kWarps + 1];
+  __shared__ uint32_t s_gt[kCompactTiles], s_eq[kCompactTiles];
   __shared__ uint32_t s_ticket, s_gen;
   __shared__ uint64_t s_excl;
   TopkCtl* c = L.ctl;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t kth = c->kth;
   const uint64_t need = c->need;
   if (tid == 0) s_gen = c->scan.gen;
   __syncthreads();
   const uint32_t gen = s_gen;
+  const uint32_t nchunks = (uint32_t)((L.ntiles + kCompactTiles - 1) / kCompactTiles);
   while (true) {
     if (tid == 0) s_ticket = atomicAdd(&c->scan.ticket, 1u);
     __syncthreads();
-    const uint32_t t = s_ticket;
-    if (t >= L.ntiles) break;
-    const uint32_t n = L.tile_count[t];
-    const uint32_t* ci = L.cand_idx + (uint64_t)t * kTopkTile;
-    const float* cv = L.cand_val + (uint64_t)t * kTopkTile;
-    // pass 1: tile aggregate (gt in low 32 bits, eq in high 32 bits)
-    uint64_t local = 0;
-    for (uint32_t i = tid; i < n; i += kThreads) {
-      const uint32_t key = abs_key(cv[i]);
-      local += key > kth ? 1ull : (key == kth ? (1ull << 32) : 0ull);
+    const uint32_t ch = s_ticket;
+    if (ch >= nchunks) break;
+    const uint64_t t0 = (uint64_t)ch * kCompactTiles;
+    const int nt = (int)(L.ntiles - t0 < (uint64_t)kCompactTiles ? L.ntiles - t0 : (uint64_t)kCompactTiles);
+    for (int j = warp; j < nt; j += kWarps) {
+      uint32_t g, e;
+      count_tile(L.cand_val + (t0 + j) * kTopkTile, L.tile_count[t0 + j], kth, &g, &e);
+      if (lane == 0) {
+        s_gt[j] = g;
+        s_eq[j] = e;
+      }
     }
-    uint64_t agg;
-    block_exclusive_sum<uint64_t>(local, s_scan, &agg);
-    if (tid == 0) s_excl = tile_lookback(L.status, t, 0, agg, gen);
     __syncthreads();
-    uint64_t run = s_excl;
-    // pass 2: ordered placement
-    for (uint32_t i0 = 0; i0 < n; i0 += kThreads) {
-      const uint32_t i = i0 + tid;
-      uint64_t f = 0;
-      uint32_t key = 0;
-      if (i < n) {
-        key = abs_key(cv[i]);
-        f = key > kth ? 1ull : (key == kth ? (1ull << 32) : 0ull);
+    if (warp == 0) {
+      // exclusive scan over the chunk's tiles (lanes = tiles)
+      const uint32_t g = lane < nt ? s_gt[lane] : 0u, e = lane < nt ? s_eq[lane] : 0u;
+      const uint32_t gi = warp_inclusive_sum<uint32_t>(g), ei = warp_inclusive_sum<uint32_t>(e);
+      const uint32_t gtot = __shfl_sync(0xffffffffu, gi, 31), etot = __shfl_sync(0xffffffffu, ei, 31);
+      const uint64_t agg = (uint64_t)gtot | ((uint64_t)etot << 32);
+      const uint64_t ex = warp_tile_lookback(L.status, ch, 0, agg, gen);
+      __syncwarp();
+      if (lane < nt) {
+        s_gt[lane] = gi - g;
+        s_eq[lane] = ei - e;
       }
-      uint64_t chunk;
-      const uint64_t ex = block_exclusive_sum<uint64_t>(f, s_scan, &chunk) + run;
-      if (f) {
-        const uint64_t gt_before = ex & 0xFFFFFFFFull, eq_before = ex >> 32;
-        const bool sel = (f & 1ull) || eq_before < need;
-        if (sel) {
+      if (lane == 0) s_excl = ex;
+    }
+    __syncthreads();
+    const uint64_t ex = s_excl;
+    for (int j = warp; j < nt; j += kWarps) {
+      const uint64_t t = t0 + j;
+      const uint32_t n = L.tile_count[t];
+      const uint32_t* ci = L.cand_idx + t * kTopkTile;
+      const float* cv = L.cand_val + t * kTopkTile;
+      uint64_t gt_run = (ex & 0xFFFFFFFFull) + s_gt[j];
+      uint64_t eq_run = (ex >> 32) + s_eq[j];
+      for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const float v = i < n ? cv[i] : 0.0f;
+        const uint32_t key = abs_key(v);
+        const bool g = i < n && key > kth, e = i < n && key == kth;
+        const uint32_t gb = __ballot_sync(0xffffffffu, g), eb = __ballot_sync(0xffffffffu, e);
+        const uint32_t lower = (1u << lane) - 1u;
+        const uint64_t gt_before = gt_run + __popc(gb & lower);
+        const uint64_t eq_before = eq_run + __popc(eb & lower);
+        if (g || (e && eq_before < need)) {
           const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
-          const uint32_t j = ci[i];
-          idx_out[pos] = j;
-          val_out[pos] = cv[i];
-          if (ZERO) zero_at[j] = 0.0f;
+          const uint32_t j2 = ci[i];
+          idx_out[pos] = j2;
+          val_out[pos] = v;
+          if (ZERO) zero_at[j2] = 0.0f;
         }
+        gt_run += __popc(gb);
+        eq_run += __popc(eb);
       }
-      run += chunk;
     }
     __syncthreads();
   }
-  // ticket protocol exit (counters in TopkCtl.scan)
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -491,8 +526,9 @@ cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, 
   TopkLayout L = topk_layout(ws, N);
   const unsigned sgrid = N < kSampleMinN ? 1u : 64u;
   const unsigned fgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(L.ntiles, (uint64_t)sms * 4));
-  const unsigned rgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((L.ntiles + kWarps - 1) / kWarps, (uint64_t)sms * 2));
-  const unsigned cgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(L.ntiles, (uint64_t)sms * 4));
+  const unsigned rgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((L.ntiles + kWarps - 1) / kWarps, 64));
+  const unsigned cgrid = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>((L.ntiles + kCompactTiles - 1) / kCompactTiles, (uint64_t)sms * 4));
   {
     SPARCML_PROF("topk_sample", s);
     if (ef) topk_sample_kernel<true><<<sgrid, kThreads, 0, s>>>(x, grad, alpha, N, k, L);

@@ -123,7 +123,10 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
   uint32_t tile_total;
   const uint32_t my_off = block_exclusive_sum<uint32_t>(__popc(emit), sm.scan, &tile_total);
   // block_exclusive_sum ended with __syncthreads: ak/av are free for staging
-  if (tid == 0) sm.excl = tile_lookback(st, gtile, gfirst, tile_total, gen);
+  if (warp == 0) {
+    const uint64_t e = warp_tile_lookback(st, gtile, gfirst, tile_total, gen);
+    if (lane == 0) sm.excl = e;
+  }
 #pragma unroll
   for (int s = 0; s < kMergeItems; ++s) {
     if (emit & (1u << s)) {
@@ -347,7 +350,10 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
   } else if (out.mode == WIN_SPARSE) {
     uint32_t total;
     const uint32_t off = block_exclusive_sum<uint32_t>(__popc(present), mc.scan, &total);
-    if (tid == 0) mc.excl = tile_lookback(st, w, 0, total, gen);
+    if (warp == 0) {
+      const uint64_t e = warp_tile_lookback(st, w, 0, total, gen);
+      if ((tid & 31) == 0) mc.excl = e;
+    }
     __syncthreads();
     const uint64_t base = mc.excl + off;
     int c = 0;

@@ -41,7 +41,7 @@ EXPORTED = [
     "sparcml_expected_nnz", "sparcml_result_bytes", "sparcml_result_val_offset", "sparcml_comm_create",
     "sparcml_comm_export_handle", "sparcml_comm_connect", "sparcml_comm_create_local", "sparcml_comm_destroy",
     "sparcml_comm_nranks", "sparcml_comm_rank", "sparcml_last_error", "sparcml_sparse_allreduce",
-    "sparcml_sparse_allreduce_local", "sparcml_read_header", "sparcml_ops_workspace_bytes",
+    "sparcml_sparse_allreduce_local", "sparcml_barrier", "sparcml_read_header", "sparcml_ops_workspace_bytes",
     "sparcml_ops_workspace_init", "sparcml_merge_sum", "sparcml_topk_workspace_bytes", "sparcml_topk_sparsify",
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
     "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
@@ -83,6 +83,7 @@ _sig = {
     "sparcml_sparse_allreduce": (_i32, [_p, _p, _p, _u64, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_sparse_allreduce_local": (_i32, [_p, _p, _p, _p, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_read_header": (_i32, [_p, C.POINTER(Header), _p]),
+    "sparcml_barrier": (_i32, [_p, _p]),
     "sparcml_ops_workspace_bytes": (_sz, [_u64]),
     "sparcml_ops_workspace_init": (_i32, [_p, _sz, _p]),
     "sparcml_merge_sum": (_i32, [_p, _p, _u64, _p, _p, _u64, _p, _p, _p, _p, _sz, _p]),
@@ -305,6 +306,10 @@ class Comm:
         _check(_lib.sparcml_sparse_allreduce(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, 0, C.byref(o),
                                              out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
         return out
+
+    def barrier(self, stream=None):
+        """Device-side barrier of all ranks (stream-ordered, over NVLink flags)."""
+        _check(_lib.sparcml_barrier(self._h, _stream(stream)), self._h)
 
     def allreduce_host(self, idx_host, val_host, N: int, out_host=None, opts: Optional[Opts] = None, stream=None):
         """End-to-end path through the C ABI with HOST buffers: H2D of the input,
