@@ -244,7 +244,7 @@ def main():
 
     # ---------------- timed region (device events per step, L2 flushed between) ----
     S.profile_reset()
-    S.profile_only("topk_filter")      # the roofline kernel: 2 events per step
+    S.profile_only("topk")             # the roofline kernel: 2 events per step
     S.profile_enable(True)
     launches0 = S.kernel_launches()
     ev = []
@@ -266,7 +266,7 @@ def main():
     S.profile_enable(False)
     t_step = sum(a.elapsed_time(b) for a, _, b in ev) / 1e3 / args.steps
     t_ar = sum(m.elapsed_time(b) for _, m, b in ev) / 1e3 / args.steps
-    nf, ms_f = S.profile_read("topk_filter")
+    nf, ms_f = S.profile_read("topk")
     # per-kernel breakdown: a separate pass with every kernel bracketed by events
     S.profile_reset()
     S.profile_only(None)
@@ -299,17 +299,17 @@ def main():
     t_ar = allmax(t_ar)
     value = P * 4 * N / t_step / 1e9
 
-    # roofline: the top-k filter (the one HBM pass over the gradient), EF-fused
+    # roofline: the fused EF top-k kernel (the one HBM pass over the gradient)
     hbm_peak, peak_src = load_peaks()
     t_filter = ms_f / 1e3 / max(nf, 1)
     alg_bytes = 12 * N + 8 * k          # read eps + grad, write eps (+ k candidates) per launch
     achieved = alg_bytes / t_filter / 1e9 if t_filter > 0 else None
     total_prof_ms = sum(v[1] for v in prof.values())
-    roofline = {"kernel": "topk_filter_kernel<EF> (ef_topk single HBM pass)", "bound": "hbm",
+    roofline = {"kernel": "topk_fused_kernel<EF> (ef_topk: one HBM pass + candidate select)", "bound": "hbm",
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic("topk_filter"),
+                "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic("topk"),
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_us": t_filter * 1e6, "peak_source": peak_src,
-                "share_of_step": (prof.get("topk_filter", (0, 0.0))[1] / total_prof_ms) if total_prof_ms else None}
+                "share_of_step": (prof.get("topk", (0, 0.0))[1] / total_prof_ms) if total_prof_ms else None}
 
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None

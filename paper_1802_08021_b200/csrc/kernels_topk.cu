@@ -1,48 +1,58 @@
 // kernels_topk.cu — top-k sparsification with error feedback (§2.2 P:216-224,
-// Algorithm 1) in one HBM pass over the N-vector.
+// Algorithm 1) in one HBM pass over the N-vector, as ONE persistent
+// cooperative kernel (grid = SMs x resident blocks).  Between phases the grid
+// meets at a barrier whose LAST arriving block computes the next decision
+// (threshold, bin, prefix) and publishes it before releasing the others.
 //
-//   1 sample   : ~N/256 values (every 256th 32-byte sector) -> 12-bit
-//                magnitude histogram -> conservative candidate threshold tau
-//                (expected candidates ~ k + 4 sigma + 16 of the sample)
-//   2 filter   : the single streaming pass: (EF) acc = fmaf(alpha, g, eps),
-//                eps <- acc; candidates |x| >= tau compacted per 4096-tile in
-//                index order; 12-bit histogram of candidate magnitudes
-//   3 hist2/3  : refine the k-th magnitude on the candidates only (12 + 7 bits)
-//   4 compact  : ordered single pass (decoupled look-back) keeping |x| > kth
-//                and the lowest-index ties (reading R-18); zero the residual.
-// If the sample under-estimates (fewer than k candidates) the filter's last
-// block re-filters with tau = 0 (exact; rare slow path, counted in `passes`).
+//   S  sample : 8192 chunks of 8 values (one 32-byte sector every N/8192) ->
+//               magnitude histogram -> conservative candidate threshold tau
+//               (expected candidates ~ k + 4 sigma + 16 of the sample)
+//   F  filter : the streaming pass over the block's contiguous 4096-tiles:
+//               (EF) acc = fmaf(alpha, g, eps), eps <- acc; values with
+//               |x| >= tau compacted per tile in index order; histogram of
+//               candidate magnitudes in 4096 bins of width 2^s above tau
+//   R  refine : histogram the candidates of the crossing bin until the bin is a
+//               single magnitude: the exact k-th magnitude `kth` and how many
+//               of its ties to keep (usually one refine level)
+//   C  place  : per-block (gt, eq) counts -> grid prefix -> ordered placement of
+//               |x| > kth and the first `need` ties (lower index wins, R-18);
+//               the residual at the selected indices is zeroed.
+// If the sample under-estimates (fewer than k candidates) every block
+// re-filters with tau = 0 (exact; rare slow path, counted in `passes`).
 #include <algorithm>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace sparcml {
 
 constexpr int kTopkTile = 4096;           // elements per filter tile (16 per thread)
 constexpr int kBins = 4096;
-constexpr int kBins3 = 128;
 constexpr uint64_t kSampleMinN = 1u << 16;   // below this: tau = 0 (all candidates)
-constexpr uint32_t kSampleChunks = 16384;    // 8-value chunks sampled
+constexpr uint32_t kSampleChunks = 8192;     // 8-value chunks sampled
+constexpr int kMaxGrid = 4096;
+#define kKeyEnd 0x80000000ull  // one past the largest |x| key (NaN included)
+constexpr int kLevels = 4;                   // histogram levels (12 + 12 + 7 key bits worst case)
 
 struct TopkCtl {
-  uint32_t hist_s[kBins];
-  uint32_t hist1[kBins];
-  uint32_t hist2[kBins];
-  uint32_t hist3[kBins3];
-  uint32_t tau_key;
-  uint32_t b1, b2, kth;
-  uint64_t above1, above2, above_k, need;
-  uint32_t done_s, done_f, done_2, done_3;
+  uint64_t t_phase[16];     // %globaltimer at phase ends (block 0), diagnostics only
+  uint32_t hist_s[kBins];   // sample histogram (key >> 19)
+  uint32_t hist[kLevels][kBins];   // candidate histogram per refinement level
+  uint64_t blk[kMaxGrid];   // per-block (gt | eq << 32) selected counts
   uint32_t status, passes;
-  uint32_t pad[2];
-  ScanCounters scan;
+  uint32_t smax;            // largest sampled key
+  uint32_t tile_ticket;     // filter tiles handed out dynamically
+  uint64_t t_blk[kMaxGrid][8];   // %globaltimer per block at phase ends (diagnostics)
 };
 
 struct TopkLayout {
   TopkCtl* ctl;
+  uint64_t* tile_sel;       // per-tile (gt | eq << 32) selected counts
   uint32_t* tile_count;
-  TileStatus* status;
   uint32_t* cand_idx;
   float* cand_val;
   uint64_t ntiles;
@@ -56,10 +66,10 @@ static TopkLayout topk_layout(void* ws, uint64_t N) {
   L.ntiles = (N + kTopkTile - 1) / kTopkTile;
   L.ctl = reinterpret_cast<TopkCtl*>(p);
   p += align256(sizeof(TopkCtl));
+  L.tile_sel = reinterpret_cast<uint64_t*>(p);
+  p += align256(L.ntiles * sizeof(uint64_t));
   L.tile_count = reinterpret_cast<uint32_t*>(p);
   p += align256(L.ntiles * sizeof(uint32_t));
-  L.status = reinterpret_cast<TileStatus*>(p);
-  p += align256(L.ntiles * sizeof(TileStatus));
   L.cand_idx = reinterpret_cast<uint32_t*>(p);
   p += align256(L.ntiles * kTopkTile * sizeof(uint32_t));
   L.cand_val = reinterpret_cast<float*>(p);
@@ -68,140 +78,114 @@ static TopkLayout topk_layout(void* ws, uint64_t N) {
 
 size_t topk_workspace_bytes(uint64_t N, uint64_t /*k*/) {
   const uint64_t nt = (N + kTopkTile - 1) / kTopkTile;
-  return align256(sizeof(TopkCtl)) + align256(nt * sizeof(uint32_t)) + align256(nt * sizeof(TileStatus)) +
+  return align256(sizeof(TopkCtl)) + align256(nt * sizeof(uint64_t)) + align256(nt * sizeof(uint32_t)) +
          2 * align256(nt * kTopkTile * sizeof(uint32_t));
 }
 
 __device__ __forceinline__ uint32_t abs_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
 
-// Whole block: find the highest bin b such that (count in bins > b) < target <=
-// (count in bins >= b).  Returns b and the count strictly above it in *above.
-// If the histogram holds fewer than `target`, returns bin 0 with above =
-// total - h[0].
-__device__ void find_bin_from_top(const uint32_t* h, int nbins, uint64_t target, uint32_t* bin_out,
-                                  uint64_t* above_out) {
+__device__ __forceinline__ void mark(TopkCtl* c, int i) {
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x == 0) c->t_phase[i] = t;
+    c->t_blk[blockIdx.x][i] = t;
+  }
+}
+
+// level binning: bins 0..kBins-2 cover [lo, split) in steps of 2^shift (the
+// shift is chosen so that they do), bin kBins-1 collects every key >= split
+__device__ __forceinline__ uint32_t bin_of(uint32_t key, uint64_t lo, uint64_t split, uint32_t shift) {
+  if ((uint64_t)key >= split) return kBins - 1;
+  const uint64_t b = ((uint64_t)key - lo) >> shift;
+  return b < (uint64_t)(kBins - 1) ? (uint32_t)b : (uint32_t)(kBins - 2);
+}
+
+__host__ __device__ __forceinline__ uint32_t shift_for(uint64_t span, uint64_t nbins) {
+  uint32_t s = 0;
+  while ((nbins << s) < span) ++s;
+  return s;
+}
+
+// Grid-wide barrier of a cooperative launch.  The last block to arrive runs
+// f() (whole block) before releasing the others; f's global writes are
+// visible to every block after the barrier.
+// Whole block: the highest bin b with above0 + (count in bins > b) < target
+// <= above0 + (count in bins >= b).  h is staged through shared memory
+// (coalesced).  Returns b and the count strictly above it (including above0).
+// If the histogram cannot reach the target: b = 0 and *reached = false.
+__device__ void find_bin(const uint32_t* h, uint64_t above0, uint64_t target, uint32_t* sm, uint32_t* bin_out,
+                         uint64_t* above_out, bool* reached, uint32_t nbins = kBins) {
   __shared__ uint64_t scan[kWarps + 1];
   __shared__ uint32_t s_bin;
   __shared__ uint64_t s_above;
+  __shared__ int s_ok;
   const int tid = threadIdx.x;
-  const int per = (nbins + kThreads - 1) / kThreads;
-  // thread t owns bins [top - (t+1)*per, top - t*per) counted from the top
-  const int hiB = nbins - tid * per;
-  const int loB = max(0, hiB - per);
-  uint64_t local = 0;
-  for (int b = loB; b < hiB; ++b) local += h[b];
+  constexpr int per = kBins / kThreads;   // 16
+  // stage: 16 independent coalesced loads in flight per thread; bin j at
+  // sm[j + j/16] so that each thread's 16 consecutive bins are bank-conflict free
+  uint32_t v[per];
+#pragma unroll
+  for (int i = 0; i < per; ++i) v[i] = (uint32_t)(i * kThreads + tid) < nbins ? __ldcg(&h[i * kThreads + tid]) : 0u;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    const int j = i * kThreads + tid;
+    sm[j + (j >> 4)] = v[i];
+  }
   if (tid == 0) {
     s_bin = 0;
-    s_above = 0;
+    s_above = above0;
+    s_ok = 0;
+  }
+  __syncthreads();
+  const int hiB = kBins - tid * per;     // this thread: bins [hiB - per, hiB), scanned downwards
+  uint32_t loc[per];
+  uint64_t local = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) {
+    const int j = hiB - 1 - i;
+    loc[i] = sm[j + (j >> 4)];
+    local += loc[i];
   }
   uint64_t total;
-  const uint64_t before = block_exclusive_sum<uint64_t>(local, scan, &total);
-  if (total < target) {
-    if (tid == 0) {
-      s_bin = 0;
-      s_above = total - h[0];
-    }
-  } else if (before < target && before + local >= target) {
+  const uint64_t before = above0 + block_exclusive_sum<uint64_t>(local, scan, &total);
+  if (before < target && before + local >= target) {
     uint64_t cum = before;
-    for (int b = hiB - 1; b >= loB; --b) {
-      if (cum + h[b] >= target) {
-        s_bin = (uint32_t)b;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < per; ++i) {
+      if (!found && cum + loc[i] >= target) {
+        s_bin = (uint32_t)(hiB - 1 - i);
         s_above = cum;
-        break;
+        s_ok = 1;
+        found = true;
       }
-      cum += h[b];
+      cum += loc[i];
     }
   }
   __syncthreads();
   *bin_out = s_bin;
   *above_out = s_above;
+  *reached = s_ok != 0;
   __syncthreads();
 }
 
-__device__ __forceinline__ bool last_block(uint32_t* done) {
-  __shared__ uint32_t s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t d = atomicAdd(done, 1u);
-    s_last = (d == gridDim.x - 1);
-    if (s_last) *done = 0;
-  }
-  __syncthreads();
-  if (s_last) __threadfence();
-  return s_last != 0;
-}
-
-__device__ __forceinline__ void flush_hist(uint32_t* sh, uint32_t* gh, int nbins) {
-  __syncthreads();
-  for (int b = threadIdx.x; b < nbins; b += kThreads) {
-    const uint32_t c = sh[b];
-    if (c) atomicAdd(&gh[b], c);
-  }
-}
-
-// ---------------------------------------------------------------- sample ---
-template <bool EF>
-__global__ void __launch_bounds__(kThreads) topk_sample_kernel(const float* __restrict__ x,
-                                                               const float* __restrict__ g, float alpha,
-                                                               uint64_t N, uint64_t k, TopkLayout L) {
-  __shared__ uint32_t sh[kBins];
-  TopkCtl* c = L.ctl;
-  if (blockIdx.x == 0 && threadIdx.x == 0) c->status = 0;   // per-call device status
-  if (N < kSampleMinN) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) c->tau_key = 0;
-    return;
-  }
-  for (int b = threadIdx.x; b < kBins; b += kThreads) sh[b] = 0;
-  __syncthreads();
-  const uint64_t nchunk = std::min<uint64_t>(kSampleChunks, N / 8);
-  for (uint64_t ch = (uint64_t)blockIdx.x * kThreads + threadIdx.x; ch < nchunk;
-       ch += (uint64_t)gridDim.x * kThreads) {
-    const uint64_t pos = (ch * (N / 8) / nchunk) * 8;
-    float v[8];
-    const float4 a0 = *reinterpret_cast<const float4*>(x + pos);
-    const float4 a1 = *reinterpret_cast<const float4*>(x + pos + 4);
-    v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
-    v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
-    if (EF) {
-      const float4 g0 = *reinterpret_cast<const float4*>(g + pos);
-      const float4 g1 = *reinterpret_cast<const float4*>(g + pos + 4);
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = __fmaf_rn(alpha, gg[i], v[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) atomicAdd(&sh[abs_key(v[i]) >> 19], 1u);
-  }
-  flush_hist(sh, c->hist_s, kBins);
-  if (last_block(&c->done_s)) {
-    const double S = (double)nchunk * 8.0;
-    const double mean = (double)k * S / (double)N;
-    const uint64_t target = (uint64_t)ceil(mean + 4.0 * sqrt(mean) + 16.0);
-    uint32_t bin;
-    uint64_t above;
-    find_bin_from_top(c->hist_s, kBins, target, &bin, &above);
-    if (threadIdx.x == 0) c->tau_key = bin << 19;
-    for (int b = threadIdx.x; b < kBins; b += kThreads) c->hist_s[b] = 0;
-  }
-}
-
-// ---------------------------------------------------------------- filter ---
 // One tile: 16 values per thread (4 coalesced float4 rows).  Candidates are
-// written in index order to the tile's region; returns nothing.
+// written in index order to the tile's region and binned into `sh`.
 template <bool EF, bool RESID, bool STORE>
-__device__ __forceinline__ void filter_tile(const float* __restrict__ x, const float* __restrict__ g,
-                                            float alpha, float* __restrict__ xout, float* __restrict__ resid,
-                                            uint64_t N, uint64_t t, uint32_t tau, const TopkLayout& L,
+__device__ __forceinline__ void filter_tile(const float* __restrict__ x, const float* __restrict__ g, float alpha,
+                                            float* __restrict__ xout, float* __restrict__ resid, uint64_t N, uint64_t t,
+                                            uint32_t tau, uint64_t split, uint32_t shift, const TopkLayout& L,
                                             uint32_t* sh, uint32_t* s_wt, uint32_t* s_status) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t base = t * kTopkTile;
+  const uint64_t pol = l2_evict_first_policy();
   float v[4][4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
     if (p + 4 <= N) {
-      const float4 a = ld_stream_f4(reinterpret_cast<const float4*>(x + p));
+      const float4 a = ld_stream_f4_ef(reinterpret_cast<const float4*>(x + p), pol);
       v[j][0] = a.x; v[j][1] = a.y; v[j][2] = a.z; v[j][3] = a.w;
     } else {
 #pragma unroll
@@ -213,7 +197,7 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
     for (int j = 0; j < 4; ++j) {
       const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
       if (p + 4 <= N) {
-        const float4 a = ld_stream_f4(reinterpret_cast<const float4*>(g + p));
+        const float4 a = ld_stream_f4_ef(reinterpret_cast<const float4*>(g + p), pol);
         v[j][0] = __fmaf_rn(alpha, a.x, v[j][0]);
         v[j][1] = __fmaf_rn(alpha, a.y, v[j][1]);
         v[j][2] = __fmaf_rn(alpha, a.z, v[j][2]);
@@ -231,7 +215,7 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
     for (int j = 0; j < 4; ++j) {
       const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
       if (p + 4 <= N) {
-        *reinterpret_cast<float4*>(dst + p) = make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
+        st_stream_f4_ef(reinterpret_cast<float4*>(dst + p), make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), pol);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -279,7 +263,7 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
       if (flags[j] & (1u << q)) {
         L.cand_idx[base + pos] = (uint32_t)(p + q);
         L.cand_val[base + pos] = v[j][q];
-        atomicAdd(&sh[abs_key(v[j][q]) >> 19], 1u);
+        atomicAdd(&sh[bin_of(abs_key(v[j][q]), tau, split, shift)], 1u);
         ++pos;
       }
     }
@@ -288,209 +272,329 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
   __syncthreads();
 }
 
-template <bool EF, bool RESID>
-__global__ void __launch_bounds__(kThreads) topk_filter_kernel(const float* __restrict__ x,
-                                                               const float* __restrict__ g, float alpha,
-                                                               float* __restrict__ xout,
-                                                               float* __restrict__ resid, uint64_t N,
-                                                               uint64_t k, TopkLayout L) {
-  __shared__ uint32_t sh[kBins];
-  __shared__ uint32_t s_wt[65];
-  __shared__ uint32_t s_status;
-  TopkCtl* c = L.ctl;
-  for (int b = threadIdx.x; b < kBins; b += kThreads) sh[b] = 0;
-  if (threadIdx.x == 0) s_status = 0;
-  __syncthreads();
-  const uint32_t tau = c->tau_key;
-  for (uint64_t t = blockIdx.x; t < L.ntiles; t += gridDim.x)
-    filter_tile<EF, RESID, EF || RESID>(x, g, alpha, xout, resid, N, t, tau, L, sh, s_wt, &s_status);
-  flush_hist(sh, c->hist1, kBins);
-  if (threadIdx.x == 0 && s_status) atomicOr(&c->status, 1u);
-  if (last_block(&c->done_f)) {
-    __shared__ uint64_t s_scan[kWarps + 1];
-    uint64_t local = 0;
-    for (uint64_t t = threadIdx.x; t < L.ntiles; t += kThreads) local += L.tile_count[t];
-    uint64_t C;
-    block_exclusive_sum<uint64_t>(local, s_scan, &C);
-    uint32_t passes = 1;
-    if (C < k) {
-      // the sample under-estimated: exact re-filter with tau = 0 (every value
-      // is a candidate), reading the stored accumulator in the EF case
-      passes = 2;
-      for (int b = threadIdx.x; b < kBins; b += kThreads) {
-        c->hist1[b] = 0;
-        sh[b] = 0;
-      }
-      __syncthreads();
-      const float* src = EF ? xout : x;
-      for (uint64_t t = 0; t < L.ntiles; ++t)
-        filter_tile<false, false, false>(src, nullptr, 0.0f, nullptr, nullptr, N, t, 0u, L, sh, s_wt, &s_status);
-      __syncthreads();
-      for (int b = threadIdx.x; b < kBins; b += kThreads) c->hist1[b] = sh[b];
-      __syncthreads();
-    }
-    uint32_t b1;
-    uint64_t above1;
-    find_bin_from_top(c->hist1, kBins, k, &b1, &above1);
-    if (threadIdx.x == 0) {
-      c->b1 = b1;
-      c->above1 = above1;
-      c->passes = passes;
-      if (passes == 2) c->tau_key = 0;
-    }
-    for (int b = threadIdx.x; b < kBins; b += kThreads) c->hist1[b] = 0;
+// A refinement level: bins 0..kBins-2 cover [lo, split) in steps of 2^shift,
+// bin kBins-1 is [split, hi); `above` counts candidates with key >= hi.
+struct Level {
+  uint64_t lo, split, hi, above;
+  uint32_t shift;
+  int exact;
+  uint32_t kth;
+  uint64_t need;
+};
+
+// Whole block (every block computes the same result from the same global
+// histogram): locate the crossing bin of `h` and narrow the level.
+__device__ __forceinline__ void narrow(Level& lv, const uint32_t* h, uint64_t k, uint32_t* sm) {
+  uint32_t b;
+  uint64_t above;
+  bool ok;
+  find_bin(h, lv.above, k, sm, &b, &above, &ok);
+  uint64_t nlo, nhi;
+  if (b == kBins - 1) {
+    nlo = lv.split;
+    nhi = lv.hi;
+  } else {
+    nlo = lv.lo + ((uint64_t)b << lv.shift);
+    nhi = min(lv.split, lv.lo + ((uint64_t)(b + 1) << lv.shift));
+  }
+  lv.above = above;
+  lv.lo = nlo;
+  lv.split = nhi;
+  lv.hi = nhi;
+  if (nhi - nlo <= 1) {
+    lv.exact = 1;
+    lv.kth = (uint32_t)nlo;
+    lv.need = k - above;
+  } else {
+    lv.shift = shift_for(nhi - nlo, kBins - 1);
   }
 }
 
-// -------------------------------------------------------------- refine -----
-template <int LEVEL>
-__global__ void __launch_bounds__(kThreads) topk_refine_kernel(uint64_t k, TopkLayout L) {
-  constexpr int NB = LEVEL == 2 ? kBins : kBins3;
-  __shared__ uint32_t sh[NB];
-  TopkCtl* c = L.ctl;
-  for (int b = threadIdx.x; b < NB; b += kThreads) sh[b] = 0;
-  __syncthreads();
-  const uint32_t b1 = c->b1;
-  const uint32_t pre = LEVEL == 2 ? b1 : ((b1 << 12) | c->b2);
-  const int shift = LEVEL == 2 ? 19 : 7;
-  // warp per tile
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint64_t t = (uint64_t)blockIdx.x * kWarps + warp; t < L.ntiles; t += (uint64_t)gridDim.x * kWarps) {
-    const uint32_t n = L.tile_count[t];
-    const float* cv = L.cand_val + t * kTopkTile;
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t key = abs_key(cv[i]);
-      if ((key >> shift) == pre) atomicAdd(&sh[LEVEL == 2 ? ((key >> 7) & 4095u) : (key & 127u)], 1u);
-    }
-  }
-  flush_hist(sh, LEVEL == 2 ? c->hist2 : c->hist3, NB);
-  if (last_block(LEVEL == 2 ? &c->done_2 : &c->done_3)) {
-    uint32_t* gh = LEVEL == 2 ? c->hist2 : c->hist3;
-    const uint64_t above_prev = LEVEL == 2 ? c->above1 : c->above2;
-    uint32_t b;
-    uint64_t above;
-    find_bin_from_top(gh, NB, k - above_prev, &b, &above);
-    if (threadIdx.x == 0) {
-      if (LEVEL == 2) {
-        c->b2 = b;
-        c->above2 = above_prev + above;
-      } else {
-        c->kth = (c->b1 << 19) | (c->b2 << 7) | b;
-        c->above_k = above_prev + above;
-        c->need = k - (above_prev + above);
-      }
-    }
-    for (int i = threadIdx.x; i < NB; i += kThreads) gh[i] = 0;
-  }
-}
-
-// ------------------------------------------------------------- compact -----
-// One ticket = a chunk of kCompactTiles filter tiles, processed warp-per-tile.
-// Selected = |x| > kth, or |x| == kth among the first `need` in index order
-// (ties to the lower index, R-18).  Chunk prefixes (gt count in the low 32
-// bits, eq count in the high 32) come from a warp-parallel decoupled look-back.
-constexpr int kCompactTiles = 16;
-
-__device__ __forceinline__ void count_tile(const float* cv, uint32_t n, uint32_t kth, uint32_t* gt, uint32_t* eq) {
+// Warp: load the (up to 128) candidates [i0, i0+128) of a tile, 4 per lane in flight.
+__device__ __forceinline__ void load4(const float* cv, uint32_t n, uint32_t i0, float v[4]) {
   const int lane = threadIdx.x & 31;
-  uint32_t g = 0, e = 0;
-  for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    const uint32_t key = i < n ? abs_key(cv[i]) : 0u;
-    g += __popc(__ballot_sync(0xffffffffu, i < n && key > kth));
-    e += __popc(__ballot_sync(0xffffffffu, i < n && key == kth));
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t i = i0 + r * 32 + lane;
+    v[r] = i < n ? __ldcg(&cv[i]) : 0.0f;
   }
-  *gt = g;
-  *eq = e;
 }
 
-template <bool ZERO>
-__global__ void __launch_bounds__(kThreads) topk_compact_kernel(uint32_t* __restrict__ idx_out,
-                                                                float* __restrict__ val_out,
-                                                                float* __restrict__ zero_at, TopkLayout L) {
-  __shared__ uint32_t s_gt[kCompactTiles], s_eq[kCompactTiles];
-  __shared__ uint32_t s_ticket, s_gen;
-  __shared__ uint64_t s_excl;
+__device__ __forceinline__ void flush_hist(const uint32_t* sh, uint32_t* gh) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += kThreads) {
+    const uint32_t v = sh[i];
+    if (v) atomicAdd(&gh[i], v);
+  }
+}
+
+constexpr int kGroup = 32;   // tiles per placement group (one warp scans their prefix)
+
+template <bool EF, bool RESID>
+__global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __restrict__ x,
+                                                                 const float* __restrict__ g, float alpha,
+                                                                 float* __restrict__ xout, float* __restrict__ resid,
+                                                                 uint64_t N, uint64_t k, uint32_t* __restrict__ idx_out,
+                                                                 float* __restrict__ val_out, float* zero_at,
+                                                                 TopkLayout L) {
+  __shared__ uint32_t sh[kBins + kBins / 16];   // histogram; find_bin staging (padded)
+  __shared__ uint32_t s_wt[65];
+  __shared__ uint32_t s_status, s_ticket;
+  __shared__ uint64_t s_sum[kWarps + 1];
+  __shared__ uint64_t s_pref[kGroup];
+  __shared__ uint64_t s_base;
+  cg::grid_group grid = cg::this_grid();
   TopkCtl* c = L.ctl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t kth = c->kth;
-  const uint64_t need = c->need;
-  if (tid == 0) s_gen = c->scan.gen;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t gwarp = b * kWarps + warp, nwarps = G * kWarps;
+  const uint64_t t0 = L.ntiles * b / G, t1 = L.ntiles * (b + 1) / G;   // this block's tiles in C
+  for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+  if (tid == 0) s_status = 0;
+  if (b == 0 && tid == 0) {
+    c->tile_ticket = 0;
+    c->status = 0;
+  }
+  mark(c, 0);
+
+  // ---- S: sample ----------------------------------------------------------------
+  const uint64_t nchunk = N >= kSampleMinN ? std::min<uint64_t>(kSampleChunks, N / 8) : 0;
+  const uint32_t sblocks = (uint32_t)std::min<uint64_t>(G, (nchunk + kThreads - 1) / kThreads);
   __syncthreads();
-  const uint32_t gen = s_gen;
-  const uint32_t nchunks = (uint32_t)((L.ntiles + kCompactTiles - 1) / kCompactTiles);
+  if (b < sblocks) {
+    const uint64_t ch = (uint64_t)b * kThreads + tid;
+    uint32_t mx = 0;
+    if (ch < nchunk) {
+      const uint64_t pos = (ch * (N / 8) / nchunk) * 8;
+      float v[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(x + pos);
+      const float4 a1 = *reinterpret_cast<const float4*>(x + pos + 4);
+      v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
+      v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+      if (EF) {
+        const float4 g0 = *reinterpret_cast<const float4*>(g + pos);
+        const float4 g1 = *reinterpret_cast<const float4*>(g + pos + 4);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __fmaf_rn(alpha, gg[i], v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t key = abs_key(v[i]);
+        mx = max(mx, key);
+        atomicAdd(&sh[key >> 19], 1u);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx) atomicMax(&c->smax, mx);
+    flush_hist(sh, c->hist_s);
+    __syncthreads();
+    for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+  }
+  mark(c, 1);
+  grid.sync();
+  // tau: where the sample's count from the top reaches mean + 4 sigma + 16;
+  // split: where it reaches mean - 4 sigma - 16.  The k-th magnitude lies in
+  // [tau, split) with overwhelming probability: level-1 bins cover that range
+  // finely, everything above it is one bin.  (Same result in every block.)
+  Level lv;
+  lv.lo = 0;
+  lv.split = kKeyEnd;
+  lv.hi = kKeyEnd;
+  lv.above = 0;
+  lv.shift = shift_for(kKeyEnd, kBins - 1);
+  lv.exact = 0;
+  lv.kth = 0;
+  lv.need = 0;
+  if (nchunk) {
+    const double S = (double)nchunk * 8.0;
+    const double mean = (double)k * S / (double)N;
+    const uint64_t t_lo = (uint64_t)ceil(mean + 4.0 * sqrt(mean) + 16.0);
+    const double th = mean - 4.0 * sqrt(mean) - 16.0;
+    const uint64_t t_hi = th > 1.0 ? (uint64_t)th : 1;
+    uint32_t bn, bh;
+    uint64_t above;
+    bool ok, okh;
+    find_bin(c->hist_s, 0, t_lo, sh, &bn, &above, &ok);
+    find_bin(c->hist_s, 0, t_hi, sh, &bh, &above, &okh);
+    const uint64_t tau = ok ? ((uint64_t)bn << 19) : 0ull;
+    const uint64_t top = (uint64_t)__ldcg(&c->smax) + (1ull << 23);   // 2 x the largest sample
+    uint64_t split = okh ? min((uint64_t)(bh + 1) << 19, (uint64_t)kKeyEnd) : min(top, (uint64_t)kKeyEnd);
+    if (split <= tau) split = tau + 1;
+    lv.lo = tau;
+    lv.split = split;
+    lv.shift = shift_for(split - tau, kBins - 1);
+  }
+  for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+  __syncthreads();
+  mark(c, 2);
+  const uint32_t tau = (uint32_t)lv.lo;
+
+  // ---- F: the streaming pass (tiles handed out dynamically for balance) ------
   while (true) {
-    if (tid == 0) s_ticket = atomicAdd(&c->scan.ticket, 1u);
+    if (tid == 0) s_ticket = atomicAdd(&c->tile_ticket, 1u);
     __syncthreads();
-    const uint32_t ch = s_ticket;
-    if (ch >= nchunks) break;
-    const uint64_t t0 = (uint64_t)ch * kCompactTiles;
-    const int nt = (int)(L.ntiles - t0 < (uint64_t)kCompactTiles ? L.ntiles - t0 : (uint64_t)kCompactTiles);
-    for (int j = warp; j < nt; j += kWarps) {
-      uint32_t g, e;
-      count_tile(L.cand_val + (t0 + j) * kTopkTile, L.tile_count[t0 + j], kth, &g, &e);
-      if (lane == 0) {
-        s_gt[j] = g;
-        s_eq[j] = e;
+    const uint64_t t = s_ticket;
+    if (t >= L.ntiles) break;
+    filter_tile<EF, RESID, EF || RESID>(x, g, alpha, xout, resid, N, t, tau, lv.split, lv.shift, L, sh, s_wt,
+                                        &s_status);
+  }
+  mark(c, 3);
+  flush_hist(sh, c->hist[0]);
+  if (tid == 0 && s_status) atomicOr(&c->status, 1u);
+  grid.sync();
+  mark(c, 4);
+  {
+    uint64_t loc = 0;
+    for (int i = 0; i < kBins / kThreads; ++i) loc += __ldcg(&c->hist[0][i * kThreads + tid]);
+    uint64_t C;
+    block_exclusive_sum<uint64_t>(loc, s_sum, &C);
+    if (C < k) {   // the sample under-estimated: exact re-filter with tau = 0 (rare)
+      grid.sync();   // every block has read hist[0]
+      if (b == 0) {
+        for (int i = tid; i < kBins; i += kThreads) c->hist[0][i] = 0;
+        if (tid == 0) {
+          c->tile_ticket = 0;
+          c->passes = 2;
+        }
+      }
+      for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+      grid.sync();
+      lv.lo = 0;
+      lv.split = kKeyEnd;
+      lv.shift = shift_for(kKeyEnd, kBins - 1);
+      const float* src = EF ? xout : x;
+      while (true) {
+        if (tid == 0) s_ticket = atomicAdd(&c->tile_ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_ticket;
+        if (t >= L.ntiles) break;
+        filter_tile<false, false, false>(src, nullptr, 0.0f, nullptr, nullptr, N, t, 0u, lv.split, lv.shift, L, sh,
+                                         s_wt, &s_status);
+      }
+      flush_hist(sh, c->hist[0]);
+      grid.sync();
+    } else if (b == 0 && tid == 0) {
+      c->passes = 1;
+    }
+  }
+  narrow(lv, c->hist[0], k, sh);
+  mark(c, 5);
+
+  // ---- R: refine the crossing bin until it is one magnitude ------------------
+  int level = 1;
+  while (!lv.exact) {
+    uint32_t* gh = c->hist[level < kLevels ? level : kLevels - 1];
+    for (uint64_t t = gwarp; t < L.ntiles; t += nwarps) {
+      const uint32_t n = __ldcg(&L.tile_count[t]);
+      const float* cv = L.cand_val + t * kTopkTile;
+      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
+        float v[4];
+        load4(cv, n, i0, v);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t key = abs_key(v[r]);
+          if (i0 + r * 32 + lane < n && key >= lv.lo && key < lv.hi)
+            atomicAdd(&gh[bin_of(key, lv.lo, lv.split, lv.shift)], 1u);
+        }
       }
     }
-    __syncthreads();
+    grid.sync();
+    narrow(lv, gh, k, sh);
+    ++level;
+  }
+  mark(c, 6);
+  const uint32_t kth = lv.kth;
+  const uint64_t need = lv.need;
+
+  // ---- C: ordered placement over block-contiguous tiles ----------------------
+  uint64_t bsum = 0;
+  for (uint64_t t = t0 + warp; t < t1; t += kWarps) {
+    const uint32_t n = __ldcg(&L.tile_count[t]);
+    const float* cv = L.cand_val + t * kTopkTile;
+    uint32_t ng = 0, ne = 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 128) {
+      float v[4];
+      load4(cv, n, i0, v);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const bool in = i0 + r * 32 + lane < n;
+        const uint32_t key = abs_key(v[r]);
+        ng += __popc(__ballot_sync(0xffffffffu, in && key > kth));
+        ne += __popc(__ballot_sync(0xffffffffu, in && key == kth));
+      }
+    }
+    const uint64_t sel = (uint64_t)ng | ((uint64_t)ne << 32);
+    if (lane == 0) {
+      L.tile_sel[t] = sel;
+      bsum += sel;
+    }
+  }
+  {
+    uint64_t tot;
+    block_exclusive_sum<uint64_t>(bsum, s_sum, &tot);
+    if (tid == 0) c->blk[b] = tot;
+  }
+  grid.sync();
+  mark(c, 7);
+  // every histogram has been read by every block: clear them for the next call
+  if (b < (uint32_t)(kLevels + 1)) {
+    uint32_t* h = b == 0 ? c->hist_s : c->hist[b - 1];
+    for (int i = tid; i < kBins; i += kThreads) h[i] = 0;
+    if (b == 0 && tid == 0) c->smax = 0;
+  }
+  {
+    uint64_t v = 0;
+    for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&c->blk[j]));
+    uint64_t tot;
+    block_exclusive_sum<uint64_t>(v, s_sum, &tot);
+    if (tid == 0) s_base = tot;
+  }
+  __syncthreads();
+  for (uint64_t gs = t0; gs < t1; gs += kGroup) {
+    const int nt = (int)std::min<uint64_t>(kGroup, t1 - gs);
     if (warp == 0) {
-      // exclusive scan over the chunk's tiles (lanes = tiles)
-      const uint32_t g = lane < nt ? s_gt[lane] : 0u, e = lane < nt ? s_eq[lane] : 0u;
-      const uint32_t gi = warp_inclusive_sum<uint32_t>(g), ei = warp_inclusive_sum<uint32_t>(e);
-      const uint32_t gtot = __shfl_sync(0xffffffffu, gi, 31), etot = __shfl_sync(0xffffffffu, ei, 31);
-      const uint64_t agg = (uint64_t)gtot | ((uint64_t)etot << 32);
-      const uint64_t ex = warp_tile_lookback(L.status, ch, 0, agg, gen);
+      const uint64_t v = lane < nt ? __ldcg(reinterpret_cast<const unsigned long long*>(&L.tile_sel[gs + lane])) : 0ull;
+      const uint64_t inc = warp_inclusive_sum<uint64_t>(v);
+      s_pref[lane] = s_base + inc - v;
       __syncwarp();
-      if (lane < nt) {
-        s_gt[lane] = gi - g;
-        s_eq[lane] = ei - e;
-      }
-      if (lane == 0) s_excl = ex;
+      if (lane == 31) s_base += inc;
     }
     __syncthreads();
-    const uint64_t ex = s_excl;
     for (int j = warp; j < nt; j += kWarps) {
-      const uint64_t t = t0 + j;
-      const uint32_t n = L.tile_count[t];
+      const uint64_t t = gs + j;
+      const uint32_t n = __ldcg(&L.tile_count[t]);
       const uint32_t* ci = L.cand_idx + t * kTopkTile;
       const float* cv = L.cand_val + t * kTopkTile;
-      uint64_t gt_run = (ex & 0xFFFFFFFFull) + s_gt[j];
-      uint64_t eq_run = (ex >> 32) + s_eq[j];
-      for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const float v = i < n ? cv[i] : 0.0f;
-        const uint32_t key = abs_key(v);
-        const bool g = i < n && key > kth, e = i < n && key == kth;
-        const uint32_t gb = __ballot_sync(0xffffffffu, g), eb = __ballot_sync(0xffffffffu, e);
-        const uint32_t lower = (1u << lane) - 1u;
-        const uint64_t gt_before = gt_run + __popc(gb & lower);
-        const uint64_t eq_before = eq_run + __popc(eb & lower);
-        if (g || (e && eq_before < need)) {
-          const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
-          const uint32_t j2 = ci[i];
-          idx_out[pos] = j2;
-          val_out[pos] = v;
-          if (ZERO) zero_at[j2] = 0.0f;
+      uint64_t gt_run = s_pref[j] & 0xFFFFFFFFull, eq_run = s_pref[j] >> 32;
+      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
+        float v[4];
+        load4(cv, n, i0, v);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t i = i0 + r * 32 + lane;
+          const uint32_t key = abs_key(v[r]);
+          const bool gsel = i < n && key > kth, esel = i < n && key == kth;
+          const uint32_t gbal = __ballot_sync(0xffffffffu, gsel), ebal = __ballot_sync(0xffffffffu, esel);
+          const uint32_t lower = (1u << lane) - 1u;
+          const uint64_t gt_before = gt_run + __popc(gbal & lower);
+          const uint64_t eq_before = eq_run + __popc(ebal & lower);
+          if (gsel || (esel && eq_before < need)) {
+            const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
+            const uint32_t j2 = ci[i];
+            idx_out[pos] = j2;
+            val_out[pos] = v[r];
+            if (zero_at) zero_at[j2] = 0.0f;   // acc - TopK(acc)
+          }
+          gt_run += __popc(gbal);
+          eq_run += __popc(ebal);
         }
-        gt_run += __popc(gb);
-        eq_run += __popc(eb);
       }
     }
     __syncthreads();
   }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const uint32_t d = atomicAdd(&c->scan.done, 1u);
-    if (d == gridDim.x - 1) {
-      c->scan.ticket = 0;
-      c->scan.done = 0;
-      c->scan.gen = c->scan.gen + 1;
-      __threadfence();
-    }
-  }
+  mark(c, 7);
 }
 
 // --------------------------------------------------------- k >= N ---------
@@ -511,6 +615,24 @@ __global__ void topk_all_kernel(const float* __restrict__ x, const float* __rest
 }
 
 // ------------------------------------------------------------ launcher -----
+template <bool EF, bool RESID>
+static cudaError_t launch_fused(const float* x, const float* grad, float alpha, float* x_out, float* residual,
+                                uint64_t N, uint64_t k, uint32_t* idx_out, float* val_out, float* zero_at,
+                                const TopkLayout& L, cudaStream_t s) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_fused_kernel<EF, RESID>, kThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)per_sm * device_sm_count(), L.ntiles,
+                                                                (uint64_t)kMaxGrid}));
+  TopkLayout Lc = L;
+  void* args[] = {(void*)&x,      (void*)&grad,    (void*)&alpha,   (void*)&x_out,   (void*)&residual, (void*)&N,
+                  (void*)&k,      (void*)&idx_out, (void*)&val_out, (void*)&zero_at, (void*)&Lc};
+  return cudaLaunchCooperativeKernel((const void*)topk_fused_kernel<EF, RESID>, dim3((unsigned)G), dim3(kThreads), args,
+                                     0, s);
+}
+
 cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, float* x_out, uint64_t N,
                         uint64_t k, uint32_t* idx_out, float* val_out, float* residual, void* ws,
                         cudaStream_t s) {
@@ -524,38 +646,17 @@ cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, 
     return cudaGetLastError();
   }
   TopkLayout L = topk_layout(ws, N);
-  const unsigned sgrid = N < kSampleMinN ? 1u : 64u;
-  const unsigned fgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(L.ntiles, (uint64_t)sms * 4));
-  const unsigned rgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((L.ntiles + kWarps - 1) / kWarps, 64));
-  const unsigned cgrid = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>((L.ntiles + kCompactTiles - 1) / kCompactTiles, (uint64_t)sms * 4));
+  cudaError_t e;
   {
-    SPARCML_PROF("topk_sample", s);
-    if (ef) topk_sample_kernel<true><<<sgrid, kThreads, 0, s>>>(x, grad, alpha, N, k, L);
-    else topk_sample_kernel<false><<<sgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, N, k, L);
-  }
-  {
-    SPARCML_PROF("topk_filter", s);
-    if (ef) topk_filter_kernel<true, false><<<fgrid, kThreads, 0, s>>>(x, grad, alpha, x_out, nullptr, N, k, L);
+    SPARCML_PROF("topk", s);
+    if (ef) e = launch_fused<true, false>(x, grad, alpha, x_out, nullptr, N, k, idx_out, val_out, x_out, L, s);
     else if (residual && residual != x)
-      topk_filter_kernel<false, true><<<fgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, residual, N, k, L);
-    else topk_filter_kernel<false, false><<<fgrid, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, nullptr, N, k, L);
+      e = launch_fused<false, true>(x, nullptr, 0.0f, nullptr, residual, N, k, idx_out, val_out, residual, L, s);
+    else   // no residual, or residual aliasing x (in place)
+      e = launch_fused<false, false>(x, nullptr, 0.0f, nullptr, nullptr, N, k, idx_out, val_out, residual, L, s);
   }
-  {
-    SPARCML_PROF("topk_refine", s);
-    topk_refine_kernel<2><<<rgrid, kThreads, 0, s>>>(k, L);
-  }
-  {
-    SPARCML_PROF("topk_refine", s);
-    topk_refine_kernel<3><<<rgrid, kThreads, 0, s>>>(k, L);
-  }
-  float* zero_at = ef ? x_out : residual;
-  {
-    SPARCML_PROF("topk_compact", s);
-    if (zero_at) topk_compact_kernel<true><<<cgrid, kThreads, 0, s>>>(idx_out, val_out, zero_at, L);
-    else topk_compact_kernel<false><<<cgrid, kThreads, 0, s>>>(idx_out, val_out, nullptr, L);
-  }
-  g_launches += 5;
+  ++g_launches;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

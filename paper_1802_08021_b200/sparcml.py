@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparcml.so")
+LIB_PATH = os.environ.get("SPARCML_LIB") or os.path.join(_HERE, "libsparcml.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -148,7 +148,7 @@ def profile_read(name: str):
     return int(n.value), float(ms.value)
 
 
-PROFILED_KERNELS = ["topk_sample", "topk_filter", "topk_refine", "topk_compact", "topk_all", "split_push",
+PROFILED_KERNELS = ["topk", "topk_all", "split_push",
                     "barrier", "merge", "window", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
                     "dequantize"]
 

@@ -97,6 +97,36 @@ def test_topk_sparse_input_and_in_place_residual(orc):
     np.testing.assert_array_equal(xt.cpu().numpy(), er)
 
 
+def test_topk_fallback_when_sample_underestimates(orc):
+    """Adversarial input: every sampled chunk (8 values every N/16384) holds a
+    large value, the rest are small, and k exceeds the number of large values.
+    The sampled threshold then admits fewer than k candidates and the kernel
+    must take its exact re-filter path (passes == 2) and still be exact."""
+    N, k = 1 << 20, 1 << 18
+    rng = np.random.default_rng(5)
+    x = rng.random(N, dtype=np.float32)
+    pos = (np.arange(16384, dtype=np.int64) * (N // 8) // 16384) * 8
+    for q in range(8):
+        x[pos + q] = 100.0 + rng.random(16384, dtype=np.float32) * 100.0
+    ws = S.TopkWorkspace(N, k)
+    io, vo = S.topk_sparsify(cu(x, torch.float32), k, ws=ws)
+    ei, ev = orc.topk(x, k)
+    np.testing.assert_array_equal(host_idx(io), ei)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    assert ws.status() == (0, 2)
+
+
+def test_topk_nonfinite_reported():
+    x = synth.gaussian_vector(1 << 17, seed=9)
+    x[777] = np.inf
+    ws = S.TopkWorkspace(len(x), 100)
+    S.topk_sparsify(cu(x, torch.float32), 100, ws=ws)
+    assert ws.status()[0] == S.ERR_NONFINITE
+    x[777] = 1.0
+    S.topk_sparsify(cu(x, torch.float32), 100, ws=ws)
+    assert ws.status()[0] == 0
+
+
 def test_topk_k_ge_n(orc):
     x = synth.gaussian_vector(1000, seed=2)
     io, vo = S.topk_sparsify(cu(x, torch.float32), 5000)
