@@ -224,9 +224,10 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
+    def topk():
         S.ef_topk(eps, grad, alpha, k, ws=ws, idx_out=idx, val_out=val)
-        mid.record(stream)
+
+    def allreduce():
         comm.allreduce(idx, val, N, out=out, opts=opts)
 
     def barrier():
@@ -234,19 +235,36 @@ def main():
         if P > 1:
             dist.barrier()
 
-    mid = torch.cuda.Event(enable_timing=True)
     for _ in range(max(3, args.warmup)):
         flush.zero_()
-        step()
+        topk()
+        allreduce()
+    barrier()
+    res = S.read_result(out)
+    assert res.header.status == 0 and res.header.k_sum == P * k
+
+    # The step runs as two CUDA graphs (launch-bound inner sequence, captured once):
+    # g_topk = the fused EF top-k kernel, g_ar = the whole sparse allreduce.
+    l0 = S.kernel_launches()
+    g_topk, g_ar = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_topk):
+        topk()
+    l1 = S.kernel_launches()
+    with torch.cuda.graph(g_ar):
+        allreduce()
+    launches_per_step = S.kernel_launches() - l0
+    topk_launches = l1 - l0
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        barrier()
+        comm.barrier()
+        g_topk.replay()
+        g_ar.replay()
     barrier()
     res = S.read_result(out)
     assert res.header.status == 0 and res.header.k_sum == P * k
 
     # ---------------- timed region (device events per step, L2 flushed between) ----
-    S.profile_reset()
-    S.profile_only("topk")             # the roofline kernel: 2 events per step
-    S.profile_enable(True)
-    launches0 = S.kernel_launches()
     ev = []
     barrier()
     with ClockSampler(local_rank) as clk:
@@ -255,31 +273,38 @@ def main():
             barrier()
             comm.barrier()     # device-side alignment of the ranks before the events
             a = torch.cuda.Event(enable_timing=True)
-            mid = torch.cuda.Event(enable_timing=True)
+            m = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            step()
+            g_topk.replay()
+            m.record(stream)
+            g_ar.replay()
             b.record(stream)
-            ev.append((a, mid, b))
+            ev.append((a, m, b))
         barrier()
-    launches = S.kernel_launches() - launches0
-    S.profile_enable(False)
+    launches = launches_per_step * args.steps
     t_step = sum(a.elapsed_time(b) for a, _, b in ev) / 1e3 / args.steps
     t_ar = sum(m.elapsed_time(b) for _, m, b in ev) / 1e3 / args.steps
-    nf, ms_f = S.profile_read("topk")
-    # per-kernel breakdown: a separate pass with every kernel bracketed by events
+    t_topk_kernel = sum(a.elapsed_time(m) for a, m, _ in ev) / 1e3 / args.steps   # the fused top-k launch
+    # per-kernel breakdown (eager, every kernel bracketed by library events)
     S.profile_reset()
     S.profile_only(None)
-    S.profile_enable(True)
+    ev2 = []
     for _ in range(args.steps):
         flush.zero_()
         barrier()
-        S.profile_enable(False)
         comm.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
         S.profile_enable(True)
-        step()
+        a.record(stream)
+        topk()
+        allreduce()
+        b.record(stream)
+        S.profile_enable(False)
+        ev2.append((a, b))
     barrier()
-    S.profile_enable(False)
+    t_eager = sum(a.elapsed_time(b) for a, b in ev2) / 1e3 / args.steps
     prof = {name: S.profile_read(name) for name in S.PROFILED_KERNELS}
     prof = {n: v for n, v in prof.items() if v[0] > 0}
     S.profile_reset()
@@ -297,11 +322,13 @@ def main():
 
     t_step = allmax(t_step)
     t_ar = allmax(t_ar)
+    t_topk_kernel = allmax(t_topk_kernel)
+    t_eager = allmax(t_eager)
     value = P * 4 * N / t_step / 1e9
 
     # roofline: the fused EF top-k kernel (the one HBM pass over the gradient)
     hbm_peak, peak_src = load_peaks()
-    t_filter = ms_f / 1e3 / max(nf, 1)
+    t_filter = t_topk_kernel
     alg_bytes = 12 * N + 8 * k          # read eps + grad, write eps (+ k candidates) per launch
     achieved = alg_bytes / t_filter / 1e9 if t_filter > 0 else None
     total_prof_ms = sum(v[1] for v in prof.values())
@@ -322,12 +349,13 @@ def main():
         for it in range(max(2, args.steps // 2)):
             flush.zero_()
             barrier()
+            comm.barrier()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
-            mid = torch.cuda.Event(enable_timing=True)
             a.record(stream)
             grad.copy_(gh, non_blocking=True)                 # H2D of the step's input
-            step()
+            topk()                                            # the public API, eager
+            allreduce()
             hdr_h.copy_(out[:64], non_blocking=True)          # D2H: header, then the payload
             stream.synchronize()
             h = S.Header.from_buffer_copy(bytes(hdr_h.numpy()))
@@ -389,6 +417,8 @@ def main():
                        "quant_bits": cfg["bits"], "l2": "flushed before every step (512 MiB write)",
                        "exchange": "CUDA IPC over NVLink (fused push/pull kernels)" if P > 1 else "none (P=1)"},
             "latency_us": t_step * 1e6, "allreduce_us": t_ar * 1e6, "topk_us": (t_step - t_ar) * 1e6,
+            "timing": "CUDA graphs (g_topk, g_ar) replayed per step; eager API step measured too",
+            "eager_ms_per_step": t_eager * 1e3,
             "result_nnz": K, "bytes_recv_per_rank": bytes_recv,
             "exchange_gbs_per_rank": bytes_recv / t_ar / 1e9 if P > 1 else None,
             "dense_nccl_allreduce_us": dense_us,
