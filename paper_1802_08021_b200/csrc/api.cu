@@ -67,16 +67,18 @@ TreeSched make_sched(int P) {
 // symmetric workspace layout (identical on every rank)
 // ---------------------------------------------------------------------------
 struct Layout {
-  int P;
+  int P, L;                 // ranks, recursive-doubling stages (0 if P is not a power of two)
   uint64_t max_N, max_nnz;
-  uint64_t part_cap;     // largest partition
-  uint64_t cap_s;        // pairs per receive region (one per source)
+  uint64_t part_cap;        // largest partition (rounded to 64)
+  uint64_t cap_s;           // pairs per receive region (one per source)
+  uint64_t nwin;            // windows of the largest partition
   size_t status_off, n_status;
   size_t recv_off, region_bytes;
+  size_t win_off, win_bytes;            // per-source window-offset tables (nwin + 1 each)
   size_t part_off, part_bytes, scales_off;
-  std::vector<size_t> node_off;     // tree internal nodes (non-root)
-  std::vector<uint64_t> node_cap;
-  size_t rd_off, rd_bytes, rd_val_off;   // 5 stream buffers: cur0 cur1 recv0 recv1 recv_init
+  size_t stage_off;                     // owner staging: nwin * kWin pairs (SoA)
+  size_t wcnt_off, blk_off;
+  size_t rd_off, rd_bytes, rd_val_off;  // cur[2] + recv[2 parities][L stages]
   size_t total;
 };
 
@@ -85,8 +87,9 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.P = P;
   L.max_N = max_N;
   L.max_nnz = max_nnz;
-  L.part_cap = max_N / P + P;
+  L.part_cap = align_up(max_N / P + P, 64);
   L.cap_s = std::min<uint64_t>(max_nnz, L.part_cap);
+  L.nwin = (L.part_cap + kWin - 1) / kWin;
   size_t off = align_up(sizeof(Ctrl), 256);
   L.status_off = off;
   L.n_status = max_N / 1024 + 2 * max_nnz / kMergeTile + 256;
@@ -94,26 +97,28 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.recv_off = off;
   L.region_bytes = align_up(8 * L.cap_s, 256);
   off += (size_t)P * L.region_bytes;
+  L.win_off = off;
+  L.win_bytes = align_up(4 * (L.nwin + 1), 256);
+  off += (size_t)P * L.win_bytes;
   L.part_off = off;
   L.part_bytes = align_up(8 * L.part_cap + 256, 256);
   L.scales_off = off + align_up(L.part_cap + 16, 256);   // codes <= part_cap bytes (8 bits)
   off += L.part_bytes;
-  std::vector<TreeNode> nodes;
-  build_tree(0, P, nodes);
-  L.node_off.assign(nodes.size(), 0);
-  L.node_cap.assign(nodes.size(), 0);
-  for (size_t i = 0; i + 1 < nodes.size(); ++i) {   // the root (last) writes the partition result
-    const uint64_t cap = std::min<uint64_t>((uint64_t)(nodes[i].hi - nodes[i].lo) * L.cap_s, L.part_cap);
-    L.node_off[i] = off;
-    L.node_cap[i] = cap;
-    off = align_up(off + 8 * cap, 256);
-  }
+  L.stage_off = off;
+  off += align_up(8 * L.nwin * kWin, 256);
+  L.wcnt_off = off;
+  off += align_up(4 * L.nwin, 256);
+  L.blk_off = off;
+  off += align_up(8 * 8192, 256);
+  L.L = 0;
+  const bool pow2 = (P & (P - 1)) == 0;
+  if (pow2)
+    while ((1 << L.L) < P) ++L.L;
   L.rd_off = off;
   // sparse slots: stage outputs hold <= delta <= N/2 pairs, the stage-1 push a whole input
   L.rd_val_off = align_up(4 * std::max<uint64_t>(half_cap(max_N), max_nnz) + 64, 256);
   L.rd_bytes = align_up(std::max<size_t>(2 * L.rd_val_off, 4 * max_N) + 256, 256);
-  const bool pow2 = (P & (P - 1)) == 0;
-  if (pow2 && P > 1) off += 5 * L.rd_bytes;
+  if (pow2 && P > 1) off += (size_t)(2 + 2 * L.L) * L.rd_bytes;
   L.total = align_up(off, 1 << 20);
   return L;
 }
@@ -159,9 +164,18 @@ inline uint32_t* recv_idx(const Layout& L, char* base, int src) {
 inline float* recv_val(const Layout& L, char* base, int src) {
   return reinterpret_cast<float*>(base + L.recv_off + (size_t)src * L.region_bytes + 4 * L.cap_s);
 }
-inline StreamBuf rd_buf(const Layout& L, char* base, int which) {   // 0,1 cur; 2,3 recv; 4 recv_init
+inline uint32_t* win_table(const Layout& L, char* base, int src) {
+  return reinterpret_cast<uint32_t*>(base + L.win_off + (size_t)src * L.win_bytes);
+}
+inline StreamBuf rd_cur(const Layout& L, char* base, int i) {
   StreamBuf b;
-  b.base = base + L.rd_off + (size_t)which * L.rd_bytes;
+  b.base = base + L.rd_off + (size_t)i * L.rd_bytes;
+  b.val_off = L.rd_val_off;
+  return b;
+}
+inline StreamBuf rd_recv(const Layout& L, char* base, int par, int t) {   // t = 1..L
+  StreamBuf b;
+  b.base = base + L.rd_off + (size_t)(2 + par * L.L + (t - 1)) * L.rd_bytes;
   b.val_off = L.rd_val_off;
   return b;
 }
@@ -196,92 +210,69 @@ struct CallCtx {
   cudaStream_t s;
 };
 
-BarrierArgs barrier_args(sparcml_comm* c, int r, int first) {
+BarrierArgs barrier_args(sparcml_comm* c, int r) {
   BarrierArgs b = {};
   b.my = ctrl_of(c->peer[r]);
   b.P = c->P;
   b.rank = r;
-  b.first_in_call = first;
   b.loopback = c->local ? 1 : 0;
   for (int p = 0; p < c->P; ++p) b.peer_flags[p] = &ctrl_of(c->peer[p])->flags[r];
   return b;
 }
 
 // ------------------------------------------------------------ RD schedule ---
+// push (stage-1 partner) ; stage 1 .. L, each waiting for its partner's flag
 sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
                       const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
   const Layout& L = c->L;
-  const int P = c->P;
-  int Lg = 0;
-  while ((1 << Lg) < P) ++Lg;
-  if (P == 2)   // one stage: protect recv_init from the next call (graph-replay safe)
-    for (int r : R) CK(c, launch_barrier(barrier_args(c, r, 1), cc.s));
+  const int Lg = L.L;
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i], q = r ^ 1;
     RdPushArgs a = {};
     a.idx = idx[i];
     a.val = val[i];
     a.n = nnz[i];
-    a.dst = rd_buf(L, c->peer[q], 4);
-    a.dst_n = &ctrl_of(c->peer[q])->rd_n[2];
-    a.dst_dense = &ctrl_of(c->peer[q])->rd_dense[2];
-    a.dst_ksum = &ctrl_of(c->peer[q])->rd_ksum[2];
+    a.dst[0] = rd_recv(L, c->peer[q], 0, 1);
+    a.dst[1] = rd_recv(L, c->peer[q], 1, 1);
+    a.peer = ctrl_of(c->peer[q]);
     a.ctl = ctrl_of(c->peer[r]);
     a.N = cc.N;
     a.validate = cc.o.validate;
     CK(c, launch_rd_push(a, cc.s));
   }
   for (int t = 1; t <= Lg; ++t) {
-    for (int r : R) CK(c, launch_barrier(barrier_args(c, r, t == 1 && P != 2), cc.s));
     for (size_t i = 0; i < R.size(); ++i) {
       const int r = R[i];
-      Ctrl* my = ctrl_of(c->peer[r]);
+      char* base = c->peer[r];
       RdStageArgs a = {};
-      if (t == 1) {
-        a.a_idx = idx[i];
-        a.a_val = val[i];
-        a.a_n = nnz[i];
-      } else {
-        StreamBuf cur = rd_buf(L, c->peer[r], (t - 1) % 2);
-        a.a_idx = reinterpret_cast<const uint32_t*>(cur.base);
-        a.a_val = reinterpret_cast<const float*>(cur.base + cur.val_off);
-        a.a_n_dev = &my->own_n[(t - 1) % 2];
-        a.a_dense_dev = &my->own_dense[(t - 1) % 2];
-        a.a_ksum_dev = &my->own_ksum[(t - 1) % 2];
-      }
-      const int rb = t == 1 ? 4 : 2 + (t % 2);
-      const int ci = t == 1 ? 2 : t % 2;   // ctrl slot of that recv buffer
-      a.b = rd_buf(L, c->peer[r], rb);
-      a.b_n_dev = &my->rd_n[ci];
-      a.b_dense_dev = &my->rd_dense[ci];
-      a.b_ksum_dev = &my->rd_ksum[ci];
+      a.a_idx = idx[i];
+      a.a_val = val[i];
+      a.a_n = nnz[i];
+      a.a_from_cur = t > 1;
+      a.cur[0] = rd_cur(L, base, 0);
+      a.cur[1] = rd_cur(L, base, 1);
+      a.b[0] = rd_recv(L, base, 0, t);
+      a.b[1] = rd_recv(L, base, 1, t);
       a.N = cc.N;
       a.delta = cc.delta;
       if (t == Lg) {
         a.o.base = out[i] + SPARCML_HEADER_BYTES;
         a.o.val_off = cc.val_offset - SPARCML_HEADER_BYTES;
-        a.o_n_dev = &my->own_n[t % 2];   // scratch copies of the final counts
-        a.o_dense_dev = &my->own_dense[t % 2];
-        a.o_ksum_dev = &my->own_ksum[t % 2];
+        a.o_cur = 0;
         a.hdr = reinterpret_cast<sparcml_header*>(out[i]);
         a.last = 1;
+        a.mpeer = nullptr;
       } else {
-        a.o = rd_buf(L, c->peer[r], t % 2);
-        a.o_n_dev = &my->own_n[t % 2];
-        a.o_dense_dev = &my->own_dense[t % 2];
-        a.o_ksum_dev = &my->own_ksum[t % 2];
+        a.o_cur = 1;
         const int q = r ^ (1 << t);   // next stage's partner
-        Ctrl* qc = ctrl_of(c->peer[q]);
-        const int qslot = (t + 1) % 2;
-        a.m = rd_buf(L, c->peer[q], 2 + qslot);
-        a.m_n_dev = &qc->rd_n[qslot];
-        a.m_dense_dev = &qc->rd_dense[qslot];
-        a.m_ksum_dev = &qc->rd_ksum[qslot];
+        a.m[0] = rd_recv(L, c->peer[q], 0, t + 1);
+        a.m[1] = rd_recv(L, c->peer[q], 1, t + 1);
+        a.mpeer = ctrl_of(c->peer[q]);
       }
-      a.ctl = my;
+      a.ctl = ctrl_of(base);
       a.stage = t;
-      a.ctr = &my->scan[0];
-      a.status = status_of(L, c->peer[r]);
+      a.ctr = &ctrl_of(base)->scan[0];
+      a.status = status_of(L, base);
       CK(c, launch_rd_stage(a, cc.s));
     }
   }
@@ -289,6 +280,8 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
 }
 
 // --------------------------------------------------------- split schedule ---
+// push (slices + window tables -> owners) ; owner reduction (waits for the P
+// slices) ; pull-concat (waits for the P owners)
 sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
                          const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
   const Layout& L = c->L;
@@ -297,7 +290,6 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
   uint64_t bnd[kMaxRanks + 1];
   for (int j = 0; j < P; ++j) bnd[j] = (uint64_t)j * part;
   bnd[P] = cc.N;
-  // phase 1: split + push to owners
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
     PushArgs a = {};
@@ -311,104 +303,49 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     for (int j = 0; j < P; ++j) {
       a.dst_idx[j] = recv_idx(L, c->peer[j], r);
       a.dst_val[j] = recv_val(L, c->peer[j], r);
-      a.dst_cnt[j] = &ctrl_of(c->peer[j])->slice_cnt[r];
-      a.dst_k[j] = &ctrl_of(c->peer[j])->k_in[r];
+      a.dst_win[j] = win_table(L, c->peer[j], r);
+      a.peer[j] = ctrl_of(c->peer[j]);
     }
     a.ctl = ctrl_of(c->peer[r]);
     a.validate = cc.o.validate;
     CK(c, launch_split_push(a, cc.s));
   }
-  for (int r : R) {
-    Ctrl* my = ctrl_of(c->peer[r]);
-    DecideArgs d;
-    d.k_in = my->k_in;
-    d.P = P;
-    d.algo = cc.o.algo == SPARCML_SSAR_RECURSIVE_DOUBLE ? SPARCML_ALGO_AUTO : cc.o.algo;
-    d.delta = (uint64_t)std::floor((double)cc.delta);
-    d.dsar_out = &my->dsar;
-    d.k_sum_out = &my->k_sum;
-    CK(c, launch_barrier_decide(barrier_args(c, r, 1), d, cc.s));
-  }
-  const bool run_ssar = cc.host_dsar != 1, run_dsar = cc.host_dsar != 0;
-  std::vector<TreeNode> nodes;
-  build_tree(0, P, nodes);
-  int H = 0;
-  for (auto& n : nodes) H = std::max(H, n.height);
+  const TreeSched ts = make_sched(P);
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
     char* base = c->peer[r];
-    Ctrl* my = ctrl_of(base);
-    if (run_ssar) {
-      // owner reduction: canonical tree of union-merges, one batched launch per height
-      for (int h = 1; h <= H; ++h) {
-        MergeJobsArgs m = {};
-        for (size_t ni = 0; ni < nodes.size(); ++ni) {
-          const TreeNode& nd = nodes[ni];
-          if (nd.height != h) continue;
-          MergeJob& jb = m.job[m.njobs++];
-          auto src = [&](int child, int leaf, const uint32_t** ix, const float** vx, const uint64_t** nx) {
-            if (child < 0) {
-              *ix = recv_idx(L, base, leaf);
-              *vx = recv_val(L, base, leaf);
-              *nx = &my->slice_cnt[leaf];
-            } else {
-              *ix = reinterpret_cast<const uint32_t*>(base + L.node_off[child]);
-              *vx = reinterpret_cast<const float*>(base + L.node_off[child] + 4 * L.node_cap[child]);
-              *nx = &my->node_n[child];
-            }
-          };
-          src(nd.left, nd.lo, &jb.a_idx, &jb.a_val, &jb.a_n_dev);
-          src(nd.right, nd.mid, &jb.b_idx, &jb.b_val, &jb.b_n_dev);
-          if ((size_t)nd.id + 1 == nodes.size()) {   // root -> partition result
-            jb.out.idx = reinterpret_cast<uint32_t*>(base + L.part_off);
-            jb.out.val = reinterpret_cast<float*>(base + L.part_off + 4 * L.part_cap);
-            jb.out.n = &my->owner_K;
-          } else {
-            jb.out.idx = reinterpret_cast<uint32_t*>(base + L.node_off[nd.id]);
-            jb.out.val = reinterpret_cast<float*>(base + L.node_off[nd.id] + 4 * L.node_cap[nd.id]);
-            jb.out.n = &my->node_n[nd.id];
-          }
-        }
-        m.ctr = &my->scan[0];
-        m.status = status_of(L, base);
-        if (cc.host_dsar < 0) m.gate = Gate{&my->dsar, 0u};
-        CK(c, launch_merge_jobs(m, 1 << 30, cc.s));
-      }
+    OwnerArgs w = {};
+    w.P = P;
+    w.rank = r;
+    w.algo = cc.o.algo == SPARCML_SSAR_RECURSIVE_DOUBLE ? SPARCML_ALGO_AUTO : cc.o.algo;
+    w.delta = cc.delta;
+    w.lo = bnd[r];
+    w.hi = bnd[r + 1];
+    for (int s = 0; s < P; ++s) {
+      w.src_idx[s] = recv_idx(L, base, s);
+      w.src_val[s] = recv_val(L, base, s);
+      w.src_win[s] = win_table(L, base, s);
+      w.peer[s] = ctrl_of(c->peer[s]);
     }
-    if (run_dsar) {
-      // DSAR owner: P sparse slices -> dense partition (+ QSGD), one fused window pass
-      WindowArgs w = {};
-      w.nsrc = P;
-      for (int s = 0; s < P; ++s) {
-        w.src[s].idx = recv_idx(L, base, s);
-        w.src[s].val = recv_val(L, base, s);
-        w.src[s].n_dev = &my->slice_cnt[s];
-      }
-      w.sched = make_sched(P);
-      w.lo = bnd[r];
-      w.hi = bnd[r + 1];
-      if (cc.o.quant_bits) {
-        w.out.mode = WIN_QUANT;
-        w.out.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
-        w.out.scales = reinterpret_cast<float*>(base + L.scales_off);
-        w.out.qbase = bnd[r];
-        w.out.bits = cc.o.quant_bits;
-        w.out.bucket = cc.o.quant_bucket;
-        w.out.seed_lo = (uint32_t)cc.o.seed;
-        w.out.seed_hi = (uint32_t)(cc.o.seed >> 32);
-      } else {
-        w.out.mode = WIN_DENSE;
-        w.out.dense = reinterpret_cast<float*>(base + L.part_off);
-        w.out.dense_base = bnd[r];
-      }
-      w.ctr = &my->scan[0];
-      w.status = status_of(L, base);
-      if (cc.host_dsar < 0) w.gate = Gate{&my->dsar, 1u};
-      CK(c, launch_window(w, cc.s));
-    }
+    w.sched = ts;
+    w.r_idx = reinterpret_cast<uint32_t*>(base + L.part_off);
+    w.r_val = reinterpret_cast<float*>(base + L.part_off + 4 * L.part_cap);
+    w.st_idx = reinterpret_cast<uint32_t*>(base + L.stage_off);
+    w.st_val = reinterpret_cast<float*>(base + L.stage_off + 4 * L.nwin * kWin);
+    w.win_cnt = reinterpret_cast<uint32_t*>(base + L.wcnt_off);
+    w.blk = reinterpret_cast<uint64_t*>(base + L.blk_off);
+    w.dense = reinterpret_cast<float*>(base + L.part_off);
+    w.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
+    w.scales = reinterpret_cast<float*>(base + L.scales_off);
+    w.bits = cc.o.quant_bits;
+    w.bucket = cc.o.quant_bucket;
+    w.seed_lo = (uint32_t)cc.o.seed;
+    w.seed_hi = (uint32_t)(cc.o.seed >> 32);
+    w.host_dsar = cc.host_dsar;
+    w.wait = 1;
+    w.ctl = ctrl_of(base);
+    CK(c, launch_owner(w, cc.s));
   }
-  for (int r : R) CK(c, launch_barrier(barrier_args(c, r, 0), cc.s));
-  // phase 2: pull every partition result into out
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
     ConcatArgs a = {};
@@ -427,12 +364,12 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
       a.r_dense[j] = reinterpret_cast<const float*>(pb + L.part_off);
     }
     a.ctl = ctrl_of(c->peer[r]);
+    a.wait_owners = 1;
     a.bits = cc.o.quant_bits;
     a.bucket = cc.o.quant_bucket ? cc.o.quant_bucket : 1024;
     a.out = out[i];
     a.val_offset = cc.val_offset;
     a.algo = SPARCML_SSAR_SPLIT_ALLGATHER;
-    a.ctr = &ctrl_of(c->peer[r])->scan[0];
     a.status = status_of(L, c->peer[r]);
     CK(c, launch_concat(a, cc.s));
   }
@@ -455,8 +392,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   p.ctl = my;
   p.validate = cc.o.validate;
   CK(c, launch_p1_prep(p, cc.s));
-  const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER ||
-                    (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
+  const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER || (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
   ConcatArgs a = {};
   a.P = 1;
   a.rank = 0;
@@ -498,12 +434,12 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
     a.r_dense[0] = reinterpret_cast<const float*>(base + L.part_off);
   }
   a.ctl = my;
+  a.wait_owners = 0;
   a.bits = cc.o.quant_bits;
   a.bucket = cc.o.quant_bucket ? cc.o.quant_bucket : 1024;
   a.out = out;
   a.val_offset = cc.val_offset;
   a.algo = cc.o.algo == SPARCML_ALGO_AUTO ? SPARCML_SSAR_SPLIT_ALLGATHER : cc.o.algo;
-  a.ctr = &my->scan[0];
   a.status = status_of(L, base);
   CK(c, launch_concat(a, cc.s));
   return SPARCML_OK;
@@ -771,9 +707,9 @@ sparcml_status sparcml_barrier(sparcml_comm* c, void* stream) {
   CK(c, cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (c->local) {
-    for (int r = 0; r < c->P; ++r) CK(c, launch_barrier(barrier_args(c, r, 0), s));
+    for (int r = 0; r < c->P; ++r) CK(c, launch_barrier(barrier_args(c, r), s));
   } else if (c->P > 1) {
-    CK(c, launch_barrier(barrier_args(c, c->rank, 0), s));
+    CK(c, launch_barrier(barrier_args(c, c->rank), s));
   }
   return SPARCML_OK;
 }

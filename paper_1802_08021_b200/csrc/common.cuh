@@ -47,6 +47,11 @@ __device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
 __device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// acquire-release fences: ordering without the sequentially-consistent drain
+// (__threadfence_system() is fence.sc.sys, several microseconds under load)
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // streaming (read-once) vector load, no L1 allocation
 __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   float4 r;
@@ -299,30 +304,43 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
 }
 
 // ---------------------------------------------------------------------------
+// cross-GPU signalling: a flag holds the sequence number of the call that set
+// it; waiters compare wrap-safely against seq + 1 of their own call
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void wait_flag_geq(const uint32_t* f, uint32_t target) {
+  while ((int)(ld_acquire_sys(f) - target) < 0) __nanosleep(32);
+}
+
+constexpr int kMaxStages = 5;   // recursive doubling: log2(16) stages (+1)
+
+// ---------------------------------------------------------------------------
 // per-rank control block at offset 0 of the symmetric workspace
 // ---------------------------------------------------------------------------
 struct alignas(128) Ctrl {
-  uint32_t flags[kMaxRanks];      // barrier arrivals; slot p written by rank p
+  uint32_t flags[kMaxRanks];      // sparcml_barrier arrivals; slot p written by rank p
   uint32_t epoch;                 // this rank's barrier epoch
-  uint32_t call_count;            // collectives started (bumped by the first barrier)
+  uint32_t seq;                   // collectives this rank has completed
   uint32_t dsar;                  // split-allgather decision of the current call
   uint32_t status;                // device-detected sparcml_status bits
+  uint32_t src_done[kMaxRanks];   // split: rank i's slice of call seq+1 is in my receive region i
+  uint32_t owner_done[kMaxRanks]; // split: owner j's partition result of call seq+1 is ready
+  uint32_t done_ctr[4];           // last-block detection counters (push, stage, concat, owner)
   uint32_t pad0[12];
-  // split-allgather
   uint64_t k_in[kMaxRanks];       // nnz of rank i (written by rank i)
   uint64_t slice_cnt[kMaxRanks];  // pairs rank i pushed into my receive region i
   uint64_t slice_out[kMaxRanks];  // pairs I pushed to owner j
   uint64_t owner_K;               // my partition's reduced pair count
-  uint64_t k_sum;                 // sum of k_i (owner stage)
-  uint64_t node_n[2 * kMaxRanks]; // tree-merge internal node counts
-  // recursive doubling: recv[0], recv[1] (stage parity) and recv_init [2]
-  uint64_t rd_n[3];               // pairs (or N) of the stream in my recv buffer
-  uint64_t rd_ksum[3];            // k-sum of the group that stream covers
-  uint32_t rd_dense[3];
-  uint32_t own_dense[2];
-  uint64_t own_n[2];              // my own stream in cur[b]
+  uint64_t k_sum;                 // sum of k_i
+  // recursive doubling, per call parity (seq & 1) and stage t = 1..L: the
+  // partner's stream in my receive buffer [par][t] and its flag
+  uint32_t rd_flag[2][kMaxStages];
+  uint32_t rd_dense[2][kMaxStages];
+  uint64_t rd_n[2][kMaxStages];
+  uint64_t rd_ksum[2][kMaxStages];
+  uint32_t own_dense[2];          // my own stream in cur[b]
+  uint64_t own_n[2];
   uint64_t own_ksum[2];
-  uint64_t rd_sent[8];            // bytes I pushed before stage t (t = 1..log2 P)
+  uint64_t rd_sent[8];            // bytes I pushed for stage t (index t-1)
   uint64_t rd_recv[8];            // bytes I received for stage t
   ScanCounters scan[4];           // ticket counters of the tile kernels
 };

@@ -10,14 +10,6 @@
 
 namespace sparcml {
 
-// --------------------------------------------------------------- gating ----
-// A kernel whose work depends on a device-side decision reads it from
-// (*gate_ptr == gate_value); gate_ptr == nullptr means "always run".
-struct Gate {
-  const uint32_t* ptr;
-  uint32_t value;
-};
-
 // -------------------------------------------------------- batched merges ---
 struct MergeJob {
   const uint32_t* a_idx;
@@ -31,26 +23,23 @@ struct MergeJob {
   MergeOutput out;
 };
 
-struct MergeJobsArgs {
+struct MergeJobsArgs {   // stand-alone sparcml_merge_sum
   int njobs;
   MergeJob job[kMaxJobs];
   ScanCounters* ctr;
   TileStatus* status;
-  Gate gate;
 };
 
 // ----------------------------------------------------------- window ------
-struct WinSourceDesc {      // device-resolved at kernel start
+struct WinSourceDesc {
   const uint32_t* idx;
   const float* val;
-  const uint64_t* n_dev;    // nullable -> n
   uint64_t n;
-  const uint32_t* dense_dev;  // nullable -> dense
   int dense;
   uint64_t dense_base;
 };
 
-struct WindowArgs {
+struct WindowArgs {      // P == 1 densify / QSGD of one stream
   int nsrc;
   WinSourceDesc src[kMaxRanks];
   TreeSched sched;
@@ -58,7 +47,6 @@ struct WindowArgs {
   WinOutput out;
   ScanCounters* ctr;
   TileStatus* status;
-  Gate gate;
 };
 
 // ----------------------------------------------------- recursive doubling ---
@@ -68,50 +56,39 @@ struct StreamBuf {
   uint64_t val_off;
 };
 
-struct RdStageArgs {
-  // own stream (stage 1: the caller's input)
-  const uint32_t* a_idx;
-  const float* a_val;
-  const uint64_t* a_n_dev;  // nullable -> a_n
-  uint64_t a_n;
-  const uint32_t* a_dense_dev;  // nullable -> sparse
-  const uint64_t* a_ksum_dev;   // nullable -> a_n
-  // partner stream, in my recv buffer
-  StreamBuf b;
-  const uint64_t* b_n_dev;
-  const uint32_t* b_dense_dev;
-  const uint64_t* b_ksum_dev;
-  uint64_t N, delta;
-  // output stream (cur buffer, or the caller's out payload)
-  StreamBuf o;
-  uint64_t* o_n_dev;
-  uint32_t* o_dense_dev;
-  uint64_t* o_ksum_dev;
-  // optional mirror into the next partner's recv buffer
-  StreamBuf m;
-  uint64_t* m_n_dev;
-  uint32_t* m_dense_dev;
-  uint64_t* m_ksum_dev;
-  Ctrl* ctl;            // my control block (bytes accounting, status)
-  int stage;            // 1-based
-  int last;
-  sparcml_header* hdr;  // last stage only
-  ScanCounters* ctr;
-  TileStatus* status;
-};
-
-// Stage-1 push: my input -> partner's recv buffer (+counts).
+// Stage-1 push: my input -> stage-1 partner's receive buffer [par][1] (+ flag).
 struct RdPushArgs {
   const uint32_t* idx;
   const float* val;
   uint64_t n;
-  StreamBuf dst;
-  uint64_t* dst_n;
-  uint32_t* dst_dense;
-  uint64_t* dst_ksum;
-  Ctrl* ctl;            // my control block
+  StreamBuf dst[2];          // by call parity
+  Ctrl* peer;                // the stage-1 partner's control block
+  Ctrl* ctl;                 // mine
   uint64_t N;
   int validate;
+};
+
+struct RdStageArgs {
+  // own stream (stage 1: the caller's input)
+  const uint32_t* a_idx;
+  const float* a_val;
+  uint64_t a_n;              // stage 1 only
+  int a_from_cur;            // stages > 1: my cur[(t-1)%2]
+  StreamBuf cur[2];          // my cur buffers
+  StreamBuf b[2];            // my receive buffer [par][t]
+  uint64_t N, delta;
+  // output: cur[t%2] (or the caller's out payload at the last stage)
+  StreamBuf o;
+  int o_cur;                 // 1: o = cur[t % 2]
+  // mirror into the next partner's receive buffer [par][t+1]
+  StreamBuf m[2];
+  Ctrl* mpeer;               // that partner's control block (nullptr at the last stage)
+  Ctrl* ctl;                 // mine
+  int stage;                 // 1-based
+  int last;
+  sparcml_header* hdr;       // last stage only
+  ScanCounters* ctr;
+  TileStatus* status;
 };
 
 // ---------------------------------------------------------- split phase ---
@@ -124,40 +101,59 @@ struct PushArgs {
   uint64_t bnd[kMaxRanks + 1];
   uint32_t* dst_idx[kMaxRanks];    // owner j's receive region for source `rank`
   float* dst_val[kMaxRanks];
-  uint64_t* dst_cnt[kMaxRanks];    // &owner_j.ctrl.slice_cnt[rank]
-  uint64_t* dst_k[kMaxRanks];      // &peer_j.ctrl.k_in[rank]
-  Ctrl* ctl;                       // my control block
+  uint32_t* dst_win[kMaxRanks];    // owner j's window-offset table for source `rank` (nwin_j + 1)
+  Ctrl* peer[kMaxRanks];           // every rank's control block
+  Ctrl* ctl;                       // mine
   int validate;
 };
 
-// Owner decision (SSAR vs DSAR) evaluated at the start of the owner stage.
-struct DecideArgs {
-  const uint64_t* k_in;   // my Ctrl.k_in
-  int P;
-  int algo;               // sparcml_algo (2 or 3 forced; 0 auto)
+struct OwnerArgs {
+  int P, rank;
+  int algo;                        // sparcml_algo (AUTO decides on the device)
   uint64_t delta;
-  uint32_t* dsar_out;     // my Ctrl.dsar
-  uint64_t* k_sum_out;    // my Ctrl.k_sum
+  uint64_t lo, hi;                 // my partition
+  const uint32_t* src_idx[kMaxRanks];
+  const float* src_val[kMaxRanks];
+  const uint32_t* src_win[kMaxRanks];
+  TreeSched sched;
+  // SSAR: compacted partition result (via per-window staging)
+  uint32_t* r_idx;
+  float* r_val;
+  uint32_t* st_idx;                // staging: window w at [w * kWin, ...)
+  float* st_val;
+  uint32_t* win_cnt;               // per-window output counts
+  uint64_t* blk;                   // per-block totals (grid-sized)
+  // DSAR: dense partition or QSGD codes + scales
+  float* dense;
+  uint8_t* codes;
+  float* scales;
+  int bits;
+  uint32_t bucket;
+  uint32_t seed_lo, seed_hi;
+  int host_dsar;                   // -1 device decides, else 0/1
+  int wait;                        // 1: wait for the sources' flags (P > 1)
+  Ctrl* peer[kMaxRanks];
+  Ctrl* ctl;
 };
 
 struct ConcatArgs {
   int P, rank;
   uint64_t N, delta;
   uint64_t bnd[kMaxRanks + 1];
-  // owner j's partial result (peer pointers)
+  // owner j's partition result (peer pointers)
   const uint32_t* r_idx[kMaxRanks];
   const float* r_val[kMaxRanks];
   const uint64_t* r_n[kMaxRanks];
   const uint8_t* r_codes[kMaxRanks];
   const float* r_scales[kMaxRanks];
   const float* r_dense[kMaxRanks];
-  Ctrl* ctl;                       // my control block (dsar, k_sum, slice counts, status)
+  Ctrl* ctl;                       // mine (dsar, k_sum, slice counts, owner flags, status)
+  int wait_owners;                 // 1: wait for owner_done flags (P > 1)
   int bits;
   uint32_t bucket;
   char* out;                       // caller's out (header + payload)
   uint64_t val_offset;
   uint32_t algo;
-  ScanCounters* ctr;
   TileStatus* status;
 };
 
@@ -165,7 +161,6 @@ struct BarrierArgs {
   Ctrl* my;
   uint32_t* peer_flags[kMaxRanks];  // &peer_p.ctrl.flags[rank]
   int P, rank;
-  int first_in_call;
   int loopback;                     // no waiting (all ranks on one stream)
 };
 
@@ -200,10 +195,11 @@ cudaError_t launch_window(const WindowArgs& a, cudaStream_t s);
 cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s);
 cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s);
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s);
-cudaError_t launch_barrier_decide(const BarrierArgs& a, const DecideArgs& d, cudaStream_t s);
+cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);
+int owner_grid_size();
 
 // top-k / QSGD (kernels_topk.cu, kernels_qsgd.cu)
 size_t topk_workspace_bytes(uint64_t N, uint64_t k);

@@ -1,26 +1,37 @@
 // kernels_comm.cu — collective kernels of the sparse allreduce (§5.3).
 //
 // Exchange model: every rank owns a symmetric workspace that
-// its peers map over NVLink (CUDA IPC).  Data moves by *pushes* fused into
-// the producing kernel (split phase, RD stage outputs) and *pulls* fused into
-// the consuming kernel (allgather phase); ranks synchronise with a one-warp
-// flag barrier.  No host round trip, no NCCL on the data path.
+// its peers map over NVLink (CUDA IPC).  Data moves inside the kernels:
+// *pushes* fused into the producer (split phase, recursive-doubling stage
+// outputs) and *pulls* fused into the consumer (allgather phase).  Phases are
+// ordered by per-call flags (the call's sequence number) that the producer's
+// last block stores into the consumer's control block with release semantics
+// at system scope — no barrier kernels, no host round trip, no NCCL.
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace sparcml {
 
 unsigned long long g_launches = 0;
 
 int device_sm_count() {
-  int dev = 0, sms = 148;
+  static int cached_dev = -1, cached = 148;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
+  if (dev != cached_dev) {
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    cached_dev = dev;
+  }
+  return cached;
 }
 
-// Returns true in the last block to finish (after the counters are reset).
+__device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Returns true in the last block to finish (after the ticket counters are reset).
 __device__ __forceinline__ bool scan_block_exit_last(ScanCounters* c) {
   __shared__ uint32_t s_last;
   __syncthreads();
@@ -39,17 +50,61 @@ __device__ __forceinline__ bool scan_block_exit_last(ScanCounters* c) {
   return s_last != 0;
 }
 
+// Last block to finish.  Every block releases its writes (at system scope when
+// `sys`, i.e. when they went to peers over NVLink) before counting itself; the
+// last block acquires them before it returns true.
+template <bool SYS>
+__device__ __forceinline__ bool last_block(uint32_t* ctr) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (SYS) fence_acq_rel_sys(); else fence_acq_rel_gpu();
+    const uint32_t d = atomicAdd(ctr, 1u);
+    s_last = (d == gridDim.x - 1);
+    if (s_last) {
+      *ctr = 0;
+      if (SYS) fence_acq_rel_sys(); else fence_acq_rel_gpu();
+    }
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
 __device__ __forceinline__ uint32_t next_ticket(ScanCounters* c, uint32_t* s_ticket) {
   if (threadIdx.x == 0) *s_ticket = atomicAdd(&c->ticket, 1u);
   __syncthreads();
-  const uint32_t t = *s_ticket;
-  return t;
+  return *s_ticket;
 }
 
-__device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+__device__ __forceinline__ void write_header(sparcml_header* h, uint32_t repr, uint64_t nnz, uint64_t N,
+                                             uint64_t ksum, uint64_t sent, uint64_t recv, uint32_t algo,
+                                             uint32_t status_bits, uint64_t val_offset) {
+  uint32_t st = 0;
+  for (uint32_t b = 1; b < 32; ++b)
+    if (status_bits & (1u << b)) {
+      st = b;
+      break;
+    }
+  h->magic = SPARCML_HEADER_MAGIC;
+  h->repr = repr;
+  h->nnz = nnz;
+  h->N = N;
+  h->k_sum = ksum;
+  h->bytes_sent = sent;
+  h->bytes_recv = recv;
+  h->algo_used = algo;
+  h->status = st;
+  h->val_offset = val_offset;
+}
+
+__device__ __forceinline__ void check_input(const uint32_t* idx, uint64_t e, uint64_t n, uint64_t N, uint32_t x,
+                                            float v, uint32_t* status) {
+  if (x >= N || (e + 1 < n && idx[e + 1] <= x)) atomicOr(status, 1u << SPARCML_ERR_UNSORTED);
+  if (!isfinite(v)) atomicOr(status, 1u << SPARCML_ERR_NONFINITE);
+}
 
 // ===========================================================================
-// batched union-merge-with-sum (split owner tree levels; stand-alone merge)
+// stand-alone union-merge-with-sum (sparcml_merge_sum)
 // ===========================================================================
 __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -57,7 +112,6 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
   __shared__ uint64_t s_na[kMaxJobs], s_nb[kMaxJobs];
   __shared__ uint32_t s_base[kMaxJobs + 1];
   __shared__ uint32_t s_ticket, s_gen;
-  if (a.gate.ptr && *a.gate.ptr != a.gate.value) return;   // grid-uniform
   const int tid = threadIdx.x;
   if (tid < a.njobs) {
     const MergeJob& j = a.job[tid];
@@ -84,8 +138,8 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
     int j = 0;
     while (t >= s_base[j + 1]) ++j;
     const MergeJob& jb = a.job[j];
-    merge_tile(jb.a_idx, jb.a_val, s_na[j], jb.b_idx, jb.b_val, s_nb[j],
-               (uint64_t)(t - s_base[j]) * kMergeTile, sm, a.status, t, s_base[j], s_gen, jb.out);
+    merge_tile(jb.a_idx, jb.a_val, s_na[j], jb.b_idx, jb.b_val, s_nb[j], (uint64_t)(t - s_base[j]) * kMergeTile, sm,
+               a.status, t, s_base[j], s_gen, jb.out);
   }
   scan_block_exit_last(a.ctr);
 }
@@ -105,33 +159,23 @@ cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t
 }
 
 // ===========================================================================
-// window kernel (DSAR owner: P sparse slices -> dense / QSGD partition)
+// window kernel (P == 1: densify / QSGD-encode one stream)
 // ===========================================================================
-__device__ __forceinline__ void resolve_sources(const WinSourceDesc* d, int n, WinSource* s) {
-  const int tid = threadIdx.x;
-  if (tid < n) {
-    s[tid].idx = d[tid].idx;
-    s[tid].val = d[tid].val;
-    s[tid].n = d[tid].n_dev ? *d[tid].n_dev : d[tid].n;
-    s[tid].dense = d[tid].dense_dev ? (int)*d[tid].dense_dev : d[tid].dense;
-    s[tid].dense_base = d[tid].dense_base;
-  }
-  __syncthreads();
-}
-
 __global__ void __launch_bounds__(kThreads) window_kernel(WindowArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ WinSource s_src[kMaxRanks];
   __shared__ uint32_t s_ticket, s_gen;
-  if (a.gate.ptr && *a.gate.ptr != a.gate.value) return;
-  resolve_sources(a.src, a.nsrc, s_src);
+  if (threadIdx.x < a.nsrc) {
+    const WinSourceDesc& d = a.src[threadIdx.x];
+    s_src[threadIdx.x].idx = d.idx;
+    s_src[threadIdx.x].val = d.val;
+    s_src[threadIdx.x].n = d.n;
+    s_src[threadIdx.x].dense = d.dense;
+    s_src[threadIdx.x].dense_base = d.dense_base;
+  }
   if (threadIdx.x == 0) s_gen = a.ctr->gen;
   __syncthreads();
   const uint32_t nwin = (uint32_t)ceil_div(a.hi - a.lo, kWin);
-  if (nwin == 0 && blockIdx.x == 0 && threadIdx.x == 0 && a.out.mode == WIN_SPARSE) {
-    if (a.out.n) *a.out.n = 0;
-    if (a.out.n2) *a.out.n2 = 0;
-  }
   while (true) {
     const uint32_t w = next_ticket(a.ctr, &s_ticket);
     if (w >= nwin) break;
@@ -144,8 +188,7 @@ cudaError_t launch_window(const WindowArgs& a, cudaStream_t s) {
   static bool attr = false;
   const size_t smem = win_smem_bytes(a.nsrc);
   if (!attr) {
-    cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)win_smem_bytes(kMaxRanks));
+    cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem_bytes(kMaxRanks));
     attr = true;
   }
   const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
@@ -157,55 +200,37 @@ cudaError_t launch_window(const WindowArgs& a, cudaStream_t s) {
 }
 
 // ===========================================================================
-// recursive doubling (§5.3.1): push of the input, then one kernel per stage
+// recursive doubling (§5.3.1): push of the input, one kernel per stage
 // ===========================================================================
 __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
-  uint32_t* di = reinterpret_cast<uint32_t*>(a.dst.base);
-  float* dv = reinterpret_cast<float*>(a.dst.base + a.dst.val_off);
+  const uint32_t seq = a.ctl->seq;
+  const int par = seq & 1;
+  uint32_t* di = reinterpret_cast<uint32_t*>(a.dst[par].base);
+  float* dv = reinterpret_cast<float*>(a.dst[par].base + a.dst[par].val_off);
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride) {
     const uint32_t x = a.idx[e];
     const float v = a.val[e];
     di[e] = x;
     dv[e] = v;
-    if (a.validate) {
-      if (x >= a.N || (e + 1 < a.n && a.idx[e + 1] <= x)) atomicOr(&a.ctl->status, 1u << SPARCML_ERR_UNSORTED);
-      if (!isfinite(v)) atomicOr(&a.ctl->status, 1u << SPARCML_ERR_NONFINITE);
-    }
+    if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *a.dst_n = a.n;
-    *a.dst_dense = 0;
-    *a.dst_ksum = a.n;
+  if (last_block<true>(&a.ctl->done_ctr[0]) && threadIdx.x == 0) {
+    a.peer->rd_n[par][1] = a.n;
+    a.peer->rd_dense[par][1] = 0;
+    a.peer->rd_ksum[par][1] = a.n;
     a.ctl->rd_sent[0] = 8 * a.n;
+    st_release_sys(&a.peer->rd_flag[par][1], seq + 1);
   }
 }
 
 cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s) {
-  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads,
-                                                                    (uint64_t)device_sm_count() * 8));
+  const uint64_t blocks =
+      std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, (uint64_t)device_sm_count() * 8));
   SPARCML_PROF("rd_push", s);
   rd_push_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
-}
-
-__device__ __forceinline__ void write_header(sparcml_header* h, uint32_t repr, uint64_t nnz, uint64_t N,
-                                             uint64_t ksum, uint64_t sent, uint64_t recv, uint32_t algo,
-                                             uint32_t status_bits, uint64_t val_offset) {
-  uint32_t st = 0;
-  for (uint32_t b = 1; b < 32; ++b)
-    if (status_bits & (1u << b)) { st = b; break; }
-  h->magic = SPARCML_HEADER_MAGIC;
-  h->repr = repr;
-  h->nnz = nnz;
-  h->N = N;
-  h->k_sum = ksum;
-  h->bytes_sent = sent;
-  h->bytes_recv = recv;
-  h->algo_used = algo;
-  h->status = st;
-  h->val_offset = val_offset;
 }
 
 __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
@@ -213,48 +238,55 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   __shared__ uint32_t s_ticket, s_gen;
   __shared__ WinSource s_src[2];
   const int tid = threadIdx.x;
-  const uint64_t an = a.a_n_dev ? *a.a_n_dev : a.a_n;
-  const uint32_t ad = a.a_dense_dev ? *a.a_dense_dev : 0u;
-  const uint64_t aks = a.a_ksum_dev ? *a.a_ksum_dev : a.a_n;
-  const uint64_t bn = *a.b_n_dev;
-  const uint32_t bd = *a.b_dense_dev;
-  const uint64_t bks = *a.b_ksum_dev;
+  Ctrl* ctl = a.ctl;
+  const uint32_t seq = ctl->seq;
+  const int par = seq & 1, t = a.stage;
+  if (tid == 0) wait_flag_geq(&ctl->rd_flag[par][t], seq + 1);   // the partner's stream is in place
+  __syncthreads();
+  const int cp = (t - 1) & 1;   // cur buffer holding my stage t-1 output
+  const uint32_t* a_idx = a.a_from_cur ? reinterpret_cast<const uint32_t*>(a.cur[cp].base) : a.a_idx;
+  const float* a_val = a.a_from_cur ? reinterpret_cast<const float*>(a.cur[cp].base + a.cur[cp].val_off) : a.a_val;
+  const uint64_t an = a.a_from_cur ? *(volatile uint64_t*)&ctl->own_n[cp] : a.a_n;
+  const uint32_t ad = a.a_from_cur ? *(volatile uint32_t*)&ctl->own_dense[cp] : 0u;
+  const uint64_t aks = a.a_from_cur ? *(volatile uint64_t*)&ctl->own_ksum[cp] : a.a_n;
+  const uint64_t bn = *(volatile uint64_t*)&ctl->rd_n[par][t];
+  const uint32_t bd = *(volatile uint32_t*)&ctl->rd_dense[par][t];
+  const uint64_t bks = *(volatile uint64_t*)&ctl->rd_ksum[par][t];
+  const StreamBuf b = a.b[par];
+  const StreamBuf o = a.o_cur ? a.cur[t & 1] : a.o;
+  const StreamBuf m = a.mpeer ? a.m[par] : StreamBuf{nullptr, 0};
   // dense switch: upper bound |H1|+|H2| > delta; once dense, dense
   const bool sparse_out = !ad && !bd && (an + bn <= a.delta);
   if (tid == 0) s_gen = a.ctr->gen;
-  const uint32_t* b_idx = reinterpret_cast<const uint32_t*>(a.b.base);
-  const float* b_val = reinterpret_cast<const float*>(a.b.base + a.b.val_off);
+  const uint32_t* b_idx = reinterpret_cast<const uint32_t*>(b.base);
+  const float* b_val = reinterpret_cast<const float*>(b.base + b.val_off);
   if (sparse_out) {
     MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem);
-    MergeOutput o;
-    o.idx = reinterpret_cast<uint32_t*>(a.o.base);
-    o.val = reinterpret_cast<float*>(a.o.base + a.o.val_off);
-    o.n = a.o_n_dev;
-    o.idx2 = a.m.base ? reinterpret_cast<uint32_t*>(a.m.base) : nullptr;
-    o.val2 = a.m.base ? reinterpret_cast<float*>(a.m.base + a.m.val_off) : nullptr;
-    o.n2 = a.m.base ? a.m_n_dev : nullptr;
+    MergeOutput mo;
+    mo.idx = reinterpret_cast<uint32_t*>(o.base);
+    mo.val = reinterpret_cast<float*>(o.base + o.val_off);
+    mo.n = &ctl->own_n[t & 1];
+    mo.idx2 = m.base ? reinterpret_cast<uint32_t*>(m.base) : nullptr;
+    mo.val2 = m.base ? reinterpret_cast<float*>(m.base + m.val_off) : nullptr;
+    mo.n2 = nullptr;
     __syncthreads();
     const uint32_t total = (uint32_t)ceil_div(an + bn, kMergeTile);
-    if (total == 0 && blockIdx.x == 0 && tid == 0) {
-      if (o.n) *o.n = 0;
-      if (o.n2) *o.n2 = 0;
-    }
+    if (total == 0 && blockIdx.x == 0 && tid == 0) ctl->own_n[t & 1] = 0;
     while (true) {
-      const uint32_t t = next_ticket(a.ctr, &s_ticket);
-      if (t >= total) break;
-      merge_tile(a.a_idx, a.a_val, an, b_idx, b_val, bn, (uint64_t)t * kMergeTile, sm, a.status, t, 0,
-                 s_gen, o);
+      const uint32_t tk = next_ticket(a.ctr, &s_ticket);
+      if (tk >= total) break;
+      merge_tile(a_idx, a_val, an, b_idx, b_val, bn, (uint64_t)tk * kMergeTile, sm, a.status, tk, 0, s_gen, mo);
     }
   } else {
     // densify: window over [0, N) with the two streams (sparse or dense)
     if (tid == 0) {
-      s_src[0].idx = a.a_idx;
-      s_src[0].val = ad ? reinterpret_cast<const float*>(a.a_idx) : a.a_val;
+      s_src[0].idx = a_idx;
+      s_src[0].val = ad ? reinterpret_cast<const float*>(a_idx) : a_val;
       s_src[0].n = an;
       s_src[0].dense = (int)ad;
       s_src[0].dense_base = 0;
       s_src[1].idx = b_idx;
-      s_src[1].val = bd ? reinterpret_cast<const float*>(a.b.base) : b_val;
+      s_src[1].val = bd ? reinterpret_cast<const float*>(b.base) : b_val;
       s_src[1].n = bn;
       s_src[1].dense = (int)bd;
       s_src[1].dense_base = 0;
@@ -264,46 +296,51 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     ts.n = 1;
     ts.dst[0] = 0;
     ts.src[0] = 1;
-    WinOutput o = {};
-    o.mode = WIN_DENSE;
-    o.dense = reinterpret_cast<float*>(a.o.base);
-    o.dense2 = a.m.base ? reinterpret_cast<float*>(a.m.base) : nullptr;
-    o.dense_base = 0;
+    WinOutput wo = {};
+    wo.mode = WIN_DENSE;
+    wo.dense = reinterpret_cast<float*>(o.base);
+    wo.dense2 = m.base ? reinterpret_cast<float*>(m.base) : nullptr;
+    wo.dense_base = 0;
     const uint32_t nwin = (uint32_t)ceil_div(a.N, kWin);
     while (true) {
       const uint32_t w = next_ticket(a.ctr, &s_ticket);
       if (w >= nwin) break;
-      window_tile(s_src, 2, ts, 0, a.N, w, smem, a.status, s_gen, nwin, o);
+      window_tile(s_src, 2, ts, 0, a.N, w, smem, a.status, s_gen, nwin, wo);
     }
   }
+  // every block fences its (remote) stores before the last block publishes the
+  // stream metadata and the partner's flag
+  __syncthreads();
+  if (tid == 0) fence_acq_rel_sys();
   if (scan_block_exit_last(a.ctr) && tid == 0) {
-    __threadfence();
-    const uint64_t on = sparse_out ? *(volatile uint64_t*)a.o_n_dev : a.N;
+    fence_acq_rel_sys();
+    const uint64_t on = sparse_out ? *(volatile uint64_t*)&ctl->own_n[t & 1] : a.N;
     const uint64_t ksum = aks + bks;
     const uint64_t obytes = sparse_out ? 8 * on : 4 * a.N;
     const uint64_t bbytes = bd ? 4 * a.N : 8 * bn;
-    *a.o_n_dev = on;
-    *a.o_dense_dev = sparse_out ? 0u : 1u;
-    *a.o_ksum_dev = ksum;
-    Ctrl* ctl = a.ctl;
-    ctl->rd_recv[a.stage - 1] = bbytes;
-    if (a.m.base) {
-      *a.m_n_dev = on;
-      *a.m_dense_dev = sparse_out ? 0u : 1u;
-      *a.m_ksum_dev = ksum;
-      ctl->rd_sent[a.stage] = obytes;
+    ctl->own_n[t & 1] = on;
+    ctl->own_dense[t & 1] = sparse_out ? 0u : 1u;
+    ctl->own_ksum[t & 1] = ksum;
+    ctl->rd_recv[t - 1] = bbytes;
+    if (a.mpeer) {
+      a.mpeer->rd_n[par][t + 1] = on;
+      a.mpeer->rd_dense[par][t + 1] = sparse_out ? 0u : 1u;
+      a.mpeer->rd_ksum[par][t + 1] = ksum;
+      ctl->rd_sent[t] = obytes;
+      st_release_sys(&a.mpeer->rd_flag[par][t + 1], seq + 1);
     }
     if (a.last && a.hdr) {
       uint64_t sent = 0, recv = 0;
-      for (int t = 0; t < a.stage; ++t) {
-        sent += ctl->rd_sent[t];
-        recv += ctl->rd_recv[t];
+      for (int i = 0; i < t; ++i) {
+        sent += ctl->rd_sent[i];
+        recv += ctl->rd_recv[i];
       }
       write_header(a.hdr, sparse_out ? SPARCML_REPR_SPARSE : SPARCML_REPR_DENSE, on, a.N, ksum, sent, recv,
                    SPARCML_SSAR_RECURSIVE_DOUBLE, ctl->status,
-                   sparse_out ? (uint64_t)((char*)a.o.base + a.o.val_off - (char*)a.hdr)
-                              : (uint64_t)SPARCML_HEADER_BYTES);
+                   sparse_out ? (uint64_t)((char*)o.base + o.val_off - (char*)a.hdr) : (uint64_t)SPARCML_HEADER_BYTES);
       ctl->status = 0;
+      __threadfence();
+      ctl->seq = seq + 1;   // the call is complete on this rank
     }
   }
 }
@@ -323,16 +360,26 @@ cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
 }
 
 // ===========================================================================
-// split phase (§5.3.2): slice by partition, push each slice to its
-// owner's receive region over NVLink
+// split phase (§5.3.2): slice by partition, push every slice and its
+// window-offset table into the owner's receive region over NVLink, then flag
 // ===========================================================================
 constexpr int kPushItems = 4;
 
 __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
   __shared__ uint64_t s_off[kMaxRanks + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // slice boundaries: first position with idx >= b_j (P binary searches)
-  for (int j = warp; j <= a.P; j += kWarps) {
+  const uint64_t base = (uint64_t)blockIdx.x * kThreads * kPushItems;
+  const uint64_t last = std::min<uint64_t>(a.n, base + (uint64_t)kThreads * kPushItems) - 1;
+  const uint64_t part = a.bnd[1];   // floor(N/P); owner(x) = min(x / part, P - 1)
+  // slice boundaries s_off[j] = first position with idx >= b_j: block 0 needs
+  // all of them (counts, empty slices), the others only those of the owners
+  // their element range touches (usually two searches)
+  int j0 = 0, j1 = a.P;
+  if (blockIdx.x != 0 && a.n > 0) {
+    j0 = (int)std::min<uint64_t>(a.idx[base] / part, a.P - 1);
+    j1 = (int)std::min<uint64_t>(a.idx[last] / part, a.P - 1) + 1;
+  }
+  for (int j = j0 + warp; j <= j1; j += kWarps) {
     uint64_t o;
     if (j == 0) o = 0;
     else if (j == a.P) o = a.n;
@@ -340,29 +387,45 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
     if (lane == 0) s_off[j] = o;
   }
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * kThreads * kPushItems;
 #pragma unroll
   for (int i = 0; i < kPushItems; ++i) {
     const uint64_t e = base + (uint64_t)i * kThreads + tid;
     if (e < a.n) {
       const uint32_t x = a.idx[e];
       const float v = a.val[e];
-      int j = 0;
-      while (j + 1 < a.P && e >= s_off[j + 1]) ++j;
+      const int j = (int)std::min<uint64_t>(x / part, a.P - 1);
       const uint64_t p = e - s_off[j];
       a.dst_idx[j][p] = x;
       a.dst_val[j][p] = v;
-      if (a.validate) {
-        if (x >= a.N || (e + 1 < a.n && a.idx[e + 1] <= x)) atomicOr(&a.ctl->status, 1u << SPARCML_ERR_UNSORTED);
-        if (!isfinite(v)) atomicOr(&a.ctl->status, 1u << SPARCML_ERR_NONFINITE);
+      // window-offset table: win[w] = first slice position whose window >= w
+      const uint64_t lo = a.bnd[j];
+      const int64_t w = (int64_t)((x - lo) / kWin);
+      const int64_t wprev = p == 0 ? -1 : (int64_t)((a.idx[e - 1] - lo) / kWin);
+      for (int64_t q = wprev + 1; q <= w; ++q) a.dst_win[j][q] = (uint32_t)p;
+      if (e + 1 == s_off[j + 1]) {   // last element of the slice
+        const int64_t nwin = (int64_t)ceil_div(a.bnd[j + 1] - lo, kWin);
+        for (int64_t q = w + 1; q <= nwin; ++q) a.dst_win[j][q] = (uint32_t)(p + 1);
       }
+      if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
     }
   }
-  if (blockIdx.x == 0 && tid < a.P) {
-    const uint64_t c = s_off[tid + 1] - s_off[tid];
-    *a.dst_cnt[tid] = c;
-    *a.dst_k[tid] = a.n;
-    a.ctl->slice_out[tid] = c;
+  if (blockIdx.x == 0) {
+    // empty slices: their whole table is zero
+    for (int j = 0; j < a.P; ++j) {
+      if (s_off[j + 1] != s_off[j]) continue;
+      const uint64_t nwin = ceil_div(a.bnd[j + 1] - a.bnd[j], kWin);
+      for (uint64_t q = tid; q <= nwin; q += kThreads) a.dst_win[j][q] = 0;
+    }
+    if (tid < a.P) {
+      const uint64_t c = s_off[tid + 1] - s_off[tid];
+      a.peer[tid]->slice_cnt[a.rank] = c;
+      a.peer[tid]->k_in[a.rank] = a.n;
+      a.ctl->slice_out[tid] = c;
+    }
+  }
+  if (last_block<true>(&a.ctl->done_ctr[0]) && tid < a.P) {
+    const uint32_t seq = a.ctl->seq;
+    st_release_sys(&a.peer[tid]->src_done[a.rank], seq + 1);
   }
 }
 
@@ -376,109 +439,220 @@ cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s) {
 }
 
 // ===========================================================================
-// flag barrier over NVLink (one warp); optional SSAR/DSAR decision after it
+// owner reduction (one cooperative kernel): the P slices of my partition are
+// reduced window by window in the canonical tree order (R-8).  SSAR: each
+// window is compacted into a staging slot, one grid sync gives every window
+// its output offset, a copy makes the partition result contiguous.  DSAR: each
+// window is densified and QSGD-encoded in place (§5.3.3 + §6, fused).
 // ===========================================================================
-struct BarrierDecide {
-  int enabled;
-  DecideArgs d;
-};
+__host__ __device__ constexpr size_t owner_smem_bytes(int nsrc) {
+  return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)nsrc;
+}
 
-__global__ void barrier_kernel(BarrierArgs a, BarrierDecide dec) {
-  const int lane = threadIdx.x;
-  uint32_t e = 0;
-  if (lane == 0) {
-    e = a.my->epoch + 1;
-    a.my->epoch = e;
-    if (a.first_in_call) a.my->call_count = a.my->call_count + 1;
-  }
-  e = __shfl_sync(0xffffffffu, e, 0);
-  __threadfence_system();
-  if (!a.loopback && lane < a.P && lane != a.rank) {
-    st_release_sys(a.peer_flags[lane], e);
-    while ((int)(ld_acquire_sys(&a.my->flags[lane]) - e) < 0) {
-    }
-  }
-  __syncwarp();
-  __threadfence_system();
-  if (dec.enabled && lane == 0) {
-    uint64_t ks = 0;
-    for (int i = 0; i < dec.d.P; ++i) ks += *(volatile const uint64_t*)&dec.d.k_in[i];
+__global__ void __launch_bounds__(kThreads) owner_kernel(OwnerArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
+  float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
+  __shared__ uint32_t s_rng[kMaxRanks][2];
+  __shared__ uint32_t s_epre[kMaxRanks + 1];
+  __shared__ uint32_t s_scan[kWarps + 1];
+  __shared__ uint32_t s_bmax[kWin / 8];
+  __shared__ uint64_t s_sum[kWarps + 1];
+  __shared__ uint32_t s_dsar;
+  __shared__ uint64_t s_base;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, P = a.P;
+  Ctrl* ctl = a.ctl;
+  const uint32_t seq = ctl->seq;
+  if (a.wait && tid == 0)
+    for (int i = 0; i < P; ++i) wait_flag_geq(&ctl->src_done[i], seq + 1);
+  __syncthreads();
+  if (tid == 0) {
     uint32_t dsar;
-    if (dec.d.algo == SPARCML_DSAR_SPLIT_ALLGATHER) dsar = 1;
-    else if (dec.d.algo == SPARCML_SSAR_SPLIT_ALLGATHER) dsar = 0;
-    else dsar = ks > dec.d.delta ? 1u : 0u;   // AUTO: upper bound sum k_i > delta (R-5)
-    *dec.d.dsar_out = dsar;
-    *dec.d.k_sum_out = ks;
-  }
-}
-
-cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
-  BarrierDecide d = {};
-  SPARCML_PROF("barrier", s);
-  barrier_kernel<<<1, 32, 0, s>>>(a, d);
-  ++g_launches;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_barrier_decide(const BarrierArgs& a, const DecideArgs& da, cudaStream_t s) {
-  BarrierDecide d;
-  d.enabled = 1;
-  d.d = da;
-  SPARCML_PROF("barrier", s);
-  barrier_kernel<<<1, 32, 0, s>>>(a, d);
-  ++g_launches;
-  return cudaGetLastError();
-}
-
-// P == 1: the collective is the identity on the stream (or its densified /
-// QSGD-coded form); validate and fill the control block the concat reads.
-__global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
-  if (a.validate) {
-    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride) {
-      const uint32_t x = a.idx[e];
-      if (x >= a.N || (e + 1 < a.n && a.idx[e + 1] <= x)) atomicOr(&a.ctl->status, 1u << SPARCML_ERR_UNSORTED);
-      if (!isfinite(a.val[e])) atomicOr(&a.ctl->status, 1u << SPARCML_ERR_NONFINITE);
+    uint64_t ks = 0;
+    for (int i = 0; i < P; ++i) ks += *(volatile uint64_t*)&ctl->k_in[i];
+    if (a.host_dsar >= 0) dsar = (uint32_t)a.host_dsar;
+    else if (a.algo == SPARCML_DSAR_SPLIT_ALLGATHER) dsar = 1;
+    else if (a.algo == SPARCML_SSAR_SPLIT_ALLGATHER) dsar = 0;
+    else dsar = ks > a.delta ? 1u : 0u;   // AUTO: upper bound sum k_i > delta (R-5)
+    s_dsar = dsar;
+    if (blockIdx.x == 0) {
+      ctl->dsar = dsar;
+      ctl->k_sum = ks;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    Ctrl* c = a.ctl;
-    c->k_in[0] = a.n;
-    c->slice_cnt[0] = a.n;
-    c->slice_out[0] = a.n;
-    c->owner_K = a.n;
-    c->k_sum = a.n;
-    if (a.algo == SPARCML_DSAR_SPLIT_ALLGATHER) c->dsar = 1;
-    else if (a.algo == SPARCML_SSAR_SPLIT_ALLGATHER || a.algo == SPARCML_SSAR_RECURSIVE_DOUBLE) c->dsar = 0;
-    else c->dsar = a.n > a.delta ? 1u : 0u;
+  __syncthreads();
+  const bool dsar = s_dsar != 0;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint64_t nwin = ceil_div(a.hi - a.lo, kWin);
+  const uint64_t w0 = nwin * b / G, w1 = nwin * (b + 1) / G;
+  uint64_t my_total = 0;
+  for (uint64_t w = w0; w < w1; ++w) {
+    const uint64_t wlo = a.lo + w * kWin;
+    const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
+    if (tid < P) {
+      s_rng[tid][0] = a.src_win[tid][w];
+      s_rng[tid][1] = a.src_win[tid][w + 1];
+    }
+#pragma unroll
+    for (int i = 0; i < kWinPerThread; ++i) pres[tid + i * kThreads] = 0u;
+    __syncthreads();
+    if (tid == 0) {   // element prefix over the sources
+      uint32_t run = 0;
+      for (int s = 0; s < P; ++s) {
+        s_epre[s] = run;
+        run += s_rng[s][1] - s_rng[s][0];
+      }
+      s_epre[P] = run;
+    }
+    __syncthreads();
+    // all sources' elements of this window at once: one load latency per window
+    for (uint32_t u = tid; u < s_epre[P]; u += kThreads) {
+      int s = 0;
+      while (u >= s_epre[s + 1]) ++s;
+      const uint32_t e = s_rng[s][0] + (u - s_epre[s]);
+      const uint32_t pos = a.src_idx[s][e] - (uint32_t)wlo;
+      if (pos < (uint32_t)wn) {
+        vals[s * kWin + pos] = a.src_val[s][e];
+        atomicOr(&pres[pos], 1u << s);
+      }
+    }
+    __syncthreads();
+    const int p0 = tid * kWinPerThread;
+    float r[kWinPerThread];
+    uint32_t present = 0;
+#pragma unroll
+    for (int i = 0; i < kWinPerThread; ++i) {
+      const int p = p0 + i;
+      uint32_t m = (p < wn) ? pres[p] : 0u;
+      for (int q = 0; q < a.sched.n; ++q) {
+        const int d = a.sched.dst[q], s = a.sched.src[q];
+        if (m & (1u << s)) {
+          if (m & (1u << d)) {
+            vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[s * kWin + p]);
+          } else {
+            vals[d * kWin + p] = vals[s * kWin + p];
+            m |= 1u << d;
+          }
+        }
+      }
+      r[i] = (m & 1u) ? vals[p] : 0.0f;
+      if (m & 1u) present |= 1u << i;
+    }
+    if (!dsar) {
+      uint32_t total;
+      const uint32_t off = block_exclusive_sum<uint32_t>(__popc(present), s_scan, &total);
+      uint32_t* si = a.st_idx + w * kWin;
+      float* sv = a.st_val + w * kWin;
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < kWinPerThread; ++i)
+        if (present & (1u << i)) {
+          si[off + c] = (uint32_t)(wlo + p0 + i);
+          sv[off + c] = r[i];
+          ++c;
+        }
+      if (tid == 0) a.win_cnt[w] = total;
+      my_total += total;
+    } else if (a.bits) {
+      const uint64_t e = w * kWin + p0;   // partition-relative
+      const int rem = wn - p0;
+      const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+      qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
+    } else {
+      float* d = a.dense + w * kWin + p0;
+      for (int i = 0; i < kWinPerThread && p0 + i < wn; ++i) d[i] = r[i];
+    }
+    __syncthreads();
+  }
+  if (!dsar) {
+    if (tid == 0) a.blk[b] = my_total;
+    grid.sync();
+    uint64_t v = 0;
+    for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&a.blk[j]));
+    uint64_t tot;
+    block_exclusive_sum<uint64_t>(v, s_sum, &tot);
+    if (tid == 0) s_base = tot;
+    __syncthreads();
+    uint64_t run = s_base;
+    for (uint64_t w = w0; w < w1; ++w) {
+      const uint32_t n = __ldcg(&a.win_cnt[w]);
+      const uint32_t* si = a.st_idx + w * kWin;
+      const float* sv = a.st_val + w * kWin;
+      for (uint32_t i = tid; i < n; i += kThreads) {
+        a.r_idx[run + i] = si[i];
+        a.r_val[run + i] = sv[i];
+      }
+      run += n;
+    }
+    if (b == G - 1 && tid == 0) ctl->owner_K = run;
+  }
+  grid.sync();
+  if (b == 0 && tid < P) {
+    fence_acq_rel_sys();
+    st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
   }
 }
 
-cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
-  const uint64_t blocks = a.validate ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 1024)) : 1;
-  SPARCML_PROF("p1_prep", s);
-  p1_prep_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+static int owner_occupancy(int nsrc) {
+  static int cache[kMaxRanks + 1] = {0};
+  if (!cache[nsrc]) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, owner_kernel, kThreads, owner_smem_bytes(nsrc));
+    cache[nsrc] = std::max(1, per);
+  }
+  return cache[nsrc];
+}
+
+cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(owner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)owner_smem_bytes(kMaxRanks));
+    attr = true;
+  }
+  const size_t smem = owner_smem_bytes(a.P);
+  const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
+  const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)owner_occupancy(a.P) * device_sm_count()));
+  OwnerArgs ac = a;
+  void* args[] = {(void*)&ac};
+  SPARCML_PROF("owner", s);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_kernel, dim3((unsigned)G), dim3(kThreads), args, smem, s);
   ++g_launches;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
+
+int owner_grid_size() { return device_sm_count() * 8; }
 
 // ===========================================================================
 // allgather phase (§5.3.2 P:757-758 / §5.3.3): pull every owner's
-// partition result over NVLink into the caller's out (concatenation,
-// densification, or QSGD decode), then write the header
+// partition result over NVLink straight into the caller's out (sparse
+// concatenation, densification, or QSGD decode), then write the header
 // ===========================================================================
 __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t s_pref[kMaxRanks + 1];
+  __shared__ uint64_t s_upref[kMaxRanks + 1];
   __shared__ uint32_t s_dsar;
-  __shared__ uint32_t s_gen;
   __shared__ WinSource s_src[1];
   const int tid = threadIdx.x;
+  Ctrl* ctl = a.ctl;
+  const uint32_t seq = ctl->seq;
+  __shared__ uint64_t s_k[kMaxRanks];
+  if (tid < a.P) {   // one lane per owner: wait for its flag, read its result size
+    if (a.wait_owners) wait_flag_geq(&ctl->owner_done[tid], seq + 1);
+    s_k[tid] = *(volatile const uint64_t*)a.r_n[tid];
+  }
+  __syncthreads();
   if (tid == 0) {
-    s_dsar = a.ctl->dsar;
+    s_dsar = *(volatile uint32_t*)&ctl->dsar;
     s_pref[0] = 0;
-    for (int j = 0; j < a.P; ++j) s_pref[j + 1] = s_pref[j] + (s_dsar ? 0 : *(volatile const uint64_t*)a.r_n[j]);
-    s_gen = a.ctr->gen;
+    s_upref[0] = 0;
+    for (int j = 0; j < a.P; ++j) {
+      const uint64_t kj = s_dsar ? 0 : s_k[j];
+      s_pref[j + 1] = s_pref[j] + kj;
+      s_upref[j + 1] = s_upref[j] + ceil_div(kj, 4);
+    }
   }
   __syncthreads();
   const bool dsar = s_dsar != 0;
@@ -510,12 +684,11 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
         else if (cnt == 8 && a.bits == 8) word = *reinterpret_cast<const unsigned long long*>(cp);
         else if (cnt == 8 && a.bits == 2) word = *reinterpret_cast<const uint16_t*>(cp);
         else
-          for (int b = 0; b < nbytes; ++b) word |= (uint64_t)cp[b] << (8 * b);
+          for (int q = 0; q < nbytes; ++q) word |= (uint64_t)cp[q] << (8 * q);
         const float scale = a.r_scales[j][e / a.bucket];
         const uint32_t mask = (1u << a.bits) - 1u;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          v[i] = qsgd_decode((uint32_t)(word >> (i * a.bits)) & mask, scale, s, a.bits);
+        for (int i = 0; i < 8; ++i) v[i] = qsgd_decode((uint32_t)(word >> (i * a.bits)) & mask, scale, s, a.bits);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = i < cnt ? a.r_dense[j][e + i] : 0.0f;
@@ -529,13 +702,32 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
       }
     }
   } else if (K <= a.delta) {
-    // sparse concatenation: disjoint ranges, globally sorted by construction (P:511-515)
-    for (uint64_t o = gtid; o < K; o += gstride) {
+    // sparse concatenation: disjoint ranges, globally sorted by construction
+    // (P:511-515).  Units of 4 pairs of one owner: 16-byte loads over NVLink.
+    const uint64_t units = s_upref[a.P];
+    for (uint64_t u = gtid; u < units; u += gstride) {
       int j = 0;
-      while (o >= s_pref[j + 1]) ++j;
-      const uint64_t p = o - s_pref[j];
-      out_idx[o] = a.r_idx[j][p];
-      out_val[o] = a.r_val[j][p];
+      while (u >= s_upref[j + 1]) ++j;
+      const uint64_t p = (u - s_upref[j]) * 4;
+      const uint64_t kj = s_pref[j + 1] - s_pref[j];
+      const uint64_t o = s_pref[j] + p;
+      if (p + 4 <= kj) {
+        const uint4 ix = *reinterpret_cast<const uint4*>(a.r_idx[j] + p);
+        const float4 vx = *reinterpret_cast<const float4*>(a.r_val[j] + p);
+        out_idx[o] = ix.x;
+        out_idx[o + 1] = ix.y;
+        out_idx[o + 2] = ix.z;
+        out_idx[o + 3] = ix.w;
+        out_val[o] = vx.x;
+        out_val[o + 1] = vx.y;
+        out_val[o + 2] = vx.z;
+        out_val[o + 3] = vx.w;
+      } else {
+        for (uint64_t q = p; q < kj; ++q) {
+          out_idx[s_pref[j] + q] = a.r_idx[j][q];
+          out_val[s_pref[j] + q] = a.r_val[j][q];
+        }
+      }
     }
   } else {
     // K > delta cannot be stored sparse: densify partition by partition
@@ -557,17 +749,17 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
       __syncthreads();
       const uint32_t nwin = (uint32_t)ceil_div(a.bnd[j + 1] - a.bnd[j], kWin);
       for (uint32_t w = blockIdx.x; w < nwin; w += gridDim.x)
-        window_tile(s_src, 1, ts, a.bnd[j], a.bnd[j + 1], w, smem, a.status, s_gen, nwin, wo);
+        window_tile(s_src, 1, ts, a.bnd[j], a.bnd[j + 1], w, smem, a.status, 0, nwin, wo);
       __syncthreads();
     }
   }
-  if (scan_block_exit_last(a.ctr) && tid == 0) {
+  if (last_block<false>(&ctl->done_ctr[2]) && tid == 0) {
     // bytes this rank put on / took off NVLink (pull model counted at the owner)
     uint64_t sent = 0, recv = 0;
     for (int j = 0; j < a.P; ++j) {
       if (j == a.rank) continue;
-      sent += 8 * a.ctl->slice_out[j];
-      recv += 8 * a.ctl->slice_cnt[j];
+      sent += 8 * ctl->slice_out[j];
+      recv += 8 * ctl->slice_cnt[j];
     }
     for (int j = 0; j < a.P; ++j) {
       uint64_t w;
@@ -577,13 +769,12 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
       if (j == a.rank) sent += (uint64_t)(a.P - 1) * w;
       else recv += w;
     }
-    Ctrl* ctl = a.ctl;
-    const uint32_t st = ctl->status;
     write_header(reinterpret_cast<sparcml_header*>(a.out), dense_result ? SPARCML_REPR_DENSE : SPARCML_REPR_SPARSE,
-                 dense_result ? a.N : K, a.N, ctl->k_sum, sent, recv,
-                 dsar ? SPARCML_DSAR_SPLIT_ALLGATHER : a.algo, st,
-                 dense_result ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset);
+                 dense_result ? a.N : K, a.N, ctl->k_sum, sent, recv, dsar ? SPARCML_DSAR_SPLIT_ALLGATHER : a.algo,
+                 ctl->status, dense_result ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset);
     ctl->status = 0;
+    __threadfence();
+    ctl->seq = seq + 1;   // the call is complete on this rank
   }
 }
 
@@ -597,6 +788,64 @@ cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
   const int grid = device_sm_count() * 4;
   SPARCML_PROF("concat", s);
   concat_kernel<<<grid, kThreads, smem, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ===========================================================================
+// flag barrier over NVLink (one warp): sparcml_barrier
+// ===========================================================================
+__global__ void barrier_kernel(BarrierArgs a) {
+  const int lane = threadIdx.x;
+  uint32_t e = 0;
+  if (lane == 0) {
+    e = a.my->epoch + 1;
+    a.my->epoch = e;
+  }
+  e = __shfl_sync(0xffffffffu, e, 0);
+  fence_acq_rel_sys();
+  if (!a.loopback && lane < a.P && lane != a.rank) {
+    st_release_sys(a.peer_flags[lane], e);
+    while ((int)(ld_acquire_sys(&a.my->flags[lane]) - e) < 0) {
+    }
+  }
+  __syncwarp();
+  fence_acq_rel_sys();
+}
+
+cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
+  SPARCML_PROF("barrier", s);
+  barrier_kernel<<<1, 32, 0, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// P == 1: the collective is the identity on the stream (or its densified /
+// QSGD-coded form); validate and fill the control block the concat reads.
+__global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
+  if (a.validate) {
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride)
+      check_input(a.idx, e, a.n, a.N, a.idx[e], a.val[e], &a.ctl->status);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    Ctrl* c = a.ctl;
+    c->k_in[0] = a.n;
+    c->slice_cnt[0] = a.n;
+    c->slice_out[0] = a.n;
+    c->owner_K = a.n;
+    c->k_sum = a.n;
+    if (a.algo == SPARCML_DSAR_SPLIT_ALLGATHER) c->dsar = 1;
+    else if (a.algo == SPARCML_SSAR_SPLIT_ALLGATHER || a.algo == SPARCML_SSAR_RECURSIVE_DOUBLE) c->dsar = 0;
+    else c->dsar = a.n > a.delta ? 1u : 0u;
+  }
+}
+
+cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
+  const uint64_t blocks =
+      a.validate ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 1024)) : 1;
+  SPARCML_PROF("p1_prep", s);
+  p1_prep_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }

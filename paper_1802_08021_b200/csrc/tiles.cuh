@@ -190,6 +190,7 @@ struct WinOutput {
 // Dynamic shared memory: pres[kWin] | vals[nsrc][kWin] | misc
 struct WinMisc {
   uint64_t rng[kMaxRanks][2];
+  uint64_t epre[kMaxRanks + 1];
   uint32_t scan[kWarps + 1];
   uint64_t excl;
   uint32_t bmax[kWin / 8];
@@ -292,20 +293,32 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
 #pragma unroll
   for (int i = 0; i < kWinPerThread; ++i) pres[tid + i * kThreads] = 0u;
   __syncthreads();
+  // dense sources: their window values; sparse sources: all elements of all
+  // sources at once (one load latency for the window, not one per source)
   for (int s = 0; s < nsrc; ++s) {
     if (src[s].dense) {
       const float* dv = src[s].val + (wlo - src[s].dense_base);
       for (int p = tid; p < wn; p += kThreads) vals[s * kWin + p] = dv[p];
       for (int p = tid; p < wn; p += kThreads) atomicOr(&pres[p], 1u << s);
-    } else {
-      const uint64_t p0 = mc.rng[s][0], p1 = mc.rng[s][1];
-      for (uint64_t e = p0 + tid; e < p1; e += kThreads) {
-        const uint32_t pos = src[s].idx[e] - (uint32_t)wlo;
-        if (pos < (uint32_t)wn) {   // guards against unsorted (invalid) input only
-          vals[s * kWin + pos] = src[s].val[e];
-          atomicOr(&pres[pos], 1u << s);
-        }
-      }
+    }
+  }
+  if (tid == 0) {
+    uint64_t run = 0;
+    for (int s = 0; s < nsrc; ++s) {
+      mc.epre[s] = run;
+      if (!src[s].dense) run += mc.rng[s][1] - mc.rng[s][0];
+    }
+    mc.epre[nsrc] = run;
+  }
+  __syncthreads();
+  for (uint64_t u = tid; u < mc.epre[nsrc]; u += kThreads) {
+    int s = 0;
+    while (u >= mc.epre[s + 1]) ++s;
+    const uint64_t e = mc.rng[s][0] + (u - mc.epre[s]);
+    const uint32_t pos = src[s].idx[e] - (uint32_t)wlo;
+    if (pos < (uint32_t)wn) {   // guards against unsorted (invalid) input only
+      vals[s * kWin + pos] = src[s].val[e];
+      atomicOr(&pres[pos], 1u << s);
     }
   }
   __syncthreads();

@@ -148,7 +148,7 @@ def profile_read(name: str):
     return int(n.value), float(ms.value)
 
 
-PROFILED_KERNELS = ["topk", "topk_all", "split_push",
+PROFILED_KERNELS = ["topk", "topk_all", "split_push", "owner",
                     "barrier", "merge", "window", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
                     "dequantize"]
 
