@@ -142,6 +142,9 @@ sparcml_status sparcml_comm_create_local(sparcml_comm** comm_out_host, int nrank
 
 sparcml_status sparcml_comm_destroy(sparcml_comm* comm);
 int sparcml_comm_nranks(const sparcml_comm* comm);
+/* Diagnostics: device pointer of rank `rank`'s symmetric workspace (its
+ * control block first) as seen from this process; NULL if unknown. */
+const void* sparcml_comm_workspace(const sparcml_comm* comm, int rank);
 int sparcml_comm_rank(const sparcml_comm* comm);   /* -1 for a loopback world */
 const char* sparcml_last_error(const sparcml_comm* comm);  /* NULL comm: global */
 

@@ -59,6 +59,13 @@ TreeSched make_sched(int P) {
   for (size_t i = 0; i < nodes.size(); ++i) {   // post-order: children before parents
     ts.dst[i] = (uint8_t)nodes[i].lo;
     ts.src[i] = (uint8_t)nodes[i].mid;
+    ts.h[i] = (uint8_t)nodes[i].height;
+    ts.hmax = std::max(ts.hmax, nodes[i].height);
+    const int hh = nodes[i].height - 1;
+    ts.role[hh][nodes[i].lo] = 1;
+    ts.part[hh][nodes[i].lo] = (uint8_t)nodes[i].mid;
+    ts.role[hh][nodes[i].mid] = 2;
+    ts.part[hh][nodes[i].mid] = (uint8_t)nodes[i].lo;
   }
   return ts;
 }
@@ -72,12 +79,13 @@ struct Layout {
   uint64_t part_cap;        // largest partition (rounded to 64)
   uint64_t cap_s;           // pairs per receive region (one per source)
   uint64_t nwin;            // windows of the largest partition
+  uint64_t ntab;            // window-offset table entries of the largest partition (kTab positions each)
   size_t status_off, n_status;
   size_t recv_off, region_bytes;
-  size_t win_off, win_bytes;            // per-source window-offset tables (nwin + 1 each)
+  size_t win_off, win_bytes;            // per-source window-offset tables (ntab + 1 each)
+  size_t stage_off;                     // owner spill area: P * cap_s pairs (SoA)
+  size_t blk_off;                       // owner per-block output counts
   size_t part_off, part_bytes, scales_off;
-  size_t stage_off;                     // owner staging: nwin * kWin pairs (SoA)
-  size_t wcnt_off, blk_off;
   size_t rd_off, rd_bytes, rd_val_off;  // cur[2] + recv[2 parities][L stages]
   size_t total;
 };
@@ -90,6 +98,7 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.part_cap = align_up(max_N / P + P, 64);
   L.cap_s = std::min<uint64_t>(max_nnz, L.part_cap);
   L.nwin = (L.part_cap + kWin - 1) / kWin;
+  L.ntab = (L.part_cap + kTab - 1) / kTab;
   size_t off = align_up(sizeof(Ctrl), 256);
   L.status_off = off;
   L.n_status = max_N / 1024 + 2 * max_nnz / kMergeTile + 256;
@@ -98,18 +107,16 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.region_bytes = align_up(8 * L.cap_s, 256);
   off += (size_t)P * L.region_bytes;
   L.win_off = off;
-  L.win_bytes = align_up(4 * (L.nwin + 1), 256);
+  L.win_bytes = align_up(4 * (L.ntab + 1), 256);
   off += (size_t)P * L.win_bytes;
+  L.stage_off = off;
+  off += align_up(8 * (size_t)P * L.cap_s, 256);
+  L.blk_off = off;
+  off += align_up(8 * 8192, 256);
   L.part_off = off;
   L.part_bytes = align_up(8 * L.part_cap + 256, 256);
   L.scales_off = off + align_up(L.part_cap + 16, 256);   // codes <= part_cap bytes (8 bits)
   off += L.part_bytes;
-  L.stage_off = off;
-  off += align_up(8 * L.nwin * kWin, 256);
-  L.wcnt_off = off;
-  off += align_up(4 * L.nwin, 256);
-  L.blk_off = off;
-  off += align_up(8 * 8192, 256);
   L.L = 0;
   const bool pow2 = (P & (P - 1)) == 0;
   if (pow2)
@@ -330,10 +337,6 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.sched = ts;
     w.r_idx = reinterpret_cast<uint32_t*>(base + L.part_off);
     w.r_val = reinterpret_cast<float*>(base + L.part_off + 4 * L.part_cap);
-    w.st_idx = reinterpret_cast<uint32_t*>(base + L.stage_off);
-    w.st_val = reinterpret_cast<float*>(base + L.stage_off + 4 * L.nwin * kWin);
-    w.win_cnt = reinterpret_cast<uint32_t*>(base + L.wcnt_off);
-    w.blk = reinterpret_cast<uint64_t*>(base + L.blk_off);
     w.dense = reinterpret_cast<float*>(base + L.part_off);
     w.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
     w.scales = reinterpret_cast<float*>(base + L.scales_off);
@@ -344,6 +347,9 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.host_dsar = cc.host_dsar;
     w.wait = 1;
     w.ctl = ctrl_of(base);
+    w.st_idx = reinterpret_cast<uint32_t*>(base + L.stage_off);
+    w.st_val = reinterpret_cast<float*>(base + L.stage_off + 4 * (size_t)P * L.cap_s);
+    w.blk = reinterpret_cast<uint64_t*>(base + L.blk_off);
     CK(c, launch_owner(w, cc.s));
   }
   for (size_t i = 0; i < R.size(); ++i) {
@@ -680,6 +686,10 @@ sparcml_status sparcml_comm_destroy(sparcml_comm* c) {
 }
 
 int sparcml_comm_nranks(const sparcml_comm* c) { return c ? c->P : 0; }
+const void* sparcml_comm_workspace(const sparcml_comm* c, int rank) {
+  if (!c || rank < 0 || rank >= (int)c->peer.size()) return nullptr;
+  return c->peer[rank];
+}
 int sparcml_comm_rank(const sparcml_comm* c) { return c ? c->rank : -1; }
 const char* sparcml_last_error(const sparcml_comm* c) {
   return c ? c->err.c_str() : g_last_error.c_str();

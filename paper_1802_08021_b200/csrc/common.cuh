@@ -18,6 +18,8 @@ constexpr int kMergeItems = 8;           // merge-path items per thread
 constexpr int kMergeTile = kThreads * kMergeItems;   // 2048 merged inputs per tile
 constexpr int kWin = 1024;               // window kernel: index positions per window
 constexpr int kWinPerThread = kWin / kThreads;       // 4
+constexpr int kTab = 256;                // window-offset table granularity (index positions)
+constexpr int kTabPerWin = kWin / kTab;  // 4
 constexpr int kMaxJobs = kMaxRanks / 2;  // batched merges per launch
 
 // ---------------------------------------------------------------------------
@@ -38,6 +40,19 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 }
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Spin loops poll with relaxed loads (an acquire load also invalidates the
+// SM's L1, which starves the other warps' LSU traffic) and order the data
+// reads with one acquire fence after the flag is seen.
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
   uint64_t v;
@@ -171,8 +186,9 @@ __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t 
     if (t >= (int64_t)first) {
       uint32_t f;
       do {
-        f = ld_acquire_gpu(&st[t].flag);
+        f = ld_relaxed_gpu_u32(&st[t].flag);
       } while ((f & ~3u) != tag || (f & 3u) == 0);
+      fence_acq_rel_gpu();
       state = f & 3u;
       v = state == 2u ? ld_relaxed_gpu(&st[t].incl) : ld_relaxed_gpu(&st[t].agg);
     }
@@ -308,7 +324,8 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
 // it; waiters compare wrap-safely against seq + 1 of their own call
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void wait_flag_geq(const uint32_t* f, uint32_t target) {
-  while ((int)(ld_acquire_sys(f) - target) < 0) __nanosleep(32);
+  while ((int)(ld_relaxed_sys_u32(f) - target) < 0) __nanosleep(32);
+  fence_acq_rel_sys();
 }
 
 constexpr int kMaxStages = 5;   // recursive doubling: log2(16) stages (+1)
@@ -343,6 +360,17 @@ struct alignas(128) Ctrl {
   uint64_t rd_sent[8];            // bytes I pushed for stage t (index t-1)
   uint64_t rd_recv[8];            // bytes I received for stage t
   ScanCounters scan[4];           // ticket counters of the tile kernels
+  uint64_t dbg[2][16];            // %globaltimer phase marks (diagnostics): block 0, last block
 };
+
+__device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {
+  // block 0: dbg[0] = %globaltimer (ns), dbg[1] = SM clock (cycles)
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    c->dbg[0][slot] = t;
+    c->dbg[1][slot] = clock64();
+  }
+}
 
 }  // namespace sparcml

@@ -101,7 +101,7 @@ struct PushArgs {
   uint64_t bnd[kMaxRanks + 1];
   uint32_t* dst_idx[kMaxRanks];    // owner j's receive region for source `rank`
   float* dst_val[kMaxRanks];
-  uint32_t* dst_win[kMaxRanks];    // owner j's window-offset table for source `rank` (nwin_j + 1)
+  uint32_t* dst_win[kMaxRanks];    // owner j's window-offset table for source `rank` (ntab_j + 1)
   Ctrl* peer[kMaxRanks];           // every rank's control block
   Ctrl* ctl;                       // mine
   int validate;
@@ -116,13 +116,9 @@ struct OwnerArgs {
   const float* src_val[kMaxRanks];
   const uint32_t* src_win[kMaxRanks];
   TreeSched sched;
-  // SSAR: compacted partition result (via per-window staging)
+  // SSAR: compacted partition result
   uint32_t* r_idx;
   float* r_val;
-  uint32_t* st_idx;                // staging: window w at [w * kWin, ...)
-  float* st_val;
-  uint32_t* win_cnt;               // per-window output counts
-  uint64_t* blk;                   // per-block totals (grid-sized)
   // DSAR: dense partition or QSGD codes + scales
   float* dense;
   uint8_t* codes;
@@ -134,6 +130,11 @@ struct OwnerArgs {
   int wait;                        // 1: wait for the sources' flags (P > 1)
   Ctrl* peer[kMaxRanks];
   Ctrl* ctl;
+  // SSAR merge path: spill area for dense block ranges (P * cap_s pairs, SoA)
+  // and per-block output counts
+  uint32_t* st_idx;
+  float* st_val;
+  uint64_t* blk;
 };
 
 struct ConcatArgs {
@@ -195,7 +196,7 @@ cudaError_t launch_window(const WindowArgs& a, cudaStream_t s);
 cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s);
 cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s);
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s);
-cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);
+cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);   // host_dsar selects merge / window
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);

@@ -397,13 +397,14 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
       const uint64_t p = e - s_off[j];
       a.dst_idx[j][p] = x;
       a.dst_val[j][p] = v;
-      // window-offset table: win[w] = first slice position whose window >= w
+      // window-offset table (kTab positions per entry): win[w] = first slice
+    // position whose table window >= w
       const uint64_t lo = a.bnd[j];
-      const int64_t w = (int64_t)((x - lo) / kWin);
-      const int64_t wprev = p == 0 ? -1 : (int64_t)((a.idx[e - 1] - lo) / kWin);
+      const int64_t w = (int64_t)((x - lo) / kTab);
+      const int64_t wprev = p == 0 ? -1 : (int64_t)((a.idx[e - 1] - lo) / kTab);
       for (int64_t q = wprev + 1; q <= w; ++q) a.dst_win[j][q] = (uint32_t)p;
       if (e + 1 == s_off[j + 1]) {   // last element of the slice
-        const int64_t nwin = (int64_t)ceil_div(a.bnd[j + 1] - lo, kWin);
+        const int64_t nwin = (int64_t)ceil_div(a.bnd[j + 1] - lo, kTab);
         for (int64_t q = w + 1; q <= nwin; ++q) a.dst_win[j][q] = (uint32_t)(p + 1);
       }
       if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
@@ -413,8 +414,8 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
     // empty slices: their whole table is zero
     for (int j = 0; j < a.P; ++j) {
       if (s_off[j + 1] != s_off[j]) continue;
-      const uint64_t nwin = ceil_div(a.bnd[j + 1] - a.bnd[j], kWin);
-      for (uint64_t q = tid; q <= nwin; q += kThreads) a.dst_win[j][q] = 0;
+      const uint64_t ntab = ceil_div(a.bnd[j + 1] - a.bnd[j], kTab);
+      for (uint64_t q = tid; q <= ntab; q += kThreads) a.dst_win[j][q] = 0;
     }
     if (tid < a.P) {
       const uint64_t c = s_off[tid + 1] - s_off[tid];
@@ -439,153 +440,533 @@ cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s) {
 }
 
 // ===========================================================================
-// owner reduction (one cooperative kernel): the P slices of my partition are
-// reduced window by window in the canonical tree order (R-8).  SSAR: each
-// window is compacted into a staging slot, one grid sync gives every window
-// its output offset, a copy makes the partition result contiguous.  DSAR: each
-// window is densified and QSGD-encoded in place (§5.3.3 + §6, fused).
+// owner reduction, SSAR (§5.3.2): the P sorted slices of my
+// partition are cut into tiles of ~kMT elements at window-table boundaries
+// (table windows are kTab positions, so one tile holds < kMT + P*kTab
+// elements).  A tile is staged in shared memory and reduced by the canonical
+// tree (R-8) one height at a time: every node of that height merges its two
+// sorted runs (left run first on equal keys, fl(left + right)) by rank
+// arithmetic -- left element i goes to i + #right<key, right element j to
+// j + #left<=key, a right duplicate dies -- then the tile is compacted.  Tiles
+// are ticketed; a decoupled look-back gives each its output offset, so the
+// partition result is written once, contiguous, with no grid-wide sync.
 // ===========================================================================
-__host__ __device__ constexpr size_t owner_smem_bytes(int nsrc) {
-  return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)nsrc;
+constexpr int kMT = 512;                  // merge tile capacity beyond one table window
+constexpr uint32_t kDead = 0xFFFFFFFFu;   // never an index: N <= 2^32 - 1
+
+__host__ __device__ constexpr int mtile_cap(int P) { return kMT + kTab * P; }
+__host__ __device__ constexpr size_t owner_merge_smem_bytes(int P) { return 16 * (size_t)mtile_cap(P); }
+
+
+__device__ __forceinline__ uint32_t sm_lower_bound(const uint32_t* k, uint32_t n, uint32_t x) {
+  uint32_t lo = 0;
+  while (n > 0) {
+    const uint32_t half = n >> 1;
+    if (k[lo + half] < x) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
 }
 
-__global__ void __launch_bounds__(kThreads) owner_kernel(OwnerArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
-  float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
-  __shared__ uint32_t s_rng[kMaxRanks][2];
-  __shared__ uint32_t s_epre[kMaxRanks + 1];
-  __shared__ uint32_t s_scan[kWarps + 1];
-  __shared__ uint32_t s_bmax[kWin / 8];
-  __shared__ uint64_t s_sum[kWarps + 1];
-  __shared__ uint32_t s_dsar;
-  __shared__ uint64_t s_base;
-  cg::grid_group grid = cg::this_grid();
+__device__ __forceinline__ uint32_t sm_upper_bound(const uint32_t* k, uint32_t n, uint32_t x) {
+  uint32_t lo = 0;
+  while (n > 0) {
+    const uint32_t half = n >> 1;
+    if (k[lo + half] <= x) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+
+// One lane per source waits for its slice; block 0 records k_sum and the
+// algorithm decision (AUTO: sum k_i > delta -> DSAR, reading R-5).
+__device__ __forceinline__ bool owner_prologue(const OwnerArgs& a, uint32_t seq, uint64_t* s_ks, uint32_t* s_dsar,
+                                               uint64_t* s_sc = nullptr) {
   const int tid = threadIdx.x, P = a.P;
   Ctrl* ctl = a.ctl;
-  const uint32_t seq = ctl->seq;
-  if (a.wait && tid == 0)
-    for (int i = 0; i < P; ++i) wait_flag_geq(&ctl->src_done[i], seq + 1);
+  if (tid < P) {
+    if (a.wait) wait_flag_geq(&ctl->src_done[tid], seq + 1);
+    s_ks[tid] = *(volatile uint64_t*)&ctl->k_in[tid];
+    if (s_sc) s_sc[tid] = *(volatile uint64_t*)&ctl->slice_cnt[tid];
+  }
   __syncthreads();
   if (tid == 0) {
-    uint32_t dsar;
     uint64_t ks = 0;
-    for (int i = 0; i < P; ++i) ks += *(volatile uint64_t*)&ctl->k_in[i];
+    for (int i = 0; i < P; ++i) ks += s_ks[i];
+    uint32_t dsar;
     if (a.host_dsar >= 0) dsar = (uint32_t)a.host_dsar;
     else if (a.algo == SPARCML_DSAR_SPLIT_ALLGATHER) dsar = 1;
     else if (a.algo == SPARCML_SSAR_SPLIT_ALLGATHER) dsar = 0;
-    else dsar = ks > a.delta ? 1u : 0u;   // AUTO: upper bound sum k_i > delta (R-5)
-    s_dsar = dsar;
+    else dsar = ks > a.delta ? 1u : 0u;
+    *s_dsar = dsar;
     if (blockIdx.x == 0) {
       ctl->dsar = dsar;
       ctl->k_sum = ks;
     }
   }
   __syncthreads();
-  const bool dsar = s_dsar != 0;
-  const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint64_t nwin = ceil_div(a.hi - a.lo, kWin);
-  const uint64_t w0 = nwin * b / G, w1 = nwin * (b + 1) / G;
-  uint64_t my_total = 0;
-  for (uint64_t w = w0; w < w1; ++w) {
-    const uint64_t wlo = a.lo + w * kWin;
-    const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
-    if (tid < P) {
-      s_rng[tid][0] = a.src_win[tid][w];
-      s_rng[tid][1] = a.src_win[tid][w + 1];
+  return *s_dsar != 0;
+}
+
+// count of run elements k[0..n) below x (x already +1 for "at most"):
+// fixed halving steps from TOP (> any run length), branch-free so the
+// searches of several elements interleave
+template <uint32_t TOP>
+__device__ __forceinline__ uint32_t run_rank(const uint32_t* k, uint32_t n, uint32_t x) {
+  uint32_t lo = 0;
+#pragma unroll
+  for (uint32_t step = TOP; step; step >>= 1) {
+    const uint32_t c = lo + step;
+    if (c <= n && k[c - 1] < x) lo = c;
+  }
+  return lo;
+}
+
+__host__ __device__ constexpr uint32_t pow2_floor(uint32_t x) {
+  uint32_t p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+// Shared-memory state of one merge tile.
+template <int P>
+struct MergeShared {
+  uint32_t off[P + 1], len[P], dup[P], ta[P];
+  uint8_t role[kMaxTreeH][P], part[kMaxTreeH][P];
+  uint32_t wtot[kWarps];
+  uint64_t excl;
+};
+
+// warp 0, lanes < P hold run lengths: offsets = exclusive prefix (off[P] = total)
+template <int P>
+__device__ __forceinline__ void runs_prefix(MergeShared<P>& m, uint32_t len) {
+  const int lane = threadIdx.x & 31;
+  uint32_t x = lane < P ? len : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane < P) {
+    m.len[lane] = len;
+    m.off[lane] = x - len;
+  }
+  if (lane == P - 1) m.off[P] = x;
+}
+
+// Reduce the elements of table windows [w0, w1) of the block's range (at
+// most cap of them; s_c holds table entries, row = window, column = source).
+// The result (sorted, unique, canonical-tree sums) is left in xk/xv, or, if
+// oi != nullptr, written to oi/ov.  Returns its length.
+template <int P>
+__device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const uint32_t* s_c, int w0, int w1,
+                                   uint32_t* oi, float* ov_out, uint32_t* xk, float* xv, uint32_t* yk, float* yv) {
+  constexpr int cap = mtile_cap(P);
+  constexpr uint32_t kTop = pow2_floor(cap);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    uint32_t len = 0;
+    if (lane < P) {
+      const uint32_t ea = s_c[w0 * P + lane];
+      m.ta[lane] = ea;
+      m.dup[lane] = 0;
+      len = s_c[w1 * P + lane] - ea;
+    }
+    runs_prefix<P>(m, len);
+  }
+  __syncthreads();
+  // (2) stage the runs, source-major (run s = slot s); all loads in flight
+  uint32_t n = m.off[P];
+  {
+    constexpr int Q = (cap + kThreads - 1) / kThreads;
+    uint32_t kk[Q];
+    float vv[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t u = q * kThreads + tid;
+      if (u < n) {
+        int s = 0;
+#pragma unroll
+        for (int j = 1; j < P; ++j) s += m.off[j] <= u ? 1 : 0;
+        const uint32_t e = m.ta[s] + (u - m.off[s]);
+        kk[q] = __ldcg(&a.src_idx[s][e]);
+        vv[q] = __ldcg(&a.src_val[s][e]);
+      }
     }
 #pragma unroll
-    for (int i = 0; i < kWinPerThread; ++i) pres[tid + i * kThreads] = 0u;
-    __syncthreads();
-    if (tid == 0) {   // element prefix over the sources
-      uint32_t run = 0;
-      for (int s = 0; s < P; ++s) {
-        s_epre[s] = run;
-        run += s_rng[s][1] - s_rng[s][0];
-      }
-      s_epre[P] = run;
-    }
-    __syncthreads();
-    // all sources' elements of this window at once: one load latency per window
-    for (uint32_t u = tid; u < s_epre[P]; u += kThreads) {
-      int s = 0;
-      while (u >= s_epre[s + 1]) ++s;
-      const uint32_t e = s_rng[s][0] + (u - s_epre[s]);
-      const uint32_t pos = a.src_idx[s][e] - (uint32_t)wlo;
-      if (pos < (uint32_t)wn) {
-        vals[s * kWin + pos] = a.src_val[s][e];
-        atomicOr(&pres[pos], 1u << s);
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t u = q * kThreads + tid;
+      if (u < n) {
+        xk[u] = kk[q];
+        xv[u] = vv[q];
       }
     }
-    __syncthreads();
-    const int p0 = tid * kWinPerThread;
-    float r[kWinPerThread];
-    uint32_t present = 0;
+  }
+  __syncthreads();
+  // (3) canonical tree, one height per round
+  const int hmax = a.sched.hmax > 0 ? a.sched.hmax : 1;
+  uint32_t total = n;
+  for (int h = 1; h <= hmax; ++h) {
+    const uint8_t* role_h = m.role[h - 1];
+    const uint8_t* part_h = m.part[h - 1];
+    uint32_t off[P];
 #pragma unroll
-    for (int i = 0; i < kWinPerThread; ++i) {
-      const int p = p0 + i;
-      uint32_t m = (p < wn) ? pres[p] : 0u;
-      for (int q = 0; q < a.sched.n; ++q) {
-        const int d = a.sched.dst[q], s = a.sched.src[q];
-        if (m & (1u << s)) {
-          if (m & (1u << d)) {
-            vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[s * kWin + p]);
-          } else {
-            vals[d * kWin + p] = vals[s * kWin + p];
-            m |= 1u << d;
+    for (int j = 0; j < P; ++j) off[j] = m.off[j];
+    for (uint32_t b0 = 0; b0 < n; b0 += 2 * kThreads) {
+      constexpr int Q = 2;
+      uint32_t key[Q], rank[Q], qoff[Q], qlen[Q], pos0[Q];
+      float v[Q];
+      int role[Q], part[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const uint32_t u = b0 + q * kThreads + tid;
+        int s = 0;
+#pragma unroll
+        for (int j = 1; j < P; ++j) s += off[j] <= u ? 1 : 0;
+        const bool in = u < n;
+        key[q] = in ? xk[u] : 0u;
+        v[q] = in ? xv[u] : 0.0f;
+        role[q] = in ? (int)role_h[s] : -1;
+        const int pq = part_h[s];
+        part[q] = pq;
+        qoff[q] = m.off[pq];
+        qlen[q] = role[q] > 0 ? m.len[pq] : 0u;
+        pos0[q] = role[q] == 2 ? m.off[pq] + (u - off[s]) : u;   // right run lands in the left one's span
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q)   // left: #right < key ; right: #left <= key
+        rank[q] = run_rank<kTop>(xk + qoff[q], qlen[q], key[q] + (role[q] == 2 ? 1u : 0u));
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (role[q] < 0) continue;
+        uint32_t k = key[q];
+        float val = v[q];
+        const uint32_t pos = pos0[q] + rank[q];
+        if (role[q] == 1) {   // left run (lower ranks): first on ties, fl(left + right)
+          if (rank[q] < qlen[q] && xk[qoff[q] + rank[q]] == k) val = __fadd_rn(val, xv[qoff[q] + rank[q]]);
+        } else if (role[q] == 2) {   // right run: a key the left run holds was summed there
+          if (rank[q] > 0 && xk[qoff[q] + rank[q] - 1] == k) {
+            k = kDead;
+            atomicAdd(&m.dup[part[q]], 1u);
           }
         }
+        yk[pos] = k;
+        yv[pos] = val;
       }
-      r[i] = (m & 1u) ? vals[p] : 0.0f;
-      if (m & 1u) present |= 1u << i;
     }
-    if (!dsar) {
-      uint32_t total;
-      const uint32_t off = block_exclusive_sum<uint32_t>(__popc(present), s_scan, &total);
-      uint32_t* si = a.st_idx + w * kWin;
-      float* sv = a.st_val + w * kWin;
-      int c = 0;
-#pragma unroll
-      for (int i = 0; i < kWinPerThread; ++i)
-        if (present & (1u << i)) {
-          si[off + c] = (uint32_t)(wlo + p0 + i);
-          sv[off + c] = r[i];
-          ++c;
-        }
-      if (tid == 0) a.win_cnt[w] = total;
-      my_total += total;
-    } else if (a.bits) {
-      const uint64_t e = w * kWin + p0;   // partition-relative
-      const int rem = wn - p0;
-      const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
-      qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
-    } else {
-      float* d = a.dense + w * kWin + p0;
-      for (int i = 0; i < kWinPerThread && p0 + i < wn; ++i) d[i] = r[i];
+    __syncthreads();
+    // (4) compact y -> x (or, after the last height, -> the partition result)
+    const uint32_t seg = (uint32_t)ceil_div(n, (uint64_t)kWarps * 32) * 32;
+    const uint32_t u0 = warp * seg, u1 = std::min<uint32_t>(n, u0 + seg);
+    uint32_t cnt = 0;
+    for (uint32_t u = u0 + lane; u < u0 + seg; u += 32) {
+      const bool alive = u < u1 && yk[u] != kDead;
+      cnt += __popc(__ballot_sync(0xffffffffu, alive));
     }
+    if (lane == 0) m.wtot[warp] = cnt;
+    uint32_t nl = 0;
+    if (warp == 0 && lane < P) {   // merged runs: new lengths
+      const int r = role_h[lane];
+      nl = r == 1 ? m.len[lane] + m.len[part_h[lane]] - m.dup[lane] : (r == 2 ? 0u : m.len[lane]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      runs_prefix<P>(m, nl);
+      if (lane < P) m.dup[lane] = 0;
+    }
+    __syncthreads();
+    total = m.off[P];
+    const bool last = h == hmax;
+    uint32_t base = 0;
+    for (int w = 0; w < warp; ++w) base += m.wtot[w];
+    uint32_t* ok = last && oi ? oi : xk;
+    float* ov = last && oi ? ov_out : xv;
+    for (uint32_t u = u0 + lane; u < u0 + seg; u += 32) {
+      const uint32_t key = u < u1 ? yk[u] : kDead;
+      const bool alive = key != kDead;
+      const uint32_t mm = __ballot_sync(0xffffffffu, alive);
+      if (alive) {
+        const uint32_t pos = base + __popc(mm & ((1u << lane) - 1u));
+        ok[pos] = key;
+        ov[pos] = yv[u];
+      }
+      base += __popc(mm);
+    }
+    n = total;
     __syncthreads();
   }
-  if (!dsar) {
-    if (tid == 0) a.blk[b] = my_total;
-    grid.sync();
-    uint64_t v = 0;
-    for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&a.blk[j]));
-    uint64_t tot;
-    block_exclusive_sum<uint64_t>(v, s_sum, &tot);
-    if (tid == 0) s_base = tot;
-    __syncthreads();
-    uint64_t run = s_base;
-    for (uint64_t w = w0; w < w1; ++w) {
-      const uint32_t n = __ldcg(&a.win_cnt[w]);
-      const uint32_t* si = a.st_idx + w * kWin;
-      const float* sv = a.st_val + w * kWin;
-      for (uint32_t i = tid; i < n; i += kThreads) {
-        a.r_idx[run + i] = si[i];
-        a.r_val[run + i] = sv[i];
-      }
-      run += n;
+  __syncthreads();
+  return total;
+}
+
+constexpr int kTabSmem = 2048;   // table entries staged per chunk (general path)
+
+// Cooperative: block b reduces table windows [b*W, (b+1)*W) of my partition.
+// Common case -- the range holds at most one tile (cap elements): reduced in
+// shared memory and kept there across the grid sync.  Otherwise the range is
+// cut into pieces (< kMT + one window each) whose results are appended to the
+// staging area at the range's input offset.  After one grid sync every block
+// knows its output offset (sum of the block counts before it) and writes its
+// result contiguously; the last block to finish flags the P sources.
+template <int P>
+__global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int cap = mtile_cap(P);
+  uint32_t* xk = reinterpret_cast<uint32_t*>(smem);
+  float* xv = reinterpret_cast<float*>(xk + cap);
+  uint32_t* yk = reinterpret_cast<uint32_t*>(xv + cap);
+  float* yv = reinterpret_cast<float*>(yk + cap);
+  __shared__ MergeShared<P> m;
+  __shared__ uint64_t s_ks[kMaxRanks], s_sc[kMaxRanks];
+  __shared__ uint32_t s_c[kTabSmem];                 // table entries of the current chunk
+  __shared__ uint32_t s_dsar, s_scan[kWarps + 1];
+  __shared__ uint64_t s_sum[kWarps + 1], s_excl;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  Ctrl* ctl = a.ctl;
+  const uint32_t seq = ctl->seq;
+  dbg_mark(ctl, 0);
+  for (int q = tid; q < kMaxTreeH * P; q += kThreads) {
+    const int hh = q / P, sl = q - hh * P;
+    m.role[hh][sl] = a.sched.role[hh][sl];
+    m.part[hh][sl] = a.sched.part[hh][sl];
+  }
+  if (owner_prologue(a, seq, s_ks, &s_dsar, s_sc)) return;   // DSAR: the window kernel reduces
+  dbg_mark(ctl, 1);
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint32_t ntab = (uint32_t)ceil_div(a.hi - a.lo, kTab);
+  const uint32_t W = (ntab + G - 1) / G;
+  const uint32_t wa = std::min<uint32_t>(b * W, ntab), wb = std::min<uint32_t>(wa + W, ntab);
+  bool in_smem = true;
+  uint32_t cnt = 0;
+  uint64_t ibase = 0;
+  if (wa < wb) {
+    if (tid < P) {
+      s_c[tid] = __ldcg(&a.src_win[tid][wa]);
+      s_c[P + tid] = __ldcg(&a.src_win[tid][wb]);
     }
-    if (b == G - 1 && tid == 0) ctl->owner_K = run;
+    __syncthreads();
+    uint32_t tot = 0;
+#pragma unroll
+    for (int src = 0; src < P; ++src) {
+      tot += s_c[P + src] - s_c[src];
+      ibase += s_c[src];
+    }
+    dbg_mark(ctl, 2);
+    if (tot <= (uint32_t)cap) {
+      cnt = merge_subrange<P>(a, m, s_c, 0, 1, nullptr, nullptr, xk, xv, yk, yv);
+    } else {
+      in_smem = false;
+      const uint32_t wchunk = kTabSmem / P - 1;   // windows per chunk
+      for (uint32_t cw = wa; cw < wb; cw += wchunk) {
+        const int nw = (int)std::min<uint32_t>(wchunk, wb - cw);
+        __syncthreads();
+        for (int q = tid; q < (nw + 1) * P; q += kThreads) {
+          const int w = q / P, src = q - w * P;
+          s_c[q] = __ldcg(&a.src_win[src][cw + w]);
+        }
+        __syncthreads();
+        // greedy maximal pieces of at most cap elements (one window always fits)
+        for (int pos = 0; pos < nw;) {
+          const int w = pos + tid;
+          uint32_t c = 0;
+          if (w < nw) {
+#pragma unroll
+            for (int src = 0; src < P; ++src) c += s_c[(w + 1) * P + src] - s_c[w * P + src];
+          }
+          uint32_t tsum;
+          const uint32_t incl = block_exclusive_sum<uint32_t>(c, s_scan, &tsum) + c;
+          const int take = __syncthreads_count(w < nw && incl <= (uint32_t)cap);
+          cnt += merge_subrange<P>(a, m, s_c, pos, pos + take, a.st_idx + ibase + cnt, a.st_val + ibase + cnt, xk,
+                                   xv, yk, yv);
+          pos += take;
+        }
+      }
+    }
+  }
+  if (tid == 0) a.blk[b] = cnt;
+  dbg_mark(ctl, 3);
+  grid.sync();
+  dbg_mark(ctl, 4);
+  uint64_t v = 0;
+  for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&a.blk[j]));
+  uint64_t tot_before;
+  block_exclusive_sum<uint64_t>(v, s_sum, &tot_before);
+  if (tid == 0) s_excl = tot_before;
+  __syncthreads();
+  const uint64_t excl = s_excl;
+  if (in_smem) {
+    for (uint32_t i = tid; i < cnt; i += kThreads) {
+      a.r_idx[excl + i] = xk[i];
+      a.r_val[excl + i] = xv[i];
+    }
+  } else {
+    for (uint32_t i = tid; i < cnt; i += kThreads) {
+      a.r_idx[excl + i] = __ldcg(&a.st_idx[ibase + i]);
+      a.r_val[excl + i] = __ldcg(&a.st_val[ibase + i]);
+    }
+  }
+  if (b == G - 1 && tid == 0) ctl->owner_K = excl + cnt;
+  dbg_mark(ctl, 5);
+  if (last_block<true>(&ctl->done_ctr[3]) && tid < P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
+}
+
+// ===========================================================================
+// owner reduction, DSAR (§5.3.3 + §6): one cooperative kernel
+// densifies my partition window by window in the canonical tree order (R-8)
+// and stores it dense or QSGD-encoded in place.
+// ===========================================================================
+constexpr int kOwnElems = 2048;   // elements staged in shared memory per chunk
+constexpr int kOwnWins = 32;      // windows per chunk
+
+__host__ __device__ constexpr size_t owner_smem_bytes(int nsrc) {
+  return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)nsrc + 8 * (size_t)kOwnElems;
+}
+
+__global__ void __launch_bounds__(kThreads) owner_kernel(OwnerArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int P = a.P;
+  uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
+  float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
+  uint32_t* eidx = reinterpret_cast<uint32_t*>(smem + sizeof(uint32_t) * kWin + sizeof(float) * kWin * P);
+  float* evals = reinterpret_cast<float*>(eidx + kOwnElems);
+  __shared__ uint32_t s_tab[kMaxRanks][kOwnWins + 1];   // window offsets of this chunk
+  __shared__ uint32_t s_soff[kMaxRanks + 1];             // staged-element offset per source
+  __shared__ uint32_t s_wpre[kMaxRanks + 1];             // per-window element prefix over sources
+  __shared__ uint32_t s_bmax[kWin / 8];
+  __shared__ uint32_t s_dsar, s_nfit, s_direct;
+  __shared__ uint64_t s_ks[kMaxRanks];
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  Ctrl* ctl = a.ctl;
+  const uint32_t seq = ctl->seq;
+  if (!owner_prologue(a, seq, s_ks, &s_dsar)) return;   // SSAR: the merge kernel reduces
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const uint64_t nwin = ceil_div(a.hi - a.lo, kWin);
+  const uint64_t ntab = ceil_div(a.hi - a.lo, kTab);
+  const uint64_t w0 = nwin * b / G, w1 = nwin * (b + 1) / G;
+  for (uint64_t cw = w0; cw < w1;) {
+    const int nw = (int)std::min<uint64_t>(kOwnWins, w1 - cw);
+    // (1) the chunk's window offsets, every source at once
+    for (int q = tid; q < P * (nw + 1); q += kThreads) {
+      const int s = q / (nw + 1), i = q % (nw + 1);
+      s_tab[s][i] = a.src_win[s][std::min<uint64_t>((cw + i) * kTabPerWin, ntab)];
+    }
+    __syncthreads();
+    if (tid == 0) {   // how many windows fit in the staging buffer
+      int nfit = 0;
+      for (int i = 1; i <= nw; ++i) {
+        uint32_t tot = 0;
+        for (int s = 0; s < P; ++s) tot += s_tab[s][i] - s_tab[s][0];
+        if (tot > (uint32_t)kOwnElems) break;
+        nfit = i;
+      }
+      s_direct = nfit == 0;   // a single window larger than the buffer: read it from global
+      if (nfit == 0) nfit = 1;
+      s_nfit = nfit;
+      uint32_t run = 0;
+      for (int s = 0; s < P; ++s) {
+        s_soff[s] = run;
+        if (!s_direct) run += s_tab[s][nfit] - s_tab[s][0];
+      }
+      s_soff[P] = run;
+    }
+    __syncthreads();
+    const int nfit = (int)s_nfit;
+    const bool direct = s_direct != 0;
+    // (2) stage the elements of those windows, every source at once
+    for (uint32_t u = tid; u < s_soff[P]; u += kThreads) {
+      int s = 0;
+      while (u >= s_soff[s + 1]) ++s;
+      const uint32_t e = s_tab[s][0] + (u - s_soff[s]);
+      eidx[u] = a.src_idx[s][e];
+      evals[u] = a.src_val[s][e];
+    }
+    __syncthreads();
+    for (int i = 0; i < nfit; ++i) {
+      const uint64_t w = cw + i;
+      const uint64_t wlo = a.lo + w * kWin;
+      const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
+#pragma unroll
+      for (int q = 0; q < kWinPerThread; ++q) pres[tid + q * kThreads] = 0u;
+      if (tid == 0) {
+        uint32_t run = 0;
+        for (int s = 0; s < P; ++s) {
+          s_wpre[s] = run;
+          run += s_tab[s][i + 1] - s_tab[s][i];
+        }
+        s_wpre[P] = run;
+      }
+      __syncthreads();
+      for (uint32_t u = tid; u < s_wpre[P]; u += kThreads) {
+        int s = 0;
+        while (u >= s_wpre[s + 1]) ++s;
+        const uint32_t k = u - s_wpre[s];
+        uint32_t x;
+        float v;
+        if (direct) {
+          const uint32_t e = s_tab[s][i] + k;
+          x = a.src_idx[s][e];
+          v = a.src_val[s][e];
+        } else {
+          const uint32_t su = s_soff[s] + (s_tab[s][i] - s_tab[s][0]) + k;
+          x = eidx[su];
+          v = evals[su];
+        }
+        const uint32_t pos = x - (uint32_t)wlo;
+        if (pos < (uint32_t)wn) {
+          vals[s * kWin + pos] = v;
+          atomicOr(&pres[pos], 1u << s);
+        }
+      }
+      __syncthreads();
+      const int p0 = tid * kWinPerThread;
+      float r[kWinPerThread];
+      uint32_t present = 0;
+#pragma unroll
+      for (int q = 0; q < kWinPerThread; ++q) {
+        const int p = p0 + q;
+        uint32_t m = (p < wn) ? pres[p] : 0u;
+        if (m & (m - 1)) {   // two or more sources: canonical tree (R-8)
+          for (int t = 0; t < a.sched.n; ++t) {
+            const int d = a.sched.dst[t], sr = a.sched.src[t];
+            if (m & (1u << sr)) {
+              if (m & (1u << d)) {
+                vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[sr * kWin + p]);
+              } else {
+                vals[d * kWin + p] = vals[sr * kWin + p];
+                m |= 1u << d;
+              }
+            }
+          }
+          r[q] = vals[p];
+        } else if (m) {
+          r[q] = vals[(__ffs(m) - 1) * kWin + p];
+        } else {
+          r[q] = 0.0f;
+        }
+        if (m) present |= 1u << q;
+      }
+      if (a.bits) {
+        const uint64_t e = w * kWin + p0;   // partition-relative
+        const int rem = wn - p0;
+        const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+        qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
+      } else {
+        float* d = a.dense + w * kWin + p0;
+        for (int q = 0; q < kWinPerThread && p0 + q < wn; ++q) d[q] = r[q];
+      }
+      __syncthreads();
+    }
+    cw += nfit;
   }
   grid.sync();
   if (b == 0 && tid < P) {
@@ -604,22 +985,64 @@ static int owner_occupancy(int nsrc) {
   return cache[nsrc];
 }
 
+using OwnerMergeFn = void (*)(OwnerArgs);
+template <int... Ps>
+struct OwnerMergeTable {
+  static OwnerMergeFn get(int P) {
+    OwnerMergeFn f = nullptr;
+    ((P == Ps ? (f = owner_merge_kernel<Ps>, 0) : 0), ...);
+    return f;
+  }
+};
+static OwnerMergeFn owner_merge_fn(int P) {
+  return OwnerMergeTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P);
+}
+
+static int owner_merge_occupancy(int P) {
+  static int cache[kMaxRanks + 1] = {0};
+  if (!cache[P]) {
+    const OwnerMergeFn f = owner_merge_fn(P);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)owner_merge_smem_bytes(P));
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kThreads, owner_merge_smem_bytes(P));
+    cache[P] = std::max(1, per);
+  }
+  return cache[P];
+}
+
 cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(owner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)owner_smem_bytes(kMaxRanks));
     attr = true;
   }
-  const size_t smem = owner_smem_bytes(a.P);
-  const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
-  const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)owner_occupancy(a.P) * device_sm_count()));
-  OwnerArgs ac = a;
-  void* args[] = {(void*)&ac};
-  SPARCML_PROF("owner", s);
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_kernel, dim3((unsigned)G), dim3(kThreads), args, smem, s);
-  ++g_launches;
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  if (a.host_dsar != 1) {   // SSAR (or undecided: the kernel exits if the device picks DSAR)
+    const uint64_t G = (uint64_t)owner_merge_occupancy(a.P) * device_sm_count();
+    OwnerArgs ac = a;
+    void* args[] = {(void*)&ac};
+    SPARCML_PROF("owner", s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_merge_fn(a.P), dim3((unsigned)G), dim3(kThreads),
+                                                args, owner_merge_smem_bytes(a.P), s);
+    ++g_launches;
+    if (e != cudaSuccess) return e;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (a.host_dsar != 0) {   // DSAR (or undecided: the kernel exits if the device picks SSAR)
+    const size_t smem = owner_smem_bytes(a.P);
+    const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
+    const uint64_t G =
+        std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)owner_occupancy(a.P) * device_sm_count()));
+    OwnerArgs ac = a;
+    void* args[] = {(void*)&ac};
+    SPARCML_PROF("owner_dsar", s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_kernel, dim3((unsigned)G), dim3(kThreads), args,
+                                                smem, s);
+    ++g_launches;
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
+  return cudaSuccess;
 }
 
 int owner_grid_size() { return device_sm_count() * 8; }
@@ -806,7 +1229,7 @@ __global__ void barrier_kernel(BarrierArgs a) {
   fence_acq_rel_sys();
   if (!a.loopback && lane < a.P && lane != a.rank) {
     st_release_sys(a.peer_flags[lane], e);
-    while ((int)(ld_acquire_sys(&a.my->flags[lane]) - e) < 0) {
+    while ((int)(ld_relaxed_sys_u32(&a.my->flags[lane]) - e) < 0) {
     }
   }
   __syncwarp();

@@ -202,10 +202,17 @@ __host__ __device__ constexpr size_t win_smem_bytes(int nsrc) {
 
 // Canonical tree schedule (reading R-8): post-order list of (dst, src) slot
 // pairs for tree(lo, hi) with mid = lo + (hi - lo)/2, result in slot lo.
+constexpr int kMaxTreeH = 5;   // ceil(log2(kMaxRanks)) + 1
+
 struct TreeSched {
   uint8_t dst[kMaxRanks];
   uint8_t src[kMaxRanks];
+  uint8_t h[kMaxRanks];   // node height (leaves 0): nodes of one height touch disjoint slots
   int n;
+  int hmax;
+  // per height h (index h-1), per slot: 0 untouched, 1 left child (dst), 2 right child (src)
+  uint8_t role[kMaxTreeH][kMaxRanks];
+  uint8_t part[kMaxTreeH][kMaxRanks];   // the other child of the same node
 };
 
 // QSGD-encode 4 consecutive values v[0..3] at partition-relative position e

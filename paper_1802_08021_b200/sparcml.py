@@ -40,7 +40,7 @@ EXPORTED = [
     "sparcml_version", "sparcml_status_string", "sparcml_opts_default", "sparcml_switch_threshold",
     "sparcml_expected_nnz", "sparcml_result_bytes", "sparcml_result_val_offset", "sparcml_comm_create",
     "sparcml_comm_export_handle", "sparcml_comm_connect", "sparcml_comm_create_local", "sparcml_comm_destroy",
-    "sparcml_comm_nranks", "sparcml_comm_rank", "sparcml_last_error", "sparcml_sparse_allreduce",
+    "sparcml_comm_nranks", "sparcml_comm_workspace", "sparcml_comm_rank", "sparcml_last_error", "sparcml_sparse_allreduce",
     "sparcml_sparse_allreduce_local", "sparcml_barrier", "sparcml_read_header", "sparcml_ops_workspace_bytes",
     "sparcml_ops_workspace_init", "sparcml_merge_sum", "sparcml_topk_workspace_bytes", "sparcml_topk_sparsify",
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
@@ -78,6 +78,7 @@ _sig = {
     "sparcml_comm_create_local": (_i32, [C.POINTER(_p), _i32, _i32, _u64, _u64]),
     "sparcml_comm_destroy": (_i32, [_p]),
     "sparcml_comm_nranks": (_i32, [_p]),
+    "sparcml_comm_workspace": (_p, [_p, _i32]),
     "sparcml_comm_rank": (_i32, [_p]),
     "sparcml_last_error": (C.c_char_p, [_p]),
     "sparcml_sparse_allreduce": (_i32, [_p, _p, _p, _u64, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
@@ -148,7 +149,7 @@ def profile_read(name: str):
     return int(n.value), float(ms.value)
 
 
-PROFILED_KERNELS = ["topk", "topk_all", "split_push", "owner",
+PROFILED_KERNELS = ["topk", "topk_all", "split_push", "owner", "owner_dsar",
                     "barrier", "merge", "window", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
                     "dequantize"]
 
@@ -275,6 +276,16 @@ class LocalWorld:
             self.close()
         except Exception:
             pass
+
+    def debug_ctrl(self, rank: int, offset: int, nbytes: int, stream=None) -> bytes:
+        """Diagnostics: nbytes of rank's control block at `offset` (syncs)."""
+        ptr = _lib.sparcml_comm_workspace(self._h, rank)
+        out = bytearray()
+        for o in range(0, nbytes, HEADER_BYTES):
+            h = Header()
+            _check(_lib.sparcml_read_header(ptr + offset + o, C.byref(h), _stream(stream)))
+            out += bytes(h)
+        return bytes(out[:nbytes])
 
 
 class Comm:
