@@ -10,7 +10,7 @@ value = whole-job "effective GB/s": dense-equivalent bytes reduced per second,
         P * 4N / t_step.  ms_per_step is the step latency.
 
 Timing: W warm-up steps, then K steps, each bracketed by CUDA events on the
-launching stream; L2 is flushed (512 MiB write) before every step outside the
+launching stream; L2 is flushed (512 MiB write, then read back clean) before every step outside the
 events; barrier + synchronize around the timed region; max over ranks.
 
 Launch: python bench.py [--gpus N --steps K --warmup W] ; N > 1 under
@@ -53,6 +53,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
+
+
+# A ~100 us spin kernel ahead of each timed step: the start event then fires
+# when the GPU reaches the step, not while it idles waiting for the host to
+# finish enqueueing (host launch latency is not kernel time; e2e keeps it).
+HOLD_CYCLES = 200_000
 
 
 def load_peaks():
@@ -222,6 +228,13 @@ def main():
     val = torch.empty(k, dtype=torch.float32, device=dev)
     out = S.new_out(N, dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_i64 = flush.view(torch.int64)
+
+    def flush_l2():
+        # write a buffer 4x the L2, then read it back: the L2 holds none of the
+        # step's data and no dirty lines whose write-back the next kernel would pay
+        flush.zero_()
+        flush_i64.sum()
     stream = torch.cuda.current_stream()
 
     def topk():
@@ -236,7 +249,7 @@ def main():
             dist.barrier()
 
     for _ in range(max(3, args.warmup)):
-        flush.zero_()
+        flush_l2()
         topk()
         allreduce()
     barrier()
@@ -255,7 +268,7 @@ def main():
     launches_per_step = S.kernel_launches() - l0
     topk_launches = l1 - l0
     for _ in range(max(3, args.warmup)):
-        flush.zero_()
+        flush_l2()
         barrier()
         comm.barrier()
         g_topk.replay()
@@ -269,9 +282,10 @@ def main():
     barrier()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
-            flush.zero_()
+            flush_l2()
             barrier()
             comm.barrier()     # device-side alignment of the ranks before the events
+            torch.cuda._sleep(HOLD_CYCLES)   # keep the GPU busy while the host enqueues the step
             a = torch.cuda.Event(enable_timing=True)
             m = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -291,9 +305,10 @@ def main():
     S.profile_only(None)
     ev2 = []
     for _ in range(args.steps):
-        flush.zero_()
+        flush_l2()
         barrier()
         comm.barrier()
+        torch.cuda._sleep(HOLD_CYCLES)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         S.profile_enable(True)
@@ -347,7 +362,7 @@ def main():
         pay_h = torch.empty(S.result_bytes(N), dtype=torch.uint8, pin_memory=True)
         t_e2e, d2h = 0.0, 0
         for it in range(max(2, args.steps // 2)):
-            flush.zero_()
+            flush_l2()
             barrier()
             comm.barrier()
             a = torch.cuda.Event(enable_timing=True)
@@ -414,7 +429,7 @@ def main():
             "config": {"workload": args.config, "desc": cfg["desc"], "N": N, "k_per_rank": k,
                        "density": cfg["density"], "P": P, "algo": {1: "SSAR_Recursive_double",
                        2: "SSAR_Split_allgather", 3: "DSAR_Split_allgather"}[algo],
-                       "quant_bits": cfg["bits"], "l2": "flushed before every step (512 MiB write)",
+                       "quant_bits": cfg["bits"], "l2": "flushed before every step (512 MiB write + 512 MiB read, no dirty lines left)",
                        "exchange": "CUDA IPC over NVLink (fused push/pull kernels)" if P > 1 else "none (P=1)"},
             "latency_us": t_step * 1e6, "allreduce_us": t_ar * 1e6, "topk_us": (t_step - t_ar) * 1e6,
             "timing": "CUDA graphs (g_topk, g_ar) replayed per step; eager API step measured too",
