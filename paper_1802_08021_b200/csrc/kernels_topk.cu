@@ -46,6 +46,7 @@ struct TopkCtl {
   uint32_t status, passes;
   uint32_t smax;            // largest sampled key
   uint32_t tile_ticket;     // filter tiles handed out dynamically
+  uint32_t spill;           // some block could not keep its candidates in shared memory
   uint64_t t_blk[kMaxGrid][8];   // %globaltimer per block at phase ends (diagnostics)
 };
 
@@ -55,8 +56,11 @@ struct TopkLayout {
   uint32_t* tile_count;
   uint32_t* cand_idx;
   float* cand_val;
-  uint64_t ntiles;
+  uint64_t* gsum;           // per 64-tile group: sum of tile_sel (fast placement path)
+  uint64_t ntiles, ngroups;
 };
+
+constexpr int kGroupTiles = 64;
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -73,13 +77,16 @@ static TopkLayout topk_layout(void* ws, uint64_t N) {
   L.cand_idx = reinterpret_cast<uint32_t*>(p);
   p += align256(L.ntiles * kTopkTile * sizeof(uint32_t));
   L.cand_val = reinterpret_cast<float*>(p);
+  p += align256(L.ntiles * kTopkTile * sizeof(float));
+  L.ngroups = (L.ntiles + kGroupTiles - 1) / kGroupTiles;
+  L.gsum = reinterpret_cast<uint64_t*>(p);
   return L;
 }
 
 size_t topk_workspace_bytes(uint64_t N, uint64_t /*k*/) {
   const uint64_t nt = (N + kTopkTile - 1) / kTopkTile;
   return align256(sizeof(TopkCtl)) + align256(nt * sizeof(uint64_t)) + align256(nt * sizeof(uint32_t)) +
-         2 * align256(nt * kTopkTile * sizeof(uint32_t));
+         2 * align256(nt * kTopkTile * sizeof(uint32_t)) + align256(((nt + 63) / 64) * sizeof(uint64_t));
 }
 
 __device__ __forceinline__ uint32_t abs_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
@@ -89,7 +96,7 @@ __device__ __forceinline__ void mark(TopkCtl* c, int i) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x == 0) c->t_phase[i] = t;
-    c->t_blk[blockIdx.x][i] = t;
+    if (i < 8) c->t_blk[blockIdx.x][i] = t;
   }
 }
 
@@ -114,12 +121,19 @@ __host__ __device__ __forceinline__ uint32_t shift_for(uint64_t span, uint64_t n
 // <= above0 + (count in bins >= b).  h is staged through shared memory
 // (coalesced).  Returns b and the count strictly above it (including above0).
 // If the histogram cannot reach the target: b = 0 and *reached = false.
-__device__ void find_bin(const uint32_t* h, uint64_t above0, uint64_t target, uint32_t* sm, uint32_t* bin_out,
-                         uint64_t* above_out, bool* reached, uint32_t nbins = kBins) {
+struct BinFind {
+  uint32_t bin;
+  uint64_t above;
+  bool reached;
+};
+
+// Up to two targets from one staging of h and one scan.
+__device__ void find_bins(const uint32_t* h, uint64_t above0, const uint64_t* target, int ntarget, uint32_t* sm,
+                          BinFind* out, uint32_t nbins = kBins) {
   __shared__ uint64_t scan[kWarps + 1];
-  __shared__ uint32_t s_bin;
-  __shared__ uint64_t s_above;
-  __shared__ int s_ok;
+  __shared__ uint32_t s_bin[2];
+  __shared__ uint64_t s_above[2];
+  __shared__ int s_ok[2];
   const int tid = threadIdx.x;
   constexpr int per = kBins / kThreads;   // 16
   // stage: 16 independent coalesced loads in flight per thread; bin j at
@@ -132,10 +146,10 @@ __device__ void find_bin(const uint32_t* h, uint64_t above0, uint64_t target, ui
     const int j = i * kThreads + tid;
     sm[j + (j >> 4)] = v[i];
   }
-  if (tid == 0) {
-    s_bin = 0;
-    s_above = above0;
-    s_ok = 0;
+  if (tid < 2) {
+    s_bin[tid] = 0;
+    s_above[tid] = above0;
+    s_ok[tid] = 0;
   }
   __syncthreads();
   const int hiB = kBins - tid * per;     // this thread: bins [hiB - per, hiB), scanned downwards
@@ -149,34 +163,62 @@ __device__ void find_bin(const uint32_t* h, uint64_t above0, uint64_t target, ui
   }
   uint64_t total;
   const uint64_t before = above0 + block_exclusive_sum<uint64_t>(local, scan, &total);
-  if (before < target && before + local >= target) {
-    uint64_t cum = before;
-    bool found = false;
+  for (int q = 0; q < ntarget; ++q) {
+    const uint64_t tg = target[q];
+    if (before < tg && before + local >= tg) {
+      uint64_t cum = before;
+      bool found = false;
 #pragma unroll
-    for (int i = 0; i < per; ++i) {
-      if (!found && cum + loc[i] >= target) {
-        s_bin = (uint32_t)(hiB - 1 - i);
-        s_above = cum;
-        s_ok = 1;
-        found = true;
+      for (int i = 0; i < per; ++i) {
+        if (!found && cum + loc[i] >= tg) {
+          s_bin[q] = (uint32_t)(hiB - 1 - i);
+          s_above[q] = cum;
+          s_ok[q] = 1;
+          found = true;
+        }
+        cum += loc[i];
       }
-      cum += loc[i];
     }
   }
   __syncthreads();
-  *bin_out = s_bin;
-  *above_out = s_above;
-  *reached = s_ok != 0;
+  for (int q = 0; q < ntarget; ++q) {
+    out[q].bin = s_bin[q];
+    out[q].above = s_above[q];
+    out[q].reached = s_ok[q] != 0;
+  }
   __syncthreads();
 }
 
 // One tile: 16 values per thread (4 coalesced float4 rows).  Candidates are
 // written in index order to the tile's region and binned into `sh`.
+#ifndef SPARCML_TOPK_KEEP
+#define SPARCML_TOPK_KEEP 1      // 0: always take the global-memory path (A/B diagnostics)
+#endif
+#ifndef SPARCML_TOPK_CANDCAP
+#define SPARCML_TOPK_CANDCAP 2048
+#endif
+#ifndef SPARCML_TOPK_MINB
+#define SPARCML_TOPK_MINB 4
+#endif
+constexpr int kCandCap = SPARCML_TOPK_CANDCAP;   // candidates a block keeps in shared memory
+constexpr int kTileCap = 32;     // tiles a block tracks
+
+// The block's filtered tiles and their candidates, kept in shared memory for
+// the refine / count / place phases (no global re-reads).  spill = some tile
+// did not fit: the whole grid then takes the global-memory path.
+struct KeepSmem {
+  uint32_t ci[kCandCap];
+  float cv[kCandCap];
+  uint32_t tl[kTileCap], tn[kTileCap], to[kTileCap];
+  uint64_t tp[kTileCap];
+  uint32_t ntl, nc, spill;
+};
+
 template <bool EF, bool RESID, bool STORE>
 __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const float* __restrict__ g, float alpha,
                                             float* __restrict__ xout, float* __restrict__ resid, uint64_t N, uint64_t t,
                                             uint32_t tau, uint64_t split, uint32_t shift, const TopkLayout& L,
-                                            uint32_t* sh, uint32_t* s_wt, uint32_t* s_status) {
+                                            uint32_t* sh, uint32_t* s_wt, uint32_t* s_status, KeepSmem* ks) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t base = t * kTopkTile;
   const uint64_t pol = l2_evict_first_policy();
@@ -254,6 +296,9 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
     if (lane == 31) s_wt[64] = wi;
   }
   __syncthreads();
+  const uint32_t tcount = s_wt[64];
+  const uint32_t kb = ks ? ks->nc : 0u;
+  const bool keep = ks && kb + tcount <= (uint32_t)kCandCap && ks->ntl < (uint32_t)kTileCap;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     uint32_t pos = s_wt[32 + j * kWarps + warp] + incl[j] - __popc(flags[j]);
@@ -263,13 +308,28 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
       if (flags[j] & (1u << q)) {
         L.cand_idx[base + pos] = (uint32_t)(p + q);
         L.cand_val[base + pos] = v[j][q];
+        if (keep) {
+          ks->ci[kb + pos] = (uint32_t)(p + q);
+          ks->cv[kb + pos] = v[j][q];
+        }
         atomicAdd(&sh[bin_of(abs_key(v[j][q]), tau, split, shift)], 1u);
         ++pos;
       }
     }
   }
-  if (tid == 0) L.tile_count[t] = s_wt[64];
+  if (tid == 0) L.tile_count[t] = tcount;
   __syncthreads();
+  if (ks && tid == 0) {   // read by every thread only after the next tile's first barrier
+    if (keep) {
+      ks->tl[ks->ntl] = (uint32_t)t;
+      ks->tn[ks->ntl] = tcount;
+      ks->to[ks->ntl] = kb;
+      ks->ntl = ks->ntl + 1;
+      ks->nc = kb + tcount;
+    } else {
+      ks->spill = 1;
+    }
+  }
 }
 
 // A refinement level: bins 0..kBins-2 cover [lo, split) in steps of 2^shift,
@@ -282,32 +342,35 @@ struct Level {
   uint64_t need;
 };
 
-// Whole block (every block computes the same result from the same global
-// histogram): locate the crossing bin of `h` and narrow the level.
-__device__ __forceinline__ void narrow(Level& lv, const uint32_t* h, uint64_t k, uint32_t* sm) {
-  uint32_t b;
-  uint64_t above;
-  bool ok;
-  find_bin(h, lv.above, k, sm, &b, &above, &ok);
+// Narrow the level to the crossing bin f (found in this level's histogram).
+__device__ __forceinline__ void apply_narrow(Level& lv, const BinFind& f, uint64_t k) {
   uint64_t nlo, nhi;
-  if (b == kBins - 1) {
+  if (f.bin == kBins - 1) {
     nlo = lv.split;
     nhi = lv.hi;
   } else {
-    nlo = lv.lo + ((uint64_t)b << lv.shift);
-    nhi = min(lv.split, lv.lo + ((uint64_t)(b + 1) << lv.shift));
+    nlo = lv.lo + ((uint64_t)f.bin << lv.shift);
+    nhi = min(lv.split, lv.lo + ((uint64_t)(f.bin + 1) << lv.shift));
   }
-  lv.above = above;
+  lv.above = f.above;
   lv.lo = nlo;
   lv.split = nhi;
   lv.hi = nhi;
   if (nhi - nlo <= 1) {
     lv.exact = 1;
     lv.kth = (uint32_t)nlo;
-    lv.need = k - above;
+    lv.need = k - f.above;
   } else {
     lv.shift = shift_for(nhi - nlo, kBins - 1);
   }
+}
+
+// Whole block (every block computes the same result from the same global
+// histogram): locate the crossing bin of `h` and narrow the level.
+__device__ __forceinline__ void narrow(Level& lv, const uint32_t* h, uint64_t k, uint32_t* sm) {
+  BinFind f;
+  find_bins(h, lv.above, &k, 1, sm, &f);
+  apply_narrow(lv, f, k);
 }
 
 // Warp: load the (up to 128) candidates [i0, i0+128) of a tile, 4 per lane in flight.
@@ -331,7 +394,7 @@ __device__ __forceinline__ void flush_hist(const uint32_t* sh, uint32_t* gh) {
 constexpr int kGroup = 32;   // tiles per placement group (one warp scans their prefix)
 
 template <bool EF, bool RESID>
-__global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel(const float* __restrict__ x,
                                                                  const float* __restrict__ g, float alpha,
                                                                  float* __restrict__ xout, float* __restrict__ resid,
                                                                  uint64_t N, uint64_t k, uint32_t* __restrict__ idx_out,
@@ -343,6 +406,8 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
   __shared__ uint64_t s_sum[kWarps + 1];
   __shared__ uint64_t s_pref[kGroup];
   __shared__ uint64_t s_base;
+  __shared__ KeepSmem ks;
+  __shared__ uint32_t s_fast;
   cg::grid_group grid = cg::this_grid();
   TopkCtl* c = L.ctl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -350,11 +415,18 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
   const uint32_t gwarp = b * kWarps + warp, nwarps = G * kWarps;
   const uint64_t t0 = L.ntiles * b / G, t1 = L.ntiles * (b + 1) / G;   // this block's tiles in C
   for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
-  if (tid == 0) s_status = 0;
+  if (tid == 0) {
+    s_status = 0;
+    ks.ntl = 0;
+    ks.nc = 0;
+    ks.spill = SPARCML_TOPK_KEEP ? 0u : 1u;
+  }
   if (b == 0 && tid == 0) {
     c->tile_ticket = 0;
     c->status = 0;
+    c->spill = 0;
   }
+  for (uint64_t i = (uint64_t)b * kThreads + tid; i < L.ngroups; i += (uint64_t)G * kThreads) L.gsum[i] = 0;
   mark(c, 0);
 
   // ---- S: sample ----------------------------------------------------------------
@@ -413,11 +485,11 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
     const uint64_t t_lo = (uint64_t)ceil(mean + 4.0 * sqrt(mean) + 16.0);
     const double th = mean - 4.0 * sqrt(mean) - 16.0;
     const uint64_t t_hi = th > 1.0 ? (uint64_t)th : 1;
-    uint32_t bn, bh;
-    uint64_t above;
-    bool ok, okh;
-    find_bin(c->hist_s, 0, t_lo, sh, &bn, &above, &ok);
-    find_bin(c->hist_s, 0, t_hi, sh, &bh, &above, &okh);
+    const uint64_t tg[2] = {t_lo, t_hi};
+    BinFind fb[2];
+    find_bins(c->hist_s, 0, tg, 2, sh, fb);
+    const bool ok = fb[0].reached, okh = fb[1].reached;
+    const uint32_t bn = fb[0].bin, bh = fb[1].bin;
     const uint64_t tau = ok ? ((uint64_t)bn << 19) : 0ull;
     const uint64_t top = (uint64_t)__ldcg(&c->smax) + (1ull << 23);   // 2 x the largest sample
     uint64_t split = okh ? min((uint64_t)(bh + 1) << 19, (uint64_t)kKeyEnd) : min(top, (uint64_t)kKeyEnd);
@@ -438,19 +510,19 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
     const uint64_t t = s_ticket;
     if (t >= L.ntiles) break;
     filter_tile<EF, RESID, EF || RESID>(x, g, alpha, xout, resid, N, t, tau, lv.split, lv.shift, L, sh, s_wt,
-                                        &s_status);
+                                        &s_status, SPARCML_TOPK_KEEP ? &ks : nullptr);
   }
   mark(c, 3);
   flush_hist(sh, c->hist[0]);
   if (tid == 0 && s_status) atomicOr(&c->status, 1u);
+  if (tid == 0 && ks.spill) atomicOr(&c->spill, 1u);
   grid.sync();
+  if (tid == 0) s_fast = __ldcg(&c->spill) == 0u;
   mark(c, 4);
   {
-    uint64_t loc = 0;
-    for (int i = 0; i < kBins / kThreads; ++i) loc += __ldcg(&c->hist[0][i * kThreads + tid]);
-    uint64_t C;
-    block_exclusive_sum<uint64_t>(loc, s_sum, &C);
-    if (C < k) {   // the sample under-estimated: exact re-filter with tau = 0 (rare)
+    BinFind f0;
+    find_bins(c->hist[0], lv.above, &k, 1, sh, &f0);
+    if (!f0.reached) {   // fewer than k candidates: the sample under-estimated; exact re-filter with tau = 0 (rare)
       grid.sync();   // every block has read hist[0]
       if (b == 0) {
         for (int i = tid; i < kBins; i += kThreads) c->hist[0][i] = 0;
@@ -460,6 +532,7 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
         }
       }
       for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+      if (tid == 0) s_fast = 0;   // the re-filtered candidates live in global memory only
       grid.sync();
       lv.lo = 0;
       lv.split = kKeyEnd;
@@ -471,21 +544,28 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
         const uint64_t t = s_ticket;
         if (t >= L.ntiles) break;
         filter_tile<false, false, false>(src, nullptr, 0.0f, nullptr, nullptr, N, t, 0u, lv.split, lv.shift, L, sh,
-                                         s_wt, &s_status);
+                                         s_wt, &s_status, nullptr);
       }
       flush_hist(sh, c->hist[0]);
       grid.sync();
-    } else if (b == 0 && tid == 0) {
-      c->passes = 1;
+      narrow(lv, c->hist[0], k, sh);
+    } else {
+      if (b == 0 && tid == 0) c->passes = 1;
+      apply_narrow(lv, f0, k);
     }
   }
-  narrow(lv, c->hist[0], k, sh);
   mark(c, 5);
 
   // ---- R: refine the crossing bin until it is one magnitude ------------------
   int level = 1;
   while (!lv.exact) {
     uint32_t* gh = c->hist[level < kLevels ? level : kLevels - 1];
+    if (s_fast) {
+      for (uint32_t i = tid; i < ks.nc; i += kThreads) {
+        const uint32_t key = abs_key(ks.cv[i]);
+        if (key >= lv.lo && key < lv.hi) atomicAdd(&gh[bin_of(key, lv.lo, lv.split, lv.shift)], 1u);
+      }
+    } else
     for (uint64_t t = gwarp; t < L.ntiles; t += nwarps) {
       const uint32_t n = __ldcg(&L.tile_count[t]);
       const float* cv = L.cand_val + t * kTopkTile;
@@ -508,91 +588,154 @@ __global__ void __launch_bounds__(kThreads, 4) topk_fused_kernel(const float* __
   const uint32_t kth = lv.kth;
   const uint64_t need = lv.need;
 
-  // ---- C: ordered placement over block-contiguous tiles ----------------------
-  uint64_t bsum = 0;
-  for (uint64_t t = t0 + warp; t < t1; t += kWarps) {
-    const uint32_t n = __ldcg(&L.tile_count[t]);
-    const float* cv = L.cand_val + t * kTopkTile;
-    uint32_t ng = 0, ne = 0;
-    for (uint32_t i0 = 0; i0 < n; i0 += 128) {
-      float v[4];
-      load4(cv, n, i0, v);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const bool in = i0 + r * 32 + lane < n;
-        const uint32_t key = abs_key(v[r]);
-        ng += __popc(__ballot_sync(0xffffffffu, in && key > kth));
-        ne += __popc(__ballot_sync(0xffffffffu, in && key == kth));
+  // ---- C: ordered placement (index order = tile order, then in-tile order) --
+  if (s_fast) {
+    // per kept tile: (#|v| > kth) | (#|v| == kth) << 32, from shared memory
+    for (uint32_t j = warp; j < ks.ntl; j += kWarps) {
+      const uint32_t n = ks.tn[j], o = ks.to[j];
+      uint32_t ng = 0, ne = 0;
+      for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t key = abs_key(ks.cv[o + i]);
+        ng += key > kth;
+        ne += key == kth;
+      }
+      ng = warp_sum<uint32_t>(ng);
+      ne = warp_sum<uint32_t>(ne);
+      if (lane == 0) {
+        const uint64_t sel = (uint64_t)ng | ((uint64_t)ne << 32);
+        L.tile_sel[ks.tl[j]] = sel;
+        if (sel) atomicAdd(reinterpret_cast<unsigned long long*>(&L.gsum[ks.tl[j] / kGroupTiles]), sel);
       }
     }
-    const uint64_t sel = (uint64_t)ng | ((uint64_t)ne << 32);
-    if (lane == 0) {
-      L.tile_sel[t] = sel;
-      bsum += sel;
+    mark(c, 10);
+  } else {
+    uint64_t bsum = 0;
+    for (uint64_t t = t0 + warp; t < t1; t += kWarps) {
+      const uint32_t n = __ldcg(&L.tile_count[t]);
+      const float* cv = L.cand_val + t * kTopkTile;
+      uint32_t ng = 0, ne = 0;
+      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
+        float v[4];
+        load4(cv, n, i0, v);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const bool in = i0 + r * 32 + lane < n;
+          const uint32_t key = abs_key(v[r]);
+          ng += __popc(__ballot_sync(0xffffffffu, in && key > kth));
+          ne += __popc(__ballot_sync(0xffffffffu, in && key == kth));
+        }
+      }
+      const uint64_t sel = (uint64_t)ng | ((uint64_t)ne << 32);
+      if (lane == 0) {
+        L.tile_sel[t] = sel;
+        bsum += sel;
+      }
+    }
+    {
+      uint64_t tot;
+      block_exclusive_sum<uint64_t>(bsum, s_sum, &tot);
+      if (tid == 0) c->blk[b] = tot;
     }
   }
-  {
-    uint64_t tot;
-    block_exclusive_sum<uint64_t>(bsum, s_sum, &tot);
-    if (tid == 0) c->blk[b] = tot;
-  }
   grid.sync();
-  mark(c, 7);
+  mark(c, 8);
   // every histogram has been read by every block: clear them for the next call
   if (b < (uint32_t)(kLevels + 1)) {
     uint32_t* h = b == 0 ? c->hist_s : c->hist[b - 1];
     for (int i = tid; i < kBins; i += kThreads) h[i] = 0;
     if (b == 0 && tid == 0) c->smax = 0;
   }
-  {
-    uint64_t v = 0;
-    for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&c->blk[j]));
-    uint64_t tot;
-    block_exclusive_sum<uint64_t>(v, s_sum, &tot);
-    if (tid == 0) s_base = tot;
-  }
-  __syncthreads();
-  for (uint64_t gs = t0; gs < t1; gs += kGroup) {
-    const int nt = (int)std::min<uint64_t>(kGroup, t1 - gs);
-    if (warp == 0) {
-      const uint64_t v = lane < nt ? __ldcg(reinterpret_cast<const unsigned long long*>(&L.tile_sel[gs + lane])) : 0ull;
-      const uint64_t inc = warp_inclusive_sum<uint64_t>(v);
-      s_pref[lane] = s_base + inc - v;
-      __syncwarp();
-      if (lane == 31) s_base += inc;
+  if (s_fast) {
+    // exclusive prefix of tile_sel at each kept tile: the group sums before
+    // its 64-tile group plus the tiles before it in the group (one warp per tile)
+    for (uint32_t j = warp; j < ks.ntl; j += kWarps) {
+      const uint64_t t = ks.tl[j], g0 = t / kGroupTiles;
+      uint64_t v = 0;
+      for (uint64_t i = lane; i < g0; i += 32) v += __ldcg(reinterpret_cast<const unsigned long long*>(&L.gsum[i]));
+#pragma unroll
+      for (int q = 0; q < kGroupTiles / 32; ++q) {
+        const uint64_t tt = g0 * kGroupTiles + q * 32 + lane;
+        if (tt < t) v += __ldcg(reinterpret_cast<const unsigned long long*>(&L.tile_sel[tt]));
+      }
+      v = warp_sum<uint64_t>(v);
+      if (lane == 0) ks.tp[j] = v;
     }
     __syncthreads();
-    for (int j = warp; j < nt; j += kWarps) {
-      const uint64_t t = gs + j;
-      const uint32_t n = __ldcg(&L.tile_count[t]);
-      const uint32_t* ci = L.cand_idx + t * kTopkTile;
-      const float* cv = L.cand_val + t * kTopkTile;
-      uint64_t gt_run = s_pref[j] & 0xFFFFFFFFull, eq_run = s_pref[j] >> 32;
-      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
-        float v[4];
-        load4(cv, n, i0, v);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint32_t i = i0 + r * 32 + lane;
-          const uint32_t key = abs_key(v[r]);
-          const bool gsel = i < n && key > kth, esel = i < n && key == kth;
-          const uint32_t gbal = __ballot_sync(0xffffffffu, gsel), ebal = __ballot_sync(0xffffffffu, esel);
-          const uint32_t lower = (1u << lane) - 1u;
-          const uint64_t gt_before = gt_run + __popc(gbal & lower);
-          const uint64_t eq_before = eq_run + __popc(ebal & lower);
-          if (gsel || (esel && eq_before < need)) {
-            const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
-            const uint32_t j2 = ci[i];
-            idx_out[pos] = j2;
-            val_out[pos] = v[r];
-            if (zero_at) zero_at[j2] = 0.0f;   // acc - TopK(acc)
-          }
-          gt_run += __popc(gbal);
-          eq_run += __popc(ebal);
+    mark(c, 9);
+    for (uint32_t j = warp; j < ks.ntl; j += kWarps) {
+      const uint32_t n = ks.tn[j], o = ks.to[j];
+      uint64_t gt_run = ks.tp[j] & 0xFFFFFFFFull, eq_run = ks.tp[j] >> 32;
+      for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const float vv = i < n ? ks.cv[o + i] : 0.0f;
+        const uint32_t key = abs_key(vv);
+        const bool gsel = i < n && key > kth, esel = i < n && key == kth;
+        const uint32_t gbal = __ballot_sync(0xffffffffu, gsel), ebal = __ballot_sync(0xffffffffu, esel);
+        const uint32_t lower = (1u << lane) - 1u;
+        const uint64_t gt_before = gt_run + __popc(gbal & lower);
+        const uint64_t eq_before = eq_run + __popc(ebal & lower);
+        if (gsel || (esel && eq_before < need)) {
+          const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
+          const uint32_t j2 = ks.ci[o + i];
+          idx_out[pos] = j2;
+          val_out[pos] = vv;
+          if (zero_at) zero_at[j2] = 0.0f;   // acc - TopK(acc)
         }
+        gt_run += __popc(gbal);
+        eq_run += __popc(ebal);
       }
     }
+  } else {
+    {
+      uint64_t v = 0;
+      for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&c->blk[j]));
+      uint64_t tot;
+      block_exclusive_sum<uint64_t>(v, s_sum, &tot);
+      if (tid == 0) s_base = tot;
+    }
     __syncthreads();
+    for (uint64_t gs = t0; gs < t1; gs += kGroup) {
+      const int nt = (int)std::min<uint64_t>(kGroup, t1 - gs);
+      if (warp == 0) {
+        const uint64_t v = lane < nt ? __ldcg(reinterpret_cast<const unsigned long long*>(&L.tile_sel[gs + lane])) : 0ull;
+        const uint64_t inc = warp_inclusive_sum<uint64_t>(v);
+        s_pref[lane] = s_base + inc - v;
+        __syncwarp();
+        if (lane == 31) s_base += inc;
+      }
+      __syncthreads();
+      for (int j = warp; j < nt; j += kWarps) {
+        const uint64_t t = gs + j;
+        const uint32_t n = __ldcg(&L.tile_count[t]);
+        const uint32_t* ci = L.cand_idx + t * kTopkTile;
+        const float* cv = L.cand_val + t * kTopkTile;
+        uint64_t gt_run = s_pref[j] & 0xFFFFFFFFull, eq_run = s_pref[j] >> 32;
+        for (uint32_t i0 = 0; i0 < n; i0 += 128) {
+          float v[4];
+          load4(cv, n, i0, v);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t i = i0 + r * 32 + lane;
+            const uint32_t key = abs_key(v[r]);
+            const bool gsel = i < n && key > kth, esel = i < n && key == kth;
+            const uint32_t gbal = __ballot_sync(0xffffffffu, gsel), ebal = __ballot_sync(0xffffffffu, esel);
+            const uint32_t lower = (1u << lane) - 1u;
+            const uint64_t gt_before = gt_run + __popc(gbal & lower);
+            const uint64_t eq_before = eq_run + __popc(ebal & lower);
+            if (gsel || (esel && eq_before < need)) {
+              const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
+              const uint32_t j2 = ci[i];
+              idx_out[pos] = j2;
+              val_out[pos] = v[r];
+              if (zero_at) zero_at[j2] = 0.0f;   // acc - TopK(acc)
+            }
+            gt_run += __popc(gbal);
+            eq_run += __popc(ebal);
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
   mark(c, 7);
 }
