@@ -185,10 +185,13 @@ __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t 
     uint64_t v = 0;
     if (t >= (int64_t)first) {
       uint32_t f;
-      do {
-        f = ld_relaxed_gpu_u32(&st[t].flag);
-      } while ((f & ~3u) != tag || (f & 3u) == 0);
-      fence_acq_rel_gpu();
+      f = ld_acquire_gpu(&st[t].flag);
+      if ((f & ~3u) != tag || (f & 3u) == 0) {
+        do {
+          f = ld_relaxed_gpu_u32(&st[t].flag);
+        } while ((f & ~3u) != tag || (f & 3u) == 0);
+        f = ld_acquire_gpu(&st[t].flag);
+      }
       state = f & 3u;
       v = state == 2u ? ld_relaxed_gpu(&st[t].incl) : ld_relaxed_gpu(&st[t].agg);
     }
@@ -324,8 +327,11 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
 // it; waiters compare wrap-safely against seq + 1 of their own call
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void wait_flag_geq(const uint32_t* f, uint32_t target) {
+  // relaxed polling, then one acquire load of the (already satisfied) flag:
+  // synchronizes-with the producer's release without a full system fence
+  if ((int)(ld_acquire_sys(f) - target) >= 0) return;
   while ((int)(ld_relaxed_sys_u32(f) - target) < 0) __nanosleep(32);
-  fence_acq_rel_sys();
+  (void)ld_acquire_sys(f);
 }
 
 constexpr int kMaxStages = 5;   // recursive doubling: log2(16) stages (+1)
@@ -364,12 +370,12 @@ struct alignas(128) Ctrl {
 };
 
 __device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {
-  // block 0: dbg[0] = %globaltimer (ns), dbg[1] = SM clock (cycles)
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    uint64_t t;
+  // dbg[0][slot] = %globaltimer (ns) of block 0, dbg[1][slot] = the latest block's
+  uint64_t t;
+  if (threadIdx.x == 0) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    c->dbg[0][slot] = t;
-    c->dbg[1][slot] = clock64();
+    if (blockIdx.x == 0) c->dbg[0][slot] = t;
+    atomicMax(reinterpret_cast<unsigned long long*>(&c->dbg[1][slot]), (unsigned long long)t);
   }
 }
 

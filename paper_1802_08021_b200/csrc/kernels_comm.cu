@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
     dv[e] = v;
     if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
   }
-  if (last_block<true>(&a.ctl->done_ctr[0]) && threadIdx.x == 0) {
+  if (last_block<false>(&a.ctl->done_ctr[0]) && threadIdx.x == 0) {   // see split_push_kernel
     a.peer->rd_n[par][1] = a.n;
     a.peer->rd_dense[par][1] = 0;
     a.peer->rd_ksum[par][1] = a.n;
@@ -308,12 +308,13 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
       window_tile(s_src, 2, ts, 0, a.N, w, smem, a.status, s_gen, nwin, wo);
     }
   }
-  // every block fences its (remote) stores before the last block publishes the
-  // stream metadata and the partner's flag
+  // every block completes its (remote) stores at gpu scope before the last
+  // block publishes the stream metadata and the partner's flag (system-scope
+  // release, cumulative over the blocks it synchronized with)
   __syncthreads();
-  if (tid == 0) fence_acq_rel_sys();
+  if (tid == 0) fence_acq_rel_gpu();
   if (scan_block_exit_last(a.ctr) && tid == 0) {
-    fence_acq_rel_sys();
+    fence_acq_rel_gpu();
     const uint64_t on = sparse_out ? *(volatile uint64_t*)&ctl->own_n[t & 1] : a.N;
     const uint64_t ksum = aks + bks;
     const uint64_t obytes = sparse_out ? 8 * on : 4 * a.N;
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
   // slice boundaries s_off[j] = first position with idx >= b_j: block 0 needs
   // all of them (counts, empty slices), the others only those of the owners
   // their element range touches (usually two searches)
+  dbg_mark(a.ctl, 8);
   int j0 = 0, j1 = a.P;
   if (blockIdx.x != 0 && a.n > 0) {
     j0 = (int)std::min<uint64_t>(a.idx[base] / part, a.P - 1);
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
     if (lane == 0) s_off[j] = o;
   }
   __syncthreads();
+  dbg_mark(a.ctl, 9);
 #pragma unroll
   for (int i = 0; i < kPushItems; ++i) {
     const uint64_t e = base + (uint64_t)i * kThreads + tid;
@@ -424,10 +427,15 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
       a.ctl->slice_out[tid] = c;
     }
   }
-  if (last_block<true>(&a.ctl->done_ctr[0]) && tid < a.P) {
+  dbg_mark(a.ctl, 10);
+  // gpu-scope arrival: a gpu-scope fence completes this block's NVLink stores
+  // (they must be visible to every thread of this GPU, which reads the owner's
+  // memory at the owner's L2); the last block then releases at system scope
+  if (last_block<false>(&a.ctl->done_ctr[0]) && tid < a.P) {
     const uint32_t seq = a.ctl->seq;
     st_release_sys(&a.peer[tid]->src_done[a.rank], seq + 1);
   }
+  dbg_mark(a.ctl, 11);
 }
 
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s) {
@@ -816,7 +824,10 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
   }
   if (b == G - 1 && tid == 0) ctl->owner_K = excl + cnt;
   dbg_mark(ctl, 5);
-  if (last_block<true>(&ctl->done_ctr[3]) && tid < P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
+  // every block's writes are local: a gpu-scope arrival suffices; the release
+  // to the peers is system scope (and cumulative over what the last block saw)
+  if (last_block<false>(&ctl->done_ctr[3]) && tid < P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
+  dbg_mark(ctl, 6);
 }
 
 // ===========================================================================
@@ -968,11 +979,8 @@ __global__ void __launch_bounds__(kThreads) owner_kernel(OwnerArgs a) {
     }
     cw += nfit;
   }
-  grid.sync();
-  if (b == 0 && tid < P) {
-    fence_acq_rel_sys();
-    st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
-  }
+  grid.sync();   // orders every block's (local) writes before block 0's system-scope release
+  if (b == 0 && tid < P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
 }
 
 static int owner_occupancy(int nsrc) {
@@ -1062,6 +1070,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
   __shared__ uint64_t s_k[kMaxRanks];
+  dbg_mark(ctl, 12);
   if (tid < a.P) {   // one lane per owner: wait for its flag, read its result size
     if (a.wait_owners) wait_flag_geq(&ctl->owner_done[tid], seq + 1);
     s_k[tid] = *(volatile const uint64_t*)a.r_n[tid];
@@ -1199,6 +1208,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     __threadfence();
     ctl->seq = seq + 1;   // the call is complete on this rank
   }
+  dbg_mark(ctl, 13);
 }
 
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
