@@ -66,6 +66,10 @@ def lib():
         _lib.or_topk.argtypes = [p, u64, u64, p, p, p]
         _lib.or_ef_topk.restype = u64
         _lib.or_ef_topk.argtypes = [p, p, f32, u64, u64, p, p]
+        _lib.or_topk_bucketed.restype = u64
+        _lib.or_topk_bucketed.argtypes = [p, u64, u64, u64, p, p, p]
+        _lib.or_ef_topk_bucketed.restype = u64
+        _lib.or_ef_topk_bucketed.argtypes = [p, p, f32, u64, u64, u64, p, p]
         _lib.or_philox4x32_10.restype = None
         _lib.or_philox4x32_10.argtypes = [p, p, p]
         _lib.or_qsgd_uniform.restype = f32
@@ -233,6 +237,38 @@ def ef_topk(eps, grad, alpha, k):
     io = np.zeros(max(m, 1), np.uint32)
     vo = np.zeros(max(m, 1), np.float32)
     lib().or_ef_topk(_ptr(eps), _ptr(grad), C.c_float(alpha), N, k, _ptr(io), _ptr(vo))
+    return io[:m], vo[:m], eps
+
+
+def bucketed_count(N, k, B):
+    """sum over buckets of min(k, |bucket|)."""
+    full, tail = divmod(N, B)
+    return full * min(k, B) + (min(k, tail) if tail else 0)
+
+
+def topk_bucketed(x, k, B, residual=False):
+    x = _f32(x)
+    N = len(x)
+    m = bucketed_count(N, k, B)
+    io = np.zeros(max(m, 1), np.uint32)
+    vo = np.zeros(max(m, 1), np.float32)
+    res = np.zeros(max(N, 1), np.float32) if residual else None
+    got = lib().or_topk_bucketed(_ptr(x), N, k, B, _ptr(io), _ptr(vo), _ptr(res) if residual else None)
+    assert got == m
+    if residual:
+        return io[:m], vo[:m], res[:N]
+    return io[:m], vo[:m]
+
+
+def ef_topk_bucketed(eps, grad, alpha, k, B):
+    eps = _f32(eps).copy()
+    grad = _f32(grad)
+    N = len(eps)
+    m = bucketed_count(N, k, B)
+    io = np.zeros(max(m, 1), np.uint32)
+    vo = np.zeros(max(m, 1), np.float32)
+    got = lib().or_ef_topk_bucketed(_ptr(eps), _ptr(grad), C.c_float(alpha), N, k, B, _ptr(io), _ptr(vo))
+    assert got == m
     return io[:m], vo[:m], eps
 
 

@@ -418,6 +418,30 @@ uint64_t or_ef_topk(float* eps, const float* grad, float alpha, uint64_t N,
   return or_topk(eps, N, k, idx_out, val_out, eps);              /* eps <- acc - TopK(acc) */
 }
 
+uint64_t or_topk_bucketed(const float* x, uint64_t N, uint64_t k, uint64_t B,
+                          uint32_t* idx_out, float* val_out, float* residual) {
+  /* every bucket of B consecutive coordinates selects its own top k */
+  uint64_t m = 0, b0, j;
+  if (residual && residual != x) memcpy(residual, x, N * sizeof(float));
+  for (b0 = 0; b0 < N; b0 += B) {
+    const uint64_t n = (N - b0 < B) ? N - b0 : B;
+    const uint64_t mb = or_topk(x + b0, n, k, idx_out + m, val_out + m, NULL);
+    for (j = 0; j < mb; j++) {
+      idx_out[m + j] += (uint32_t)b0;                     /* bucket-relative -> global index */
+      if (residual) residual[idx_out[m + j]] = 0.0f;      /* the rest is saved locally */
+    }
+    m += mb;
+  }
+  return m;
+}
+
+uint64_t or_ef_topk_bucketed(float* eps, const float* grad, float alpha, uint64_t N,
+                             uint64_t k, uint64_t B, uint32_t* idx_out, float* val_out) {
+  uint64_t j;
+  for (j = 0; j < N; j++) eps[j] = fmaf(alpha, grad[j], eps[j]);   /* acc */
+  return or_topk_bucketed(eps, N, k, B, idx_out, val_out, eps);
+}
+
 /* ------------------------------------------------------------------------- */
 /* §6 QSGD low-precision encoding                                             */
 /* ------------------------------------------------------------------------- */

@@ -134,6 +134,21 @@ uint64_t or_topk(const float* x, uint64_t N, uint64_t k,
 uint64_t or_ef_topk(float* eps, const float* grad, float alpha, uint64_t N,
                     uint64_t k, uint32_t* idx_out, float* val_out);
 
+/* Bucketed top-k (§7 P:1106-1107 "select k entries from every bucket of 512
+ * consecutive elements"; "split into groups of 512 consecutive
+ * coordinates, out of which we select the 4 largest ones ... saving the rest
+ * locally"): the or_topk rule applied independently to every bucket
+ * [bB, min((b+1)B, N)), reading R-26.  Output: buckets in order, each bucket's
+ * min(k, |bucket|) entries sorted by index, so the whole output is sorted.
+ * residual as in or_topk.  Returns m = sum_b min(k, |bucket b|). */
+uint64_t or_topk_bucketed(const float* x, uint64_t N, uint64_t k, uint64_t B,
+                          uint32_t* idx_out, float* val_out, float* residual);
+
+/* Error feedback with bucketed selection (Algorithm 1 with the §7 selector):
+ * acc = fmaf(alpha, g, eps); (idx, val) = bucketed TopK(acc); eps <- acc - TopK(acc). */
+uint64_t or_ef_topk_bucketed(float* eps, const float* grad, float alpha, uint64_t N,
+                             uint64_t k, uint64_t B, uint32_t* idx_out, float* val_out);
+
 /* Philox4x32-10 block (Salmon et al. SC'11 / Random123; reading R-16 RNG). */
 void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 
