@@ -205,16 +205,21 @@ sparcml_status sparcml_merge_sum(const uint32_t* ia, const float* va, uint64_t n
  * largest |x_j|, ties to the lower index; written sorted by index to
  * idx_out[m], val_out[m] (= x_j).  residual (nullable, may alias x) receives
  * x with the selected coordinates zeroed (acc - TopK(acc)).
- * bucket must be 0 (global top-k).  Requires finite x (NaN/Inf are
- * reported through sparcml_topk_status).  ws from sparcml_topk_workspace_bytes,
- * zero-initialised once with sparcml_ops_workspace_init. */
+ * bucket = 0: global top-k.  bucket > 0 (a multiple of 128, at most 1024):
+ * bucketed top-k (§7; reading R-26) -- the same rule in
+ * every bucket [bB, min((b+1)B, N)) with k per bucket; m = sum_b min(k,|b|)
+ * entries, buckets in order (sorted overall); ws may then be NULL (it only
+ * receives the status).  Requires finite x (NaN/Inf are reported through
+ * sparcml_topk_status).  ws from sparcml_topk_workspace_bytes, zero-initialised
+ * once with sparcml_ops_workspace_init. */
 size_t sparcml_topk_workspace_bytes(uint64_t N, uint64_t k);
 sparcml_status sparcml_topk_sparsify(const float* x, uint64_t N, uint64_t k, uint64_t bucket,
                                      uint32_t* idx_out, float* val_out, float* residual,
                                      void* ws, size_t ws_bytes, void* stream);
 
 /* Error-feedback top-k, Algorithm 1: acc = fmaf(alpha, grad, eps)
- * (one rounding), (idx, val) = TopK(acc), eps <- acc - TopK(acc), in place. */
+ * (one rounding), (idx, val) = TopK(acc), eps <- acc - TopK(acc), in place.
+ * bucket as in sparcml_topk_sparsify. */
 sparcml_status sparcml_ef_topk(float* eps, const float* grad, float alpha, uint64_t N,
                                uint64_t k, uint64_t bucket, uint32_t* idx_out, float* val_out,
                                void* ws, size_t ws_bytes, void* stream);

@@ -774,11 +774,20 @@ static sparcml_status topk_common(const float* x, const float* grad, float alpha
                                   size_t ws_bytes, void* stream) {
   if (N == 0 || k == 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "N and k must be positive");
   if (N > 0xFFFFFFFFull) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "N must fit u32 indices");
-  if (bucket != 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bucketed top-k is not implemented (bucket must be 0)");
+  if (bucket != 0 && (bucket % 128 != 0 || bucket > 1024))
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bucket must be 0 (global) or a multiple of 128 up to 1024");
   if (!x || !io || !vo || (ef && !grad)) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
   auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; };
   if (mis(x) || (grad && mis(grad)) || (resid && mis(resid)))
     return fail(nullptr, SPARCML_ERR_INVALID_ARG, "vectors must be 16-byte aligned");
+  if (bucket != 0) {   // bucketed (§7): no workspace needed; ws (optional) receives the status
+    if (ws && ws_bytes < sizeof(uint64_t) * 64)
+      return fail(nullptr, SPARCML_ERR_INVALID_ARG, "workspace too small");
+    if (resid == x) resid = const_cast<float*>(x);
+    CK(nullptr, launch_topk_bucketed(x, grad, alpha, ef, ef ? xout : resid, N, k, bucket, io, vo, ws,
+                                     static_cast<cudaStream_t>(stream)));
+    return SPARCML_OK;
+  }
   if (k < N && (!ws || ws_bytes < topk_workspace_bytes(N, k)))
     return fail(nullptr, SPARCML_ERR_INVALID_ARG, "workspace too small");
   CK(nullptr, launch_topk(x, grad, alpha, ef, xout, N, k, io, vo, resid, ws, static_cast<cudaStream_t>(stream)));

@@ -207,6 +207,10 @@ size_t topk_workspace_bytes(uint64_t N, uint64_t k);
 cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, float* x_out,
                         uint64_t N, uint64_t k, uint32_t* idx_out, float* val_out, float* residual,
                         void* ws, cudaStream_t s);
+// bucket = 128 * R, R in 1..8; dst = new eps (ef), residual (nullable) otherwise; ws nullable (status)
+cudaError_t launch_topk_bucketed(const float* x, const float* grad, float alpha, int ef, float* dst, uint64_t N,
+                                 uint64_t k, uint64_t bucket, uint32_t* idx_out, float* val_out, void* ws,
+                                 cudaStream_t s);
 cudaError_t launch_quantize(const float* x, uint64_t n, int bits, uint32_t bucket, uint64_t seed,
                             uint64_t ctr_base, uint8_t* codes, float* scales, cudaStream_t s);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, uint64_t n, int bits,

@@ -740,6 +740,212 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
   mark(c, 7);
 }
 
+// ------------------------------------------------------- bucketed ---------
+// Bucketed top-k (§7; reading R-26): one warp per bucket
+// of B = 128*R consecutive values, held in registers (R float4 per lane).
+// The k-th largest |v| of the bucket is found by a 4-pass 8-bit radix select
+// over the magnitude bit patterns (per-warp 256-bin shared histogram); the
+// selected pairs are written in index order at bucket * min(k, B), and the
+// residual / new eps (the unselected values, "saving the rest
+// locally") is stored in the same pass.  HBM-bound: one read of x (+ g), one
+// write of the residual.
+struct BucketCtl {   // in the top-k workspace's control block (status only)
+  uint32_t bad, done;
+};
+
+template <int R, bool EF, bool STORE>
+__global__ void __launch_bounds__(kThreads) topk_bucketed_kernel(const float* __restrict__ x,
+                                                                 const float* __restrict__ g, float alpha,
+                                                                 float* __restrict__ dst, uint64_t N, uint32_t k,
+                                                                 uint32_t* __restrict__ idx_out,
+                                                                 float* __restrict__ val_out, TopkCtl* ctl) {
+  constexpr int B = 128 * R;
+  __shared__ uint32_t hist[kWarps][256];
+  __shared__ uint32_t s_bad;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  uint32_t* h = hist[warp];
+  const uint64_t nb = (N + B - 1) / B;
+  const uint32_t kb = k < (uint32_t)B ? k : (uint32_t)B;   // outputs of a full bucket
+  const uint64_t pol = l2_evict_first_policy();
+  uint32_t bad = 0;
+  for (uint64_t bk = (uint64_t)blockIdx.x * kWarps + warp; bk < nb; bk += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t b0 = bk * B;
+    const uint32_t n = (uint32_t)std::min<uint64_t>(B, N - b0);
+    float v[R][4];
+    uint32_t key[R][4];
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const uint32_t e = c * 128 + lane * 4;
+      if (e + 4 <= n) {
+        const float4 a = ld_stream_f4_ef(reinterpret_cast<const float4*>(x + b0 + e), pol);
+        v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+        if (EF) {
+          const float4 q = ld_stream_f4_ef(reinterpret_cast<const float4*>(g + b0 + e), pol);
+          v[c][0] = __fmaf_rn(alpha, q.x, v[c][0]);
+          v[c][1] = __fmaf_rn(alpha, q.y, v[c][1]);
+          v[c][2] = __fmaf_rn(alpha, q.z, v[c][2]);
+          v[c][3] = __fmaf_rn(alpha, q.w, v[c][3]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[c][q] = e + q < n ? x[b0 + e + q] : 0.0f;
+          if (EF && e + q < n) v[c][q] = __fmaf_rn(alpha, g[b0 + e + q], v[c][q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        key[c][q] = e + q < n ? abs_key(v[c][q]) : 0u;
+        bad |= (e + q < n) && key[c][q] >= 0x7F800000u;
+      }
+    }
+    const uint32_t m = k < n ? k : n;   // selected in this bucket
+    uint32_t kth = 0, ties = n;         // select key > kth, plus the first `ties` with key == kth
+    if (m < n) {
+      uint32_t prefix = 0, pmask = 0, need = m;
+#pragma unroll 1
+      for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) h[lane * 8 + i] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c * 128 + lane * 4 + q < n && (key[c][q] & pmask) == prefix) atomicAdd(&h[(key[c][q] >> shift) & 255u], 1u);
+        __syncwarp();
+        // lane l scans digits 255-8l .. 248-8l (descending)
+        uint32_t cnt[8], loc = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          cnt[i] = h[255 - lane * 8 - i];
+          loc += cnt[i];
+        }
+        const uint32_t incl = warp_inclusive_sum<uint32_t>(loc);
+        const uint32_t before = incl - loc;
+        const bool mine = before < need && incl >= need;
+        uint32_t d = 0, above = 0;
+        if (mine) {
+          uint32_t cum = before;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (cum + cnt[i] >= need && cum < need) {
+              d = 255 - lane * 8 - i;
+              above = cum;
+            }
+            cum += cnt[i];
+          }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        d = __shfl_sync(0xffffffffu, d, src);
+        above = __shfl_sync(0xffffffffu, above, src);
+        need -= above;
+        prefix |= d << shift;
+        pmask |= 0xFFu << shift;
+        __syncwarp();
+      }
+      kth = prefix;
+      ties = need;
+    }
+    // index order: chunk c, then lane, then q
+    const uint64_t obase = bk * kb;
+    uint32_t run_sel = 0, run_eq = 0;
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      uint32_t gtf = 0, eqf = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool in = c * 128 + lane * 4 + q < n;
+        if (in && (m == n || key[c][q] > kth)) gtf |= 1u << q;
+        else if (in && key[c][q] == kth) eqf |= 1u << q;
+      }
+      const uint32_t ne = __popc(eqf);
+      const uint32_t eq_incl = warp_inclusive_sum<uint32_t>(ne);
+      uint32_t eq_before = run_eq + eq_incl - ne;
+      uint32_t self = gtf;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (eqf & (1u << q)) {
+          if (eq_before < ties) self |= 1u << q;
+          ++eq_before;
+        }
+      const uint32_t ns = __popc(self);
+      const uint32_t s_incl = warp_inclusive_sum<uint32_t>(ns);
+      uint32_t pos = run_sel + s_incl - ns;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (self & (1u << q)) {
+          idx_out[obase + pos] = (uint32_t)(b0 + c * 128 + lane * 4 + q);
+          val_out[obase + pos] = v[c][q];
+          ++pos;
+        }
+      run_sel += __shfl_sync(0xffffffffu, s_incl, 31);
+      run_eq += __shfl_sync(0xffffffffu, eq_incl, 31);
+      if (STORE) {   // residual / new eps: the unselected values
+        const uint32_t e = c * 128 + lane * 4;
+        float o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = (self & (1u << q)) ? 0.0f : v[c][q];
+        if (e + 4 <= n) st_stream_f4_ef(reinterpret_cast<float4*>(dst + b0 + e), make_float4(o[0], o[1], o[2], o[3]), pol);
+        else
+          for (int q = 0; q < 4; ++q)
+            if (e + q < n) dst[b0 + e + q] = o[q];
+      }
+    }
+  }
+  // status: non-finite input seen by any block (the last block publishes it)
+  if (ctl) {
+    if (bad) s_bad = 1;
+    __syncthreads();
+    if (tid == 0) {
+      BucketCtl* bc = reinterpret_cast<BucketCtl*>(&ctl->t_phase[15]);
+      if (s_bad) atomicOr(&bc->bad, 1u);
+      __threadfence();
+      if (atomicAdd(&bc->done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        ctl->status = atomicExch(&bc->bad, 0u) ? 1u : 0u;
+        ctl->passes = 1;
+        bc->done = 0;
+      }
+    }
+  }
+}
+
+template <int R>
+static cudaError_t launch_bucketed_r(const float* x, const float* grad, float alpha, int ef, float* dst, uint64_t N,
+                                     uint32_t k, uint32_t* io, float* vo, TopkCtl* ctl, cudaStream_t s) {
+  const uint64_t nb = (N + 128 * R - 1) / (128 * R);
+  const unsigned blocks = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>((nb + kWarps - 1) / kWarps, (uint64_t)device_sm_count() * 8));
+  if (ef) topk_bucketed_kernel<R, true, true><<<blocks, kThreads, 0, s>>>(x, grad, alpha, dst, N, k, io, vo, ctl);
+  else if (dst) topk_bucketed_kernel<R, false, true><<<blocks, kThreads, 0, s>>>(x, nullptr, 0.0f, dst, N, k, io, vo, ctl);
+  else topk_bucketed_kernel<R, false, false><<<blocks, kThreads, 0, s>>>(x, nullptr, 0.0f, nullptr, N, k, io, vo, ctl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_bucketed(const float* x, const float* grad, float alpha, int ef, float* dst, uint64_t N,
+                                 uint64_t k, uint64_t bucket, uint32_t* io, float* vo, void* ws, cudaStream_t s) {
+  TopkCtl* ctl = ws ? reinterpret_cast<TopkCtl*>(ws) : nullptr;
+  const uint32_t kk = (uint32_t)std::min<uint64_t>(k, bucket);
+  SPARCML_PROF("topk_bucketed", s);
+  cudaError_t e;
+  switch (bucket / 128) {
+    case 1: e = launch_bucketed_r<1>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 2: e = launch_bucketed_r<2>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 3: e = launch_bucketed_r<3>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 4: e = launch_bucketed_r<4>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 5: e = launch_bucketed_r<5>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 6: e = launch_bucketed_r<6>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 7: e = launch_bucketed_r<7>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    case 8: e = launch_bucketed_r<8>(x, grad, alpha, ef, dst, N, kk, io, vo, ctl, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  ++g_launches;
+  return e;
+}
+
 // --------------------------------------------------------- k >= N ---------
 template <bool EF>
 __global__ void topk_all_kernel(const float* __restrict__ x, const float* __restrict__ g, float alpha,

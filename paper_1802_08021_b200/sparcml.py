@@ -149,7 +149,7 @@ def profile_read(name: str):
     return int(n.value), float(ms.value)
 
 
-PROFILED_KERNELS = ["topk", "topk_all", "split_push", "owner", "owner_dsar",
+PROFILED_KERNELS = ["topk", "topk_all", "topk_bucketed", "split_push", "owner", "owner_dsar",
                     "barrier", "merge", "window", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
                     "dequantize"]
 
@@ -373,32 +373,44 @@ class TopkWorkspace:
         return int(st.value), int(ps.value)
 
 
+def topk_count(N: int, k: int, bucket: int = 0) -> int:
+    """Entries a top-k call writes: min(k, N) (global) or sum over buckets of min(k, |bucket|)."""
+    if bucket == 0:
+        return min(k, N)
+    full, tail = divmod(N, bucket)
+    return full * min(k, bucket) + (min(k, tail) if tail else 0)
+
+
 def topk_sparsify(x: torch.Tensor, k: int, residual: Optional[torch.Tensor] = None, ws: Optional[TopkWorkspace] = None,
-                  idx_out=None, val_out=None, stream=None):
-    """Top-k by magnitude, ties to the lower index; returns (idx int32, val float32) sorted by index."""
+                  idx_out=None, val_out=None, stream=None, bucket: int = 0):
+    """Top-k by magnitude, ties to the lower index; returns (idx int32, val float32) sorted by index.
+    bucket > 0 (a multiple of 128, <= 1024): k per bucket of `bucket` consecutive values (§7)."""
     _need(x, torch.float32, "x")
     N = x.numel()
-    m = min(k, N)
-    ws = ws or TopkWorkspace(N, k, x.device)
+    m = topk_count(N, k, bucket)
+    if bucket == 0:
+        ws = ws or TopkWorkspace(N, k, x.device)
     io = idx_out if idx_out is not None else torch.empty(m, dtype=torch.int32, device=x.device)
     vo = val_out if val_out is not None else torch.empty(m, dtype=torch.float32, device=x.device)
-    _check(_lib.sparcml_topk_sparsify(x.data_ptr(), N, k, 0, io.data_ptr(), vo.data_ptr(), _ptr(residual),
-                                      ws.buf.data_ptr(), ws.bytes, _stream(stream)))
+    _check(_lib.sparcml_topk_sparsify(x.data_ptr(), N, k, bucket, io.data_ptr(), vo.data_ptr(), _ptr(residual),
+                                      ws.buf.data_ptr() if ws else None, ws.bytes if ws else 0, _stream(stream)))
     return io, vo
 
 
 def ef_topk(eps: torch.Tensor, grad: torch.Tensor, alpha: float, k: int, ws: Optional[TopkWorkspace] = None,
-            idx_out=None, val_out=None, stream=None):
-    """Algorithm 1: acc = eps + alpha*grad (one fma), select TopK(acc), eps <- acc - TopK(acc)."""
+            idx_out=None, val_out=None, stream=None, bucket: int = 0):
+    """Algorithm 1: acc = eps + alpha*grad (one fma), select TopK(acc), eps <- acc - TopK(acc).
+    bucket > 0: the §7 per-bucket selection."""
     _need(eps, torch.float32, "eps")
     _need(grad, torch.float32, "grad")
     N = eps.numel()
-    m = min(k, N)
-    ws = ws or TopkWorkspace(N, k, eps.device)
+    m = topk_count(N, k, bucket)
+    if bucket == 0:
+        ws = ws or TopkWorkspace(N, k, eps.device)
     io = idx_out if idx_out is not None else torch.empty(m, dtype=torch.int32, device=eps.device)
     vo = val_out if val_out is not None else torch.empty(m, dtype=torch.float32, device=eps.device)
-    _check(_lib.sparcml_ef_topk(eps.data_ptr(), grad.data_ptr(), alpha, N, k, 0, io.data_ptr(), vo.data_ptr(),
-                                ws.buf.data_ptr(), ws.bytes, _stream(stream)))
+    _check(_lib.sparcml_ef_topk(eps.data_ptr(), grad.data_ptr(), alpha, N, k, bucket, io.data_ptr(), vo.data_ptr(),
+                                ws.buf.data_ptr() if ws else None, ws.bytes if ws else 0, _stream(stream)))
     return io, vo
 
 

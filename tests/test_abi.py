@@ -75,7 +75,13 @@ def test_argument_errors_need_no_gpu(lib):
     assert e.value.status == S.ERR_INVALID_ARG
     rc = S._lib.sparcml_topk_sparsify(None, 0, 1, 0, None, None, None, None, 0, None)
     assert rc == S.ERR_INVALID_ARG
+    rc = S._lib.sparcml_topk_sparsify(None, 100, 5, 500, None, None, None, None, 0, None)
+    assert rc == S.ERR_INVALID_ARG        # bucket must be a multiple of 128
+    rc = S._lib.sparcml_topk_sparsify(None, 100, 5, 2048, None, None, None, None, 0, None)
+    assert rc == S.ERR_INVALID_ARG        # ... at most 1024
     rc = S._lib.sparcml_topk_sparsify(None, 100, 5, 512, None, None, None, None, 0, None)
-    assert rc == S.ERR_INVALID_ARG        # bucketed top-k: not on the hot path yet
+    assert rc == S.ERR_INVALID_ARG        # null x
+    assert S.topk_count(1000, 4, 512) == 8 and S.topk_count(1100, 600, 512) == 512 + 512 + 76
+    assert S.topk_count(10, 3, 0) == 3
     rc = S._lib.sparcml_sparse_allreduce(None, None, None, 0, 10, 0, None, None, 0, None)
     assert rc == S.ERR_INVALID_ARG

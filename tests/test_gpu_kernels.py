@@ -161,3 +161,61 @@ def test_qsgd_parity(orc, n, bits, B):
     np.testing.assert_array_equal(s.cpu().numpy(), es)
     d = S.dequantize(c.clone(), s, n, bits, bucket=B)
     np.testing.assert_array_equal(d.cpu().numpy(), orc.qsgd_dequantize(ec, es, n, bits, B))
+
+
+# ---- bucketed top-k (§7; reading R-26) -------------------
+BUCKET_CASES = [
+    (512, 4, 512), (513, 4, 512), (1 << 20, 4, 512), (1 << 20, 16, 512), (1_000_003, 8, 512),
+    (100_000, 2, 128), (100_000, 50, 384), (300_001, 100, 1024), (70_000, 1024, 1024), (5000, 700, 512),
+    (129, 1, 128), (1, 1, 128),
+]
+
+
+@pytest.mark.parametrize("N,k,B", BUCKET_CASES)
+def test_topk_bucketed_parity(orc, N, k, B):
+    x = synth.gaussian_vector(N, seed=N % 89 + k + B)
+    xt = cu(x, torch.float32)
+    res = torch.empty_like(xt)
+    io, vo = S.topk_sparsify(xt, k, residual=res, bucket=B)
+    ei, ev, er = orc.topk_bucketed(x, k, B, residual=True)
+    np.testing.assert_array_equal(host_idx(io), ei)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    np.testing.assert_array_equal(res.cpu().numpy(), er)
+
+
+def test_topk_bucketed_ties_and_in_place(orc):
+    rng = np.random.default_rng(12)
+    for N, k, B in [(4096, 5, 512), (200_003, 17, 256), (1 << 20, 8, 1024)]:
+        x = (rng.integers(-4, 5, size=N) * 0.5).astype(np.float32)   # massive ties, zeros
+        xt = cu(x, torch.float32)
+        io, vo = S.topk_sparsify(xt, k, residual=xt, bucket=B)        # residual aliases x
+        ei, ev, er = orc.topk_bucketed(x, k, B, residual=True)
+        np.testing.assert_array_equal(host_idx(io), ei)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+        np.testing.assert_array_equal(xt.cpu().numpy(), er)
+
+
+@pytest.mark.parametrize("N,k,B", [(1 << 20, 4, 512), (25_557_032 // 16, 8, 512), (99_999, 3, 128)])
+def test_ef_topk_bucketed_parity(orc, N, k, B):
+    eps = synth.gaussian_vector(N, seed=15) * np.float32(0.1)
+    g = synth.gaussian_vector(N, seed=16)
+    et, gt = cu(eps, torch.float32), cu(g, torch.float32)
+    ws = S.TopkWorkspace(N, k)
+    for step in range(3):
+        io, vo = S.ef_topk(et, gt, 0.05, k, bucket=B, ws=ws)
+        ei, ev, eps = orc.ef_topk_bucketed(eps, g, 0.05, k, B)
+        np.testing.assert_array_equal(host_idx(io), ei)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+        np.testing.assert_array_equal(et.cpu().numpy(), eps)
+        assert ws.status() == (0, 1)
+
+
+def test_topk_bucketed_nonfinite_reported():
+    x = synth.gaussian_vector(1 << 16, seed=19)
+    x[4321] = np.nan
+    ws = S.TopkWorkspace(len(x), 4)
+    S.topk_sparsify(cu(x, torch.float32), 4, ws=ws, bucket=512)
+    assert ws.status()[0] == S.ERR_NONFINITE
+    x[4321] = 0.5
+    S.topk_sparsify(cu(x, torch.float32), 4, ws=ws, bucket=512)
+    assert ws.status()[0] == 0
