@@ -40,7 +40,22 @@ CONFIGS = {
                  N=25_557_032, density=0.001, algo="rd", bits=0),
     "cfg4": dict(desc="BASELINE configs[3]: N=2^24, density 10%, DSAR_Split_allgather with QSGD 4-bit",
                  N=1 << 24, density=0.10, algo="dsar", bits=4),
+    # the paper's DNN selector, k of every bucket of 512
+    "bucket512": dict(desc="NEXT (SURVEY 8f rank 2): bucketed EF top-k, 4 of every 512 (P:1238), of a "
+                           "25,557,032-parameter Gaussian gradient, SSAR_Split_allgather",
+                      N=25_557_032, density=4 / 512, algo="ssar_split", bits=0, bucket=512, kb=4),
 }
+
+
+def step_k(cfg, N=None):
+    """(k passed to top-k, entries it writes)."""
+    N = cfg["N"] if N is None else N
+    if cfg.get("bucket"):
+        B, kb = cfg["bucket"], cfg["kb"]
+        full, tail = divmod(N, B)
+        return kb, full * min(kb, B) + (min(kb, tail) if tail else 0)
+    k = max(1, int(cfg["density"] * N))
+    return k, k
 
 
 def parse():
@@ -140,13 +155,16 @@ def oracle_step_time(cfg, P_sim, N_s, seed=0):
     import numpy as np
     import oracle
     from paper_1802_08021_b200 import synth
-    k = max(1, int(cfg["density"] * N_s))
+    k, _ = step_k(cfg, N_s)
     grads = [synth.gaussian_vector(N_s, seed=seed, rank=r) for r in range(P_sim)]
     eps = [np.zeros(N_s, np.float32) for _ in range(P_sim)]
     t0 = time.perf_counter()
     streams = []
     for r in range(P_sim):
-        i, v, eps[r] = oracle.ef_topk(eps[r], grads[r], 0.01, k)
+        if cfg.get("bucket"):
+            i, v, eps[r] = oracle.ef_topk_bucketed(eps[r], grads[r], 0.01, k, cfg["bucket"])
+        else:
+            i, v, eps[r] = oracle.ef_topk(eps[r], grads[r], 0.01, k)
         streams.append((i, v))
     if P_sim > 1:
         if cfg["algo"] == "rd":
@@ -212,7 +230,10 @@ def main():
     from paper_1802_08021_b200 import synth
 
     N = cfg["N"]
-    k = synth.k_for_density(N, cfg["density"])
+    bucket = cfg.get("bucket", 0)
+    kk, k = step_k(cfg)                 # kk: top-k's k (per bucket if bucketed), k: entries per rank
+    if not bucket:
+        assert k == synth.k_for_density(N, cfg["density"])
     algo = {"ssar_split": S.SSAR_SPLIT_ALLGATHER, "rd": S.SSAR_RECURSIVE_DOUBLE,
             "dsar": S.DSAR_SPLIT_ALLGATHER}[cfg["algo"]]
     if algo == S.SSAR_RECURSIVE_DOUBLE and (P & (P - 1)) != 0:
@@ -238,7 +259,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def topk():
-        S.ef_topk(eps, grad, alpha, k, ws=ws, idx_out=idx, val_out=val)
+        S.ef_topk(eps, grad, alpha, kk, ws=ws, idx_out=idx, val_out=val, bucket=bucket)
 
     def allreduce():
         comm.allreduce(idx, val, N, out=out, opts=opts)
@@ -347,11 +368,15 @@ def main():
     alg_bytes = 12 * N + 8 * k          # read eps + grad, write eps (+ k candidates) per launch
     achieved = alg_bytes / t_filter / 1e9 if t_filter > 0 else None
     total_prof_ms = sum(v[1] for v in prof.values())
-    roofline = {"kernel": "topk_fused_kernel<EF> (ef_topk: one HBM pass + candidate select)", "bound": "hbm",
+    kname = ("topk_bucketed_kernel<EF> (ef_topk, bucket %d: one HBM pass, radix select per bucket)" % bucket
+             if bucket else "topk_fused_kernel<EF> (ef_topk: one HBM pass + candidate select)")
+    roofline = {"kernel": kname, "bound": "hbm",
                 "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": (achieved / hbm_peak) if achieved else None, "traffic": ncu_traffic("topk"),
+                "frac": (achieved / hbm_peak) if achieved else None,
+                "traffic": ncu_traffic("topk_bucketed" if bucket else "topk"),
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_us": t_filter * 1e6, "peak_source": peak_src,
-                "share_of_step": (prof.get("topk", (0, 0.0))[1] / total_prof_ms) if total_prof_ms else None}
+                "share_of_step": (prof.get("topk_bucketed" if bucket else "topk", (0, 0.0))[1] / total_prof_ms)
+                if total_prof_ms else None}
 
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
@@ -416,7 +441,7 @@ def main():
         ts = [oracle_step_time(cfg, 1, N_s, seed=s) for s in range(2)]
         t_cpu = min(ts)
         cpu = {"value": 4 * N_s / t_cpu / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"EF top-k (qsort) of N/4 = {N_s} values, 1 rank, best of 2; "
+               "sample": f"EF top-k{' (bucketed)' if bucket else ''} (qsort) of N/4 = {N_s} values, 1 rank, best of 2; "
                          f"{t_cpu:.2f} s per sample on one host core"}
 
     clocks = clk.summary()
@@ -427,6 +452,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "N": N, "k_per_rank": k,
+                       "bucket": bucket or None, "k_per_bucket": kk if bucket else None,
                        "density": cfg["density"], "P": P, "algo": {1: "SSAR_Recursive_double",
                        2: "SSAR_Split_allgather", 3: "DSAR_Split_allgather"}[algo],
                        "quant_bits": cfg["bits"], "l2": "flushed before every step (512 MiB write + 512 MiB read, no dirty lines left)",

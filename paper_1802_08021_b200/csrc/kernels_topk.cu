@@ -754,7 +754,7 @@ struct BucketCtl {   // in the top-k workspace's control block (status only)
 };
 
 template <int R, bool EF, bool STORE>
-__global__ void __launch_bounds__(kThreads) topk_bucketed_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(kThreads, (R <= 4 ? 4 : 2)) topk_bucketed_kernel(const float* __restrict__ x,
                                                                  const float* __restrict__ g, float alpha,
                                                                  float* __restrict__ dst, uint64_t N, uint32_t k,
                                                                  uint32_t* __restrict__ idx_out,
@@ -774,7 +774,6 @@ __global__ void __launch_bounds__(kThreads) topk_bucketed_kernel(const float* __
     const uint64_t b0 = bk * B;
     const uint32_t n = (uint32_t)std::min<uint64_t>(B, N - b0);
     float v[R][4];
-    uint32_t key[R][4];
 #pragma unroll
     for (int c = 0; c < R; ++c) {
       const uint32_t e = c * 128 + lane * 4;
@@ -796,58 +795,95 @@ __global__ void __launch_bounds__(kThreads) topk_bucketed_kernel(const float* __
         }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        key[c][q] = e + q < n ? abs_key(v[c][q]) : 0u;
-        bad |= (e + q < n) && key[c][q] >= 0x7F800000u;
-      }
+      for (int q = 0; q < 4; ++q) bad |= (e + q < n) && abs_key(v[c][q]) >= 0x7F800000u;
     }
     const uint32_t m = k < n ? k : n;   // selected in this bucket
-    uint32_t kth = 0, ties = n;         // select key > kth, plus the first `ties` with key == kth
+    // selected: (key & selmask) > kth, plus the first `ties` (index order) of
+    // the group (key & selmask) == kth with key >= T
+    uint32_t kth = 0, ties = n, selmask = 0xFFFFFFFFu, T = 0;
     if (m < n) {
-      uint32_t prefix = 0, pmask = 0, need = m;
-#pragma unroll 1
-      for (int shift = 24; shift >= 0; shift -= 8) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) h[lane * 8 + i] = 0;
-        __syncwarp();
+      // prefilter: T = the m-th largest lane maximum (m <= 32).  At least m
+      // elements are >= T, so the k-th largest is >= T: only elements >= T
+      // (usually about m of them) enter the radix select.
+      if (m <= 32) {
+        uint32_t lm = 0;
 #pragma unroll
         for (int c = 0; c < R; ++c)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (c * 128 + lane * 4 + q < n && (key[c][q] & pmask) == prefix) atomicAdd(&h[(key[c][q] >> shift) & 255u], 1u);
-        __syncwarp();
-        // lane l scans digits 255-8l .. 248-8l (descending)
-        uint32_t cnt[8], loc = 0;
+            if (c * 128 + lane * 4 + q < n) lm = max(lm, abs_key(v[c][q]));
+        // bitonic sort of the 32 lane maxima, descending along the lanes
+        uint32_t sv = lm;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          cnt[i] = h[255 - lane * 8 - i];
-          loc += cnt[i];
-        }
-        const uint32_t incl = warp_inclusive_sum<uint32_t>(loc);
-        const uint32_t before = incl - loc;
-        const bool mine = before < need && incl >= need;
-        uint32_t d = 0, above = 0;
-        if (mine) {
-          uint32_t cum = before;
+        for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+          for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, sv, jj);
+            const bool up = ((lane & kk) == 0) == ((lane & jj) == 0);   // keep the larger
+            sv = up ? max(sv, o) : min(sv, o);
+          }
+        T = __shfl_sync(0xffffffffu, sv, (int)m - 1);
+      }
+      uint32_t C = 0;
+#pragma unroll
+      for (int c = 0; c < R; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) C += (c * 128 + lane * 4 + q < n && abs_key(v[c][q]) >= T) ? 1u : 0u;
+      C = warp_sum<uint32_t>(C);
+      if (C == m) {   // exactly the candidates: select key >= T
+        kth = T;
+        ties = n;
+      } else {
+        uint32_t prefix = 0, pmask = 0, need = m;
+#pragma unroll
+        for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) h[lane * 8 + i] = 0;
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < R; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (c * 128 + lane * 4 + q < n && abs_key(v[c][q]) >= T && (abs_key(v[c][q]) & pmask) == prefix)
+                atomicAdd(&h[(abs_key(v[c][q]) >> shift) & 255u], 1u);
+          __syncwarp();
+          // lane l scans digits 255-8l .. 248-8l (descending)
+          uint32_t cnt[8], loc = 0;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (cum + cnt[i] >= need && cum < need) {
-              d = 255 - lane * 8 - i;
-              above = cum;
-            }
-            cum += cnt[i];
+            cnt[i] = h[255 - lane * 8 - i];
+            loc += cnt[i];
           }
+          const uint32_t incl = warp_inclusive_sum<uint32_t>(loc);
+          const uint32_t before = incl - loc;
+          const bool mine = before < need && incl >= need;
+          uint32_t d = 0, above = 0, grp = 0;
+          if (mine) {
+            uint32_t cum = before;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (cum + cnt[i] >= need && cum < need) {
+                d = 255 - lane * 8 - i;
+                above = cum;
+                grp = cnt[i];
+              }
+              cum += cnt[i];
+            }
+          }
+          const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+          d = __shfl_sync(0xffffffffu, d, src);
+          above = __shfl_sync(0xffffffffu, above, src);
+          grp = __shfl_sync(0xffffffffu, grp, src);
+          need -= above;
+          prefix |= d << shift;
+          pmask |= 0xFFu << shift;
+          __syncwarp();
+          if (grp == need) break;   // the whole group is selected: stop at this digit
         }
-        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
-        d = __shfl_sync(0xffffffffu, d, src);
-        above = __shfl_sync(0xffffffffu, above, src);
-        need -= above;
-        prefix |= d << shift;
-        pmask |= 0xFFu << shift;
-        __syncwarp();
+        kth = prefix;
+        selmask = pmask;
+        ties = need;
       }
-      kth = prefix;
-      ties = need;
     }
     // index order: chunk c, then lane, then q
     const uint64_t obase = bk * kb;
@@ -858,19 +894,24 @@ __global__ void __launch_bounds__(kThreads) topk_bucketed_kernel(const float* __
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const bool in = c * 128 + lane * 4 + q < n;
-        if (in && (m == n || key[c][q] > kth)) gtf |= 1u << q;
-        else if (in && key[c][q] == kth) eqf |= 1u << q;
+        const uint32_t mk = abs_key(v[c][q]) & selmask;
+        if (in && (m == n || mk > kth)) gtf |= 1u << q;
+        else if (in && mk == kth && abs_key(v[c][q]) >= T) eqf |= 1u << q;
       }
-      const uint32_t ne = __popc(eqf);
-      const uint32_t eq_incl = warp_inclusive_sum<uint32_t>(ne);
-      uint32_t eq_before = run_eq + eq_incl - ne;
-      uint32_t self = gtf;
+      uint32_t self = gtf | eqf;
+      if (ties < n) {   // only a prefix of the group (index order) is selected
+        const uint32_t ne = __popc(eqf);
+        const uint32_t eq_incl = warp_inclusive_sum<uint32_t>(ne);
+        uint32_t eq_before = run_eq + eq_incl - ne;
+        self = gtf;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (eqf & (1u << q)) {
-          if (eq_before < ties) self |= 1u << q;
-          ++eq_before;
-        }
+        for (int q = 0; q < 4; ++q)
+          if (eqf & (1u << q)) {
+            if (eq_before < ties) self |= 1u << q;
+            ++eq_before;
+          }
+        run_eq += __shfl_sync(0xffffffffu, eq_incl, 31);
+      }
       const uint32_t ns = __popc(self);
       const uint32_t s_incl = warp_inclusive_sum<uint32_t>(ns);
       uint32_t pos = run_sel + s_incl - ns;
@@ -882,7 +923,6 @@ __global__ void __launch_bounds__(kThreads) topk_bucketed_kernel(const float* __
           ++pos;
         }
       run_sel += __shfl_sync(0xffffffffu, s_incl, 31);
-      run_eq += __shfl_sync(0xffffffffu, eq_incl, 31);
       if (STORE) {   // residual / new eps: the unselected values
         const uint32_t e = c * 128 + lane * 4;
         float o[4];
