@@ -397,8 +397,9 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   p.algo = cc.o.algo;
   p.ctl = my;
   p.validate = cc.o.validate;
-  CK(c, launch_p1_prep(p, cc.s));
   const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER || (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
+  p.win = dsar ? win_table(L, base, 0) : nullptr;
+  CK(c, launch_p1_prep(p, cc.s));
   ConcatArgs a = {};
   a.P = 1;
   a.rank = 0;
@@ -409,32 +410,31 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   a.r_idx[0] = idx;
   a.r_val[0] = val;
   a.r_n[0] = &my->owner_K;
-  if (dsar) {
-    WindowArgs w = {};
-    w.nsrc = 1;
-    w.src[0].idx = idx;
-    w.src[0].val = val;
-    w.src[0].n = n;
-    w.sched.n = 0;
+  if (dsar) {   // densify (+ QSGD) the one partition with the DSAR owner kernel
+    OwnerArgs w = {};
+    w.P = 1;
+    w.rank = 0;
+    w.algo = SPARCML_DSAR_SPLIT_ALLGATHER;
+    w.delta = cc.delta;
     w.lo = 0;
     w.hi = cc.N;
-    if (cc.o.quant_bits) {
-      w.out.mode = WIN_QUANT;
-      w.out.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
-      w.out.scales = reinterpret_cast<float*>(base + L.scales_off);
-      w.out.qbase = 0;
-      w.out.bits = cc.o.quant_bits;
-      w.out.bucket = cc.o.quant_bucket;
-      w.out.seed_lo = (uint32_t)cc.o.seed;
-      w.out.seed_hi = (uint32_t)(cc.o.seed >> 32);
-    } else {
-      w.out.mode = WIN_DENSE;
-      w.out.dense = reinterpret_cast<float*>(base + L.part_off);
-      w.out.dense_base = 0;
-    }
-    w.ctr = &my->scan[0];
-    w.status = status_of(L, base);
-    CK(c, launch_window(w, cc.s));
+    w.src_idx[0] = idx;
+    w.src_val[0] = val;
+    w.src_win[0] = win_table(L, base, 0);   // built by p1_prep
+    w.n1 = n;
+    w.sched = make_sched(1);
+    w.dense = reinterpret_cast<float*>(base + L.part_off);
+    w.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
+    w.scales = reinterpret_cast<float*>(base + L.scales_off);
+    w.bits = cc.o.quant_bits;
+    w.bucket = cc.o.quant_bucket;
+    w.seed_lo = (uint32_t)cc.o.seed;
+    w.seed_hi = (uint32_t)(cc.o.seed >> 32);
+    w.host_dsar = 1;
+    w.wait = 0;
+    w.peer[0] = my;
+    w.ctl = my;
+    CK(c, launch_owner(w, cc.s));
     a.r_codes[0] = reinterpret_cast<const uint8_t*>(base + L.part_off);
     a.r_scales[0] = reinterpret_cast<const float*>(base + L.scales_off);
     a.r_dense[0] = reinterpret_cast<const float*>(base + L.part_off);

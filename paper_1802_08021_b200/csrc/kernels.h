@@ -135,6 +135,7 @@ struct OwnerArgs {
   uint32_t* st_idx;
   float* st_val;
   uint64_t* blk;
+  uint64_t n1;                     // P == 1 without window tables (src_win[0] == nullptr): the input's nnz
 };
 
 struct ConcatArgs {
@@ -165,13 +166,14 @@ struct BarrierArgs {
   int loopback;                     // no waiting (all ranks on one stream)
 };
 
-struct P1PrepArgs {                 // P == 1: validate and fill the control block
+struct P1PrepArgs {                 // P == 1: validate, fill the control block, (DSAR) window table
   const uint32_t* idx;
   const float* val;
   uint64_t n, N, delta;
   int algo;
   Ctrl* ctl;
   int validate;
+  uint32_t* win;                    // nullable: build the window-offset table (ntab + 1 entries)
 };
 
 // ----------------------------------------------------------- launchers -----

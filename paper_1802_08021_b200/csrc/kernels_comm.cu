@@ -831,167 +831,136 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
 }
 
 // ===========================================================================
-// owner reduction, DSAR (§5.3.3 + §6): one cooperative kernel
-// densifies my partition window by window in the canonical tree order (R-8)
-// and stores it dense or QSGD-encoded in place.
+// owner reduction, DSAR (§5.3.3 + §6): one block per 1024-position
+// window of my partition (windows never straddle a QSGD bucket, B <= 1024).
+// The P sources' elements of the window (located with the window-offset
+// tables, or a binary search when P == 1) are scattered into per-source value
+// rows, combined per position by the canonical tree (R-8), and the dense
+// window is stored, or QSGD-encoded in place (Philox per element, the bucket
+// max from a block reduction).  Every output lands at a fixed offset: no
+// prefix, no grid-wide sync; the last block to finish flags the P readers.
 // ===========================================================================
-constexpr int kOwnElems = 2048;   // elements staged in shared memory per chunk
-constexpr int kOwnWins = 32;      // windows per chunk
+__host__ __device__ constexpr size_t dsar_smem_bytes(int P) { return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)P; }
 
-__host__ __device__ constexpr size_t owner_smem_bytes(int nsrc) {
-  return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)nsrc + 8 * (size_t)kOwnElems;
-}
-
-__global__ void __launch_bounds__(kThreads) owner_kernel(OwnerArgs a) {
+template <int P>
+__global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int P = a.P;
   uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
   float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
-  uint32_t* eidx = reinterpret_cast<uint32_t*>(smem + sizeof(uint32_t) * kWin + sizeof(float) * kWin * P);
-  float* evals = reinterpret_cast<float*>(eidx + kOwnElems);
-  __shared__ uint32_t s_tab[kMaxRanks][kOwnWins + 1];   // window offsets of this chunk
-  __shared__ uint32_t s_soff[kMaxRanks + 1];             // staged-element offset per source
-  __shared__ uint32_t s_wpre[kMaxRanks + 1];             // per-window element prefix over sources
-  __shared__ uint32_t s_bmax[kWin / 8];
-  __shared__ uint32_t s_dsar, s_nfit, s_direct;
   __shared__ uint64_t s_ks[kMaxRanks];
-  cg::grid_group grid = cg::this_grid();
-  const int tid = threadIdx.x;
+  __shared__ uint32_t s_dsar, s_bmax[kWin / 8];
+  __shared__ uint32_t s_e0[P], s_pre[P + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
   if (!owner_prologue(a, seq, s_ks, &s_dsar)) return;   // SSAR: the merge kernel reduces
-  const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint64_t nwin = ceil_div(a.hi - a.lo, kWin);
-  const uint64_t ntab = ceil_div(a.hi - a.lo, kTab);
-  const uint64_t w0 = nwin * b / G, w1 = nwin * (b + 1) / G;
-  for (uint64_t cw = w0; cw < w1;) {
-    const int nw = (int)std::min<uint64_t>(kOwnWins, w1 - cw);
-    // (1) the chunk's window offsets, every source at once
-    for (int q = tid; q < P * (nw + 1); q += kThreads) {
-      const int s = q / (nw + 1), i = q % (nw + 1);
-      s_tab[s][i] = a.src_win[s][std::min<uint64_t>((cw + i) * kTabPerWin, ntab)];
+  const uint64_t w = blockIdx.x;
+  const uint64_t wlo = a.lo + w * kWin;
+  const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
+  // (1) each source's element range in this window
+  if (P == 1 && a.src_win[0] == nullptr) {
+    if (warp == 0) {
+      const uint64_t e0 = warp_lower_bound(a.src_idx[0], a.n1, wlo);
+      const uint64_t e1 = e0 + warp_lower_bound(a.src_idx[0] + e0, a.n1 - e0, wlo + wn);
+      if (lane == 0) {
+        s_e0[0] = (uint32_t)e0;
+        s_pre[0] = 0;
+        s_pre[1] = (uint32_t)(e1 - e0);
+      }
     }
-    __syncthreads();
-    if (tid == 0) {   // how many windows fit in the staging buffer
-      int nfit = 0;
-      for (int i = 1; i <= nw; ++i) {
-        uint32_t tot = 0;
-        for (int s = 0; s < P; ++s) tot += s_tab[s][i] - s_tab[s][0];
-        if (tot > (uint32_t)kOwnElems) break;
-        nfit = i;
-      }
-      s_direct = nfit == 0;   // a single window larger than the buffer: read it from global
-      if (nfit == 0) nfit = 1;
-      s_nfit = nfit;
-      uint32_t run = 0;
-      for (int s = 0; s < P; ++s) {
-        s_soff[s] = run;
-        if (!s_direct) run += s_tab[s][nfit] - s_tab[s][0];
-      }
-      s_soff[P] = run;
+  } else if (warp == 0) {
+    const uint64_t ntab = ceil_div(a.hi - a.lo, kTab);
+    uint32_t e0 = 0, n = 0;
+    if (lane < P) {
+      e0 = __ldcg(&a.src_win[lane][std::min<uint64_t>(w * kTabPerWin, ntab)]);
+      n = __ldcg(&a.src_win[lane][std::min<uint64_t>((w + 1) * kTabPerWin, ntab)]) - e0;
     }
-    __syncthreads();
-    const int nfit = (int)s_nfit;
-    const bool direct = s_direct != 0;
-    // (2) stage the elements of those windows, every source at once
-    for (uint32_t u = tid; u < s_soff[P]; u += kThreads) {
-      int s = 0;
-      while (u >= s_soff[s + 1]) ++s;
-      const uint32_t e = s_tab[s][0] + (u - s_soff[s]);
-      eidx[u] = a.src_idx[s][e];
-      evals[u] = a.src_val[s][e];
+    const uint32_t incl = warp_inclusive_sum<uint32_t>(n);
+    if (lane < P) {
+      s_e0[lane] = e0;
+      s_pre[lane] = incl - n;
     }
-    __syncthreads();
-    for (int i = 0; i < nfit; ++i) {
-      const uint64_t w = cw + i;
-      const uint64_t wlo = a.lo + w * kWin;
-      const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
-#pragma unroll
-      for (int q = 0; q < kWinPerThread; ++q) pres[tid + q * kThreads] = 0u;
-      if (tid == 0) {
-        uint32_t run = 0;
-        for (int s = 0; s < P; ++s) {
-          s_wpre[s] = run;
-          run += s_tab[s][i + 1] - s_tab[s][i];
-        }
-        s_wpre[P] = run;
-      }
-      __syncthreads();
-      for (uint32_t u = tid; u < s_wpre[P]; u += kThreads) {
-        int s = 0;
-        while (u >= s_wpre[s + 1]) ++s;
-        const uint32_t k = u - s_wpre[s];
-        uint32_t x;
-        float v;
-        if (direct) {
-          const uint32_t e = s_tab[s][i] + k;
-          x = a.src_idx[s][e];
-          v = a.src_val[s][e];
-        } else {
-          const uint32_t su = s_soff[s] + (s_tab[s][i] - s_tab[s][0]) + k;
-          x = eidx[su];
-          v = evals[su];
-        }
-        const uint32_t pos = x - (uint32_t)wlo;
-        if (pos < (uint32_t)wn) {
-          vals[s * kWin + pos] = v;
-          atomicOr(&pres[pos], 1u << s);
-        }
-      }
-      __syncthreads();
-      const int p0 = tid * kWinPerThread;
-      float r[kWinPerThread];
-      uint32_t present = 0;
-#pragma unroll
-      for (int q = 0; q < kWinPerThread; ++q) {
-        const int p = p0 + q;
-        uint32_t m = (p < wn) ? pres[p] : 0u;
-        if (m & (m - 1)) {   // two or more sources: canonical tree (R-8)
-          for (int t = 0; t < a.sched.n; ++t) {
-            const int d = a.sched.dst[t], sr = a.sched.src[t];
-            if (m & (1u << sr)) {
-              if (m & (1u << d)) {
-                vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[sr * kWin + p]);
-              } else {
-                vals[d * kWin + p] = vals[sr * kWin + p];
-                m |= 1u << d;
-              }
-            }
-          }
-          r[q] = vals[p];
-        } else if (m) {
-          r[q] = vals[(__ffs(m) - 1) * kWin + p];
-        } else {
-          r[q] = 0.0f;
-        }
-        if (m) present |= 1u << q;
-      }
-      if (a.bits) {
-        const uint64_t e = w * kWin + p0;   // partition-relative
-        const int rem = wn - p0;
-        const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
-        qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
-      } else {
-        float* d = a.dense + w * kWin + p0;
-        for (int q = 0; q < kWinPerThread && p0 + q < wn; ++q) d[q] = r[q];
-      }
-      __syncthreads();
-    }
-    cw += nfit;
+    if (lane == P - 1) s_pre[P] = incl;
   }
-  grid.sync();   // orders every block's (local) writes before block 0's system-scope release
-  if (b == 0 && tid < P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
+#pragma unroll
+  for (int q = 0; q < kWinPerThread; ++q) pres[tid + q * kThreads] = 0u;
+  __syncthreads();
+  // (2) scatter, every source at once, 4 element loads in flight per thread
+  const uint32_t tot = s_pre[P];
+  for (uint32_t b0 = 0; b0 < tot; b0 += 4 * kThreads) {
+    uint32_t xi[4];
+    float xv[4];
+    int xs[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t u = b0 + q * kThreads + tid;
+      xs[q] = -1;
+      if (u < tot) {
+        int s = 0;
+#pragma unroll
+        for (int j = 1; j < P; ++j) s += s_pre[j] <= u ? 1 : 0;
+        const uint32_t e = s_e0[s] + (u - s_pre[s]);
+        xi[q] = __ldcg(&a.src_idx[s][e]);
+        xv[q] = __ldcg(&a.src_val[s][e]);
+        xs[q] = s;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (xs[q] >= 0) {
+        const uint32_t pos = xi[q] - (uint32_t)wlo;
+        vals[xs[q] * kWin + pos] = xv[q];
+        atomicOr(&pres[pos], 1u << xs[q]);
+      }
+  }
+  __syncthreads();
+  // (3) combine per position in the canonical tree order
+  const int p0 = tid * kWinPerThread;
+  float r[kWinPerThread];
+#pragma unroll
+  for (int q = 0; q < kWinPerThread; ++q) {
+    const int p = p0 + q;
+    uint32_t m = (p < wn) ? pres[p] : 0u;
+    if (P > 1 && (m & (m - 1))) {
+      for (int t = 0; t < a.sched.n; ++t) {
+        const int d = a.sched.dst[t], sr = a.sched.src[t];
+        if (m & (1u << sr)) {
+          if (m & (1u << d)) vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[sr * kWin + p]);
+          else {
+            vals[d * kWin + p] = vals[sr * kWin + p];
+            m |= 1u << d;
+          }
+        }
+      }
+      r[q] = vals[p];
+    } else {
+      r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : 0.0f;
+    }
+  }
+  // (4) store: QSGD codes + scales, or dense
+  const uint64_t e = w * kWin + p0;   // partition-relative
+  if (a.bits) {
+    const int rem = wn - p0;
+    const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+    qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
+  } else if (p0 + 4 <= wn) {
+    reinterpret_cast<float4*>(a.dense + e)[0] = make_float4(r[0], r[1], r[2], r[3]);
+  } else {
+    for (int q = 0; q < kWinPerThread && p0 + q < wn; ++q) a.dense[e + q] = r[q];
+  }
+  if (last_block<false>(&ctl->done_ctr[3]) && tid < a.P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
 }
 
-static int owner_occupancy(int nsrc) {
-  static int cache[kMaxRanks + 1] = {0};
-  if (!cache[nsrc]) {
-    int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, owner_kernel, kThreads, owner_smem_bytes(nsrc));
-    cache[nsrc] = std::max(1, per);
+using DsarFn = void (*)(OwnerArgs);
+template <int... Ps>
+struct DsarTable {
+  static DsarFn get(int P) {
+    DsarFn f = nullptr;
+    ((P == Ps ? (f = dsar_owner_kernel<Ps>, 0) : 0), ...);
+    return f;
   }
-  return cache[nsrc];
-}
+};
+static DsarFn dsar_fn(int P) { return DsarTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P); }
 
 using OwnerMergeFn = void (*)(OwnerArgs);
 template <int... Ps>
@@ -1019,11 +988,6 @@ static int owner_merge_occupancy(int P) {
 }
 
 cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(owner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)owner_smem_bytes(kMaxRanks));
-    attr = true;
-  }
   if (a.host_dsar != 1) {   // SSAR (or undecided: the kernel exits if the device picks DSAR)
     const uint64_t G = (uint64_t)owner_merge_occupancy(a.P) * device_sm_count();
     OwnerArgs ac = a;
@@ -1037,18 +1001,18 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   if (a.host_dsar != 0) {   // DSAR (or undecided: the kernel exits if the device picks SSAR)
-    const size_t smem = owner_smem_bytes(a.P);
+    const DsarFn f = dsar_fn(a.P);
+    static bool dattr[kMaxRanks + 1] = {false};
+    if (!dattr[a.P]) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsar_smem_bytes(a.P));
+      dattr[a.P] = true;
+    }
     const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
-    const uint64_t G =
-        std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)owner_occupancy(a.P) * device_sm_count()));
-    OwnerArgs ac = a;
-    void* args[] = {(void*)&ac};
     SPARCML_PROF("owner_dsar", s);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_kernel, dim3((unsigned)G), dim3(kThreads), args,
-                                                smem, s);
+    f<<<(unsigned)std::max<uint64_t>(1, nwin), kThreads, dsar_smem_bytes(a.P), s>>>(a);
     ++g_launches;
+    const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return cudaGetLastError();
   }
   return cudaSuccess;
 }
@@ -1101,36 +1065,75 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     groups[0] = 0;
     for (int j = 0; j < a.P; ++j) groups[j + 1] = groups[j] + ceil_div(a.bnd[j + 1] - a.bnd[j], 8);
     const uint32_t s = a.bits ? (1u << (a.bits - 1)) - 1u : 0u;
-    for (uint64_t g = gtid; g < groups[a.P]; g += gstride) {
-      int j = 0;
-      while (g >= groups[j + 1]) ++j;
-      const uint64_t e = (g - groups[j]) * 8;
-      const uint64_t nj = a.bnd[j + 1] - a.bnd[j];
-      const int cnt = (int)((nj - e) < 8 ? (nj - e) : 8);
-      float v[8];
-      if (a.bits) {
-        const uint8_t* cp = a.r_codes[j] + (e * a.bits) / 8;
-        uint64_t word = 0;
-        const int nbytes = (cnt * a.bits + 7) / 8;
-        if (cnt == 8 && a.bits == 4) word = *reinterpret_cast<const uint32_t*>(cp);
-        else if (cnt == 8 && a.bits == 8) word = *reinterpret_cast<const unsigned long long*>(cp);
-        else if (cnt == 8 && a.bits == 2) word = *reinterpret_cast<const uint16_t*>(cp);
-        else
-          for (int q = 0; q < nbytes; ++q) word |= (uint64_t)cp[q] << (8 * q);
-        const float scale = a.r_scales[j][e / a.bucket];
-        const uint32_t mask = (1u << a.bits) - 1u;
+    // fl(level / s) for every level: the decode's one division, tabulated
+    __shared__ float s_lvl[128];
+    for (uint32_t l = tid; l <= s && a.bits; l += kThreads) s_lvl[l] = __fdiv_rn(__uint2float_rn(l), __uint2float_rn(s));
+    __syncthreads();
+    constexpr int U = 4;   // groups per thread per iteration: all their loads in flight
+    for (uint64_t g0 = gtid; g0 < groups[a.P]; g0 += gstride * U) {
+      uint64_t word[U];
+      float scale[U];
+      float4 dv[U][2];
+      int jj[U], cnt[U];
+      uint64_t ee[U];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = qsgd_decode((uint32_t)(word >> (i * a.bits)) & mask, scale, s, a.bits);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = i < cnt ? a.r_dense[j][e + i] : 0.0f;
+      for (int u = 0; u < U; ++u) {
+        const uint64_t g = g0 + (uint64_t)u * gstride;
+        cnt[u] = 0;
+        if (g >= groups[a.P]) continue;
+        int j = 0;
+        while (g >= groups[j + 1]) ++j;
+        const uint64_t e = (g - groups[j]) * 8;
+        const uint64_t nj = a.bnd[j + 1] - a.bnd[j];
+        jj[u] = j;
+        ee[u] = e;
+        cnt[u] = (int)((nj - e) < 8 ? (nj - e) : 8);
+        if (a.bits) {
+          const uint8_t* cp = a.r_codes[j] + (e * a.bits) / 8;
+          uint64_t wv = 0;
+          if (cnt[u] == 8 && a.bits == 4) wv = *reinterpret_cast<const uint32_t*>(cp);
+          else if (cnt[u] == 8 && a.bits == 8) wv = *reinterpret_cast<const unsigned long long*>(cp);
+          else if (cnt[u] == 8 && a.bits == 2) wv = *reinterpret_cast<const uint16_t*>(cp);
+          else {
+            const int nbytes = (cnt[u] * a.bits + 7) / 8;
+            for (int q = 0; q < nbytes; ++q) wv |= (uint64_t)cp[q] << (8 * q);
+          }
+          word[u] = wv;
+          scale[u] = a.r_scales[j][e / a.bucket];
+        } else if (cnt[u] == 8) {
+          const float4* src = reinterpret_cast<const float4*>(a.r_dense[j] + e);
+          dv[u][0] = src[0];
+          dv[u][1] = src[1];
+        }
       }
-      float* d = out_dense + a.bnd[j] + e;
-      if (cnt == 8 && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
-        reinterpret_cast<float4*>(d)[0] = make_float4(v[0], v[1], v[2], v[3]);
-        reinterpret_cast<float4*>(d)[1] = make_float4(v[4], v[5], v[6], v[7]);
-      } else {
-        for (int i = 0; i < cnt; ++i) d[i] = v[i];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (cnt[u] == 0) continue;
+        const int j = jj[u];
+        const uint64_t e = ee[u];
+        float v[8];
+        if (a.bits) {
+          const uint32_t mask = (1u << a.bits) - 1u;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t code = (uint32_t)(word[u] >> (i * a.bits)) & mask;
+            const float mag = __fmul_rn(s_lvl[code & s], scale[u]);   // = qsgd_decode (R-16)
+            v[i] = (code >> (a.bits - 1)) ? -mag : mag;
+          }
+        } else if (cnt[u] == 8) {
+          v[0] = dv[u][0].x; v[1] = dv[u][0].y; v[2] = dv[u][0].z; v[3] = dv[u][0].w;
+          v[4] = dv[u][1].x; v[5] = dv[u][1].y; v[6] = dv[u][1].z; v[7] = dv[u][1].w;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = i < cnt[u] ? a.r_dense[j][e + i] : 0.0f;
+        }
+        float* d = out_dense + a.bnd[j] + e;
+        if (cnt[u] == 8 && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
+          reinterpret_cast<float4*>(d)[0] = make_float4(v[0], v[1], v[2], v[3]);
+          reinterpret_cast<float4*>(d)[1] = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
+          for (int i = 0; i < cnt[u]; ++i) d[i] = v[i];
+        }
       }
     }
   } else if (K <= a.delta) {
@@ -1256,10 +1259,23 @@ cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
 // P == 1: the collective is the identity on the stream (or its densified /
 // QSGD-coded form); validate and fill the control block the concat reads.
 __global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
-  if (a.validate) {
-    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
-    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride)
-      check_input(a.idx, e, a.n, a.N, a.idx[e], a.val[e], &a.ctl->status);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  if (a.validate || a.win) {
+    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride) {
+      const uint32_t x = a.idx[e];
+      if (a.validate) check_input(a.idx, e, a.n, a.N, x, a.val[e], &a.ctl->status);
+      if (a.win) {   // window-offset table of the one partition (as split_push builds for owners)
+        const int64_t w = (int64_t)(x / kTab);
+        const int64_t wprev = e == 0 ? -1 : (int64_t)(a.idx[e - 1] / kTab);
+        for (int64_t q = wprev + 1; q <= w; ++q) a.win[q] = (uint32_t)e;
+        if (e + 1 == a.n) {
+          const int64_t ntab = (int64_t)ceil_div(a.N, kTab);
+          for (int64_t q = w + 1; q <= ntab; ++q) a.win[q] = (uint32_t)a.n;
+        }
+      }
+    }
+    if (a.win && a.n == 0)
+      for (uint64_t q = (uint64_t)blockIdx.x * kThreads + threadIdx.x; q <= ceil_div(a.N, kTab); q += stride) a.win[q] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctrl* c = a.ctl;
@@ -1275,8 +1291,9 @@ __global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
 }
 
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
-  const uint64_t blocks =
-      a.validate ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 1024)) : 1;
+  const uint64_t blocks = (a.validate || a.win)
+                              ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 4096))
+                              : 1;
   SPARCML_PROF("p1_prep", s);
   p1_prep_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;

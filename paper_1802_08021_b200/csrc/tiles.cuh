@@ -255,21 +255,22 @@ __device__ __forceinline__ void qsgd_block_encode(const float r[4], int valid, u
                                                   uint32_t B, uint32_t k0, uint32_t k1, uint8_t* __restrict__ codes,
                                                   float* __restrict__ scales, uint32_t* bmax) {
   const int tid = threadIdx.x;
-  const uint32_t tpb = B / 4;             // threads per bucket (>= 2)
+  const uint32_t lgB = 31u - __clz(B);    // B is a power of two (8..1024)
+  const uint32_t lgt = lgB - 2;           // threads per bucket = B/4 (>= 2)
   float m = 0.0f;
 #pragma unroll
   for (int i = 0; i < 4; ++i) m = fmaxf(m, i < valid ? fabsf(r[i]) : 0.0f);
-  const uint32_t seg = tpb < 32 ? tpb : 32;
+  const uint32_t seg = lgt < 5 ? (1u << lgt) : 32u;
   for (uint32_t o = 1; o < seg; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const int nb_win = (kThreads * 4) / (int)B;
+  const int nb_win = (kThreads * 4) >> lgB;
   for (int b = tid; b < nb_win; b += kThreads) bmax[b] = 0u;
   __syncthreads();
-  if ((tid % seg) == 0) atomicMax(&bmax[tid / tpb], __float_as_uint(m));
+  if ((tid & (seg - 1)) == 0) atomicMax(&bmax[tid >> lgt], __float_as_uint(m));
   __syncthreads();
-  const float scale = __uint_as_float(bmax[tid / tpb]);
+  const float scale = __uint_as_float(bmax[tid >> lgt]);
   if (valid > 0) {
     qsgd_encode4(r, scale, e, c0, valid, bits, k0, k1, codes);
-    if ((e % B) == 0) scales[e / B] = scale;
+    if ((e & (B - 1)) == 0) scales[e >> lgB] = scale;
   }
 }
 
