@@ -377,6 +377,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     a.val_offset = cc.val_offset;
     a.algo = SPARCML_SSAR_SPLIT_ALLGATHER;
     a.status = status_of(L, c->peer[r]);
+    a.host_dsar = cc.host_dsar;
     CK(c, launch_concat(a, cc.s));
   }
   return SPARCML_OK;
@@ -447,6 +448,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   a.val_offset = cc.val_offset;
   a.algo = cc.o.algo == SPARCML_ALGO_AUTO ? SPARCML_SSAR_SPLIT_ALLGATHER : cc.o.algo;
   a.status = status_of(L, base);
+  a.host_dsar = dsar ? 1 : 0;
   CK(c, launch_concat(a, cc.s));
   return SPARCML_OK;
 }

@@ -157,6 +157,7 @@ struct ConcatArgs {
   uint64_t val_offset;
   uint32_t algo;
   TileStatus* status;
+  int host_dsar;                   // -1: launch both concat variants (the device decides), else 0/1
 };
 
 struct BarrierArgs {

@@ -1024,6 +1024,10 @@ int owner_grid_size() { return device_sm_count() * 8; }
 // partition result over NVLink straight into the caller's out (sparse
 // concatenation, densification, or QSGD decode), then write the header
 // ===========================================================================
+// MODE 0: sparse result paths only (SSAR concat, K > delta densify); MODE 1:
+// DSAR decode only.  Each instantiation returns at once unless the device's
+// SSAR/DSAR decision is its case (separate register budgets).
+template <int MODE>
 __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t s_pref[kMaxRanks + 1];
@@ -1052,6 +1056,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   }
   __syncthreads();
   const bool dsar = s_dsar != 0;
+  if (dsar != (MODE == 1)) return;
   const uint64_t K = s_pref[a.P];
   float* out_dense = reinterpret_cast<float*>(a.out + SPARCML_HEADER_BYTES);
   uint32_t* out_idx = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
@@ -1059,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   const uint64_t gstride = (uint64_t)gridDim.x * kThreads;
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + tid;
   bool dense_result = dsar;
-  if (dsar) {
+  if (MODE == 1) {
     // decode partitions in groups of 8 (partition-relative)
     uint64_t groups[kMaxRanks + 1];
     groups[0] = 0;
@@ -1218,13 +1223,20 @@ cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
   static bool attr = false;
   const size_t smem = win_smem_bytes(1);
   if (!attr) {
-    cudaFuncSetAttribute(concat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(concat_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(concat_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const int grid = device_sm_count() * 4;
   SPARCML_PROF("concat", s);
-  concat_kernel<<<grid, kThreads, smem, s>>>(a);
-  ++g_launches;
+  if (a.host_dsar != 1) {
+    concat_kernel<0><<<grid, kThreads, smem, s>>>(a);
+    ++g_launches;
+  }
+  if (a.host_dsar != 0) {
+    concat_kernel<1><<<grid, kThreads, smem, s>>>(a);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 
