@@ -370,13 +370,19 @@ struct alignas(128) Ctrl {
 };
 
 __device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {
-  // dbg[0][slot] = %globaltimer (ns) of block 0, dbg[1][slot] = the latest block's
+  // dbg[0][slot] = %globaltimer (ns) of block 0, dbg[1][slot] = the latest
+  // block's.  Compiled in only with -DSPARCML_DEBUG_MARKS (diagnostics).
+#ifdef SPARCML_DEBUG_MARKS
   uint64_t t;
   if (threadIdx.x == 0) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x == 0) c->dbg[0][slot] = t;
     atomicMax(reinterpret_cast<unsigned long long*>(&c->dbg[1][slot]), (unsigned long long)t);
   }
+#else
+  (void)c;
+  (void)slot;
+#endif
 }
 
 }  // namespace sparcml

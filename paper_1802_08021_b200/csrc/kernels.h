@@ -135,7 +135,7 @@ struct OwnerArgs {
   uint32_t* st_idx;
   float* st_val;
   uint64_t* blk;
-  uint64_t n1;                     // P == 1 without window tables (src_win[0] == nullptr): the input's nnz
+  uint64_t n1;                     // P == 1: the input's nnz (diagnostics)
 };
 
 struct ConcatArgs {

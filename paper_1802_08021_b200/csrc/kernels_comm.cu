@@ -854,99 +854,101 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
   if (!owner_prologue(a, seq, s_ks, &s_dsar)) return;   // SSAR: the merge kernel reduces
-  const uint64_t w = blockIdx.x;
-  const uint64_t wlo = a.lo + w * kWin;
-  const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
-  // (1) each source's element range in this window
-  if (P == 1 && a.src_win[0] == nullptr) {
-    if (warp == 0) {
-      const uint64_t e0 = warp_lower_bound(a.src_idx[0], a.n1, wlo);
-      const uint64_t e1 = e0 + warp_lower_bound(a.src_idx[0] + e0, a.n1 - e0, wlo + wn);
-      if (lane == 0) {
-        s_e0[0] = (uint32_t)e0;
-        s_pre[0] = 0;
-        s_pre[1] = (uint32_t)(e1 - e0);
-      }
-    }
-  } else if (warp == 0) {
-    const uint64_t ntab = ceil_div(a.hi - a.lo, kTab);
-    uint32_t e0 = 0, n = 0;
+  const uint64_t nwin = ceil_div(a.hi - a.lo, kWin);
+  const uint64_t ntab = ceil_div(a.hi - a.lo, kTab);
+  // window w's [first element, count) per source, from the tables; loaded one
+  // window ahead (warp 0, lane = source) so the loads overlap the current window
+  auto tab_load = [&](uint64_t w, uint32_t& e0, uint32_t& e1) {
     if (lane < P) {
       e0 = __ldcg(&a.src_win[lane][std::min<uint64_t>(w * kTabPerWin, ntab)]);
-      n = __ldcg(&a.src_win[lane][std::min<uint64_t>((w + 1) * kTabPerWin, ntab)]) - e0;
+      e1 = __ldcg(&a.src_win[lane][std::min<uint64_t>((w + 1) * kTabPerWin, ntab)]);
     }
-    const uint32_t incl = warp_inclusive_sum<uint32_t>(n);
-    if (lane < P) {
-      s_e0[lane] = e0;
-      s_pre[lane] = incl - n;
-    }
-    if (lane == P - 1) s_pre[P] = incl;
-  }
-#pragma unroll
-  for (int q = 0; q < kWinPerThread; ++q) pres[tid + q * kThreads] = 0u;
-  __syncthreads();
-  // (2) scatter, every source at once, 4 element loads in flight per thread
-  const uint32_t tot = s_pre[P];
-  for (uint32_t b0 = 0; b0 < tot; b0 += 4 * kThreads) {
-    uint32_t xi[4];
-    float xv[4];
-    int xs[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t u = b0 + q * kThreads + tid;
-      xs[q] = -1;
-      if (u < tot) {
-        int s = 0;
-#pragma unroll
-        for (int j = 1; j < P; ++j) s += s_pre[j] <= u ? 1 : 0;
-        const uint32_t e = s_e0[s] + (u - s_pre[s]);
-        xi[q] = __ldcg(&a.src_idx[s][e]);
-        xv[q] = __ldcg(&a.src_val[s][e]);
-        xs[q] = s;
+  };
+  uint32_t c0 = 0, c1 = 0, n0 = 0, n1 = 0;
+  if (warp == 0 && blockIdx.x < nwin) tab_load(blockIdx.x, c0, c1);
+  for (uint64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
+    const uint64_t wlo = a.lo + w * kWin;
+    const int wn = (int)std::min<uint64_t>(kWin, a.hi - wlo);
+    // (1) each source's element range in this window (and prefetch the next)
+    if (warp == 0) {
+      const uint32_t n = lane < P ? c1 - c0 : 0u;
+      const uint32_t incl = warp_inclusive_sum<uint32_t>(n);
+      if (lane < P) {
+        s_e0[lane] = c0;
+        s_pre[lane] = incl - n;
       }
+      if (lane == P - 1) s_pre[P] = incl;
+      if (w + gridDim.x < nwin) tab_load(w + gridDim.x, n0, n1);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (xs[q] >= 0) {
-        const uint32_t pos = xi[q] - (uint32_t)wlo;
-        vals[xs[q] * kWin + pos] = xv[q];
-        atomicOr(&pres[pos], 1u << xs[q]);
-      }
-  }
-  __syncthreads();
-  // (3) combine per position in the canonical tree order
-  const int p0 = tid * kWinPerThread;
-  float r[kWinPerThread];
+    for (int q = 0; q < kWinPerThread; ++q) pres[tid + q * kThreads] = 0u;
+    __syncthreads();
+    // (2) scatter, every source at once, 4 element loads in flight per thread
+    const uint32_t tot = s_pre[P];
+    for (uint32_t b0 = 0; b0 < tot; b0 += 4 * kThreads) {
+      uint32_t xi[4];
+      float xv[4];
+      int xs[4];
 #pragma unroll
-  for (int q = 0; q < kWinPerThread; ++q) {
-    const int p = p0 + q;
-    uint32_t m = (p < wn) ? pres[p] : 0u;
-    if (P > 1 && (m & (m - 1))) {
-      for (int t = 0; t < a.sched.n; ++t) {
-        const int d = a.sched.dst[t], sr = a.sched.src[t];
-        if (m & (1u << sr)) {
-          if (m & (1u << d)) vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[sr * kWin + p]);
-          else {
-            vals[d * kWin + p] = vals[sr * kWin + p];
-            m |= 1u << d;
-          }
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t u = b0 + q * kThreads + tid;
+        xs[q] = -1;
+        if (u < tot) {
+          int s = 0;
+#pragma unroll
+          for (int j = 1; j < P; ++j) s += s_pre[j] <= u ? 1 : 0;
+          const uint32_t e = s_e0[s] + (u - s_pre[s]);
+          xi[q] = __ldcg(&a.src_idx[s][e]);
+          xv[q] = __ldcg(&a.src_val[s][e]);
+          xs[q] = s;
         }
       }
-      r[q] = vals[p];
-    } else {
-      r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : 0.0f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (xs[q] >= 0) {
+          const uint32_t pos = xi[q] - (uint32_t)wlo;
+          vals[xs[q] * kWin + pos] = xv[q];
+          atomicOr(&pres[pos], 1u << xs[q]);
+        }
     }
-  }
-  // (4) store: QSGD codes + scales, or dense
-  const uint64_t e = w * kWin + p0;   // partition-relative
-  if (a.bits) {
-    const int rem = wn - p0;
-    const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
-    qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
-  } else if (p0 + 4 <= wn) {
-    reinterpret_cast<float4*>(a.dense + e)[0] = make_float4(r[0], r[1], r[2], r[3]);
-  } else {
-    for (int q = 0; q < kWinPerThread && p0 + q < wn; ++q) a.dense[e + q] = r[q];
+    __syncthreads();
+    // (3) combine per position in the canonical tree order
+    const int p0 = tid * kWinPerThread;
+    float r[kWinPerThread];
+#pragma unroll
+    for (int q = 0; q < kWinPerThread; ++q) {
+      const int p = p0 + q;
+      uint32_t m = (p < wn) ? pres[p] : 0u;
+      if (P > 1 && (m & (m - 1))) {
+        for (int t = 0; t < a.sched.n; ++t) {
+          const int d = a.sched.dst[t], sr = a.sched.src[t];
+          if (m & (1u << sr)) {
+            if (m & (1u << d)) vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[sr * kWin + p]);
+            else {
+              vals[d * kWin + p] = vals[sr * kWin + p];
+              m |= 1u << d;
+            }
+          }
+        }
+        r[q] = vals[p];
+      } else {
+        r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : 0.0f;
+      }
+    }
+    // (4) store: QSGD codes + scales, or dense
+    const uint64_t e = w * kWin + p0;   // partition-relative
+    if (a.bits) {
+      const int rem = wn - p0;
+      const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+      qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
+    } else if (p0 + 4 <= wn) {
+      reinterpret_cast<float4*>(a.dense + e)[0] = make_float4(r[0], r[1], r[2], r[3]);
+    } else {
+      for (int q = 0; q < kWinPerThread && p0 + q < wn; ++q) a.dense[e + q] = r[q];
+    }
+    c0 = n0;
+    c1 = n1;
+    __syncthreads();   // vals / pres / s_pre reused by the next window
   }
   if (last_block<false>(&ctl->done_ctr[3]) && tid < a.P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
 }
@@ -1007,9 +1009,15 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsar_smem_bytes(a.P));
       dattr[a.P] = true;
     }
+    static int occ[kMaxRanks + 1] = {0};
+    if (!occ[a.P]) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.P], f, kThreads, dsar_smem_bytes(a.P));
+      occ[a.P] = std::max(1, occ[a.P]);
+    }
     const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
+    const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)occ[a.P] * device_sm_count()));
     SPARCML_PROF("owner_dsar", s);
-    f<<<(unsigned)std::max<uint64_t>(1, nwin), kThreads, dsar_smem_bytes(a.P), s>>>(a);
+    f<<<(unsigned)G, kThreads, dsar_smem_bytes(a.P), s>>>(a);
     ++g_launches;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1065,79 +1073,90 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + tid;
   bool dense_result = dsar;
   if (MODE == 1) {
-    // decode partitions in groups of 8 (partition-relative)
-    uint64_t groups[kMaxRanks + 1];
-    groups[0] = 0;
-    for (int j = 0; j < a.P; ++j) groups[j + 1] = groups[j] + ceil_div(a.bnd[j + 1] - a.bnd[j], 8);
-    const uint32_t s = a.bits ? (1u << (a.bits - 1)) - 1u : 0u;
-    // fl(level / s) for every level: the decode's one division, tabulated
+    // decode partitions in warp units of 128 positions (partition-relative;
+    // a partition's last unit may be short): lane l decodes positions
+    // [e + 4l, e + 4l + 4) -- coalesced code loads and float4 stores
+    __shared__ uint64_t s_units[kMaxRanks + 1];
     __shared__ float s_lvl[128];
+    const uint32_t s = a.bits ? (1u << (a.bits - 1)) - 1u : 0u;
+    if (tid == 0) {
+      s_units[0] = 0;
+      for (int j = 0; j < a.P; ++j) s_units[j + 1] = s_units[j] + ceil_div(a.bnd[j + 1] - a.bnd[j], 128);
+    }
+    // fl(level / s) for every level: the decode's one division, tabulated
     for (uint32_t l = tid; l <= s && a.bits; l += kThreads) s_lvl[l] = __fdiv_rn(__uint2float_rn(l), __uint2float_rn(s));
     __syncthreads();
-    constexpr int U = 4;   // groups per thread per iteration: all their loads in flight
-    for (uint64_t g0 = gtid; g0 < groups[a.P]; g0 += gstride * U) {
-      uint64_t word[U];
-      float scale[U];
-      float4 dv[U][2];
+    const int lane = tid & 31;
+    const uint32_t lgB = 31u - __clz(a.bucket);
+    const uint32_t mask = a.bits ? (1u << a.bits) - 1u : 0u;
+    const uint64_t nunits = s_units[a.P];
+    const uint64_t gw = gtid >> 5, nw = gstride >> 5;
+    constexpr int U = 4;   // units per warp per iteration, all their loads in flight
+    for (uint64_t u0 = gw; u0 < nunits; u0 += nw * U) {
+      uint32_t word[U];
+      float scl[U];   // a lane's 4 positions share one bucket (B >= 8, 4-aligned)
+      float4 dv[U];
       int jj[U], cnt[U];
       uint64_t ee[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t g = g0 + (uint64_t)u * gstride;
-        cnt[u] = 0;
-        if (g >= groups[a.P]) continue;
+      for (int x = 0; x < U; ++x) {
+        const uint64_t u = u0 + (uint64_t)x * nw;
+        cnt[x] = 0;
+        jj[x] = 0;
+        ee[x] = 0;
+        if (u >= nunits) continue;
         int j = 0;
-        while (g >= groups[j + 1]) ++j;
-        const uint64_t e = (g - groups[j]) * 8;
+        while (u >= s_units[j + 1]) ++j;
         const uint64_t nj = a.bnd[j + 1] - a.bnd[j];
-        jj[u] = j;
-        ee[u] = e;
-        cnt[u] = (int)((nj - e) < 8 ? (nj - e) : 8);
+        const uint64_t e = (u - s_units[j]) * 128 + 4 * (uint64_t)lane;
+        jj[x] = j;
+        ee[x] = e;
+        cnt[x] = e >= nj ? 0 : (int)((nj - e) < 4 ? (nj - e) : 4);
+        if (cnt[x] == 0) continue;
         if (a.bits) {
           const uint8_t* cp = a.r_codes[j] + (e * a.bits) / 8;
-          uint64_t wv = 0;
-          if (cnt[u] == 8 && a.bits == 4) wv = *reinterpret_cast<const uint32_t*>(cp);
-          else if (cnt[u] == 8 && a.bits == 8) wv = *reinterpret_cast<const unsigned long long*>(cp);
-          else if (cnt[u] == 8 && a.bits == 2) wv = *reinterpret_cast<const uint16_t*>(cp);
+          uint32_t w;
+          if (cnt[x] == 4 && a.bits == 4) w = *reinterpret_cast<const uint16_t*>(cp);
+          else if (cnt[x] == 4 && a.bits == 8) w = *reinterpret_cast<const uint32_t*>(cp);
+          else if (cnt[x] == 4 && a.bits == 2) w = *cp;
           else {
-            const int nbytes = (cnt[u] * a.bits + 7) / 8;
-            for (int q = 0; q < nbytes; ++q) wv |= (uint64_t)cp[q] << (8 * q);
+            w = 0;
+            const int nbytes = (cnt[x] * a.bits + 7) / 8;
+            for (int q = 0; q < nbytes; ++q) w |= (uint32_t)cp[q] << (8 * q);
           }
-          word[u] = wv;
-          scale[u] = a.r_scales[j][e / a.bucket];
-        } else if (cnt[u] == 8) {
-          const float4* src = reinterpret_cast<const float4*>(a.r_dense[j] + e);
-          dv[u][0] = src[0];
-          dv[u][1] = src[1];
+          word[x] = w;
+          scl[x] = a.r_scales[j][e >> lgB];
+        } else {
+          const float* src = a.r_dense[j] + e;
+          if (cnt[x] == 4 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
+            dv[x] = *reinterpret_cast<const float4*>(src);
+          } else {
+            dv[x] = make_float4(src[0], cnt[x] > 1 ? src[1] : 0.0f, cnt[x] > 2 ? src[2] : 0.0f,
+                                cnt[x] > 3 ? src[3] : 0.0f);
+          }
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (cnt[u] == 0) continue;
-        const int j = jj[u];
-        const uint64_t e = ee[u];
-        float v[8];
+      for (int x = 0; x < U; ++x) {
+        if (cnt[x] == 0) continue;
+        float v[4];
         if (a.bits) {
-          const uint32_t mask = (1u << a.bits) - 1u;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t code = (uint32_t)(word[u] >> (i * a.bits)) & mask;
-            const float mag = __fmul_rn(s_lvl[code & s], scale[u]);   // = qsgd_decode (R-16)
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t code = (word[x] >> (i * a.bits)) & mask;
+            const float mag = __fmul_rn(s_lvl[code & s], scl[x]);   // = qsgd_decode (reading R-16)
             v[i] = (code >> (a.bits - 1)) ? -mag : mag;
           }
-        } else if (cnt[u] == 8) {
-          v[0] = dv[u][0].x; v[1] = dv[u][0].y; v[2] = dv[u][0].z; v[3] = dv[u][0].w;
-          v[4] = dv[u][1].x; v[5] = dv[u][1].y; v[6] = dv[u][1].z; v[7] = dv[u][1].w;
+        } else {
+          v[0] = dv[x].x; v[1] = dv[x].y; v[2] = dv[x].z; v[3] = dv[x].w;
+        }
+        float* d = out_dense + a.bnd[jj[x]] + ee[x];
+        if (cnt[x] == 4 && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
+          *reinterpret_cast<float4*>(d) = make_float4(v[0], v[1], v[2], v[3]);
         } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = i < cnt[u] ? a.r_dense[j][e + i] : 0.0f;
-        }
-        float* d = out_dense + a.bnd[j] + e;
-        if (cnt[u] == 8 && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
-          reinterpret_cast<float4*>(d)[0] = make_float4(v[0], v[1], v[2], v[3]);
-          reinterpret_cast<float4*>(d)[1] = make_float4(v[4], v[5], v[6], v[7]);
-        } else {
-          for (int i = 0; i < cnt[u]; ++i) d[i] = v[i];
+          for (int i = 0; i < 4; ++i)
+            if (i < cnt[x]) d[i] = v[i];
         }
       }
     }
