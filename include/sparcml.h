@@ -180,6 +180,36 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* comm,
  * collective like the allreduce.  On a loopback world it only orders. */
 sparcml_status sparcml_barrier(sparcml_comm* comm, void* stream);
 
+/* ---------------------- layer-wise tensor fusion ------------------------ */
+/* (the paper's deployment mode: "communication is
+ * done layer-wise using non-blocking calls".)  A model's L layers
+ * (dimensions N_l) are laid end to end: layer l owns global indices
+ * [off_l, off_l + N_l), off_0 = 0, off_{l+1} = off_l + N_l.  Fusing the L
+ * per-layer streams is a concatenation with index offsets -- the result is
+ * one sorted stream over N = sum N_l that one allreduce reduces; the
+ * allreduce result splits back into layers by index range.  Values are
+ * unchanged (the summation tree is over ranks, R-8), so per-layer results
+ * equal per-layer allreduces; only the dense switch sees the fused N.  All
+ * calls are stream-ordered and graph-capturable ("non-blocking": the host
+ * never waits; order work across streams with CUDA events). */
+
+/* idx_out[n_0 + ... + n_{l-1} + i] = idx_l[i] + off_l, val likewise, for the
+ * L layers (host arrays of L device pointers / counts / offsets).  idx_l
+ * strictly increasing < N_l (so the output is strictly increasing when the
+ * offsets are).  Errors: L <= 0, null arrays, decreasing offsets, a count
+ * above 2^32 -> SPARCML_ERR_INVALID_ARG. */
+sparcml_status sparcml_fuse_streams(int L, const uint32_t* const* idx_host, const float* const* val_host,
+                                    const uint64_t* nnz_host, const uint64_t* off_host,
+                                    uint32_t* idx_out, float* val_out, void* stream);
+
+/* Layer ranges of an allreduce result: starts_dev[l] (device, L+1 entries
+ * of uint64) = first payload position of layer l -- for a sparse result the
+ * lower bound of off_l in the result's sorted indices, for a dense one off_l
+ * itself; starts_dev[L] = nnz (sparse) or N (dense).  Layer l's entries are
+ * [starts[l], starts[l+1]) of the payload (idx at 64, val at val_offset). */
+sparcml_status sparcml_layer_ranges(const void* out, int L, const uint64_t* off_host, uint64_t* starts_dev,
+                                    void* stream);
+
 /* Synchronous helper: copies the 64-byte header at out[0] to the host
  * (cudaMemcpyAsync on `stream` + stream synchronize). */
 sparcml_status sparcml_read_header(const void* out, sparcml_header* hdr_host, void* stream);

@@ -806,6 +806,43 @@ sparcml_status sparcml_ef_topk(float* eps, const float* grad, float alpha, uint6
   return topk_common(eps, grad, alpha, 1, eps, N, k, bucket, io, vo, nullptr, ws, ws_bytes, stream);
 }
 
+sparcml_status sparcml_fuse_streams(int L, const uint32_t* const* idx, const float* const* val, const uint64_t* nnz,
+                                    const uint64_t* off, uint32_t* idx_out, float* val_out, void* stream) {
+  if (L <= 0 || L > kMaxLayers || !idx || !val || !nnz || !off)
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "need 1..64 layers and non-null arrays");
+  FuseArgs a = {};
+  a.L = L;
+  a.pre[0] = 0;
+  for (int l = 0; l < L; ++l) {
+    if (l > 0 && off[l] < off[l - 1]) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "layer offsets must not decrease");
+    if (nnz[l] > 0xFFFFFFFFull || off[l] > 0xFFFFFFFFull)
+      return fail(nullptr, SPARCML_ERR_INVALID_ARG, "layer counts and offsets must fit u32 indices");
+    if (nnz[l] && (!idx[l] || !val[l])) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null layer stream");
+    a.idx[l] = idx[l];
+    a.val[l] = val[l];
+    a.off[l] = off[l];
+    a.pre[l + 1] = a.pre[l] + nnz[l];
+  }
+  if (a.pre[L] && (!idx_out || !val_out)) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null output");
+  a.idx_out = idx_out;
+  a.val_out = val_out;
+  if (a.pre[L] == 0) return SPARCML_OK;
+  CK(nullptr, launch_fuse_streams(a, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_layer_ranges(const void* out, int L, const uint64_t* off, uint64_t* starts, void* stream) {
+  if (!out || !off || !starts || L <= 0 || L > kMaxLayers)
+    return fail(nullptr, SPARCML_ERR_INVALID_ARG, "need 1..64 layers and non-null arguments");
+  LayerOffsets o = {};
+  for (int l = 0; l < L; ++l) {
+    if (l > 0 && off[l] < off[l - 1]) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "layer offsets must not decrease");
+    o.v[l] = off[l];
+  }
+  CK(nullptr, launch_layer_ranges(static_cast<const char*>(out), L, o, starts, static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
 sparcml_status sparcml_topk_status(const void* ws, uint32_t* status, uint32_t* passes, void* stream) {
   if (!ws || !status || !passes) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
   CK(nullptr, topk_read_status(ws, status, passes, static_cast<cudaStream_t>(stream)));

@@ -177,6 +177,21 @@ struct P1PrepArgs {                 // P == 1: validate, fill the control block,
   uint32_t* win;                    // nullable: build the window-offset table (ntab + 1 entries)
 };
 
+// -------------------------------------------------- layer-wise fusion ------
+constexpr int kMaxLayers = 64;      // layers per fused call (by value in the kernel parameters)
+struct FuseArgs {
+  int L;
+  const uint32_t* idx[kMaxLayers];
+  const float* val[kMaxLayers];
+  uint64_t pre[kMaxLayers + 1];     // prefix of the layers' nnz
+  uint64_t off[kMaxLayers];         // index offset of each layer
+  uint32_t* idx_out;
+  float* val_out;
+};
+struct LayerOffsets {
+  uint64_t v[kMaxLayers + 1];
+};
+
 // ----------------------------------------------------------- launchers -----
 extern unsigned long long g_launches;   // kernels enqueued by this library
 
@@ -204,6 +219,8 @@ cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);
 int owner_grid_size();
+cudaError_t launch_fuse_streams(const FuseArgs& a, cudaStream_t s);
+cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off, uint64_t* starts, cudaStream_t s);
 
 // top-k / QSGD (kernels_topk.cu, kernels_qsgd.cu)
 size_t topk_workspace_bytes(uint64_t N, uint64_t k);

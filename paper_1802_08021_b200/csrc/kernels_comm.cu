@@ -1331,4 +1331,49 @@ cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ===========================================================================
+// layer-wise tensor fusion (NEXT row 1): concatenate per-layer streams with
+// index offsets; locate layer ranges in a result
+// ===========================================================================
+__global__ void __launch_bounds__(kThreads) fuse_streams_kernel(FuseArgs a) {
+  const uint64_t total = a.pre[a.L];
+  for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < total; e += (uint64_t)gridDim.x * kThreads) {
+    int l = 0;
+    while (e >= a.pre[l + 1]) ++l;
+    const uint64_t i = e - a.pre[l];
+    a.idx_out[e] = (uint32_t)(a.idx[l][i] + a.off[l]);
+    a.val_out[e] = a.val[l][i];
+  }
+}
+
+cudaError_t launch_fuse_streams(const FuseArgs& a, cudaStream_t s) {
+  const uint64_t total = a.pre[a.L];
+  const unsigned blocks =
+      (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + kThreads - 1) / kThreads, (uint64_t)device_sm_count() * 8));
+  fuse_streams_kernel<<<blocks, kThreads, 0, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// one warp per layer boundary: lower bound of off[l] in the sparse result
+__global__ void layer_ranges_kernel(const char* out, int L, LayerOffsets off, uint64_t* starts) {
+  const sparcml_header* h = reinterpret_cast<const sparcml_header*>(out);
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (l > L) return;
+  const bool dense = h->repr == SPARCML_REPR_DENSE;
+  const uint64_t n = dense ? h->N : h->nnz;
+  uint64_t r;
+  if (l == L) r = n;
+  else if (dense) r = off.v[l];
+  else r = warp_lower_bound(reinterpret_cast<const uint32_t*>(out + SPARCML_HEADER_BYTES), n, off.v[l]);
+  if ((threadIdx.x & 31) == 0) starts[l] = r;
+}
+
+cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off, uint64_t* starts, cudaStream_t s) {
+  const int warps = L + 1;
+  layer_ranges_kernel<<<(warps + 7) / 8, 256, 0, s>>>(out, L, off, starts);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 }  // namespace sparcml

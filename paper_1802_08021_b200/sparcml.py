@@ -14,7 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass
-from typing import Optional, Sequence
+from typing import Optional, Sequence, List
 
 import torch
 
@@ -45,7 +45,7 @@ EXPORTED = [
     "sparcml_ops_workspace_init", "sparcml_merge_sum", "sparcml_topk_workspace_bytes", "sparcml_topk_sparsify",
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
     "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
-    "sparcml_profile_read",
+    "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges",
 ]
 
 
@@ -95,6 +95,8 @@ _sig = {
     "sparcml_quantized_size": (_i32, [_u64, _i32, C.c_uint32, C.POINTER(_sz), C.POINTER(_sz)]),
     "sparcml_quantize": (_i32, [_p, _u64, _i32, C.c_uint32, _u64, _u64, _p, _p, _p]),
     "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
+    "sparcml_fuse_streams": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _p]),
+    "sparcml_layer_ranges": (_i32, [_p, _i32, _p, _p, _p]),
     "sparcml_kernel_launches": (_u64, []),
     "sparcml_profile_enable": (None, [_i32]),
     "sparcml_profile_reset": (None, []),
@@ -318,6 +320,18 @@ class Comm:
                                              out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
         return out
 
+    def allreduce_async(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,
+                        opts: Optional[Opts] = None, stream=None) -> "Request":
+        """Non-blocking allreduce ("layer-wise using non-blocking calls"): enqueued on
+        `stream` (default: the current stream) after the work already there; returns a Request
+        whose event marks completion.  The host never waits."""
+        st = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            out = self.allreduce(idx, val, N, out=out, opts=opts, stream=st)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        return Request(out, ev)
+
     def barrier(self, stream=None):
         """Device-side barrier of all ranks (stream-ordered, over NVLink flags)."""
         _check(_lib.sparcml_barrier(self._h, _stream(stream)), self._h)
@@ -371,6 +385,75 @@ class TopkWorkspace:
         st, ps = C.c_uint32(), C.c_uint32()
         _check(_lib.sparcml_topk_status(self.buf.data_ptr(), C.byref(st), C.byref(ps), _stream(stream)))
         return int(st.value), int(ps.value)
+
+
+class Request:
+    """Handle of a non-blocking allreduce: `wait(stream)` orders `stream` after it (device
+    side, no host sync); `result()` synchronises and returns the Result views."""
+
+    def __init__(self, out: torch.Tensor, event):
+        self.out, self.event = out, event
+
+    def wait(self, stream=None):
+        (stream if stream is not None else torch.cuda.current_stream()).wait_event(self.event)
+        return self.out
+
+    def done(self) -> bool:
+        return self.event.query()
+
+    def result(self):
+        self.event.synchronize()
+        return read_result(self.out)
+
+
+# ---------------------------------------------------------------- tensor fusion
+def layer_offsets(dims: Sequence[int]) -> List[int]:
+    """Layers laid end to end: offsets [0, N_0, N_0 + N_1, ...] (L + 1 entries)."""
+    off = [0]
+    for n in dims:
+        off.append(off[-1] + int(n))
+    return off
+
+
+def fuse_streams(streams: Sequence, offsets: Sequence[int], stream=None):
+    """One sorted stream over sum(N_l) from L per-layer (idx int32, val float32) streams:
+    idx + off_l, concatenated in layer order (one kernel)."""
+    L = len(streams)
+    if L == 0 or len(offsets) < L:
+        raise ValueError("need one offset per layer")
+    n = [int(i.numel()) for i, _ in streams]
+    dev = streams[0][0].device
+    tot = sum(n)
+    io = torch.empty(max(tot, 1), dtype=torch.int32, device=dev)
+    vo = torch.empty(max(tot, 1), dtype=torch.float32, device=dev)
+    for i, v in streams:
+        _need(i, torch.int32, "idx")
+        _need(v, torch.float32, "val")
+    ip = (C.c_void_p * L)(*[i.data_ptr() if i.numel() else None for i, _ in streams])
+    vp = (C.c_void_p * L)(*[v.data_ptr() if v.numel() else None for _, v in streams])
+    nn = (C.c_uint64 * L)(*n)
+    oo = (C.c_uint64 * L)(*[int(o) for o in offsets[:L]])
+    _check(_lib.sparcml_fuse_streams(L, ip, vp, nn, oo, io.data_ptr(), vo.data_ptr(), _stream(stream)))
+    return io[:tot], vo[:tot]
+
+
+def layer_ranges(out: torch.Tensor, offsets: Sequence[int], stream=None) -> torch.Tensor:
+    """Device tensor (L+1,) int64: layer l's payload positions are [r[l], r[l+1])."""
+    L = len(offsets) - 1 if len(offsets) > 1 else 1
+    r = torch.empty(L + 1, dtype=torch.int64, device=out.device)
+    oo = (C.c_uint64 * L)(*[int(o) for o in offsets[:L]])
+    _check(_lib.sparcml_layer_ranges(out.data_ptr(), L, oo, r.data_ptr(), _stream(stream)))
+    return r
+
+
+def split_result(out: torch.Tensor, offsets: Sequence[int], stream=None):
+    """Per-layer views (global indices) of a fused allreduce result; synchronises."""
+    res = read_result(out, stream)
+    r = layer_ranges(out, offsets, stream).cpu().tolist()
+    L = len(r) - 1
+    if res.header.repr == REPR_DENSE:
+        return [(None, res.val[r[l]:r[l + 1]]) for l in range(L)]
+    return [(res.idx[r[l]:r[l + 1]], res.val[r[l]:r[l + 1]]) for l in range(L)]
 
 
 def topk_count(N: int, k: int, bucket: int = 0) -> int:

@@ -62,6 +62,7 @@ def main():
                 fails += 1
                 print(f"rank {rank}: case {name} rep {rep} MISMATCH (dense {res.dense} vs {d}, "
                       f"nnz {res.header.nnz}, status {res.header.status})", flush=True)
+    fails += layerwise(comm, rank, P)
     t = torch.tensor([fails])
     dist.all_reduce(t)
     comm.close()
@@ -69,6 +70,68 @@ def main():
     if rank == 0:
         print(f"multigpu P={P}: {'OK' if t.item() == 0 else 'FAILED'} ({int(t.item())} mismatches)", flush=True)
     sys.exit(0 if t.item() == 0 else 1)
+
+
+def layerwise(comm, rank, P):
+    """NEXT row 1: layer-wise non-blocking allreduces on a communication stream,
+    overlapped with top-k work on the compute stream, and the tensor-fused
+    variant (one allreduce over all layers), both against the oracle per layer."""
+    dims = [100_003, 2_000_000, 777, 500_000]
+    ks = [1000, 20_000, 50, 5000]
+    off = S.layer_offsets(dims)
+    layers = [synth.uniform_streams(P, dims[l], ks[l], seed=40 + l, kind="normal") for l in range(len(dims))]
+    mine = [(torch.from_numpy(layers[l][rank][0].view(np.int32)).cuda(), torch.from_numpy(layers[l][rank][1]).cuda())
+            for l in range(len(dims))]
+    comp, cs = torch.cuda.current_stream(), torch.cuda.Stream()
+    x = torch.randn(1 << 22, device="cuda")
+    ws = S.TopkWorkspace(x.numel(), 4096)
+    opts = S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER)
+    reqs = []
+    for l in reversed(range(len(dims))):           # backward order, as gradients appear
+        S.topk_sparsify(x, 4096, ws=ws)              # compute-stream work to overlap with
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        cs.wait_event(ev)
+        reqs.append((l, comm.allreduce_async(mine[l][0], mine[l][1], dims[l], opts=opts, stream=cs)))
+    fails = 0
+    for l, rq in reqs:
+        rq.wait(comp)
+        res = rq.result()
+        ref, _, _ = oracle.split_allgather(dims[l], layers[l], algo=oracle.ALGO_SSAR_SPLIT)
+        wmask, want = oracle.result_to_dense(ref[rank], dims[l])
+        got = np.zeros(dims[l], np.float32)
+        gmask = np.ones(dims[l], np.uint8)
+        if res.dense:
+            got[:] = res.val.cpu().numpy()
+        else:
+            ii = res.idx.cpu().numpy().astype(np.int64)
+            got[ii] = res.val.cpu().numpy()
+            gmask[:] = 0
+            gmask[ii] = 1
+        if not (np.array_equal(got, want) and np.array_equal(gmask, wmask)):
+            fails += 1
+            print(f"rank {rank}: layer-wise layer {l} MISMATCH", flush=True)
+    # fused: one allreduce over sum(N_l), split back by index range
+    fi, fv = S.fuse_streams(mine, off)
+    out = comm.allreduce(fi, fv, off[-1], opts=opts)
+    parts = S.split_result(out, off)
+    for l in range(len(dims)):
+        ref, _, _ = oracle.split_allgather(dims[l], layers[l], algo=oracle.ALGO_SSAR_SPLIT)
+        wmask, want = oracle.result_to_dense(ref[rank], dims[l])
+        pi, pv = parts[l]
+        got = np.zeros(dims[l], np.float32)
+        gmask = np.ones(dims[l], np.uint8)
+        if pi is None:
+            got[:] = pv.cpu().numpy()
+        else:
+            ii = pi.cpu().numpy().astype(np.int64) - off[l]
+            got[ii] = pv.cpu().numpy()
+            gmask[:] = 0
+            gmask[ii] = 1
+        if not (np.array_equal(got, want) and np.array_equal(gmask, wmask)):
+            fails += 1
+            print(f"rank {rank}: fused layer {l} MISMATCH", flush=True)
+    return fails
 
 
 if __name__ == "__main__":

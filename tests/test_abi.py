@@ -83,5 +83,15 @@ def test_argument_errors_need_no_gpu(lib):
     assert rc == S.ERR_INVALID_ARG        # null x
     assert S.topk_count(1000, 4, 512) == 8 and S.topk_count(1100, 600, 512) == 512 + 512 + 76
     assert S.topk_count(10, 3, 0) == 3
+    # tensor fusion: argument errors return before any launch
+    assert S._lib.sparcml_fuse_streams(0, None, None, None, None, None, None, None) == S.ERR_INVALID_ARG
+    two = (ctypes.c_uint64 * 2)
+    ptrs = (ctypes.c_void_p * 2)(None, None)
+    rc = S._lib.sparcml_fuse_streams(2, ptrs, ptrs, two(0, 0), two(10, 5), None, None, None)
+    assert rc == S.ERR_INVALID_ARG        # decreasing layer offsets
+    rc = S._lib.sparcml_fuse_streams(2, ptrs, ptrs, two(3, 0), two(0, 5), None, None, None)
+    assert rc == S.ERR_INVALID_ARG        # null layer stream with a positive count
+    assert S._lib.sparcml_layer_ranges(None, 1, two(0, 0), None, None) == S.ERR_INVALID_ARG
+    assert S.layer_offsets([3, 0, 7]) == [0, 3, 3, 10]
     rc = S._lib.sparcml_sparse_allreduce(None, None, None, 0, 10, 0, None, None, 0, None)
     assert rc == S.ERR_INVALID_ARG
