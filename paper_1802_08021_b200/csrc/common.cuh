@@ -330,7 +330,9 @@ __device__ __forceinline__ void wait_flag_geq(const uint32_t* f, uint32_t target
   // relaxed polling, then one acquire load of the (already satisfied) flag:
   // synchronizes-with the producer's release without a full system fence
   if ((int)(ld_acquire_sys(f) - target) >= 0) return;
-  while ((int)(ld_relaxed_sys_u32(f) - target) < 0) __nanosleep(32);
+  int spins = 0;
+  while ((int)(ld_relaxed_sys_u32(f) - target) < 0)
+    if (++spins > 64) __nanosleep(32);   // tight polling first: a flag is usually microseconds away
   (void)ld_acquire_sys(f);
 }
 
@@ -367,6 +369,7 @@ struct alignas(128) Ctrl {
   uint64_t rd_recv[8];            // bytes I received for stage t
   ScanCounters scan[4];           // ticket counters of the tile kernels
   uint64_t dbg[2][16];            // %globaltimer phase marks (diagnostics): block 0, last block
+  uint64_t owner_k[16];           // K_j of owner j's sparse partition result, stored by owner j with its flag
 };
 
 __device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {

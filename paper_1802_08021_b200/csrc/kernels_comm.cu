@@ -800,12 +800,17 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
       }
     }
   }
-  if (tid == 0) a.blk[b] = cnt;
+  uint32_t* blk32 = reinterpret_cast<uint32_t*>(a.blk);   // per-block counts (< 2^32 each)
+  if (tid == 0) blk32[b] = cnt;
   dbg_mark(ctl, 3);
   grid.sync();
   dbg_mark(ctl, 4);
+  // sum of the counts of blocks 0..b-1: one 16-byte load (4 counts) per thread per pass
   uint64_t v = 0;
-  for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&a.blk[j]));
+  for (uint32_t j0 = 4 * tid; j0 < b; j0 += 4 * kThreads) {
+    const uint4 q = __ldcg(reinterpret_cast<const uint4*>(blk32 + j0));
+    v += (j0 < b ? q.x : 0u) + (j0 + 1 < b ? q.y : 0u) + (j0 + 2 < b ? q.z : 0u) + (j0 + 3 < b ? q.w : 0u);
+  }
   uint64_t tot_before;
   block_exclusive_sum<uint64_t>(v, s_sum, &tot_before);
   if (tid == 0) s_excl = tot_before;
@@ -826,7 +831,10 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
   dbg_mark(ctl, 5);
   // every block's writes are local: a gpu-scope arrival suffices; the release
   // to the peers is system scope (and cumulative over what the last block saw)
-  if (last_block<false>(&ctl->done_ctr[3]) && tid < P) st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
+  if (last_block<false>(&ctl->done_ctr[3]) && tid < P) {   // K travels with the flag: readers need no remote load
+    a.peer[tid]->owner_k[a.rank] = *(volatile uint64_t*)&ctl->owner_K;
+    st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
+  }
   dbg_mark(ctl, 6);
 }
 
@@ -1048,8 +1056,12 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   __shared__ uint64_t s_k[kMaxRanks];
   dbg_mark(ctl, 12);
   if (tid < a.P) {   // one lane per owner: wait for its flag, read its result size
-    if (a.wait_owners) wait_flag_geq(&ctl->owner_done[tid], seq + 1);
-    s_k[tid] = *(volatile const uint64_t*)a.r_n[tid];
+    if (a.wait_owners) {
+      wait_flag_geq(&ctl->owner_done[tid], seq + 1);
+      s_k[tid] = *(volatile const uint64_t*)&ctl->owner_k[tid];   // stored by owner tid with its flag
+    } else {
+      s_k[tid] = *(volatile const uint64_t*)a.r_n[tid];
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -1063,6 +1075,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     }
   }
   __syncthreads();
+  dbg_mark(ctl, 14);
   const bool dsar = s_dsar != 0;
   if (dsar != (MODE == 1)) return;
   const uint64_t K = s_pref[a.P];
@@ -1164,27 +1177,53 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     // sparse concatenation: disjoint ranges, globally sorted by construction
     // (P:511-515).  Units of 4 pairs of one owner: 16-byte loads over NVLink.
     const uint64_t units = s_upref[a.P];
-    for (uint64_t u = gtid; u < units; u += gstride) {
-      int j = 0;
-      while (u >= s_upref[j + 1]) ++j;
-      const uint64_t p = (u - s_upref[j]) * 4;
-      const uint64_t kj = s_pref[j + 1] - s_pref[j];
-      const uint64_t o = s_pref[j] + p;
-      if (p + 4 <= kj) {
-        const uint4 ix = *reinterpret_cast<const uint4*>(a.r_idx[j] + p);
-        const float4 vx = *reinterpret_cast<const float4*>(a.r_val[j] + p);
-        out_idx[o] = ix.x;
-        out_idx[o + 1] = ix.y;
-        out_idx[o + 2] = ix.z;
-        out_idx[o + 3] = ix.w;
-        out_val[o] = vx.x;
-        out_val[o + 1] = vx.y;
-        out_val[o + 2] = vx.z;
-        out_val[o + 3] = vx.w;
-      } else {
-        for (uint64_t q = p; q < kj; ++q) {
-          out_idx[s_pref[j] + q] = a.r_idx[j][q];
-          out_val[s_pref[j] + q] = a.r_val[j][q];
+    constexpr int U = 4;   // units per thread per iteration: all their NVLink loads in flight
+    for (uint64_t u0 = gtid; u0 < units; u0 += gstride * U) {
+      uint4 ix[U];
+      float4 vx[U];
+      uint64_t oo[U];
+      int cnt[U];   // pairs in the unit (4, or an owner's short last unit; 0 = none)
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const uint64_t u = u0 + (uint64_t)x * gstride;
+        cnt[x] = 0;
+        if (u >= units) continue;
+        int j = 0;
+        while (u >= s_upref[j + 1]) ++j;
+        const uint64_t p = (u - s_upref[j]) * 4;
+        const uint64_t kj = s_pref[j + 1] - s_pref[j];
+        oo[x] = s_pref[j] + p;
+        if (p + 4 <= kj) {
+          ix[x] = *reinterpret_cast<const uint4*>(a.r_idx[j] + p);
+          vx[x] = *reinterpret_cast<const float4*>(a.r_val[j] + p);
+          cnt[x] = 4;
+        } else {
+          const uint32_t* si = a.r_idx[j] + p;
+          const float* sv = a.r_val[j] + p;
+          const int n = (int)(kj - p);
+          ix[x] = make_uint4(si[0], n > 1 ? si[1] : 0u, n > 2 ? si[2] : 0u, 0u);
+          vx[x] = make_float4(sv[0], n > 1 ? sv[1] : 0.0f, n > 2 ? sv[2] : 0.0f, 0.0f);
+          cnt[x] = n;
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < U; ++x) {
+        const int n = cnt[x];
+        if (n == 0) continue;
+        const uint64_t o = oo[x];
+        out_idx[o] = ix[x].x;
+        out_val[o] = vx[x].x;
+        if (n > 1) {
+          out_idx[o + 1] = ix[x].y;
+          out_val[o + 1] = vx[x].y;
+        }
+        if (n > 2) {
+          out_idx[o + 2] = ix[x].z;
+          out_val[o + 2] = vx[x].z;
+        }
+        if (n > 3) {
+          out_idx[o + 3] = ix[x].w;
+          out_val[o + 3] = vx[x].w;
         }
       }
     }
@@ -1212,6 +1251,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
       __syncthreads();
     }
   }
+  dbg_mark(ctl, 15);
   if (last_block<false>(&ctl->done_ctr[2]) && tid == 0) {
     // bytes this rank put on / took off NVLink (pull model counted at the owner)
     uint64_t sent = 0, recv = 0;
@@ -1246,7 +1286,9 @@ cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(concat_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const int grid = device_sm_count() * 4;
+  // one block per SM for the sparse concatenation (fewer flag pollers and a
+  // shorter completion count), four for the dense decode
+  const int grid = device_sm_count() * (a.host_dsar == 0 ? 1 : 4);
   SPARCML_PROF("concat", s);
   if (a.host_dsar != 1) {
     concat_kernel<0><<<grid, kThreads, smem, s>>>(a);
