@@ -114,6 +114,16 @@ def test_edge_cases(orc):
             check_world(orc, P, N, [full] * P, ALGOS[algo])
 
 
+@pytest.mark.parametrize("P,frac", [(2, 0.6), (4, 0.3), (3, 0.9)])
+def test_ssar_dense_block_ranges(orc, P, frac):
+    """Forced SSAR on dense inputs: an owner block's window range holds more
+    elements than one shared-memory tile, so it is reduced in pieces through
+    the spill area (and K > delta makes the concatenation densify)."""
+    N = 1 << 20
+    streams = synth.uniform_streams(P, N, int(frac * N), seed=P + 31, kind="normal")
+    check_world(orc, P, N, streams, S.SSAR_SPLIT_ALLGATHER)
+
+
 def test_integer_values_exact_vs_definition(orc):
     """Integer-valued inputs: any summation order is exact, so the result must
     equal the plain definition (brute-force dense sum) bit for bit."""
