@@ -62,6 +62,8 @@ def lib():
         _lib.or_split_allgather.restype = i32
         _lib.or_split_allgather.argtypes = [i32, u64, u64, i32, i32, C.c_uint32, u64,
                                             p, p, p, i32, p, p, p, p, p, p]
+        _lib.or_sparse_allgather.restype = i32
+        _lib.or_sparse_allgather.argtypes = [i32, u64, u64, p, p, p, i32, p, p, p, p, p]
         _lib.or_topk.restype = u64
         _lib.or_topk.argtypes = [p, u64, u64, p, p, p]
         _lib.or_ef_topk.restype = u64
@@ -174,6 +176,28 @@ def _results(P, N, n_out, dense, n, oi, ov):
             m = int(n[r])
             res.append((False, oi[r * N:r * N + m].copy(), ov[r * N:r * N + m].copy()))
     return res
+
+
+def sparse_allgather(N, streams, delta=None, n_out=None):
+    """Sparse allgather of streams with disjoint index ranges (R-27).
+    Returns (results, stats); raises ValueError if two ranges overlap."""
+    P = len(streams)
+    if delta is None:
+        delta = switch_threshold(N)
+    n_out = P if n_out is None else n_out
+    idx, val, off = _flatten(streams)
+    dense = np.zeros(P, np.int32)
+    n = np.zeros(P, np.uint64)
+    oi = np.zeros(max(n_out * N, 1), np.uint32)
+    ov = np.zeros(max(n_out * N, 1), np.float32)
+    st = (_RankStats * P)()
+    rc = lib().or_sparse_allgather(P, N, delta, _ptr(idx), _ptr(val), _ptr(off), n_out, _ptr(dense), _ptr(n),
+                                   _ptr(oi), _ptr(ov), st)
+    if rc == -2:
+        raise ValueError("sparse allgather: index ranges of two ranks overlap")
+    if rc != 0:
+        raise ValueError("or_sparse_allgather rejected its arguments")
+    return _results(P, N, n_out, dense, n, oi, ov), _stats_list(st)
 
 
 def ssar_recursive_double(N, streams, delta=None, n_out=None):

@@ -392,6 +392,58 @@ static int cmp_u32(const void* pa, const void* pb) {
   return (a > b) - (a < b);
 }
 
+int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, const float* val,
+                        const uint64_t* off, int n_out, int* out_dense, uint64_t* out_n,
+                        uint32_t* out_idx, float* out_val, or_rank_stats* stats) {
+  int r, i, j, order[256], m = 0;
+  uint64_t K = 0, e, pos;
+  if (P < 1 || P > 256 || N == 0 || n_out < 0 || n_out > P) return -1;
+  /* non-empty ranks ordered by their first index (insertion sort, P <= 256) */
+  for (r = 0; r < P; r++) {
+    const uint64_t n = off[r + 1] - off[r];
+    K += n;
+    if (n == 0) continue;
+    for (i = m; i > 0 && idx[off[order[i - 1]]] > idx[off[r]]; i--) order[i] = order[i - 1];
+    order[i] = r;
+    m++;
+  }
+  /* the precondition: consecutive ranges do not overlap */
+  for (i = 0; i + 1 < m; i++) {
+    const int a = order[i], b = order[i + 1];
+    if (idx[off[a + 1] - 1] >= idx[off[b]]) return -2;
+  }
+  for (r = 0; r < n_out; r++) {
+    uint32_t* oi = out_idx + (uint64_t)r * N;
+    float* ov = out_val + (uint64_t)r * N;
+    if (K > delta) {   /* dense result: zeros, then every value at its index */
+      out_dense[r] = 1;
+      out_n[r] = N;
+      for (e = 0; e < N; e++) ov[e] = 0.0f;
+      for (j = 0; j < m; j++)
+        for (e = off[order[j]]; e < off[order[j] + 1]; e++) ov[idx[e]] = val[e];
+    } else {           /* sparse: the concatenation in range order */
+      out_dense[r] = 0;
+      out_n[r] = K;
+      pos = 0;
+      for (j = 0; j < m; j++)
+        for (e = off[order[j]]; e < off[order[j] + 1]; e++, pos++) {
+          oi[pos] = idx[e];
+          ov[pos] = val[e];
+        }
+    }
+  }
+  if (stats)
+    for (r = 0; r < P; r++) {
+      const uint64_t n = off[r + 1] - off[r];
+      memset(&stats[r], 0, sizeof(stats[r]));
+      stats[r].bytes_sent = 8 * n * (uint64_t)(P - 1);
+      stats[r].bytes_recv = 8 * (K - n);
+      stats[r].msgs_sent = (uint64_t)(P - 1);
+      stats[r].pairs_sent = n * (uint64_t)(P - 1);
+    }
+  return 0;
+}
+
 uint64_t or_topk(const float* x, uint64_t N, uint64_t k,
                  uint32_t* idx_out, float* val_out, float* residual) {
   /* "communicates only the k largest (by magnitude) components" */

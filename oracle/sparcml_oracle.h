@@ -119,6 +119,21 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
                        uint32_t* out_idx, float* out_val, or_rank_stats* stats,
                        int* dsar_used);
 
+/* Sparse allgather for disjoint slices (§7 SCD: "the values
+ * calculated by each node lie in different slices of the entire model
+ * vector ... the runtime of a sparse allgather"; reading R-27): every rank
+ * contributes a sorted stream whose index RANGE [first, last] is disjoint
+ * from every other non-empty rank's; the result on every rank is the union,
+ * i.e. the streams concatenated in the order of their ranges -- no
+ * arithmetic.  K = sum n_i; K > delta is stored dense.  Per-rank
+ * accounting: rank r receives 8 n_i from every i != r and sends 8 n_r to
+ * each of the P-1 others.  Returns 0, or -2 if two non-empty ranges overlap
+ * (the precondition fails), -1 on bad arguments.  Outputs as in
+ * or_split_allgather (all ranks get the same result). */
+int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, const float* val,
+                        const uint64_t* off, int n_out, int* out_dense, uint64_t* out_n,
+                        uint32_t* out_idx, float* out_val, or_rank_stats* stats);
+
 /* Top-k by magnitude (§2.2; Algorithm 1).  Orders every
  * coordinate by (|x_j| descending, j ascending) — ties to the lower index,
  * reading R-18 — keeps the first m = min(k, N), emits them sorted by j with

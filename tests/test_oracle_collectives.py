@@ -223,3 +223,59 @@ def test_dsar_quantized_decodes_within_bound(orc):
         assert np.all(np.abs(res[0][2][sl] - exact[sl]) <= scale / s * (1 + 1e-6) + 1e-6)
     for r in range(1, P):
         np.testing.assert_array_equal(res[r][2], res[0][2])
+
+
+# ---- sparse allgather for disjoint slices (§7 SCD; reading R-27) ---------
+
+def _slices(P, N, per, seed, order=None):
+    """Rank r's `per` indices inside its own slice of the model vector."""
+    rng = np.random.default_rng(seed)
+    bounds = np.linspace(0, N, P + 1).astype(np.int64)
+    order = list(range(P)) if order is None else order
+    streams = []
+    for r in range(P):
+        s = order[r]
+        lo, hi = bounds[s], bounds[s + 1]
+        n = min(per, hi - lo)
+        i = np.sort(rng.choice(np.arange(lo, hi), n, replace=False)).astype(np.uint32)
+        streams.append((i, rng.standard_normal(n).astype(np.float32)))
+    return streams
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+def test_sparse_allgather_equals_definition(orc, P):
+    """Disjoint slices: the allgather is the union, i.e. the brute-force sum
+    (one contributor per index) -- any mistake in ordering, offsets or values
+    shows up against the independent dense definition."""
+    N = 10_000
+    rng = np.random.default_rng(P)
+    order = list(rng.permutation(P))             # slices owned in a shuffled rank order
+    streams = _slices(P, N, 100, seed=P, order=order)
+    res, st = orc.sparse_allgather(N, streams)
+    bf = orc.brute_force(N, streams)
+    for r in range(P):
+        d, i, v = res[r]
+        assert not d
+        np.testing.assert_array_equal(i, np.nonzero(bf["mask"])[0])
+        np.testing.assert_array_equal(v, bf["f32"][i])
+        n_r = len(streams[r][0])
+        assert st[r]["bytes_recv"] == 8 * (sum(len(s[0]) for s in streams) - n_r)
+        assert st[r]["bytes_sent"] == 8 * n_r * (P - 1)
+
+
+def test_sparse_allgather_dense_and_empty(orc):
+    N, P = 1000, 4
+    streams = _slices(P, N, 200, seed=1)          # K = 800 > delta = 500: dense
+    streams[2] = (np.zeros(0, np.uint32), np.zeros(0, np.float32))
+    res, _ = orc.sparse_allgather(N, streams)
+    bf = orc.brute_force(N, streams)
+    d, _, v = res[0]
+    assert d
+    np.testing.assert_array_equal(v, bf["f32"])
+
+
+def test_sparse_allgather_rejects_overlapping_ranges(orc):
+    a = (np.array([1, 50], np.uint32), np.ones(2, np.float32))
+    b = (np.array([10, 20], np.uint32), np.ones(2, np.float32))   # inside a's range
+    with pytest.raises(ValueError):
+        orc.sparse_allgather(100, [a, b])
