@@ -62,7 +62,8 @@ typedef enum {
   SPARCML_ALGO_AUTO = 0,
   SPARCML_SSAR_RECURSIVE_DOUBLE = 1,   /* §5.3.1                 */
   SPARCML_SSAR_SPLIT_ALLGATHER = 2,    /* §5.3.2                 */
-  SPARCML_DSAR_SPLIT_ALLGATHER = 3     /* §5.3.3 P:782-832 (+ §6 QSGD)     */
+  SPARCML_DSAR_SPLIT_ALLGATHER = 3,    /* §5.3.3 P:782-832 (+ §6 QSGD)     */
+  SPARCML_SPARSE_ALLGATHER = 4         /* header algo_used of sparcml_sparse_allgather (§7 SCD) */
 } sparcml_algo;
 
 /* Representation flag "at the beginning of each vector". */
@@ -179,6 +180,25 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* comm,
  * peers store over NVLink).  Stream-ordered, no host synchronisation;
  * collective like the allreduce.  On a loopback world it only orders. */
 sparcml_status sparcml_barrier(sparcml_comm* comm, void* stream);
+
+/* Sparse allgather for disjoint slices (§7 SCD: "the values
+ * calculated by each node lie in different slices of the entire model vector
+ * ... a sparse allgather"; reading R-27).  Precondition: the index ranges
+ * [first, last] of the non-empty ranks are pairwise disjoint (any rank
+ * order).  `out` on every rank receives their union -- the streams
+ * concatenated in range order (K = sum nnz), dense when K > delta -- with
+ * header algo_used = SPARCML_SPARSE_ALLGATHER.  One exchange: each rank
+ * publishes its stream in its own workspace and flags every peer; every rank
+ * pulls the P streams over NVLink.  Overlapping ranges: header status
+ * SPARCML_ERR_INVALID_ARG, payload undefined.  opts: only switch_scale and
+ * validate are used (NULL = defaults).  Errors as sparcml_sparse_allreduce. */
+sparcml_status sparcml_sparse_allgather(sparcml_comm* comm, const uint32_t* idx, const float* val,
+                                        uint64_t nnz, uint64_t N, const sparcml_opts* opts_host,
+                                        void* out, size_t out_bytes, void* stream);
+sparcml_status sparcml_sparse_allgather_local(sparcml_comm* comm, const uint32_t* const* idx_host,
+                                              const float* const* val_host, const uint64_t* nnz_host,
+                                              uint64_t N, const sparcml_opts* opts_host,
+                                              void* const* out_host, size_t out_bytes, void* stream);
 
 /* ---------------------- layer-wise tensor fusion ------------------------ */
 /* (the paper's deployment mode: "communication is

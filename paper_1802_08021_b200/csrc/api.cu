@@ -87,6 +87,7 @@ struct Layout {
   size_t blk_off;                       // owner per-block output counts
   size_t part_off, part_bytes, scales_off;
   size_t rd_off, rd_bytes, rd_val_off;  // cur[2] + recv[2 parities][L stages]
+  size_t ag_off, ag_val_off;            // sparse allgather: my published stream (max_nnz pairs)
   size_t total;
 };
 
@@ -126,6 +127,9 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.rd_val_off = align_up(4 * std::max<uint64_t>(half_cap(max_N), max_nnz) + 64, 256);
   L.rd_bytes = align_up(std::max<size_t>(2 * L.rd_val_off, 4 * max_N) + 256, 256);
   if (pow2 && P > 1) off += (size_t)(2 + 2 * L.L) * L.rd_bytes;
+  L.ag_off = off;
+  L.ag_val_off = align_up(4 * max_nnz, 256);
+  off += align_up(L.ag_val_off + 4 * max_nnz, 256);
   L.total = align_up(off, 1 << 20);
   return L;
 }
@@ -510,6 +514,72 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   return run_split(c, R, idx, val, nnz, outs, cc);
 }
 
+// ------------------------------------------------------ sparse allgather ---
+sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
+                              const uint64_t* nnz, uint64_t N, const sparcml_opts* opts, void* const* out,
+                              size_t out_bytes, void* stream) {
+  if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
+  if (!c->connected) return fail(c, SPARCML_ERR_STATE, "communicator not connected");
+  if (N == 0 || N > c->L.max_N) return fail(c, SPARCML_ERR_INVALID_ARG, "N must be in [1, max_N]");
+  if (N > 0xFFFFFFFFull) return fail(c, SPARCML_ERR_INVALID_ARG, "N must fit u32 indices");
+  sparcml_opts o;
+  sparcml_opts_default(&o);
+  if (opts) o = *opts;
+  if (!(o.switch_scale > 0.0f) || o.switch_scale > 1.0f)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "switch_scale must be in (0, 1]");
+  if (out_bytes < sparcml_result_bytes(N)) return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N)");
+  const int nl = c->local ? c->P : 1;
+  for (int i = 0; i < nl; ++i) {
+    if (nnz[i] > c->L.max_nnz) return fail(c, SPARCML_ERR_INVALID_ARG, "nnz > max_nnz");
+    if (nnz[i] > N) return fail(c, SPARCML_ERR_INVALID_ARG, "nnz > N");
+    if (nnz[i] > 0 && (!idx[i] || !val[i])) return fail(c, SPARCML_ERR_INVALID_ARG, "null input with nnz > 0");
+    if (!out[i] || (reinterpret_cast<uintptr_t>(out[i]) & 15u) != 0)
+      return fail(c, SPARCML_ERR_INVALID_ARG, "out must be non-null and 16-byte aligned");
+  }
+  const Layout& L = c->L;
+  const int P = c->P;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(c, cudaSetDevice(c->device));
+  std::vector<int> R;
+  if (c->local)
+    for (int r = 0; r < P; ++r) R.push_back(r);
+  else
+    R.push_back(c->rank);
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int r = R[i];
+    AgPublishArgs a = {};
+    a.idx = idx[i];
+    a.val = val[i];
+    a.n = nnz[i];
+    a.N = N;
+    a.P = P;
+    a.rank = r;
+    a.my_idx = reinterpret_cast<uint32_t*>(c->peer[r] + L.ag_off);
+    a.my_val = reinterpret_cast<float*>(c->peer[r] + L.ag_off + L.ag_val_off);
+    for (int j = 0; j < P; ++j) a.peer[j] = ctrl_of(c->peer[j]);
+    a.ctl = ctrl_of(c->peer[r]);
+    a.validate = o.validate;
+    CK(c, launch_ag_publish(a, s));
+  }
+  for (size_t i = 0; i < R.size(); ++i) {
+    const int r = R[i];
+    AgGatherArgs g = {};
+    g.P = P;
+    g.rank = r;
+    g.N = N;
+    g.delta = effective_delta(N, o);
+    for (int j = 0; j < P; ++j) {
+      g.src_idx[j] = reinterpret_cast<const uint32_t*>(c->peer[j] + L.ag_off);
+      g.src_val[j] = reinterpret_cast<const float*>(c->peer[j] + L.ag_off + L.ag_val_off);
+    }
+    g.ctl = ctrl_of(c->peer[r]);
+    g.out = static_cast<char*>(out[i]);
+    g.val_offset = sparcml_result_val_offset(N);
+    CK(c, launch_ag_gather(g, s));
+  }
+  return SPARCML_OK;
+}
+
 sparcml_status alloc_ws(sparcml_comm* c, char** p) {
   cudaError_t e = cudaMalloc(p, c->L.total);
   if (e == cudaErrorMemoryAllocation) return fail(c, SPARCML_ERR_OOM, "workspace allocation failed");
@@ -711,6 +781,21 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* c, const uint32_t* c
   if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
   if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
   return allreduce_impl(c, idx, val, nnz, N, op, opts, out, out_bytes, stream);
+}
+
+sparcml_status sparcml_sparse_allgather(sparcml_comm* c, const uint32_t* idx, const float* val, uint64_t nnz,
+                                        uint64_t N, const sparcml_opts* opts, void* out, size_t out_bytes,
+                                        void* stream) {
+  if (c && c->local) return fail(c, SPARCML_ERR_STATE, "use sparcml_sparse_allgather_local on a loopback world");
+  return allgather_impl(c, &idx, &val, &nnz, N, opts, &out, out_bytes, stream);
+}
+
+sparcml_status sparcml_sparse_allgather_local(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
+                                              const uint64_t* nnz, uint64_t N, const sparcml_opts* opts,
+                                              void* const* out, size_t out_bytes, void* stream) {
+  if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
+  if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
+  return allgather_impl(c, idx, val, nnz, N, opts, out, out_bytes, stream);
 }
 
 sparcml_status sparcml_barrier(sparcml_comm* c, void* stream) {

@@ -370,6 +370,10 @@ struct alignas(128) Ctrl {
   ScanCounters scan[4];           // ticket counters of the tile kernels
   uint64_t dbg[2][16];            // %globaltimer phase marks (diagnostics): block 0, last block
   uint64_t owner_k[16];           // K_j of owner j's sparse partition result, stored by owner j with its flag
+  // sparse allgather: rank i's published stream (count, index range) and its flag
+  uint64_t ag_n[16];
+  uint32_t ag_first[16], ag_last[16];
+  uint32_t ag_done[16];
 };
 
 __device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {

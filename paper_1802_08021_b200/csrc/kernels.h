@@ -177,6 +177,28 @@ struct P1PrepArgs {                 // P == 1: validate, fill the control block,
   uint32_t* win;                    // nullable: build the window-offset table (ntab + 1 entries)
 };
 
+// ------------------------------------------------------ sparse allgather --
+struct AgPublishArgs {
+  const uint32_t* idx;
+  const float* val;
+  uint64_t n, N;
+  int P, rank;
+  uint32_t* my_idx;                // my published copy (my workspace)
+  float* my_val;
+  Ctrl* peer[kMaxRanks];
+  Ctrl* ctl;
+  int validate;
+};
+struct AgGatherArgs {
+  int P, rank;
+  uint64_t N, delta;
+  const uint32_t* src_idx[kMaxRanks];   // every rank's published stream (peer pointers)
+  const float* src_val[kMaxRanks];
+  Ctrl* ctl;
+  char* out;
+  uint64_t val_offset;
+};
+
 // -------------------------------------------------- layer-wise fusion ------
 constexpr int kMaxLayers = 64;      // layers per fused call (by value in the kernel parameters)
 struct FuseArgs {
@@ -220,6 +242,8 @@ cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);
 int owner_grid_size();
 cudaError_t launch_fuse_streams(const FuseArgs& a, cudaStream_t s);
+cudaError_t launch_ag_publish(const AgPublishArgs& a, cudaStream_t s);
+cudaError_t launch_ag_gather(const AgGatherArgs& a, cudaStream_t s);
 cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off, uint64_t* starts, cudaStream_t s);
 
 // top-k / QSGD (kernels_topk.cu, kernels_qsgd.cu)

@@ -30,6 +30,7 @@ _lib = C.CDLL(LIB_PATH)
 # ---------------------------------------------------------------- constants --
 OK, ERR_INVALID_ARG, ERR_UNSORTED, ERR_NONFINITE, ERR_MISMATCH, ERR_CUDA, ERR_OOM, ERR_STATE = 0, 1, 2, 3, 4, 5, 7, 8
 ALGO_AUTO, SSAR_RECURSIVE_DOUBLE, SSAR_SPLIT_ALLGATHER, DSAR_SPLIT_ALLGATHER = 0, 1, 2, 3
+SPARSE_ALLGATHER = 4   # header algo_used of sparcml_sparse_allgather
 REPR_SPARSE, REPR_DENSE = 0, 1
 HEADER_BYTES = 64
 IPC_HANDLE_BYTES = 64
@@ -45,7 +46,8 @@ EXPORTED = [
     "sparcml_ops_workspace_init", "sparcml_merge_sum", "sparcml_topk_workspace_bytes", "sparcml_topk_sparsify",
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
     "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
-    "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges",
+    "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges", "sparcml_sparse_allgather",
+    "sparcml_sparse_allgather_local",
 ]
 
 
@@ -96,6 +98,8 @@ _sig = {
     "sparcml_quantize": (_i32, [_p, _u64, _i32, C.c_uint32, _u64, _u64, _p, _p, _p]),
     "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
     "sparcml_fuse_streams": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _p]),
+    "sparcml_sparse_allgather": (_i32, [_p, _p, _p, _u64, _u64, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_sparse_allgather_local": (_i32, [_p, _p, _p, _p, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_layer_ranges": (_i32, [_p, _i32, _p, _p, _p]),
     "sparcml_kernel_launches": (_u64, []),
     "sparcml_profile_enable": (None, [_i32]),
@@ -151,7 +155,7 @@ def profile_read(name: str):
     return int(n.value), float(ms.value)
 
 
-PROFILED_KERNELS = ["topk", "topk_all", "topk_bucketed", "split_push", "owner", "owner_dsar",
+PROFILED_KERNELS = ["topk", "topk_all", "topk_bucketed", "split_push", "owner", "owner_dsar", "ag_publish", "ag_gather",
                     "barrier", "merge", "window", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
                     "dequantize"]
 
@@ -268,6 +272,22 @@ class LocalWorld:
                                                    int(outs[0].numel()), _stream(stream)), self._h)
         return list(outs)
 
+    def allgather(self, streams: Sequence, N: int, outs: Optional[Sequence[torch.Tensor]] = None,
+                  opts: Optional[Opts] = None, stream=None):
+        """Sparse allgather (§7 SCD, reading R-27): streams with disjoint index ranges.
+        Returns the P out buffers (all hold the union)."""
+        P = self.P
+        if outs is None:
+            outs = [new_out(N, streams[0][0].device) for _ in range(P)]
+        ia = (C.c_void_p * P)(*[_ptr(i) for i, _ in streams])
+        va = (C.c_void_p * P)(*[_ptr(v) for _, v in streams])
+        na = (C.c_uint64 * P)(*[int(i.numel()) for i, _ in streams])
+        oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
+        o = opts if opts is not None else make_opts()
+        _check(_lib.sparcml_sparse_allgather_local(self._h, ia, va, na, N, C.byref(o), oa, int(outs[0].numel()),
+                                                   _stream(stream)), self._h)
+        return outs
+
     def close(self):
         if self._h:
             _lib.sparcml_comm_destroy(self._h)
@@ -317,6 +337,18 @@ class Comm:
             out = new_out(N, idx.device)
         o = opts if opts is not None else make_opts()
         _check(_lib.sparcml_sparse_allreduce(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, 0, C.byref(o),
+                                             out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
+        return out
+
+    def allgather(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,
+                  opts: Optional[Opts] = None, stream=None) -> torch.Tensor:
+        """Sparse allgather of streams with disjoint index ranges (§7 SCD, reading R-27)."""
+        _need(idx, torch.int32, "idx")
+        _need(val, torch.float32, "val")
+        if out is None:
+            out = new_out(N, idx.device)
+        o = opts if opts is not None else make_opts()
+        _check(_lib.sparcml_sparse_allgather(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, C.byref(o),
                                              out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
         return out
 

@@ -63,6 +63,7 @@ def main():
                 print(f"rank {rank}: case {name} rep {rep} MISMATCH (dense {res.dense} vs {d}, "
                       f"nnz {res.header.nnz}, status {res.header.status})", flush=True)
     fails += layerwise(comm, rank, P)
+    fails += allgather(comm, rank, P)
     t = torch.tensor([fails])
     dist.all_reduce(t)
     comm.close()
@@ -131,6 +132,36 @@ def layerwise(comm, rank, P):
         if not (np.array_equal(got, want) and np.array_equal(gmask, wmask)):
             fails += 1
             print(f"rank {rank}: fused layer {l} MISMATCH", flush=True)
+    return fails
+
+
+def allgather(comm, rank, P):
+    """§7 SCD sparse allgather over the IPC world: slices owned in shuffled order."""
+    fails = 0
+    for N, per in [(1 << 20, 100), (1 << 16, 30_000)]:   # sparse, then K > delta (dense)
+        rng = np.random.default_rng(N + per)
+        bounds = np.linspace(0, N, P + 1).astype(np.int64)
+        order = rng.permutation(P)
+        streams = []
+        for r in range(P):
+            lo, hi = bounds[order[r]], bounds[order[r] + 1]
+            n = min(per, hi - lo)
+            i = np.sort(rng.choice(np.arange(lo, hi), n, replace=False)).astype(np.uint32)
+            streams.append((i, rng.standard_normal(n).astype(np.float32)))
+        i, v = streams[rank]
+        out = comm.allgather(torch.from_numpy(i.view(np.int32)).cuda(), torch.from_numpy(v).cuda(), N)
+        g = S.read_result(out)
+        ref, st = oracle.sparse_allgather(N, streams)
+        d, ei, ev = ref[rank]
+        ok = g.header.status == 0 and g.dense == d
+        if ok and d:
+            ok = np.array_equal(g.val.cpu().numpy(), ev)
+        elif ok:
+            ok = np.array_equal(g.idx.cpu().numpy().view(np.uint32), ei) and np.array_equal(g.val.cpu().numpy(), ev)
+        ok = ok and g.header.bytes_recv == st[rank]["bytes_recv"]
+        if not ok:
+            fails += 1
+            print(f"rank {rank}: allgather N={N} MISMATCH", flush=True)
     return fails
 
 
