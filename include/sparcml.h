@@ -307,8 +307,9 @@ sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uin
 uint64_t sparcml_kernel_launches(void);
 
 /* Per-kernel timing for the bench's roofline.  While enabled, every launch of
- * a kernel class ("topk_filter", "merge", "window", "concat", "split_push",
- * "barrier", "rd_stage", ...) is bracketed by CUDA events on its stream.
+ * a kernel class ("topk", "topk_bucketed", "split_push", "owner", "owner_dsar",
+ * "concat", "rd_push", "rd_stage", "ag_publish", "ag_gather", "merge", "barrier",
+ * ...) is bracketed by CUDA events on its stream.
  * sparcml_profile_read synchronises those events and returns the launch
  * count and the summed duration in milliseconds. */
 void sparcml_profile_enable(int on);

@@ -426,7 +426,6 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
     w.src_idx[0] = idx;
     w.src_val[0] = val;
     w.src_win[0] = win_table(L, base, 0);   // built by p1_prep
-    w.n1 = n;
     w.sched = make_sched(1);
     w.dense = reinterpret_cast<float*>(base + L.part_off);
     w.codes = reinterpret_cast<uint8_t*>(base + L.part_off);

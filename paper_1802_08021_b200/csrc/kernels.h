@@ -31,24 +31,6 @@ struct MergeJobsArgs {   // stand-alone sparcml_merge_sum
 };
 
 // ----------------------------------------------------------- window ------
-struct WinSourceDesc {
-  const uint32_t* idx;
-  const float* val;
-  uint64_t n;
-  int dense;
-  uint64_t dense_base;
-};
-
-struct WindowArgs {      // P == 1 densify / QSGD of one stream
-  int nsrc;
-  WinSourceDesc src[kMaxRanks];
-  TreeSched sched;
-  uint64_t lo, hi;
-  WinOutput out;
-  ScanCounters* ctr;
-  TileStatus* status;
-};
-
 // ----------------------------------------------------- recursive doubling ---
 // A "stream buffer": sparse idx at base, val at base + val_off; dense vals at base.
 struct StreamBuf {
@@ -135,7 +117,6 @@ struct OwnerArgs {
   uint32_t* st_idx;
   float* st_val;
   uint64_t* blk;
-  uint64_t n1;                     // P == 1: the input's nnz (diagnostics)
 };
 
 struct ConcatArgs {
@@ -232,7 +213,6 @@ class ProfScope {
 
 int device_sm_count();
 cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t s);
-cudaError_t launch_window(const WindowArgs& a, cudaStream_t s);
 cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s);
 cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s);
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s);
@@ -240,7 +220,6 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);   // host_dsar sel
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);
-int owner_grid_size();
 cudaError_t launch_fuse_streams(const FuseArgs& a, cudaStream_t s);
 cudaError_t launch_ag_publish(const AgPublishArgs& a, cudaStream_t s);
 cudaError_t launch_ag_gather(const AgGatherArgs& a, cudaStream_t s);

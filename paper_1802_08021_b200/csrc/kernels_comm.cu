@@ -158,46 +158,6 @@ cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t
   return cudaGetLastError();
 }
 
-// ===========================================================================
-// window kernel (P == 1: densify / QSGD-encode one stream)
-// ===========================================================================
-__global__ void __launch_bounds__(kThreads) window_kernel(WindowArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ WinSource s_src[kMaxRanks];
-  __shared__ uint32_t s_ticket, s_gen;
-  if (threadIdx.x < a.nsrc) {
-    const WinSourceDesc& d = a.src[threadIdx.x];
-    s_src[threadIdx.x].idx = d.idx;
-    s_src[threadIdx.x].val = d.val;
-    s_src[threadIdx.x].n = d.n;
-    s_src[threadIdx.x].dense = d.dense;
-    s_src[threadIdx.x].dense_base = d.dense_base;
-  }
-  if (threadIdx.x == 0) s_gen = a.ctr->gen;
-  __syncthreads();
-  const uint32_t nwin = (uint32_t)ceil_div(a.hi - a.lo, kWin);
-  while (true) {
-    const uint32_t w = next_ticket(a.ctr, &s_ticket);
-    if (w >= nwin) break;
-    window_tile(s_src, a.nsrc, a.sched, a.lo, a.hi, w, smem, a.status, s_gen, nwin, a.out);
-  }
-  scan_block_exit_last(a.ctr);
-}
-
-cudaError_t launch_window(const WindowArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  const size_t smem = win_smem_bytes(a.nsrc);
-  if (!attr) {
-    cudaFuncSetAttribute(window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem_bytes(kMaxRanks));
-    attr = true;
-  }
-  const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)device_sm_count() * 4));
-  SPARCML_PROF("window", s);
-  window_kernel<<<grid, kThreads, smem, s>>>(a);
-  ++g_launches;
-  return cudaGetLastError();
-}
 
 // ===========================================================================
 // recursive doubling (§5.3.1): push of the input, one kernel per stage
@@ -1033,7 +993,6 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
   return cudaSuccess;
 }
 
-int owner_grid_size() { return device_sm_count() * 8; }
 
 // ===========================================================================
 // allgather phase (§5.3.2 P:757-758 / §5.3.3): pull every owner's
