@@ -168,10 +168,12 @@ int or_ssar_recursive_double(int P, uint64_t N, uint64_t delta,
                              const uint32_t* idx, const float* val, const uint64_t* off,
                              int n_out, int* out_dense, uint64_t* out_n,
                              uint32_t* out_idx, float* out_val, or_rank_stats* stats) {
-  int r, t, L = 0;
+  int r, t, L = 0, P2 = 1, e;
   strm *cur, *nxt;
-  if (P < 1 || P > 256 || (P & (P - 1)) != 0) return -1;
-  while ((1 << L) < P) L++;
+  if (P < 1 || P > 256) return -1;
+  while (P2 * 2 <= P) P2 *= 2;   /* nearest lower power of two (App. A) */
+  e = P - P2;                     /* extra ranks, folded into ranks 0..e-1 (reading R-28) */
+  while ((1 << L) < P2) L++;
   cur = (strm*)calloc((size_t)P, sizeof(strm));
   nxt = (strm*)calloc((size_t)P, sizeof(strm));
   if (!cur || !nxt) return -1;
@@ -179,9 +181,24 @@ int or_ssar_recursive_double(int P, uint64_t N, uint64_t delta,
   for (r = 0; r < P; r++)
     if (strm_copy_in(&cur[r], idx + off[r], val + off[r], off[r + 1] - off[r])) return -1;
 
+  /* front step: extra rank P2+i sends its stream to rank i, which sums it in */
+  for (r = 0; r < e; r++) {
+    const int x = P2 + r;
+    if (stats) {
+      stats[x].bytes_sent += strm_bytes(&cur[x]);
+      stats[x].msgs_sent += 1;
+      if (!cur[x].dense) stats[x].pairs_sent += cur[x].n;
+      stats[r].bytes_recv += strm_bytes(&cur[x]);
+    }
+    if (strm_sum(N, delta, &cur[r], &cur[x], &nxt[r])) return -1;
+    strm_free(&cur[r]);
+    cur[r] = nxt[r];
+    memset(&nxt[r], 0, sizeof(strm));
+  }
+
   for (t = 1; t <= L; t++) {
     int d = 1 << (t - 1);     /* distance 2^(t-1) */
-    for (r = 0; r < P; r++) {
+    for (r = 0; r < P2; r++) {
       int q = r ^ d;
       /* rank r sends its whole current stream to q and receives q's */
       if (stats) {
@@ -196,7 +213,28 @@ int or_ssar_recursive_double(int P, uint64_t N, uint64_t delta,
         stats[r].stage_dense[t - 1] = nxt[r].dense;
       }
     }
-    for (r = 0; r < P; r++) { strm_free(&cur[r]); cur[r] = nxt[r]; memset(&nxt[r], 0, sizeof(strm)); }
+    for (r = 0; r < P2; r++) { strm_free(&cur[r]); cur[r] = nxt[r]; memset(&nxt[r], 0, sizeof(strm)); }
+  }
+  /* end step: rank i sends the result to extra rank P2+i */
+  for (r = 0; r < e; r++) {
+    const int x = P2 + r;
+    if (stats) {
+      stats[r].bytes_sent += strm_bytes(&cur[r]);
+      stats[r].msgs_sent += 1;
+      if (!cur[r].dense) stats[r].pairs_sent += cur[r].n;
+      stats[x].bytes_recv += strm_bytes(&cur[r]);
+    }
+    strm_free(&cur[x]);
+    if (cur[r].dense) {
+      memset(&cur[x], 0, sizeof(strm));
+      cur[x].dense = 1;
+      cur[x].n = N;
+      cur[x].val = (float*)malloc((N ? N : 1) * sizeof(float));
+      if (!cur[x].val) return -1;
+      memcpy(cur[x].val, cur[r].val, N * sizeof(float));
+    } else if (strm_copy_in(&cur[x], cur[r].idx, cur[r].val, cur[r].n)) {
+      return -1;
+    }
   }
   for (r = 0; r < P && r < n_out; r++) strm_out(&cur[r], N, r, out_dense, out_n, out_idx, out_val);
   for (r = 0; r < P; r++) strm_free(&cur[r]);

@@ -76,7 +76,13 @@ typedef struct {
 } or_rank_stats;
 
 /* SSAR_Recursive_double (§5.3.1, Fig. fig:ssar_rec_dbl).
- * P a power of two <= 256.  Stage t=1..log2 P: rank r exchanges its whole
+ * P <= 256.  When P is not a power of two (App. A P:1331 "add two
+ * additional steps in front and at the end ... to reduce the number of
+ * participating nodes to the nearest lower power of two"; reading R-28): with
+ * P' the largest power of two <= P, extra rank P'+i first sends its stream
+ * to rank i, which sums it in (dense switch applies), recursive doubling
+ * runs over ranks 0..P'-1, and rank i finally sends its result to P'+i.
+ * Stage t=1..log2 P': rank r exchanges its whole
  * current stream with r XOR 2^(t-1) (0-based reading of the figure's
  * p1<->p2, p1<->p3, p1<->p5; reading R-10) and sums with or_stream_sum using
  * delta (dense switch inside the sum; once dense stays dense).

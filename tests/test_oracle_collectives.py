@@ -279,3 +279,40 @@ def test_sparse_allgather_rejects_overlapping_ranges(orc):
     b = (np.array([10, 20], np.uint32), np.ones(2, np.float32))   # inside a's range
     with pytest.raises(ValueError):
         orc.sparse_allgather(100, [a, b])
+
+
+# ---- recursive doubling for non-power-of-two P (App. A; reading R-28) -----------
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("P", [3, 5, 6, 7, 12])
+def test_rd_folded_matches_definition(orc, seed, P):
+    """Folding the extra ranks in and out around recursive doubling still
+    computes the definition (integer values: exactly; normal values: within
+    the rounding bound), on every rank including the extra ones."""
+    rng = np.random.default_rng(7000 + 10 * P + seed)
+    N = int(rng.choice([500, 4096]))
+    d = float(rng.choice([0.01, 0.1, 0.3]))
+    k = max(1, int(d * N))
+    kind = "int" if seed % 2 == 0 else "normal"
+    streams = synth.uniform_streams(P, N, k, seed=seed, kind=kind)
+    res, st = orc.ssar_recursive_double(N, streams)
+    _check_against_definition(N, streams, res, kind == "int", orc.switch_threshold(N))
+
+
+def test_rd_folded_order_and_volume(orc):
+    """P = 3: the tree is (x0 + x2) + x1 -- pinned with values whose fp32 sums
+    differ by order -- and the extra rank sends its stream once and receives
+    the result once."""
+    N = 8
+    big, tiny = np.float32(1.0), np.float32(2.0 ** -24)
+    x0 = (np.array([0], np.uint32), np.array([big], np.float32))
+    x1 = (np.array([0], np.uint32), np.array([tiny], np.float32))
+    x2 = (np.array([0], np.uint32), np.array([tiny], np.float32))
+    res, st = orc.ssar_recursive_double(N, [x0, x1, x2])
+    want = np.float32(np.float32(big + tiny) + tiny)          # (x0 + x2) + x1, round to nearest even
+    for r in range(3):
+        d, i, v = res[r]
+        assert not d and list(i) == [0] and v[0] == want
+    assert st[2]["bytes_sent"] == 8 and st[2]["bytes_recv"] == 8 and st[2]["msgs_sent"] == 1
+    assert st[0]["bytes_recv"] == 8 + 8 and st[0]["bytes_sent"] == 8 + 8   # fold in + RD stage, RD stage + result out
+    assert st[1]["bytes_sent"] == 8 and st[1]["bytes_recv"] == 8
