@@ -118,15 +118,14 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.part_bytes = align_up(8 * L.part_cap + 256, 256);
   L.scales_off = off + align_up(L.part_cap + 16, 256);   // codes <= part_cap bytes (8 bits)
   off += L.part_bytes;
-  L.L = 0;
-  const bool pow2 = (P & (P - 1)) == 0;
-  if (pow2)
-    while ((1 << L.L) < P) ++L.L;
+  L.L = 0;   // stages of recursive doubling over P' = the largest power of two <= P (R-28)
+  while ((2 << L.L) <= P) ++L.L;
   L.rd_off = off;
   // sparse slots: stage outputs hold <= delta <= N/2 pairs, the stage-1 push a whole input
   L.rd_val_off = align_up(4 * std::max<uint64_t>(half_cap(max_N), max_nnz) + 64, 256);
   L.rd_bytes = align_up(std::max<size_t>(2 * L.rd_val_off, 4 * max_N) + 256, 256);
-  if (pow2 && P > 1) off += (size_t)(2 + 2 * L.L) * L.rd_bytes;
+  // cur x2 + recv[2 parities][stages 0..L+1] (0: fold in, L+1: result out, R-28)
+  if (P > 1) off += (size_t)(2 + 2 * (L.L + 2)) * L.rd_bytes;
   L.ag_off = off;
   L.ag_val_off = align_up(4 * max_nnz, 256);
   off += align_up(L.ag_val_off + 4 * max_nnz, 256);
@@ -184,9 +183,9 @@ inline StreamBuf rd_cur(const Layout& L, char* base, int i) {
   b.val_off = L.rd_val_off;
   return b;
 }
-inline StreamBuf rd_recv(const Layout& L, char* base, int par, int t) {   // t = 1..L
+inline StreamBuf rd_recv(const Layout& L, char* base, int par, int t) {   // t = 0..L+1
   StreamBuf b;
-  b.base = base + L.rd_off + (size_t)(2 + par * L.L + (t - 1)) * L.rd_bytes;
+  b.base = base + L.rd_off + (size_t)(2 + par * (L.L + 2) + t) * L.rd_bytes;
   b.val_off = L.rd_val_off;
   return b;
 }
@@ -237,55 +236,97 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
                       const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
   const Layout& L = c->L;
   const int Lg = L.L;
-  for (size_t i = 0; i < R.size(); ++i) {
-    const int r = R[i], q = r ^ 1;
+  const int P2 = 1 << Lg, E = c->P - P2;   // R-28: extra ranks P2..P-1 fold into 0..E-1
+  auto pos = [&](int r) -> int {           // R's slot of rank r (loopback: every rank)
+    for (size_t i = 0; i < R.size(); ++i)
+      if (R[i] == r) return (int)i;
+    return -1;
+  };
+  auto push = [&](int i, int r, int q, int tgt) -> sparcml_status {
     RdPushArgs a = {};
     a.idx = idx[i];
     a.val = val[i];
     a.n = nnz[i];
-    a.dst[0] = rd_recv(L, c->peer[q], 0, 1);
-    a.dst[1] = rd_recv(L, c->peer[q], 1, 1);
+    a.dst[0] = rd_recv(L, c->peer[q], 0, tgt);
+    a.dst[1] = rd_recv(L, c->peer[q], 1, tgt);
     a.peer = ctrl_of(c->peer[q]);
     a.ctl = ctrl_of(c->peer[r]);
     a.N = cc.N;
     a.validate = cc.o.validate;
+    a.tgt = tgt;
     CK(c, launch_rd_push(a, cc.s));
-  }
-  for (int t = 1; t <= Lg; ++t) {
-    for (size_t i = 0; i < R.size(); ++i) {
-      const int r = R[i];
-      char* base = c->peer[r];
-      RdStageArgs a = {};
-      a.a_idx = idx[i];
-      a.a_val = val[i];
-      a.a_n = nnz[i];
-      a.a_from_cur = t > 1;
-      a.cur[0] = rd_cur(L, base, 0);
-      a.cur[1] = rd_cur(L, base, 1);
-      a.b[0] = rd_recv(L, base, 0, t);
-      a.b[1] = rd_recv(L, base, 1, t);
-      a.N = cc.N;
-      a.delta = cc.delta;
-      if (t == Lg) {
-        a.o.base = out[i] + SPARCML_HEADER_BYTES;
-        a.o.val_off = cc.val_offset - SPARCML_HEADER_BYTES;
-        a.o_cur = 0;
-        a.hdr = reinterpret_cast<sparcml_header*>(out[i]);
-        a.last = 1;
-        a.mpeer = nullptr;
-      } else {
-        a.o_cur = 1;
-        const int q = r ^ (1 << t);   // next stage's partner
-        a.m[0] = rd_recv(L, c->peer[q], 0, t + 1);
-        a.m[1] = rd_recv(L, c->peer[q], 1, t + 1);
-        a.mpeer = ctrl_of(c->peer[q]);
-      }
-      a.ctl = ctrl_of(base);
-      a.stage = t;
-      a.ctr = &ctrl_of(base)->scan[0];
-      a.status = status_of(L, base);
-      CK(c, launch_rd_stage(a, cc.s));
+    return SPARCML_OK;
+  };
+  auto stage = [&](int i, int r, int t) -> sparcml_status {
+    char* base = c->peer[r];
+    const bool folded = r < E;
+    RdStageArgs a = {};
+    a.a_idx = idx[i];
+    a.a_val = val[i];
+    a.a_n = nnz[i];
+    a.a_from_cur = t > 1 || (t == 1 && folded);
+    a.cur[0] = rd_cur(L, base, 0);
+    a.cur[1] = rd_cur(L, base, 1);
+    a.b[0] = rd_recv(L, base, 0, t);
+    a.b[1] = rd_recv(L, base, 1, t);
+    a.N = cc.N;
+    a.delta = cc.delta;
+    a.fold = folded && t == Lg;
+    if (t == Lg) {
+      a.o.base = out[i] + SPARCML_HEADER_BYTES;
+      a.o.val_off = cc.val_offset - SPARCML_HEADER_BYTES;
+      a.o_cur = 0;
+      a.hdr = reinterpret_cast<sparcml_header*>(out[i]);
+      a.last = 1;
+    } else {
+      a.o_cur = 1;
     }
+    int q = -1;   // whose receive buffer [t+1] my output is mirrored into
+    if (t < Lg) q = r ^ (1 << t);   // the next stage's partner (t = 0: the stage-1 partner)
+    else if (folded) q = P2 + r;    // the result out to my extra rank
+    if (q >= 0) {
+      a.m[0] = rd_recv(L, c->peer[q], 0, t + 1);
+      a.m[1] = rd_recv(L, c->peer[q], 1, t + 1);
+      a.mpeer = ctrl_of(c->peer[q]);
+    }
+    a.ctl = ctrl_of(base);
+    a.stage = t;
+    a.ctr = &ctrl_of(base)->scan[0];
+    a.status = status_of(L, base);
+    CK(c, launch_rd_stage(a, cc.s));
+    return SPARCML_OK;
+  };
+  sparcml_status st;
+  // front: extra ranks push into their fold partner; the others push to their stage-1 partner
+  for (int r = P2; r < c->P; ++r) {
+    const int i = pos(r);
+    if (i >= 0 && (st = push(i, r, r - P2, 0)) != SPARCML_OK) return st;
+  }
+  for (int r = E; r < P2; ++r) {
+    const int i = pos(r);
+    if (i >= 0 && (st = push(i, r, r ^ 1, 1)) != SPARCML_OK) return st;
+  }
+  for (int r = 0; r < E; ++r) {   // the fold step: sum the extra rank in, mirror to the stage-1 partner
+    const int i = pos(r);
+    if (i >= 0 && (st = stage(i, r, 0)) != SPARCML_OK) return st;
+  }
+  for (int t = 1; t <= Lg; ++t)
+    for (int r = 0; r < P2; ++r) {
+      const int i = pos(r);
+      if (i >= 0 && (st = stage(i, r, t)) != SPARCML_OK) return st;
+    }
+  for (int r = P2; r < c->P; ++r) {   // end: the extra ranks take their partner's result
+    const int i = pos(r);
+    if (i < 0) continue;
+    RdUnfoldArgs u = {};
+    u.src[0] = rd_recv(L, c->peer[r], 0, Lg + 1);
+    u.src[1] = rd_recv(L, c->peer[r], 1, Lg + 1);
+    u.stage = Lg + 1;
+    u.ctl = ctrl_of(c->peer[r]);
+    u.out = out[i];
+    u.N = cc.N;
+    u.val_offset = cc.val_offset;
+    CK(c, launch_rd_unfold(u, cc.s));
   }
   return SPARCML_OK;
 }
@@ -493,8 +534,6 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   int algo = o.algo;
   if (algo == SPARCML_ALGO_AUTO && c->P > 1)
     algo = (is_pow2(c->P) && 4 * N <= (256u << 10)) ? SPARCML_SSAR_RECURSIVE_DOUBLE : SPARCML_ALGO_AUTO;
-  if (algo == SPARCML_SSAR_RECURSIVE_DOUBLE && !is_pow2(c->P))
-    return fail(c, SPARCML_ERR_INVALID_ARG, "recursive doubling needs a power-of-two world");
   cc.algo = algo;
   // SSAR/DSAR for split-allgather: forced, or AUTO by sum k_i > delta (R-5)
   if (algo == SPARCML_SSAR_SPLIT_ALLGATHER) cc.host_dsar = 0;

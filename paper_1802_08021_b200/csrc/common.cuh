@@ -374,6 +374,7 @@ struct alignas(128) Ctrl {
   uint64_t ag_n[16];
   uint32_t ag_first[16], ag_last[16];
   uint32_t ag_done[16];
+  uint64_t fold_recv;             // RD folding (R-28): bytes received from my extra rank
 };
 
 __device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {

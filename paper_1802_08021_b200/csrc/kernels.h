@@ -44,10 +44,11 @@ struct RdPushArgs {
   const float* val;
   uint64_t n;
   StreamBuf dst[2];          // by call parity
-  Ctrl* peer;                // the stage-1 partner's control block
+  Ctrl* peer;                // the stage-1 partner's control block (or my fold partner's)
   Ctrl* ctl;                 // mine
   uint64_t N;
   int validate;
+  int tgt;                   // receiving stage: 1, or 0 = fold into rank i (R-28)
 };
 
 struct RdStageArgs {
@@ -66,11 +67,22 @@ struct RdStageArgs {
   StreamBuf m[2];
   Ctrl* mpeer;               // that partner's control block (nullptr at the last stage)
   Ctrl* ctl;                 // mine
-  int stage;                 // 1-based
+  int stage;                 // 1-based; 0 = the fold step (R-28)
   int last;
+  int fold;                  // this rank folded an extra rank in (and sends it the result)
   sparcml_header* hdr;       // last stage only
   ScanCounters* ctr;
   TileStatus* status;
+};
+
+// Extra rank of a folded RD (R-28): wait for the result my fold partner
+// mirrored into my buffer, copy it into the caller's out, write the header.
+struct RdUnfoldArgs {
+  StreamBuf src[2];          // my receive buffer [par][L+1]
+  int stage;                 // L + 1
+  Ctrl* ctl;
+  char* out;
+  uint64_t N, val_offset;
 };
 
 // ---------------------------------------------------------- split phase ---
@@ -215,6 +227,7 @@ int device_sm_count();
 cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t s);
 cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s);
 cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s);
+cudaError_t launch_rd_unfold(const RdUnfoldArgs& a, cudaStream_t s);
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s);
 cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);   // host_dsar selects merge / window
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);

@@ -176,11 +176,11 @@ __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
     if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
   }
   if (last_block<false>(&a.ctl->done_ctr[0]) && threadIdx.x == 0) {   // see split_push_kernel
-    a.peer->rd_n[par][1] = a.n;
-    a.peer->rd_dense[par][1] = 0;
-    a.peer->rd_ksum[par][1] = a.n;
+    a.peer->rd_n[par][a.tgt] = a.n;
+    a.peer->rd_dense[par][a.tgt] = 0;
+    a.peer->rd_ksum[par][a.tgt] = a.n;
     a.ctl->rd_sent[0] = 8 * a.n;
-    st_release_sys(&a.peer->rd_flag[par][1], seq + 1);
+    st_release_sys(&a.peer->rd_flag[par][a.tgt], seq + 1);
   }
 }
 
@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     ctl->own_n[t & 1] = on;
     ctl->own_dense[t & 1] = sparse_out ? 0u : 1u;
     ctl->own_ksum[t & 1] = ksum;
-    ctl->rd_recv[t - 1] = bbytes;
+    if (t > 0) ctl->rd_recv[t - 1] = bbytes;
+    else ctl->fold_recv = bbytes;   // the fold step (R-28)
     if (a.mpeer) {
       a.mpeer->rd_n[par][t + 1] = on;
       a.mpeer->rd_dense[par][t + 1] = sparse_out ? 0u : 1u;
@@ -296,6 +297,10 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
         sent += ctl->rd_sent[i];
         recv += ctl->rd_recv[i];
       }
+      if (a.fold) {   // R-28: the extra rank's stream came in, the result goes out to it
+        sent += ctl->rd_sent[t];
+        recv += ctl->fold_recv;
+      }
       write_header(a.hdr, sparse_out ? SPARCML_REPR_SPARSE : SPARCML_REPR_DENSE, on, a.N, ksum, sent, recv,
                    SPARCML_SSAR_RECURSIVE_DOUBLE, ctl->status,
                    sparse_out ? (uint64_t)((char*)o.base + o.val_off - (char*)a.hdr) : (uint64_t)SPARCML_HEADER_BYTES);
@@ -304,6 +309,54 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
       ctl->seq = seq + 1;   // the call is complete on this rank
     }
   }
+}
+
+__global__ void __launch_bounds__(kThreads) rd_unfold_kernel(RdUnfoldArgs a) {
+  __shared__ uint64_t s_n;
+  __shared__ uint32_t s_d;
+  Ctrl* ctl = a.ctl;
+  const uint32_t seq = ctl->seq;
+  const int par = seq & 1, t = a.stage;
+  if (threadIdx.x == 0) {
+    wait_flag_geq(&ctl->rd_flag[par][t], seq + 1);
+    s_n = *(volatile uint64_t*)&ctl->rd_n[par][t];
+    s_d = *(volatile uint32_t*)&ctl->rd_dense[par][t];
+  }
+  __syncthreads();
+  const uint64_t n = s_n;
+  const bool dense = s_d != 0;
+  const StreamBuf b = a.src[par];
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  if (dense) {
+    const float* src = reinterpret_cast<const float*>(b.base);
+    float* d = reinterpret_cast<float*>(a.out + SPARCML_HEADER_BYTES);
+    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.N; e += stride) d[e] = __ldcg(&src[e]);
+  } else {
+    const uint32_t* si = reinterpret_cast<const uint32_t*>(b.base);
+    const float* sv = reinterpret_cast<const float*>(b.base + b.val_off);
+    uint32_t* oi = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
+    float* ov = reinterpret_cast<float*>(a.out + a.val_offset);
+    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) {
+      oi[e] = __ldcg(&si[e]);
+      ov[e] = __ldcg(&sv[e]);
+    }
+  }
+  if (last_block<false>(&ctl->done_ctr[1]) && threadIdx.x == 0) {
+    const uint64_t ksum = *(volatile uint64_t*)&ctl->rd_ksum[par][t];
+    write_header(reinterpret_cast<sparcml_header*>(a.out), dense ? SPARCML_REPR_DENSE : SPARCML_REPR_SPARSE,
+                 dense ? a.N : n, a.N, ksum, ctl->rd_sent[0], dense ? 4 * a.N : 8 * n, SPARCML_SSAR_RECURSIVE_DOUBLE,
+                 ctl->status, dense ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset);
+    ctl->status = 0;
+    __threadfence();
+    ctl->seq = seq + 1;   // the call is complete on this rank
+  }
+}
+
+cudaError_t launch_rd_unfold(const RdUnfoldArgs& a, cudaStream_t s) {
+  SPARCML_PROF("rd_unfold", s);
+  rd_unfold_kernel<<<device_sm_count() * 2, kThreads, 0, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {

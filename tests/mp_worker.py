@@ -35,8 +35,6 @@ def main():
     fails = 0
     for rep in range(2):
         for name, N, k, algo, bits in cases:
-            if algo == S.SSAR_RECURSIVE_DOUBLE and (P & (P - 1)):
-                continue
             streams = synth.uniform_streams(P, N, k, seed=rep * 10 + len(name), kind="normal")
             i, v = streams[rank]
             it = torch.from_numpy(i.view(np.int32)).cuda()

@@ -71,7 +71,7 @@ def check_world(orc, P, N, streams, algo, bits=0, bucket=1024, seed=0, world=Non
     return outs
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7, 8, 12])
 @pytest.mark.parametrize("d", [0.001, 0.01, 0.1, 0.3])
 def test_rd(orc, P, d):
     N = 100_003
@@ -105,7 +105,7 @@ def test_edge_cases(orc):
     N = 5000
     e = (np.zeros(0, np.uint32), np.zeros(0, np.float32))
     one = (np.array([4999], np.uint32), np.array([2.5], np.float32))
-    for P in [2, 4]:
+    for P in [2, 3, 4, 5]:
         for algo in ["rd", "ssar", "dsar"]:
             check_world(orc, P, N, [e] * P, ALGOS[algo])
             check_world(orc, P, N, [one] + [e] * (P - 1), ALGOS[algo])
