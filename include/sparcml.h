@@ -200,6 +200,12 @@ sparcml_status sparcml_sparse_allgather_local(sparcml_comm* comm, const uint32_t
                                               uint64_t N, const sparcml_opts* opts_host,
                                               void* const* out_host, size_t out_bytes, void* stream);
 
+/* Algorithm 1's update ("v_t <- v_{t-1} - g_t"): v[j] -= g[j] for the
+ * allreduce result g in `out` (sparse: its pairs; dense: all N values),
+ * read from the device header -- no host synchronisation.  v: N floats
+ * (N = the result's N).  Errors: null arguments -> SPARCML_ERR_INVALID_ARG. */
+sparcml_status sparcml_apply_update(float* v, const void* out, void* stream);
+
 /* ---------------------- layer-wise tensor fusion ------------------------ */
 /* (the paper's deployment mode: "communication is
  * done layer-wise using non-blocking calls".)  A model's L layers

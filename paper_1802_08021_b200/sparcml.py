@@ -47,7 +47,7 @@ EXPORTED = [
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
     "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
     "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges", "sparcml_sparse_allgather",
-    "sparcml_sparse_allgather_local",
+    "sparcml_sparse_allgather_local", "sparcml_apply_update",
 ]
 
 
@@ -98,6 +98,7 @@ _sig = {
     "sparcml_quantize": (_i32, [_p, _u64, _i32, C.c_uint32, _u64, _u64, _p, _p, _p]),
     "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
     "sparcml_fuse_streams": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _p]),
+    "sparcml_apply_update": (_i32, [_p, _p, _p]),
     "sparcml_sparse_allgather": (_i32, [_p, _p, _p, _u64, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_sparse_allgather_local": (_i32, [_p, _p, _p, _p, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_layer_ranges": (_i32, [_p, _i32, _p, _p, _p]),
@@ -486,6 +487,32 @@ def split_result(out: torch.Tensor, offsets: Sequence[int], stream=None):
     if res.header.repr == REPR_DENSE:
         return [(None, res.val[r[l]:r[l + 1]]) for l in range(L)]
     return [(res.idx[r[l]:r[l + 1]], res.val[r[l]:r[l + 1]]) for l in range(L)]
+
+
+def apply_update(v: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """Algorithm 1's update v <- v - g from an allreduce result, on the device."""
+    _need(v, torch.float32, "v")
+    _check(_lib.sparcml_apply_update(v.data_ptr(), out.data_ptr(), _stream(stream)))
+    return v
+
+
+def algorithm1_step(comm, v: torch.Tensor, eps: torch.Tensor, grad: torch.Tensor, alpha: float, k: int,
+                    bucket: int = 0, q_bits: int = 0, q_bucket: int = 512, q_seed: int = 0, opts=None,
+                    ws=None, out=None, stream=None):
+    """One step of Algorithm 1 at this node, all on the device, no host sync:
+    acc = eps + alpha*grad; eps <- acc - TopK(acc); g = allreduce(Q(TopK(acc)), SUM); v <- v - g.
+    Q (q_bits = 2/4/8) is QSGD on the k selected values, buckets of q_bucket over the
+    value array, Philox counter = rank * (k per rank) + position (reading R-29); q_bits = 0: Q = identity.
+    `comm` is a Comm (one rank per process).  Returns the allreduce out buffer."""
+    N = v.numel()
+    idx, val = ef_topk(eps, grad, alpha, k, ws=ws, stream=stream, bucket=bucket)
+    if q_bits:
+        codes, scales = quantize(val, q_bits, bucket=q_bucket, seed=q_seed, ctr_base=comm.rank * val.numel(),
+                                 stream=stream)
+        val = dequantize(codes, scales, val.numel(), q_bits, bucket=q_bucket, stream=stream)
+    out = comm.allreduce(idx, val, N, out=out, opts=opts, stream=stream)
+    apply_update(v, out, stream=stream)
+    return out
 
 
 def topk_count(N: int, k: int, bucket: int = 0) -> int:

@@ -62,6 +62,7 @@ def main():
                       f"nnz {res.header.nnz}, status {res.header.status})", flush=True)
     fails += layerwise(comm, rank, P)
     fails += allgather(comm, rank, P)
+    fails += algorithm1(comm, rank, P)
     t = torch.tensor([fails])
     dist.all_reduce(t)
     comm.close()
@@ -160,6 +161,35 @@ def allgather(comm, rank, P):
         if not ok:
             fails += 1
             print(f"rank {rank}: allgather N={N} MISMATCH", flush=True)
+    return fails
+
+
+def algorithm1(comm, rank, P):
+    """Algorithm 1 through S.algorithm1_step on the IPC world, with
+    QSGD on the selected values (R-29), against the step composed from oracle pieces."""
+    N, k, alpha, qbits, qb, seed = 300_007, 3000, 0.05, 4, 512, 5
+    v = torch.zeros(N, device="cuda")
+    e = torch.zeros(N, device="cuda")
+    ws = S.TopkWorkspace(N, k)
+    vh = np.zeros(N, np.float32)
+    eh = [np.zeros(N, np.float32) for _ in range(P)]
+    opts = S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER)
+    fails = 0
+    for step in range(2):
+        g = torch.from_numpy(synth.gaussian_vector(N, seed=50 + step, rank=rank)).cuda()
+        S.algorithm1_step(comm, v, e, g, alpha, k, q_bits=qbits, q_bucket=qb, q_seed=seed, opts=opts, ws=ws)
+        hs = []
+        for r in range(P):
+            gr = synth.gaussian_vector(N, seed=50 + step, rank=r)
+            i, val, eh[r] = oracle.ef_topk(eh[r], gr, alpha, k)
+            c, sc = oracle.qsgd_quantize(val, qbits, bucket=qb, seed=seed, ctr_base=r * k)
+            hs.append((i, oracle.qsgd_dequantize(c, sc, len(val), qbits, qb)))
+        ref, _, _ = oracle.split_allgather(N, hs, algo=oracle.ALGO_SSAR_SPLIT)
+        _, gd = oracle.result_to_dense(ref[rank], N)
+        vh = (vh - gd).astype(np.float32)
+        if not (np.array_equal(v.cpu().numpy(), vh) and np.array_equal(e.cpu().numpy(), eh[rank])):
+            fails += 1
+            print(f"rank {rank}: algorithm 1 step {step} MISMATCH", flush=True)
     return fails
 
 
