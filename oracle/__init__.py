@@ -64,6 +64,10 @@ def lib():
                                             p, p, p, i32, p, p, p, p, p, p]
         _lib.or_sparse_allgather.restype = i32
         _lib.or_sparse_allgather.argtypes = [i32, u64, u64, p, p, p, i32, p, p, p, p, p]
+        _lib.or_set_op.restype = i32
+        _lib.or_set_op.argtypes = [i32]
+        _lib.or_brute_force_op.restype = u64
+        _lib.or_brute_force_op.argtypes = [i32, u64, p, p, p, p, p]
         _lib.or_topk.restype = u64
         _lib.or_topk.argtypes = [p, u64, u64, p, p, p]
         _lib.or_ef_topk.restype = u64
@@ -143,6 +147,34 @@ def _flatten(streams):
     if len(idx) == 0:
         idx, val = np.zeros(1, np.uint32), np.zeros(1, np.float32)
     return idx, val, off
+
+
+OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
+
+
+class op_scope:
+    """`with op_scope(OP_MAX): ...` runs the collective simulators with that operator."""
+
+    def __init__(self, op):
+        self.op = op
+
+    def __enter__(self):
+        if lib().or_set_op(self.op) != 0:
+            raise ValueError("unknown operator")
+        return self
+
+    def __exit__(self, *exc):
+        lib().or_set_op(OP_SUM)
+
+
+def brute_force_op(N, streams, op):
+    """(mask, values) of the definition for operator `op`; neutral element off the union."""
+    idx, val, off = _flatten(streams)
+    mask = np.zeros(N, np.uint8)
+    f32 = np.zeros(N, np.float32)
+    with op_scope(op):
+        lib().or_brute_force_op(len(streams), N, _ptr(idx), _ptr(val), _ptr(off), _ptr(mask), _ptr(f32))
+    return mask, f32
 
 
 def brute_force(N, streams):

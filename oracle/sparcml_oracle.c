@@ -28,6 +28,30 @@ uint64_t or_switch_threshold(uint64_t N, int isize, int c, double scale) {
   return (uint64_t)floorl(d);
 }
 
+/* Reduction operator for the collective simulators (§5: "arbitrary
+ * coordinate-wise associative reduction operations for which a neutral
+ * element can be defined"): 0 SUM (neutral 0), 1 MAX (neutral -inf),
+ * 2 MIN (neutral +inf).  Set with or_set_op; SUM by default. */
+static int g_op = 0;
+
+int or_set_op(int op) {
+  if (op < 0 || op > 2) return -1;
+  g_op = op;
+  return 0;
+}
+
+static float op_combine(float a, float b) {
+  if (g_op == 1) return a > b ? a : b;
+  if (g_op == 2) return a < b ? a : b;
+  return a + b;
+}
+
+static float op_neutral(void) {
+  if (g_op == 1) return -INFINITY;
+  if (g_op == 2) return INFINITY;
+  return 0.0f;
+}
+
 uint64_t or_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
                       const uint32_t* ib, const float* vb, uint64_t nb,
                       uint32_t* io, float* vo) {
@@ -42,7 +66,7 @@ uint64_t or_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
     } else if (ib[j] < ia[i]) {
       io[o] = ib[j]; vo[o] = vb[j]; j++;
     } else {
-      io[o] = ia[i]; vo[o] = va[i] + vb[j]; i++; j++;
+      io[o] = ia[i]; vo[o] = op_combine(va[i], vb[j]); i++; j++;
     }
     o++;
   }
@@ -59,9 +83,9 @@ uint64_t or_stream_sum(uint64_t N, uint64_t delta,
   if (!a_dense && !b_dense) {
     /* upper-bound |H1|+|H2|; if bigger than delta switch to dense. */
     if (na + nb > delta) {
-      for (j = 0; j < N; j++) out_val[j] = 0.0f;          /* neutral element */
-      for (j = 0; j < na; j++) out_val[ia[j]] = out_val[ia[j]] + va[j];
-      for (j = 0; j < nb; j++) out_val[ib[j]] = out_val[ib[j]] + vb[j];
+      for (j = 0; j < N; j++) out_val[j] = op_neutral();   /* neutral element */
+      for (j = 0; j < na; j++) out_val[ia[j]] = op_combine(out_val[ia[j]], va[j]);
+      for (j = 0; j < nb; j++) out_val[ib[j]] = op_combine(out_val[ib[j]], vb[j]);
       *out_dense = 1;
       return N;
     }
@@ -70,7 +94,7 @@ uint64_t or_stream_sum(uint64_t N, uint64_t delta,
   }
   if (a_dense && b_dense) {
     /* dense + dense -> elementwise (vectorised in the paper) sum. */
-    for (j = 0; j < N; j++) out_val[j] = va[j] + vb[j];
+    for (j = 0; j < N; j++) out_val[j] = op_combine(va[j], vb[j]);
     *out_dense = 1;
     return N;
   }
@@ -82,10 +106,27 @@ uint64_t or_stream_sum(uint64_t N, uint64_t delta,
     const float* sv = a_dense ? vb : va;
     uint64_t sn = a_dense ? nb : na;
     for (j = 0; j < N; j++) out_val[j] = dv[j];
-    for (j = 0; j < sn; j++) out_val[si[j]] = out_val[si[j]] + sv[j];
+    for (j = 0; j < sn; j++) out_val[si[j]] = op_combine(out_val[si[j]], sv[j]);
   }
   *out_dense = 1;
   return N;
+}
+
+uint64_t or_brute_force_op(int P, uint64_t N, const uint32_t* idx, const float* val,
+                           const uint64_t* off, uint8_t* mask, float* f32) {
+  /* The definition for any operator: every index of the union, reduced over
+   * the ranks that hold it (rank order; MAX and MIN are order-free). */
+  uint64_t j, K = 0;
+  int i;
+  for (j = 0; j < N; j++) { mask[j] = 0; f32[j] = op_neutral(); }
+  for (i = 0; i < P; i++)
+    for (j = off[i]; j < off[i + 1]; j++) {
+      const uint32_t x = idx[j];
+      f32[x] = mask[x] ? op_combine(f32[x], val[j]) : val[j];
+      mask[x] = 1;
+    }
+  for (j = 0; j < N; j++) K += mask[j];
+  return K;
 }
 
 uint64_t or_brute_force(int P, uint64_t N, const uint32_t* idx, const float* val,
@@ -289,6 +330,7 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
   if (P < 1 || N < (uint64_t)P) return -1;
   if (quant_bits != 0 && quant_bits != 2 && quant_bits != 4 && quant_bits != 8) return -1;
   if (quant_bits && bucket == 0) return -1;
+  if (quant_bits && g_op != 0) return -1;   /* QSGD needs the 0 neutral element (max-norm scale) */
   part = N / (uint64_t)P;                         /* floor(N/P), App. A */
   bnd = (uint64_t*)malloc(((size_t)P + 1) * sizeof(uint64_t));
   slices = (strm*)calloc((size_t)P * (size_t)P, sizeof(strm));
@@ -348,8 +390,9 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
     }
     if (K > delta) {
       res.dense = 1; res.n = N;
-      res.val = (float*)calloc(N ? N : 1, sizeof(float));
+      res.val = (float*)malloc((N ? N : 1) * sizeof(float));
       if (!res.val) return -1;
+      for (e = 0; e < N; e++) res.val[e] = op_neutral();
       for (j = 0; j < P; j++)
         for (e = 0; e < R[j].n; e++) res.val[bnd[j] + R[j].idx[e]] = R[j].val[e];
     } else {
@@ -370,8 +413,9 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
   } else {
     /* DSAR: owner switches its reduced split to dense (neutral fill 0),
      * optionally QSGD-encodes it (§6), then dense allgather. */
-    float* dense = (float*)calloc(N ? N : 1, sizeof(float));
+    float* dense = (float*)malloc((N ? N : 1) * sizeof(float));
     if (!dense) return -1;
+    for (e = 0; e < N; e++) dense[e] = op_neutral();
     for (j = 0; j < P; j++) {
       uint64_t nj = bnd[j + 1] - bnd[j];
       float* Dj = dense + bnd[j];

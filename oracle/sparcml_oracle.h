@@ -64,6 +64,18 @@ uint64_t or_brute_force(int P, uint64_t N, const uint32_t* idx, const float* val
                         const uint64_t* off, uint8_t* mask, double* d64,
                         float* f32, double* abs64);
 
+/* Reduction operator of the simulators below (§5: any
+ * coordinate-wise associative operation with a neutral element): 0 SUM
+ * (neutral 0), 1 MAX (-inf), 2 MIN (+inf); SUM until set.  The neutral
+ * element fills dense results.  QSGD requires SUM.  Returns 0 or -1. */
+int or_set_op(int op);
+
+/* The definition for the current operator: mask = union of the index sets,
+ * f32[j] = the operator over the ranks holding j (rank order), the neutral
+ * element elsewhere.  Returns K. */
+uint64_t or_brute_force_op(int P, uint64_t N, const uint32_t* idx, const float* val,
+                           const uint64_t* off, uint8_t* mask, float* f32);
+
 /* Per-rank accounting of one simulated collective (the SPEC's TraceRecord,
  * S:172-179, reduced to what the tests check). */
 typedef struct {

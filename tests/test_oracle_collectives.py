@@ -316,3 +316,43 @@ def test_rd_folded_order_and_volume(orc):
     assert st[2]["bytes_sent"] == 8 and st[2]["bytes_recv"] == 8 and st[2]["msgs_sent"] == 1
     assert st[0]["bytes_recv"] == 8 + 8 and st[0]["bytes_sent"] == 8 + 8   # fold in + RD stage, RD stage + result out
     assert st[1]["bytes_sent"] == 8 and st[1]["bytes_recv"] == 8
+
+
+# ---- MAX / MIN operators (§5: any associative op with a neutral element) ---------
+
+@pytest.mark.parametrize("op", [1, 2])
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_max_min_all_algorithms_equal_definition(orc, op, P):
+    """MAX and MIN are associative and commutative, so every algorithm must
+    return exactly the definition: on the union the op over the holders, and
+    the neutral element (-inf / +inf) where a dense result has no entry."""
+    for N, k in [(4096, 40), (4096, 1500)]:          # stays sparse / switches to dense
+        streams = synth.uniform_streams(P, N, k, seed=op * 10 + P, kind="normal")
+        mask, want = orc.brute_force_op(N, streams, op)
+        with orc.op_scope(op):
+            results = [orc.ssar_recursive_double(N, streams)[0]]
+            for algo in (orc.ALGO_SSAR_SPLIT, orc.ALGO_DSAR_SPLIT):
+                results.append(orc.split_allgather(N, streams, algo=algo)[0])
+        for res in results:
+            for d, i, v in res:
+                if d:
+                    np.testing.assert_array_equal(v, want)
+                    assert np.all(np.isinf(v[mask == 0]))
+                else:
+                    np.testing.assert_array_equal(i, np.nonzero(mask)[0])
+                    np.testing.assert_array_equal(v, want[i])
+        # MAX of a set >= every member, MIN <= (the definition is not SUM)
+        vals = np.full((P, N), np.nan, np.float32)
+        for r, (i, v) in enumerate(streams):
+            vals[r, i] = v
+        sel = ~np.all(np.isnan(vals), 0)
+        ref = np.zeros(N, np.float32)
+        ref[sel] = np.nanmax(vals[:, sel], 0) if op == 1 else np.nanmin(vals[:, sel], 0)
+        np.testing.assert_array_equal(want[mask == 1], ref[mask == 1])
+
+
+def test_quantization_requires_sum(orc):
+    streams = synth.uniform_streams(2, 4096, 100, seed=1)
+    with orc.op_scope(1):
+        with pytest.raises(ValueError):
+            orc.split_allgather(4096, streams, algo=orc.ALGO_DSAR_SPLIT, quant_bits=4)
