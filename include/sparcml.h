@@ -51,9 +51,11 @@ typedef enum {
   SPARCML_ERR_STATE = 8         /* communicator not connected / wrong mode     */
 } sparcml_status;
 
-/* Coordinate-wise reduction with a neutral element.  SUM only on
- * the hot path (neutral 0). */
-typedef enum { SPARCML_OP_SUM = 0 } sparcml_op;
+/* Reduction operator (§5: "arbitrary coordinate-wise associative
+ * reduction operations for which a neutral element can be defined"; reading
+ * R-30).  Dense results hold the neutral element where no rank has an entry:
+ * 0 (SUM), -inf (MAX), +inf (MIN).  QSGD (quant_bits) requires SUM. */
+typedef enum { SPARCML_OP_SUM = 0, SPARCML_OP_MAX = 1, SPARCML_OP_MIN = 2 } sparcml_op;
 
 /* Allreduce algorithms (§5.3).  AUTO: recursive doubling for the
  * small-data case, split-allgather otherwise; inside split-

@@ -217,6 +217,7 @@ struct CallCtx {
   sparcml_opts o;
   int algo;            // resolved: RD, SPLIT (SSAR/DSAR/AUTO decided below)
   int host_dsar;       // -1 unknown (device decides), 0/1 known
+  int op;              // reduction operator (R-30)
   cudaStream_t s;
 };
 
@@ -272,6 +273,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     a.N = cc.N;
     a.delta = cc.delta;
     a.fold = folded && t == Lg;
+    a.op = cc.op;
     if (t == Lg) {
       a.o.base = out[i] + SPARCML_HEADER_BYTES;
       a.o.val_off = cc.val_offset - SPARCML_HEADER_BYTES;
@@ -391,6 +393,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.seed_hi = (uint32_t)(cc.o.seed >> 32);
     w.host_dsar = cc.host_dsar;
     w.wait = 1;
+    w.op = cc.op;
     w.ctl = ctrl_of(base);
     w.st_idx = reinterpret_cast<uint32_t*>(base + L.stage_off);
     w.st_val = reinterpret_cast<float*>(base + L.stage_off + 4 * (size_t)P * L.cap_s);
@@ -423,6 +426,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     a.algo = SPARCML_SSAR_SPLIT_ALLGATHER;
     a.status = status_of(L, c->peer[r]);
     a.host_dsar = cc.host_dsar;
+    a.op = cc.op;
     CK(c, launch_concat(a, cc.s));
   }
   return SPARCML_OK;
@@ -477,6 +481,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
     w.seed_hi = (uint32_t)(cc.o.seed >> 32);
     w.host_dsar = 1;
     w.wait = 0;
+    w.op = cc.op;
     w.peer[0] = my;
     w.ctl = my;
     CK(c, launch_owner(w, cc.s));
@@ -493,6 +498,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   a.algo = cc.o.algo == SPARCML_ALGO_AUTO ? SPARCML_SSAR_SPLIT_ALLGATHER : cc.o.algo;
   a.status = status_of(L, base);
   a.host_dsar = dsar ? 1 : 0;
+  a.op = cc.op;
   CK(c, launch_concat(a, cc.s));
   return SPARCML_OK;
 }
@@ -502,7 +508,8 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
                               void* const* out, size_t out_bytes, void* stream) {
   if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
   if (!c->connected) return fail(c, SPARCML_ERR_STATE, "communicator not connected");
-  if (op != SPARCML_OP_SUM) return fail(c, SPARCML_ERR_INVALID_ARG, "only SPARCML_OP_SUM is supported");
+  if (op != SPARCML_OP_SUM && op != SPARCML_OP_MAX && op != SPARCML_OP_MIN)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "op must be SUM, MAX or MIN");
   if (N == 0 || N > c->L.max_N) return fail(c, SPARCML_ERR_INVALID_ARG, "N must be in [1, max_N]");
   if (N > 0xFFFFFFFFull) return fail(c, SPARCML_ERR_INVALID_ARG, "N must fit u32 indices");
   if ((uint64_t)c->P > N) return fail(c, SPARCML_ERR_INVALID_ARG, "N must be >= nranks");
@@ -511,6 +518,8 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   if (opts) o = *opts;
   sparcml_status st = check_opts(c, o);
   if (st != SPARCML_OK) return st;
+  if (o.quant_bits && op != SPARCML_OP_SUM)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "QSGD (quant_bits) requires SPARCML_OP_SUM");
   if (out_bytes < sparcml_result_bytes(N)) return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N)");
   const int nl = c->local ? c->P : 1;
   uint64_t ksum_host = 0;
@@ -527,6 +536,7 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   cc.o = o;
   cc.delta = effective_delta(N, o);
   cc.val_offset = sparcml_result_val_offset(N);
+  cc.op = (int)op;
   cc.s = static_cast<cudaStream_t>(stream);
   CK(c, cudaSetDevice(c->device));
   // algorithm: AUTO -> recursive doubling for small data (latency-bound,

@@ -271,6 +271,16 @@ __device__ __forceinline__ float qsgd_decode(uint32_t code, float scale, uint32_
 }
 
 // ---------------------------------------------------------------------------
+// reduction operator (§5; reading R-30): 0 SUM, 1 MAX, 2 MIN
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float op_combine(int op, float a, float b) {
+  return op == 0 ? __fadd_rn(a, b) : (op == 1 ? fmaxf(a, b) : fminf(a, b));
+}
+__device__ __forceinline__ float op_neutral(int op) {
+  return op == 0 ? 0.0f : (op == 1 ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000));
+}
+
+// ---------------------------------------------------------------------------
 // warp-cooperative searches (32 probes per step)
 // ---------------------------------------------------------------------------
 // first position p in a[0..n) with a[p] >= key (all lanes return it)

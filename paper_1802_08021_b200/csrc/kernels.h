@@ -70,6 +70,7 @@ struct RdStageArgs {
   int stage;                 // 1-based; 0 = the fold step (R-28)
   int last;
   int fold;                  // this rank folded an extra rank in (and sends it the result)
+  int op;                    // reduction operator (R-30)
   sparcml_header* hdr;       // last stage only
   ScanCounters* ctr;
   TileStatus* status;
@@ -122,6 +123,7 @@ struct OwnerArgs {
   uint32_t seed_lo, seed_hi;
   int host_dsar;                   // -1 device decides, else 0/1
   int wait;                        // 1: wait for the sources' flags (P > 1)
+  int op;                          // reduction operator (R-30)
   Ctrl* peer[kMaxRanks];
   Ctrl* ctl;
   // SSAR merge path: spill area for dense block ranges (P * cap_s pairs, SoA)
@@ -151,6 +153,7 @@ struct ConcatArgs {
   uint32_t algo;
   TileStatus* status;
   int host_dsar;                   // -1: launch both concat variants (the device decides), else 0/1
+  int op;                          // reduction operator (R-30): neutral fill when densifying
 };
 
 struct BarrierArgs {

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   if (sparse_out) {
     MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem);
     MergeOutput mo;
+    mo.op = a.op;
     mo.idx = reinterpret_cast<uint32_t*>(o.base);
     mo.val = reinterpret_cast<float*>(o.base + o.val_off);
     mo.n = &ctl->own_n[t & 1];
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     ts.src[0] = 1;
     WinOutput wo = {};
     wo.mode = WIN_DENSE;
+    wo.op = a.op;
     wo.dense = reinterpret_cast<float*>(o.base);
     wo.dense2 = m.base ? reinterpret_cast<float*>(m.base) : nullptr;
     wo.dense_base = 0;
@@ -672,7 +674,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
         float val = v[q];
         const uint32_t pos = pos0[q] + rank[q];
         if (role[q] == 1) {   // left run (lower ranks): first on ties, fl(left + right)
-          if (rank[q] < qlen[q] && xk[qoff[q] + rank[q]] == k) val = __fadd_rn(val, xv[qoff[q] + rank[q]]);
+          if (rank[q] < qlen[q] && xk[qoff[q] + rank[q]] == k) val = op_combine(a.op, val, xv[qoff[q] + rank[q]]);
         } else if (role[q] == 2) {   // right run: a key the left run holds was summed there
           if (rank[q] > 0 && xk[qoff[q] + rank[q] - 1] == k) {
             k = kDead;
@@ -944,7 +946,7 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
         for (int t = 0; t < a.sched.n; ++t) {
           const int d = a.sched.dst[t], sr = a.sched.src[t];
           if (m & (1u << sr)) {
-            if (m & (1u << d)) vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[sr * kWin + p]);
+            if (m & (1u << d)) vals[d * kWin + p] = op_combine(a.op, vals[d * kWin + p], vals[sr * kWin + p]);
             else {
               vals[d * kWin + p] = vals[sr * kWin + p];
               m |= 1u << d;
@@ -953,7 +955,7 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
         }
         r[q] = vals[p];
       } else {
-        r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : 0.0f;
+        r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : op_neutral(a.op);
       }
     }
     // (4) store: QSGD codes + scales, or dense
@@ -1246,6 +1248,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     ts.n = 0;
     WinOutput wo = {};
     wo.mode = WIN_DENSE;
+    wo.op = a.op;
     wo.dense = out_dense;
     wo.dense_base = 0;
     for (int j = 0; j < a.P; ++j) {

@@ -35,6 +35,7 @@ struct MergeOutput {
   uint32_t* idx2;       // optional mirror (a peer's receive buffer over NVLink)
   float* val2;
   uint64_t* n2;
+  int op;               // reduction operator (R-30)
 };
 
 // Merges diagonal range [d0, d0 + kMergeTile) of merge(A, B).  Returns nothing;
@@ -102,7 +103,7 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
         const uint32_t key = sm.ak[ia + 1];
         float v = sm.av[ia + 1];
         // the element following A[ia] in merged order is B[ib] (or the look-ahead)
-        if ((ib < lb || has_next_b) && sm.bk[ib] == key) v = __fadd_rn(v, sm.bv[ib]);
+        if ((ib < lb || has_next_b) && sm.bk[ib] == key) v = op_combine(out.op, v, sm.bv[ib]);
         ok[s] = key;
         ov[s] = v;
         emit |= 1u << s;
@@ -182,6 +183,7 @@ struct WinOutput {
   uint8_t* codes;
   float* scales;
   uint64_t qbase;
+  int op;               // reduction operator (R-30): combine and neutral fill
   int bits;
   uint32_t bucket;
   uint32_t seed_lo, seed_hi;
@@ -343,14 +345,14 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
       const int d = ts.dst[q], s = ts.src[q];
       if (m & (1u << s)) {
         if (m & (1u << d)) {
-          vals[d * kWin + p] = __fadd_rn(vals[d * kWin + p], vals[s * kWin + p]);
+          vals[d * kWin + p] = op_combine(out.op, vals[d * kWin + p], vals[s * kWin + p]);
         } else {
           vals[d * kWin + p] = vals[s * kWin + p];
           m |= 1u << d;
         }
       }
     }
-    r[i] = (m & 1u) ? vals[p] : 0.0f;
+    r[i] = (m & 1u) ? vals[p] : op_neutral(out.op);
     if (m & 1u) present |= 1u << i;
   }
 

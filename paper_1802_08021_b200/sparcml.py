@@ -31,6 +31,7 @@ _lib = C.CDLL(LIB_PATH)
 OK, ERR_INVALID_ARG, ERR_UNSORTED, ERR_NONFINITE, ERR_MISMATCH, ERR_CUDA, ERR_OOM, ERR_STATE = 0, 1, 2, 3, 4, 5, 7, 8
 ALGO_AUTO, SSAR_RECURSIVE_DOUBLE, SSAR_SPLIT_ALLGATHER, DSAR_SPLIT_ALLGATHER = 0, 1, 2, 3
 SPARSE_ALLGATHER = 4   # header algo_used of sparcml_sparse_allgather
+OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
 REPR_SPARSE, REPR_DENSE = 0, 1
 HEADER_BYTES = 64
 IPC_HANDLE_BYTES = 64
@@ -255,7 +256,7 @@ class LocalWorld:
         self._h, self.P, self.max_N, self.max_nnz, self.device = h, P, max_N, max_nnz, dev
 
     def allreduce(self, streams: Sequence, N: int, outs: Optional[Sequence[torch.Tensor]] = None,
-                  opts: Optional[Opts] = None, stream=None):
+                  opts: Optional[Opts] = None, stream=None, op: int = OP_SUM):
         """streams: P pairs (idx int32 cuda, val float32 cuda).  Returns the P out buffers."""
         P = self.P
         assert len(streams) == P
@@ -269,7 +270,7 @@ class LocalWorld:
         na = (C.c_uint64 * P)(*[int(i.numel()) for i, _ in streams])
         oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
         o = opts if opts is not None else make_opts()
-        _check(_lib.sparcml_sparse_allreduce_local(self._h, ia, va, na, N, 0, C.byref(o), oa,
+        _check(_lib.sparcml_sparse_allreduce_local(self._h, ia, va, na, N, op, C.byref(o), oa,
                                                    int(outs[0].numel()), _stream(stream)), self._h)
         return list(outs)
 
@@ -331,13 +332,13 @@ class Comm:
             _check(_lib.sparcml_comm_connect(h, arr), h)
 
     def allreduce(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,
-                  opts: Optional[Opts] = None, stream=None) -> torch.Tensor:
+                  opts: Optional[Opts] = None, stream=None, op: int = OP_SUM) -> torch.Tensor:
         _need(idx, torch.int32, "idx")
         _need(val, torch.float32, "val")
         if out is None:
             out = new_out(N, idx.device)
         o = opts if opts is not None else make_opts()
-        _check(_lib.sparcml_sparse_allreduce(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, 0, C.byref(o),
+        _check(_lib.sparcml_sparse_allreduce(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, op, C.byref(o),
                                              out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
         return out
 

@@ -192,3 +192,38 @@ def test_baseline_configs_full_size(orc, cfg):
         streams = synth.lr_gradient_streams(P, N, seed=5)
         algo = S.ALGO_AUTO
     check_world(orc, P, N, streams, algo)
+
+
+@pytest.mark.parametrize("op", [S.OP_MAX, S.OP_MIN])
+@pytest.mark.parametrize("P,algo", [(1, "ssar"), (1, "dsar"), (2, "rd"), (3, "rd"), (4, "ssar"), (5, "ssar"),
+                                    (4, "dsar"), (3, "dsar"), (8, "auto")])
+def test_max_min_operators(orc, op, P, algo):
+    """MAX / MIN (reading R-30) on every algorithm: bit-exact against the
+    oracle's simulators run with the same operator (neutral -inf / +inf in
+    dense results), sparse and densifying cases."""
+    for N, k in [(50_000, 500), (20_000, 6_000)]:
+        streams = synth.uniform_streams(P, N, k, seed=op * 100 + P, kind="normal")
+        w = S.LocalWorld(P, N, k)
+        outs = w.allreduce(to_cuda(streams), N, opts=S.make_opts(algo=ALGOS[algo]), op=op)
+        with orc.op_scope(op):
+            oalgo = ALGOS[algo]
+            if algo == "auto" and P > 1:
+                oalgo = S.SSAR_RECURSIVE_DOUBLE if 4 * N <= 256 * 1024 else S.ALGO_AUTO
+            res, st, _ = oracle_run(orc, N, streams, oalgo if P > 1 else ALGOS[algo])
+        for r in range(P):
+            g = S.read_result(outs[r])
+            d, ei, ev = res[r]
+            assert g.header.status == 0 and g.dense == bool(d)
+            if d:
+                np.testing.assert_array_equal(g.val.cpu().numpy(), ev)
+            else:
+                np.testing.assert_array_equal(g.idx.cpu().numpy().view(np.uint32), ei)
+                np.testing.assert_array_equal(g.val.cpu().numpy(), ev)
+
+
+def test_max_rejects_quantization():
+    w = S.LocalWorld(2, 1000, 10)
+    i = torch.arange(10, dtype=torch.int32, device="cuda")
+    v = torch.ones(10, device="cuda")
+    with pytest.raises(S.SparcmlError):
+        w.allreduce([(i, v), (i, v)], 1000, opts=S.make_opts(algo=S.DSAR_SPLIT_ALLGATHER, quant_bits=4), op=S.OP_MAX)
