@@ -64,6 +64,8 @@ def lib():
                                             p, p, p, i32, p, p, p, p, p, p]
         _lib.or_sparse_allgather.restype = i32
         _lib.or_sparse_allgather.argtypes = [i32, u64, u64, p, p, p, i32, p, p, p, p, p]
+        _lib.or_set_qsgd_norm.restype = i32
+        _lib.or_set_qsgd_norm.argtypes = [i32]
         _lib.or_set_op.restype = i32
         _lib.or_set_op.argtypes = [i32]
         _lib.or_brute_force_op.restype = u64
@@ -165,6 +167,21 @@ class op_scope:
 
     def __exit__(self, *exc):
         lib().or_set_op(OP_SUM)
+
+
+class qsgd_norm_scope:
+    """`with qsgd_norm_scope(1): ...` quantizes with the l2-norm scale (R-31)."""
+
+    def __init__(self, norm):
+        self.norm = norm
+
+    def __enter__(self):
+        if lib().or_set_qsgd_norm(self.norm) != 0:
+            raise ValueError("unknown norm")
+        return self
+
+    def __exit__(self, *exc):
+        lib().or_set_qsgd_norm(0)
 
 
 def brute_force_op(N, streams, op):

@@ -611,6 +611,30 @@ float or_qsgd_uniform(uint64_t seed, uint64_t c) {
   return (float)(w[c & 3] >> 8) * (1.0f / 16777216.0f);   /* exact: 24-bit / 2^24 */
 }
 
+static int g_qnorm = 0;   /* 0: max-norm scale (R-16); 1: l2-norm scale (R-31) */
+
+int or_set_qsgd_norm(int norm) {
+  if (norm != 0 && norm != 1) return -1;
+  g_qnorm = norm;
+  return 0;
+}
+
+/* l2 scale of one bucket (R-31): squares fl(v*v), summed by the balanced
+ * pairwise tree over the bucket's B slots in index order (slots past a
+ * ragged end hold +0), then the correctly rounded square root. */
+static float l2_scale(const float* v, uint64_t m, uint32_t B) {
+  float* t = (float*)malloc((size_t)B * sizeof(float));
+  uint32_t len, i;
+  float r;
+  if (!t) return 0.0f;
+  for (i = 0; i < B; i++) t[i] = i < m ? v[i] * v[i] : 0.0f;
+  for (len = B; len > 1; len /= 2)
+    for (i = 0; i < len / 2; i++) t[i] = t[2 * i] + t[2 * i + 1];
+  r = sqrtf(t[0]);
+  free(t);
+  return r;
+}
+
 int or_qsgd_quantize(const float* x, uint64_t n, int bits, uint32_t B,
                      uint64_t seed, uint64_t ctr_base, uint8_t* codes, float* scales) {
   uint64_t b0, e, nb;
@@ -618,6 +642,7 @@ int or_qsgd_quantize(const float* x, uint64_t n, int bits, uint32_t B,
   int per_byte;
   if (bits != 2 && bits != 4 && bits != 8) return -1;
   if (B == 0) return -1;
+  if (g_qnorm && (B & (B - 1))) return -1;   /* the l2 tree needs a power-of-two bucket */
   s = (1u << (bits - 1)) - 1u;            /* levels per sign: 1, 7, 127 */
   per_byte = 8 / bits;
   nb = (n * (uint64_t)bits + 7) / 8;
@@ -625,9 +650,13 @@ int or_qsgd_quantize(const float* x, uint64_t n, int bits, uint32_t B,
   for (b0 = 0; b0 < n; b0 += B) {
     uint64_t m = (n - b0) < B ? (n - b0) : B;
     float scale = 0.0f;
-    for (e = 0; e < m; e++) {              /* full-precision per-bucket scale */
-      float a = fabsf(x[b0 + e]);
-      if (a > scale) scale = a;
+    if (g_qnorm) {
+      scale = l2_scale(x + b0, m, B);
+    } else {
+      for (e = 0; e < m; e++) {              /* full-precision per-bucket scale */
+        float a = fabsf(x[b0 + e]);
+        if (a > scale) scale = a;
+      }
     }
     scales[b0 / B] = scale;
     for (e = 0; e < m; e++) {

@@ -196,6 +196,12 @@ float or_qsgd_uniform(uint64_t seed, uint64_t c);
  * (0 if scale == 0), code = (v<0 && level>0) << (bits-1) | level, packed
  * little-endian: element e at byte e*bits/8, bit (e % (8/bits))*bits.
  * codes: ceil(n*bits/8) bytes, scales: ceil(n/B) floats.  bits in {2,4,8}. */
+/* QSGD scale norm for or_qsgd_quantize and the DSAR simulator (§6
+ * mentions max- and l2-normalised variants; reading R-31): 0 max |v| (R-16,
+ * default), 1 l2 = sqrtf of the balanced pairwise tree of fl(v*v) over the
+ * bucket's B slots in index order (B a power of two).  Returns 0 or -1. */
+int or_set_qsgd_norm(int norm);
+
 int or_qsgd_quantize(const float* x, uint64_t n, int bits, uint32_t B,
                      uint64_t seed, uint64_t ctr_base, uint8_t* codes, float* scales);
 

@@ -105,3 +105,50 @@ def test_counter_base_shifts_stream(orc):
     c1, _ = orc.qsgd_quantize(x[1024:], 4, seed=7, ctr_base=1024)
     c2, _ = orc.qsgd_quantize(x, 4, seed=7, ctr_base=0)
     np.testing.assert_array_equal(c1, c2[512:])
+
+
+# ---- l2-norm scale (reading R-31) ------------------------------------------------------
+
+@pytest.mark.parametrize("B", [8, 64, 1024])
+def test_l2_scale_is_the_bucket_norm(orc, B):
+    """The l2 scale is the bucket's Euclidean norm (numpy, fp64) to fp32
+    accuracy, every decoded magnitude is <= it, and a bucket holding a single
+    non-zero value has scale = |value| exactly (the tree adds only zeros)."""
+    x = synth.gaussian_vector(3001, seed=B)
+    with orc.qsgd_norm_scope(1):
+        c, s = orc.qsgd_quantize(x, 4, bucket=B, seed=3)
+        d = orc.qsgd_dequantize(c, s, len(x), 4, B)
+        for b in range(len(s)):
+            sl = slice(b * B, min((b + 1) * B, len(x)))
+            ref = np.sqrt(np.sum(x[sl].astype(np.float64) ** 2))
+            assert abs(float(s[b]) - ref) <= 2e-6 * ref
+            assert np.all(np.abs(d[sl]) <= s[b])
+        one = np.zeros(B, np.float32)
+        one[B // 3] = np.float32(-3.75)
+        _, s1 = orc.qsgd_quantize(one, 8, bucket=B, seed=1)
+        assert s1[0] == np.float32(3.75)
+
+
+def test_l2_unbiased(orc):
+    """E[dequantize(quantize(v))] = v with the l2 scale too (within 3 SE)."""
+    x = synth.gaussian_vector(64, seed=19)
+    T = 2000
+    acc = np.zeros(64)
+    acc2 = np.zeros(64)
+    with orc.qsgd_norm_scope(1):
+        for t in range(T):
+            c, s = orc.qsgd_quantize(x, 4, bucket=64, seed=t)
+            d = orc.qsgd_dequantize(c, s, 64, 4, 64).astype(np.float64)
+            acc += d
+            acc2 += d * d
+    mean = acc / T
+    var = acc2 / T - mean ** 2
+    se = np.sqrt(np.maximum(var, 1e-30) / T)
+    z = np.abs(mean - x) / se
+    assert np.mean(z < 3) > 0.97 and np.all(z < 5)
+
+
+def test_l2_needs_power_of_two_bucket(orc):
+    with orc.qsgd_norm_scope(1):
+        with pytest.raises(ValueError):
+            orc.qsgd_quantize(np.ones(10, np.float32), 4, bucket=100)
