@@ -81,6 +81,7 @@ typedef struct {
   uint64_t k_sum_hint;    /* 0 = unknown; else the exact sum of all ranks' nnz: lets
                              the host pick SSAR/DSAR without launching both paths   */
   int validate;           /* 1: check sorted/unique/< N and finiteness on device    */
+  int quant_norm;         /* QSGD bucket scale: 0 max |v| (R-16), 1 l2 norm (R-31)   */
 } sparcml_opts;
 
 /* Result header, 64 bytes at out[0] (device).  The payload follows it:
@@ -305,6 +306,13 @@ sparcml_status sparcml_quantize(const float* x, uint64_t n, int bits, uint32_t b
                                 void* stream);
 
 /* v = +-fl(fl(level/s) * scale). */
+/* sparcml_quantize with the bucket scale chosen by `norm`: 0 max |v| (R-16),
+ * 1 the l2 norm by a balanced pairwise tree in index order (R-31; bucket a
+ * power of two in [8, 1024]). */
+sparcml_status sparcml_quantize_norm(const float* x, uint64_t n, int bits, uint32_t bucket, int norm,
+                                     uint64_t seed, uint64_t ctr_base, uint8_t* codes, float* scales,
+                                     void* stream);
+
 sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uint64_t n, int bits,
                                   uint32_t bucket, float* out, void* stream);
 

@@ -206,6 +206,7 @@ sparcml_status check_opts(sparcml_comm* c, const sparcml_opts& o) {
     return fail(c, SPARCML_ERR_INVALID_ARG, "quant_bits must be 0, 2, 4 or 8");
   if (o.quant_bits && (o.quant_bucket < 8 || o.quant_bucket > 1024 || (o.quant_bucket & (o.quant_bucket - 1))))
     return fail(c, SPARCML_ERR_INVALID_ARG, "quant_bucket must be a power of two in [8, 1024]");
+  if (o.quant_norm != 0 && o.quant_norm != 1) return fail(c, SPARCML_ERR_INVALID_ARG, "quant_norm must be 0 or 1");
   if (o.algo < SPARCML_ALGO_AUTO || o.algo > SPARCML_DSAR_SPLIT_ALLGATHER)
     return fail(c, SPARCML_ERR_INVALID_ARG, "unknown algorithm");
   return SPARCML_OK;
@@ -394,6 +395,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.host_dsar = cc.host_dsar;
     w.wait = 1;
     w.op = cc.op;
+    w.qnorm = cc.o.quant_norm;
     w.ctl = ctrl_of(base);
     w.st_idx = reinterpret_cast<uint32_t*>(base + L.stage_off);
     w.st_val = reinterpret_cast<float*>(base + L.stage_off + 4 * (size_t)P * L.cap_s);
@@ -482,6 +484,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
     w.host_dsar = 1;
     w.wait = 0;
     w.op = cc.op;
+    w.qnorm = cc.o.quant_norm;
     w.peer[0] = my;
     w.ctl = my;
     CK(c, launch_owner(w, cc.s));
@@ -996,15 +999,21 @@ sparcml_status sparcml_quantized_size(uint64_t n, int bits, uint32_t bucket, siz
   return SPARCML_OK;
 }
 
-sparcml_status sparcml_quantize(const float* x, uint64_t n, int bits, uint32_t bucket, uint64_t seed,
-                                uint64_t ctr_base, uint8_t* codes, float* scales, void* stream) {
+sparcml_status sparcml_quantize_norm(const float* x, uint64_t n, int bits, uint32_t bucket, int norm, uint64_t seed,
+                                     uint64_t ctr_base, uint8_t* codes, float* scales, void* stream) {
   if ((bits != 2 && bits != 4 && bits != 8) || bucket < 8 || bucket > 1024 || (bucket & (bucket - 1)))
     return fail(nullptr, SPARCML_ERR_INVALID_ARG, "bits in {2,4,8}, bucket a power of two in [8,1024]");
+  if (norm != 0 && norm != 1) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "norm must be 0 (max) or 1 (l2)");
   if (n == 0) return SPARCML_OK;
   if (!x || !codes || !scales) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
   if ((reinterpret_cast<uintptr_t>(codes) & 3u) != 0) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "codes must be 4-byte aligned");
-  CK(nullptr, launch_quantize(x, n, bits, bucket, seed, ctr_base, codes, scales, static_cast<cudaStream_t>(stream)));
+  CK(nullptr, launch_quantize(x, n, bits, bucket, seed, ctr_base, codes, scales, static_cast<cudaStream_t>(stream), norm));
   return SPARCML_OK;
+}
+
+sparcml_status sparcml_quantize(const float* x, uint64_t n, int bits, uint32_t bucket, uint64_t seed,
+                                uint64_t ctr_base, uint8_t* codes, float* scales, void* stream) {
+  return sparcml_quantize_norm(x, n, bits, bucket, 0, seed, ctr_base, codes, scales, stream);
 }
 
 sparcml_status sparcml_dequantize(const uint8_t* codes, const float* scales, uint64_t n, int bits, uint32_t bucket,

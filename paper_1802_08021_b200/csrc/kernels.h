@@ -124,6 +124,7 @@ struct OwnerArgs {
   int host_dsar;                   // -1 device decides, else 0/1
   int wait;                        // 1: wait for the sources' flags (P > 1)
   int op;                          // reduction operator (R-30)
+  int qnorm;                       // QSGD scale norm (R-16 / R-31)
   Ctrl* peer[kMaxRanks];
   Ctrl* ctl;
   // SSAR merge path: spill area for dense block ranges (P * cap_s pairs, SoA)
@@ -252,7 +253,7 @@ cudaError_t launch_topk_bucketed(const float* x, const float* grad, float alpha,
                                  uint64_t k, uint64_t bucket, uint32_t* idx_out, float* val_out, void* ws,
                                  cudaStream_t s);
 cudaError_t launch_quantize(const float* x, uint64_t n, int bits, uint32_t bucket, uint64_t seed,
-                            uint64_t ctr_base, uint8_t* codes, float* scales, cudaStream_t s);
+                            uint64_t ctr_base, uint8_t* codes, float* scales, cudaStream_t s, int norm = 0);
 cudaError_t launch_dequantize(const uint8_t* codes, const float* scales, uint64_t n, int bits,
                               uint32_t bucket, float* out, cudaStream_t s);
 

@@ -963,7 +963,8 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
     if (a.bits) {
       const int rem = wn - p0;
       const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
-      qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax);
+      qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax,
+                        a.qnorm);
     } else if (p0 + 4 <= wn) {
       reinterpret_cast<float4*>(a.dense + e)[0] = make_float4(r[0], r[1], r[2], r[3]);
     } else {

@@ -12,7 +12,7 @@ namespace sparcml {
 __global__ void __launch_bounds__(kThreads) quantize_kernel(const float* __restrict__ x, uint64_t n, int bits,
                                                             uint32_t bucket, uint32_t k0, uint32_t k1,
                                                             uint64_t ctr_base, uint8_t* __restrict__ codes,
-                                                            float* __restrict__ scales) {
+                                                            float* __restrict__ scales, int norm) {
   __shared__ uint32_t bmax[kWin / 8];
   const uint64_t nwin = (n + kWin - 1) / kWin;
   for (uint64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(const float* __restr
     } else {
       for (int i = 0; i < valid; ++i) r[i] = x[e + i];
     }
-    qsgd_block_encode(r, valid, e, ctr_base + e, bits, bucket, k0, k1, codes, scales, bmax);
+    qsgd_block_encode(r, valid, e, ctr_base + e, bits, bucket, k0, k1, codes, scales, bmax, norm);
     __syncthreads();
   }
 }
@@ -61,12 +61,12 @@ __global__ void __launch_bounds__(kThreads) dequantize_kernel(const uint8_t* __r
 }
 
 cudaError_t launch_quantize(const float* x, uint64_t n, int bits, uint32_t bucket, uint64_t seed, uint64_t ctr_base,
-                            uint8_t* codes, float* scales, cudaStream_t s) {
+                            uint8_t* codes, float* scales, cudaStream_t s, int norm) {
   const uint64_t nwin = (n + kWin - 1) / kWin;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)device_sm_count() * 8));
   SPARCML_PROF("quantize", s);
   quantize_kernel<<<grid, kThreads, 0, s>>>(x, n, bits, bucket, (uint32_t)seed, (uint32_t)(seed >> 32), ctr_base,
-                                            codes, scales);
+                                            codes, scales, norm);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -255,21 +255,46 @@ __device__ __forceinline__ void qsgd_encode4(const float v[4], float scale, uint
 // (P:845-849), one thread per bucket stores it.  bmax: kWin/8 smem words.
 __device__ __forceinline__ void qsgd_block_encode(const float r[4], int valid, uint64_t e, uint64_t c0, int bits,
                                                   uint32_t B, uint32_t k0, uint32_t k1, uint8_t* __restrict__ codes,
-                                                  float* __restrict__ scales, uint32_t* bmax) {
+                                                  float* __restrict__ scales, uint32_t* bmax, int norm = 0) {
   const int tid = threadIdx.x;
   const uint32_t lgB = 31u - __clz(B);    // B is a power of two (8..1024)
   const uint32_t lgt = lgB - 2;           // threads per bucket = B/4 (>= 2)
-  float m = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) m = fmaxf(m, i < valid ? fabsf(r[i]) : 0.0f);
   const uint32_t seg = lgt < 5 ? (1u << lgt) : 32u;
-  for (uint32_t o = 1; o < seg; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const int nb_win = (kThreads * 4) >> lgB;
-  for (int b = tid; b < nb_win; b += kThreads) bmax[b] = 0u;
-  __syncthreads();
-  if ((tid & (seg - 1)) == 0) atomicMax(&bmax[tid >> lgt], __float_as_uint(m));
-  __syncthreads();
-  const float scale = __uint_as_float(bmax[tid >> lgt]);
+  float scale;
+  if (norm == 0) {   // max |v| (R-16)
+    float m = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m = fmaxf(m, i < valid ? fabsf(r[i]) : 0.0f);
+    for (uint32_t o = 1; o < seg; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int nb_win = (kThreads * 4) >> lgB;
+    for (int b = tid; b < nb_win; b += kThreads) bmax[b] = 0u;
+    __syncthreads();
+    if ((tid & (seg - 1)) == 0) atomicMax(&bmax[tid >> lgt], __float_as_uint(m));
+    __syncthreads();
+    scale = __uint_as_float(bmax[tid >> lgt]);
+  } else {           // l2 (R-31): balanced pairwise tree of fl(v*v) in index order, then sqrt
+    float q[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = i < valid ? __fmul_rn(r[i], r[i]) : 0.0f;
+    float t = __fadd_rn(__fadd_rn(q[0], q[1]), __fadd_rn(q[2], q[3]));
+    for (uint32_t o = 1; o < seg; o <<= 1) t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
+    float* wsum = reinterpret_cast<float*>(bmax);   // one partial per warp
+    __syncthreads();
+    if ((tid & 31) == 0) wsum[tid >> 5] = t;
+    __syncthreads();
+    if (lgt > 5) {   // buckets spanning 2, 4 or 8 warps: the tree continues over them
+      const int nw = 1 << (lgt - 5), w0 = (tid >> 5) & ~(nw - 1);
+      float a[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = i < nw ? wsum[w0 + i] : 0.0f;
+      for (int len = nw; len > 1; len >>= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i < len / 2) a[i] = __fadd_rn(a[2 * i], a[2 * i + 1]);
+      t = a[0];
+    }
+    scale = __fsqrt_rn(t);
+  }
   if (valid > 0) {
     qsgd_encode4(r, scale, e, c0, valid, bits, k0, k1, codes);
     if ((e & (B - 1)) == 0) scales[e >> lgB] = scale;

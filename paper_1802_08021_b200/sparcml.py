@@ -48,14 +48,14 @@ EXPORTED = [
     "sparcml_ef_topk", "sparcml_topk_status", "sparcml_quantized_size", "sparcml_quantize", "sparcml_dequantize",
     "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
     "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges", "sparcml_sparse_allgather",
-    "sparcml_sparse_allgather_local", "sparcml_apply_update",
+    "sparcml_sparse_allgather_local", "sparcml_apply_update", "sparcml_quantize_norm",
 ]
 
 
 class Opts(C.Structure):
     _fields_ = [("algo", C.c_int), ("switch_scale", C.c_float), ("index_bytes", C.c_int),
                 ("quant_bits", C.c_int), ("quant_bucket", C.c_uint32), ("seed", C.c_uint64),
-                ("k_sum_hint", C.c_uint64), ("validate", C.c_int)]
+                ("k_sum_hint", C.c_uint64), ("validate", C.c_int), ("quant_norm", C.c_int)]
 
 
 class Header(C.Structure):
@@ -100,6 +100,7 @@ _sig = {
     "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
     "sparcml_fuse_streams": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _p]),
     "sparcml_apply_update": (_i32, [_p, _p, _p]),
+    "sparcml_quantize_norm": (_i32, [_p, _u64, _i32, C.c_uint32, _i32, _u64, _u64, _p, _p, _p]),
     "sparcml_sparse_allgather": (_i32, [_p, _p, _p, _u64, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_sparse_allgather_local": (_i32, [_p, _p, _p, _p, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_layer_ranges": (_i32, [_p, _i32, _p, _p, _p]),
@@ -179,11 +180,11 @@ def result_val_offset(N: int) -> int:
 
 
 def make_opts(algo: int = ALGO_AUTO, switch_scale: float = 1.0, quant_bits: int = 0, quant_bucket: int = 1024,
-              seed: int = 0, k_sum_hint: int = 0, validate: bool = False) -> Opts:
+              seed: int = 0, k_sum_hint: int = 0, validate: bool = False, quant_norm: int = 0) -> Opts:
     o = Opts()
     _lib.sparcml_opts_default(C.byref(o))
     o.algo, o.switch_scale, o.quant_bits, o.quant_bucket = algo, switch_scale, quant_bits, quant_bucket
-    o.seed, o.k_sum_hint, o.validate = seed, k_sum_hint, int(validate)
+    o.seed, o.k_sum_hint, o.validate, o.quant_norm = seed, k_sum_hint, int(validate), quant_norm
     return o
 
 
@@ -563,14 +564,15 @@ def quantized_size(n: int, bits: int, bucket: int = 1024):
     return int(cb.value), int(ns.value)
 
 
-def quantize(x: torch.Tensor, bits: int, bucket: int = 1024, seed: int = 0, ctr_base: int = 0, stream=None):
+def quantize(x: torch.Tensor, bits: int, bucket: int = 1024, seed: int = 0, ctr_base: int = 0, stream=None,
+             norm: int = 0):
     _need(x, torch.float32, "x")
     n = x.numel()
     cb, ns = quantized_size(n, bits, bucket)
     codes = torch.empty(max(cb, 8), dtype=torch.uint8, device=x.device)
     scales = torch.empty(max(ns, 1), dtype=torch.float32, device=x.device)
-    _check(_lib.sparcml_quantize(x.data_ptr(), n, bits, bucket, seed, ctr_base, codes.data_ptr(),
-                                 scales.data_ptr(), _stream(stream)))
+    _check(_lib.sparcml_quantize_norm(x.data_ptr(), n, bits, bucket, norm, seed, ctr_base, codes.data_ptr(),
+                                      scales.data_ptr(), _stream(stream)))
     return codes[:cb], scales[:ns]
 
 

@@ -227,3 +227,19 @@ def test_max_rejects_quantization():
     v = torch.ones(10, device="cuda")
     with pytest.raises(S.SparcmlError):
         w.allreduce([(i, v), (i, v)], 1000, opts=S.make_opts(algo=S.DSAR_SPLIT_ALLGATHER, quant_bits=4), op=S.OP_MAX)
+
+
+@pytest.mark.parametrize("P,bits,B", [(1, 4, 1024), (2, 4, 1024), (4, 8, 256), (3, 2, 64)])
+def test_dsar_qsgd_l2(orc, P, bits, B):
+    """DSAR with the l2-norm QSGD scale (R-31), bit-exact against the oracle."""
+    N = 1 << 18
+    streams = synth.uniform_streams(P, N, N // 5, seed=P + bits + 40, kind="normal")
+    w = S.LocalWorld(P, N, N // 5)
+    opts = S.make_opts(algo=S.DSAR_SPLIT_ALLGATHER, quant_bits=bits, quant_bucket=B, seed=9, quant_norm=1)
+    outs = w.allreduce(to_cuda(streams), N, opts=opts)
+    with orc.qsgd_norm_scope(1):
+        res, _, _ = orc.split_allgather(N, streams, algo=orc.ALGO_DSAR_SPLIT, quant_bits=bits, bucket=B, seed=9)
+    for r in range(P):
+        g = S.read_result(outs[r])
+        assert g.dense and g.header.status == 0
+        np.testing.assert_array_equal(g.val.cpu().numpy(), res[r][2])

@@ -219,3 +219,17 @@ def test_topk_bucketed_nonfinite_reported():
     x[4321] = 0.5
     S.topk_sparsify(cu(x, torch.float32), 4, ws=ws, bucket=512)
     assert ws.status()[0] == 0
+
+
+@pytest.mark.parametrize("n", [7, 1000, 4099, 1 << 20])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("B", [8, 128, 256, 1024])
+def test_qsgd_l2_parity(orc, n, bits, B):
+    """l2-norm scale (reading R-31): the fixed balanced tree makes codes and
+    scales bit-exact against the oracle."""
+    x = synth.gaussian_vector(n, seed=3 * n + bits + B)
+    c, s = S.quantize(cu(x, torch.float32), bits, bucket=B, seed=77, ctr_base=5, norm=1)
+    with orc.qsgd_norm_scope(1):
+        ec, es = orc.qsgd_quantize(x, bits, bucket=B, seed=77, ctr_base=5)
+    np.testing.assert_array_equal(s.cpu().numpy(), es)
+    np.testing.assert_array_equal(c.cpu().numpy(), ec)
