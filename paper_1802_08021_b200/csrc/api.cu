@@ -450,6 +450,13 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   p.ctl = my;
   p.validate = cc.o.validate;
   const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER || (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
+  if (!dsar && n <= cc.delta) {   // the result is the input: one copy kernel is the whole call
+    p.out = out;
+    p.val_offset = cc.val_offset;
+    p.algo_used = cc.o.algo == SPARCML_ALGO_AUTO ? SPARCML_SSAR_SPLIT_ALLGATHER : cc.o.algo;
+    CK(c, launch_p1_sparse(p, cc.s));
+    return SPARCML_OK;
+  }
   p.win = dsar ? win_table(L, base, 0) : nullptr;
   CK(c, launch_p1_prep(p, cc.s));
   ConcatArgs a = {};

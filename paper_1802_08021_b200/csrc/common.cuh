@@ -76,6 +76,14 @@ __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   return r;
 }
 
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 // streaming access with an L2 evict-first policy: data touched once (the N-vector
 // pass) should not push reusable lines (candidates, control) out of L2
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {

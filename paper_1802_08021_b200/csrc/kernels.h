@@ -172,6 +172,10 @@ struct P1PrepArgs {                 // P == 1: validate, fill the control block,
   Ctrl* ctl;
   int validate;
   uint32_t* win;                    // nullable: build the window-offset table (ntab + 1 entries)
+  // p1_sparse_kernel only: the result is the input itself (sparse, nnz <= delta)
+  char* out;
+  uint64_t val_offset;
+  uint32_t algo_used;
 };
 
 // ------------------------------------------------------ sparse allgather --
@@ -237,6 +241,7 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);   // host_dsar sel
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);
+cudaError_t launch_p1_sparse(const P1PrepArgs& a, cudaStream_t s);
 cudaError_t launch_fuse_streams(const FuseArgs& a, cudaStream_t s);
 cudaError_t launch_apply_update(float* v, const char* out, cudaStream_t s);
 cudaError_t launch_ag_publish(const AgPublishArgs& a, cudaStream_t s);

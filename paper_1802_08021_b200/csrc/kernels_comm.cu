@@ -1379,6 +1379,57 @@ __global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
   }
 }
 
+// P == 1, sparse result (nnz <= delta): one kernel copies the input into out
+// (16-byte vectors where aligned) and writes the header -- the whole call.
+__global__ void __launch_bounds__(kThreads) p1_sparse_kernel(P1PrepArgs a) {
+  uint32_t* oi = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
+  float* ov = reinterpret_cast<float*>(a.out + a.val_offset);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t gt = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.idx) | reinterpret_cast<uintptr_t>(a.val)) & 15u) == 0;
+  if (vec) {
+    const uint64_t n4 = a.n / 4;
+    for (uint64_t u = gt; u < n4; u += stride) {
+      reinterpret_cast<uint4*>(oi)[u] = ld_stream_u4(reinterpret_cast<const uint4*>(a.idx) + u);
+      reinterpret_cast<float4*>(ov)[u] = ld_stream_f4(reinterpret_cast<const float4*>(a.val) + u);
+    }
+    for (uint64_t e = 4 * n4 + gt; e < a.n; e += stride) {
+      oi[e] = a.idx[e];
+      ov[e] = a.val[e];
+    }
+  } else {
+    for (uint64_t e = gt; e < a.n; e += stride) {
+      oi[e] = a.idx[e];
+      ov[e] = a.val[e];
+    }
+  }
+  if (a.validate)
+    for (uint64_t e = gt; e < a.n; e += stride) check_input(a.idx, e, a.n, a.N, a.idx[e], a.val[e], &a.ctl->status);
+  if (last_block<false>(&a.ctl->done_ctr[2]) && threadIdx.x == 0) {
+    Ctrl* c = a.ctl;
+    c->k_in[0] = a.n;
+    c->slice_cnt[0] = a.n;
+    c->slice_out[0] = a.n;
+    c->owner_K = a.n;
+    c->k_sum = a.n;
+    c->dsar = 0;
+    write_header(reinterpret_cast<sparcml_header*>(a.out), SPARCML_REPR_SPARSE, a.n, a.N, a.n, 0, 0, a.algo_used,
+                 c->status, a.val_offset);
+    c->status = 0;
+    __threadfence();
+    c->seq = c->seq + 1;   // the call is complete
+  }
+}
+
+cudaError_t launch_p1_sparse(const P1PrepArgs& a, cudaStream_t s) {
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((a.n / 4 + kThreads - 1) / kThreads,
+                                                                   (uint64_t)device_sm_count() * 4));
+  SPARCML_PROF("p1_sparse", s);
+  p1_sparse_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
   const uint64_t blocks = (a.validate || a.win)
                               ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 4096))

@@ -159,7 +159,7 @@ def profile_read(name: str):
 
 
 PROFILED_KERNELS = ["topk", "topk_all", "topk_bucketed", "split_push", "owner", "owner_dsar", "ag_publish", "ag_gather",
-                    "barrier", "merge", "concat", "rd_push", "rd_stage", "p1_prep", "quantize",
+                    "barrier", "merge", "concat", "rd_push", "rd_stage", "p1_prep", "p1_sparse", "quantize",
                     "dequantize"]
 
 
