@@ -842,12 +842,13 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
       a.r_val[excl + i] = __ldcg(&a.st_val[ibase + i]);
     }
   }
-  if (b == G - 1 && tid == 0) ctl->owner_K = excl + cnt;
   dbg_mark(ctl, 5);
-  // every block's writes are local: a gpu-scope arrival suffices; the release
-  // to the peers is system scope (and cumulative over what the last block saw)
-  if (last_block<false>(&ctl->done_ctr[3]) && tid < P) {   // K travels with the flag: readers need no remote load
-    a.peer[tid]->owner_k[a.rank] = *(volatile uint64_t*)&ctl->owner_K;
+  // every block's writes are local: the grid barrier orders them (gpu scope)
+  // before the last block's system-scope release to the P readers; K travels
+  // with the flag, so readers need no remote load
+  grid.sync();
+  if (b == G - 1 && tid < P) {
+    a.peer[tid]->owner_k[a.rank] = excl + cnt;
     st_release_sys(&a.peer[tid]->owner_done[a.rank], seq + 1);
   }
   dbg_mark(ctl, 6);
