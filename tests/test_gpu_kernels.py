@@ -233,3 +233,22 @@ def test_qsgd_l2_parity(orc, n, bits, B):
         ec, es = orc.qsgd_quantize(x, bits, bucket=B, seed=77, ctr_base=5)
     np.testing.assert_array_equal(s.cpu().numpy(), es)
     np.testing.assert_array_equal(c.cpu().numpy(), ec)
+
+
+@pytest.mark.parametrize("N,k,bucket", [(1 << 24, 167_772, 0), (25_557_032, 25_557, 0), (25_557_032, 4, 512)])
+def test_topk_bench_sizes(orc, N, k, bucket):
+    """The bench's top-k launches at full size (cfg2, cfg3, bucket512): EF over
+    two steps, bit-exact indices, values and residual against the oracle."""
+    g = synth.gaussian_vector(N, seed=0)
+    eps = np.zeros(N, np.float32)
+    et, gt = cu(eps, torch.float32), cu(g, torch.float32)
+    ws = S.TopkWorkspace(N, k if bucket == 0 else 1)
+    for step in range(2):
+        io, vo = S.ef_topk(et, gt, 0.01, k, ws=ws, bucket=bucket)
+        if bucket:
+            ei, ev, eps = orc.ef_topk_bucketed(eps, g, 0.01, k, bucket)
+        else:
+            ei, ev, eps = orc.ef_topk(eps, g, 0.01, k)
+        np.testing.assert_array_equal(host_idx(io), ei)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+        np.testing.assert_array_equal(et.cpu().numpy(), eps)
