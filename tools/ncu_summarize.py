@@ -40,8 +40,9 @@ def main():
     ap.add_argument("--key", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--match", default="", help="only launches whose kernel name contains this")
     a = ap.parse_args()
-    recs = raw(a.full)
+    recs = [(d, u) for d, u in raw(a.full) if a.match in d.get("Kernel Name", "")]
     dram, t = [], []
     lines = [f"# ncu --set full: {a.key} ({os.path.basename(a.full)}, {len(recs)} launch(es) captured)", ""]
     for d, u in recs:
@@ -64,7 +65,8 @@ def main():
     summ_path = os.path.join(PROF, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     summ.setdefault("kernels", {})
-    summ["kernels"] = {k: v for k, v in summ["kernels"].items() if k in (a.key,) or not k.startswith("topk_")}
+    summ["kernels"] = {k: v for k, v in summ["kernels"].items()
+                       if k in (a.key,) or not (k.startswith("topk_") and k not in ("topk_bucketed",))}
     summ["kernels"][a.key] = {
         "dram_bytes_per_launch": sum(r + w for r, w in dram) / n,
         "dram_read_MB": sum(r for r, _ in dram) / n / 1e6,
