@@ -245,9 +245,12 @@ def main():
     grad = torch.from_numpy(synth.gaussian_vector(N, seed=0, rank=rank)).to(dev)
     eps = torch.zeros(N, dtype=torch.float32, device=dev)
     ws = S.TopkWorkspace(N, k, dev)
-    idx = torch.empty(k, dtype=torch.int32, device=dev)
-    val = torch.empty(k, dtype=torch.float32, device=dev)
     out = S.new_out(N, dev)
+    if algo == S.SSAR_RECURSIVE_DOUBLE and P > 1:
+        idx = torch.empty(k, dtype=torch.int32, device=dev)
+        val = torch.empty(k, dtype=torch.float32, device=dev)
+    else:   # the top-k writes straight into the result's payload slots (in place, include/sparcml.h)
+        idx, val = S.payload_views(out, N, k)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     flush_i64 = flush.view(torch.int64)
 
@@ -277,29 +280,28 @@ def main():
     res = S.read_result(out)
     assert res.header.status == 0 and res.header.k_sum == P * k
 
-    # The step runs as two CUDA graphs (launch-bound inner sequence, captured once):
-    # g_topk = the fused EF top-k kernel, g_ar = the whole sparse allreduce.
+    # The step runs as ONE CUDA graph (launch-bound sequence, captured once):
+    # the fused EF top-k kernel, an external event-record node (splits the
+    # step into top-k and allreduce time on the device), the sparse allreduce.
+    ev_m = torch.cuda.Event(enable_timing=True, external=True)
     l0 = S.kernel_launches()
-    g_topk, g_ar = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_topk):
+    g_step = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_step):
         topk()
-    l1 = S.kernel_launches()
-    with torch.cuda.graph(g_ar):
+        ev_m.record()
         allreduce()
     launches_per_step = S.kernel_launches() - l0
-    topk_launches = l1 - l0
     for _ in range(max(3, args.warmup)):
         flush_l2()
         barrier()
         comm.barrier()
-        g_topk.replay()
-        g_ar.replay()
+        g_step.replay()
     barrier()
     res = S.read_result(out)
     assert res.header.status == 0 and res.header.k_sum == P * k
 
     # ---------------- timed region (device events per step, L2 flushed between) ----
-    ev = []
+    t_steps, t_tops = [], []
     barrier()
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
@@ -308,19 +310,18 @@ def main():
             comm.barrier()     # device-side alignment of the ranks before the events
             torch.cuda._sleep(HOLD_CYCLES)   # keep the GPU busy while the host enqueues the step
             a = torch.cuda.Event(enable_timing=True)
-            m = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            g_topk.replay()
-            m.record(stream)
-            g_ar.replay()
+            g_step.replay()
             b.record(stream)
-            ev.append((a, m, b))
+            b.synchronize()                 # ev_m is re-recorded by the next replay: read it now
+            t_steps.append(a.elapsed_time(b) / 1e3)
+            t_tops.append(a.elapsed_time(ev_m) / 1e3)
         barrier()
     launches = launches_per_step * args.steps
-    t_step = sum(a.elapsed_time(b) for a, _, b in ev) / 1e3 / args.steps
-    t_ar = sum(m.elapsed_time(b) for _, m, b in ev) / 1e3 / args.steps
-    t_topk_kernel = sum(a.elapsed_time(m) for a, m, _ in ev) / 1e3 / args.steps   # the fused top-k launch
+    t_step = sum(t_steps) / args.steps
+    t_topk_kernel = sum(t_tops) / args.steps    # the fused top-k launch (graph start -> event node)
+    t_ar = t_step - t_topk_kernel
     # per-kernel breakdown (eager, every kernel bracketed by library events)
     S.profile_reset()
     S.profile_only(None)
@@ -458,7 +459,7 @@ def main():
                        "quant_bits": cfg["bits"], "l2": "flushed before every step (512 MiB write + 512 MiB read, no dirty lines left)",
                        "exchange": "CUDA IPC over NVLink (fused push/pull kernels)" if P > 1 else "none (P=1)"},
             "latency_us": t_step * 1e6, "allreduce_us": t_ar * 1e6, "topk_us": (t_step - t_ar) * 1e6,
-            "timing": "CUDA graphs (g_topk, g_ar) replayed per step; eager API step measured too",
+            "timing": "one CUDA graph per step (top-k, external event node, allreduce); eager API step measured too",
             "eager_ms_per_step": t_eager * 1e3,
             "result_nnz": K, "bytes_recv_per_rank": bytes_recv,
             "exchange_gbs_per_rank": bytes_recv / t_ar / 1e9 if P > 1 else None,

@@ -159,8 +159,14 @@ const char* sparcml_last_error(const sparcml_comm* comm);  /* NULL comm: global 
  * holds x = sum_i x_i with index set exactly the union of the H_i (explicit
  * zeros kept), sparse or dense per the dense-switch rule
  * (P:501-527).  Collective: all ranks call with the same N, op and opts in
- * the same order.  `out` (out_bytes >= sparcml_result_bytes(N)) must not
- * alias the inputs; it is fully written (header + payload).  Never
+ * the same order.  `out` (out_bytes >= sparcml_result_bytes(N)) is fully
+ * written (header + payload).  In place: the input may BE the sparse payload
+ * slots of `out` (idx == out + 64, val == out + sparcml_result_val_offset(N),
+ * e.g. written there by the top-k); a one-rank call then only writes the
+ * header.  In-place is supported by split-allgather (every rank's input is
+ * consumed before its result is written) but not by recursive doubling, nor
+ * for one rank with nnz > delta under forced SSAR (SPARCML_ERR_INVALID_ARG).
+ * Any other overlap of inputs and `out` is undefined.  Never
  * synchronises the host; read the header after the stream passes.
  * Errors: N == 0, N > max_N, nnz > max_nnz, null pointers with nnz > 0,
  * unsupported opts -> SPARCML_ERR_INVALID_ARG; loopback comm ->

@@ -450,13 +450,18 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   p.ctl = my;
   p.validate = cc.o.validate;
   const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER || (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
-  if (!dsar && n <= cc.delta) {   // the result is the input: one copy kernel is the whole call
+  const bool inplace = reinterpret_cast<const char*>(idx) == out + SPARCML_HEADER_BYTES &&
+                       reinterpret_cast<const char*>(val) == out + cc.val_offset;
+  if (!dsar && n <= cc.delta) {   // the result is the input: one copy kernel (or just the header) is the call
     p.out = out;
     p.val_offset = cc.val_offset;
     p.algo_used = cc.o.algo == SPARCML_ALGO_AUTO ? SPARCML_SSAR_SPLIT_ALLGATHER : cc.o.algo;
+    p.copy = inplace ? 0 : 1;
     CK(c, launch_p1_sparse(p, cc.s));
     return SPARCML_OK;
   }
+  if (inplace && !dsar)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "in-place input with nnz > delta under forced SSAR (the dense result overwrites it)");
   p.win = dsar ? win_table(L, base, 0) : nullptr;
   CK(c, launch_p1_prep(p, cc.s));
   ConcatArgs a = {};
@@ -555,6 +560,10 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   if (algo == SPARCML_ALGO_AUTO && c->P > 1)
     algo = (is_pow2(c->P) && 4 * N <= (256u << 10)) ? SPARCML_SSAR_RECURSIVE_DOUBLE : SPARCML_ALGO_AUTO;
   cc.algo = algo;
+  if (algo == SPARCML_SSAR_RECURSIVE_DOUBLE && c->P > 1)
+    for (int i = 0; i < nl; ++i)
+      if (nnz[i] && reinterpret_cast<const char*>(idx[i]) == static_cast<const char*>(out[i]) + SPARCML_HEADER_BYTES)
+        return fail(c, SPARCML_ERR_INVALID_ARG, "in-place input is not supported by recursive doubling");
   // SSAR/DSAR for split-allgather: forced, or AUTO by sum k_i > delta (R-5)
   if (algo == SPARCML_SSAR_SPLIT_ALLGATHER) cc.host_dsar = 0;
   else if (algo == SPARCML_DSAR_SPLIT_ALLGATHER) cc.host_dsar = 1;

@@ -176,6 +176,7 @@ struct P1PrepArgs {                 // P == 1: validate, fill the control block,
   char* out;
   uint64_t val_offset;
   uint32_t algo_used;
+  int copy;                         // 0: the input already is out's payload (in place)
 };
 
 // ------------------------------------------------------ sparse allgather --

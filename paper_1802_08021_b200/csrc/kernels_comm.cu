@@ -1388,7 +1388,9 @@ __global__ void __launch_bounds__(kThreads) p1_sparse_kernel(P1PrepArgs a) {
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint64_t gt = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   const bool vec = ((reinterpret_cast<uintptr_t>(a.idx) | reinterpret_cast<uintptr_t>(a.val)) & 15u) == 0;
-  if (vec) {
+  if (!a.copy) {
+    // in place: the payload is already there
+  } else if (vec) {
     const uint64_t n4 = a.n / 4;
     for (uint64_t u = gt; u < n4; u += stride) {
       reinterpret_cast<uint4*>(oi)[u] = ld_stream_u4(reinterpret_cast<const uint4*>(a.idx) + u);
@@ -1423,7 +1425,8 @@ __global__ void __launch_bounds__(kThreads) p1_sparse_kernel(P1PrepArgs a) {
 }
 
 cudaError_t launch_p1_sparse(const P1PrepArgs& a, cudaStream_t s) {
-  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((a.n / 4 + kThreads - 1) / kThreads,
+  const uint64_t work = (a.copy || a.validate) ? a.n / 4 : 0;
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((work + kThreads - 1) / kThreads,
                                                                    (uint64_t)device_sm_count() * 4));
   SPARCML_PROF("p1_sparse", s);
   p1_sparse_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);

@@ -216,6 +216,15 @@ def new_out(N: int, device=None) -> torch.Tensor:
     return torch.empty(result_bytes(N), dtype=torch.uint8, device=device or "cuda")
 
 
+def payload_views(out: torch.Tensor, N: int, n: int):
+    """(idx int32[n], val float32[n]) views of out's sparse payload slots: a stream
+    written there (e.g. by the top-k) is an in-place allreduce input."""
+    vo = result_val_offset(N)
+    idx = out[HEADER_BYTES:HEADER_BYTES + 4 * n].view(torch.int32)
+    val = out[vo:vo + 4 * n].view(torch.float32)
+    return idx, val
+
+
 def read_result(out: torch.Tensor, stream=None) -> Result:
     """Synchronises `stream`, reads the header and returns views of the payload."""
     h = Header()

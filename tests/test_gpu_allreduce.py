@@ -243,3 +243,55 @@ def test_dsar_qsgd_l2(orc, P, bits, B):
         g = S.read_result(outs[r])
         assert g.dense and g.header.status == 0
         np.testing.assert_array_equal(g.val.cpu().numpy(), res[r][2])
+
+
+@pytest.mark.parametrize("P,algo", [(1, "ssar"), (1, "auto"), (1, "dsar"), (4, "ssar"), (3, "dsar"), (2, "auto")])
+def test_in_place_inputs(orc, P, algo):
+    """Inputs written into the result's own payload slots (include/sparcml.h,
+    in place): identical results to separate buffers; P = 1 then only writes
+    the header."""
+    N = 200_003
+    streams = synth.uniform_streams(P, N, 3000 if algo != "dsar" else 60_000, seed=P + 70, kind="normal")
+    w = S.LocalWorld(P, N, max(len(s[0]) for s in streams))
+    outs = [S.new_out(N) for _ in range(P)]
+    ins = []
+    for r, (i, v) in enumerate(streams):
+        vi, vv = S.payload_views(outs[r], N, len(i))
+        vi.copy_(torch.from_numpy(i.view(np.int32)))
+        vv.copy_(torch.from_numpy(v))
+        ins.append((vi, vv))
+    opts = S.make_opts(algo=ALGOS[algo])
+    if algo == "auto" and P == 2:
+        opts = S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER)
+    w.allreduce(ins, N, outs=outs, opts=opts)
+    ref, _, _ = oracle_run(orc, N, streams, ALGOS[algo] if algo != "auto" else S.ALGO_AUTO)
+    for r in range(P):
+        g = S.read_result(outs[r])
+        d, ei, ev = ref[r]
+        assert g.header.status == 0 and g.dense == bool(d)
+        if d:
+            np.testing.assert_array_equal(g.val.cpu().numpy(), ev)
+        else:
+            np.testing.assert_array_equal(g.idx.cpu().numpy().view(np.uint32), ei)
+            np.testing.assert_array_equal(g.val.cpu().numpy(), ev)
+
+
+def test_in_place_rejected_where_unsafe():
+    N = 10_000
+    w = S.LocalWorld(2, N, 100)
+    outs = [S.new_out(N) for _ in range(2)]
+    ins = []
+    for r in range(2):
+        vi, vv = S.payload_views(outs[r], N, 100)
+        vi.copy_(torch.arange(100, dtype=torch.int32) * 7 + r)
+        vv.fill_(1.0)
+        ins.append((vi, vv))
+    with pytest.raises(S.SparcmlError):
+        w.allreduce(ins, N, outs=outs, opts=S.make_opts(algo=S.SSAR_RECURSIVE_DOUBLE))
+    w1 = S.LocalWorld(1, 100, 100)
+    o = S.new_out(100)
+    vi, vv = S.payload_views(o, 100, 60)
+    vi.copy_(torch.arange(60, dtype=torch.int32))
+    vv.fill_(2.0)
+    with pytest.raises(S.SparcmlError):   # 60 > delta = 50 under forced SSAR
+        w1.allreduce([(vi, vv)], 100, outs=[o], opts=S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER))
