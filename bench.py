@@ -213,8 +213,8 @@ def main():
 
     import torch
     import torch.distributed as dist
-    if P > 1:
-        dist.init_process_group(backend="cpu:gloo,cuda:nccl")
+    if P > 1:   # the reference arm is the CPU oracle: it needs no GPU process group
+        dist.init_process_group(backend="gloo" if args.impl == "reference" else "cpu:gloo,cuda:nccl")
     if args.impl == "reference":
         run_reference(args, cfg, P, rank)
         if P > 1:
