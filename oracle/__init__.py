@@ -20,18 +20,21 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sparcml_oracle.c")
 _HDR = os.path.join(_HERE, "sparcml_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB64 = os.path.join(_HERE, "liboracle_f64.so")   # same source, or_val = double
 
 ALGO_AUTO, ALGO_SSAR_RD, ALGO_SSAR_SPLIT, ALGO_DSAR_SPLIT = 0, 1, 2, 3
 
 
-def build(force: bool = False) -> str:
-    """Compile oracle/liboracle.so (gcc, -O2, no FP contraction)."""
+def build(force: bool = False, f64: bool = False) -> str:
+    """Compile oracle/liboracle.so and liboracle_f64.so (gcc, -O2, no FP
+    contraction); returns the path of the one asked for."""
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-               "-fPIC", "-shared", "-Wall", "-o", _LIB, _SRC, "-lm"]
-        subprocess.run(cmd, check=True)
-    return _LIB
+    for path, extra in ((_LIB, []), (_LIB64, ["-DOR_VAL=double"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < newest:
+            cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+                   "-fPIC", "-shared", "-Wall", *extra, "-o", path, _SRC, "-lm"]
+            subprocess.run(cmd, check=True)
+    return _LIB64 if f64 else _LIB
 
 
 class _RankStats(C.Structure):
@@ -40,15 +43,19 @@ class _RankStats(C.Structure):
                 ("stage_nnz", C.c_uint64 * 8), ("stage_dense", C.c_int * 8)]
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        _lib = C.CDLL(build())
+def lib(f64: bool = False):
+    """The fp32 build, or (f64=True) the build whose collective simulators use double values."""
+    key = bool(f64)
+    if key not in _libs:
+        _lib = C.CDLL(build(f64=key))
+        _libs[key] = _lib
         u64, i32, f32, f64 = C.c_uint64, C.c_int, C.c_float, C.c_double
         p = C.c_void_p
+        _lib.or_val_bytes.restype = i32
+        _lib.or_val_bytes.argtypes = []
         _lib.or_switch_threshold.restype = u64
         _lib.or_switch_threshold.argtypes = [u64, i32, i32, f64]
         _lib.or_merge_sum.restype = u64
@@ -88,7 +95,14 @@ def lib():
         _lib.or_qsgd_dequantize.argtypes = [p, p, u64, i32, C.c_uint32, p]
         _lib.or_expected_nnz.restype = f64
         _lib.or_expected_nnz.argtypes = [u64, u64, i32]
-    return _lib
+    return _libs[key]
+
+
+def _is64(dtype) -> bool:
+    dt = np.dtype(dtype)
+    if dt not in (np.float32, np.float64):
+        raise ValueError("value dtype must be float32 or float64")
+    return dt == np.float64
 
 
 def _ptr(a: np.ndarray):
@@ -103,6 +117,10 @@ def _f32(a):
     return np.ascontiguousarray(a, dtype=np.float32)
 
 
+def _fv(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
 # --------------------------------------------------------------------------
 # thin wrappers
 # --------------------------------------------------------------------------
@@ -111,43 +129,43 @@ def switch_threshold(N, isize=4, c=4, scale=1.0) -> int:
     return int(lib().or_switch_threshold(N, isize, c, scale))
 
 
-def merge_sum(ia, va, ib, vb):
-    ia, va, ib, vb = _u32(ia), _f32(va), _u32(ib), _f32(vb)
+def merge_sum(ia, va, ib, vb, dtype=np.float32):
+    ia, va, ib, vb = _u32(ia), _fv(va, dtype), _u32(ib), _fv(vb, dtype)
     n = len(ia) + len(ib)
     io = np.zeros(max(n, 1), np.uint32)
-    vo = np.zeros(max(n, 1), np.float32)
-    m = lib().or_merge_sum(_ptr(ia), _ptr(va), len(ia), _ptr(ib), _ptr(vb), len(ib), _ptr(io), _ptr(vo))
+    vo = np.zeros(max(n, 1), dtype)
+    m = lib(_is64(dtype)).or_merge_sum(_ptr(ia), _ptr(va), len(ia), _ptr(ib), _ptr(vb), len(ib), _ptr(io), _ptr(vo))
     return io[:m], vo[:m]
 
 
-def stream_sum(N, delta, a, b):
+def stream_sum(N, delta, a, b, dtype=np.float32):
     """a, b: (dense: bool, idx|None, val).  Returns (dense, idx|None, val)."""
     ad, ai, av = a
     bd, bi, bv = b
     ai = _u32(ai if ai is not None else np.zeros(0)); bi = _u32(bi if bi is not None else np.zeros(0))
-    av, bv = _f32(av), _f32(bv)
+    av, bv = _fv(av, dtype), _fv(bv, dtype)
     na = N if ad else len(ai)
     nb = N if bd else len(bi)
     cap = max(na + nb, N, 1)
     oi = np.zeros(cap, np.uint32)
-    ov = np.zeros(cap, np.float32)
+    ov = np.zeros(cap, dtype)
     od = C.c_int(0)
-    n = lib().or_stream_sum(N, delta, int(ad), _ptr(ai), _ptr(av), na, int(bd), _ptr(bi), _ptr(bv), nb,
+    n = lib(_is64(dtype)).or_stream_sum(N, delta, int(ad), _ptr(ai), _ptr(av), na, int(bd), _ptr(bi), _ptr(bv), nb,
                             C.byref(od), _ptr(oi), _ptr(ov))
     if od.value:
         return True, None, ov[:N].copy()
     return False, oi[:n].copy(), ov[:n].copy()
 
 
-def _flatten(streams):
+def _flatten(streams, dtype=np.float32):
     P = len(streams)
     off = np.zeros(P + 1, np.uint64)
     for i, (ii, _) in enumerate(streams):
         off[i + 1] = off[i] + len(ii)
     idx = _u32(np.concatenate([s[0] for s in streams]) if P else np.zeros(0))
-    val = _f32(np.concatenate([s[1] for s in streams]) if P else np.zeros(0))
+    val = _fv(np.concatenate([s[1] for s in streams]) if P else np.zeros(0), dtype)
     if len(idx) == 0:
-        idx, val = np.zeros(1, np.uint32), np.zeros(1, np.float32)
+        idx, val = np.zeros(1, np.uint32), np.zeros(1, dtype)
     return idx, val, off
 
 
@@ -161,12 +179,14 @@ class op_scope:
         self.op = op
 
     def __enter__(self):
-        if lib().or_set_op(self.op) != 0:
-            raise ValueError("unknown operator")
+        for f64 in (False, True):
+            if lib(f64).or_set_op(self.op) != 0:
+                raise ValueError("unknown operator")
         return self
 
     def __exit__(self, *exc):
-        lib().or_set_op(OP_SUM)
+        for f64 in (False, True):
+            lib(f64).or_set_op(OP_SUM)
 
 
 class qsgd_norm_scope:
@@ -184,13 +204,13 @@ class qsgd_norm_scope:
         lib().or_set_qsgd_norm(0)
 
 
-def brute_force_op(N, streams, op):
+def brute_force_op(N, streams, op, dtype=np.float32):
     """(mask, values) of the definition for operator `op`; neutral element off the union."""
-    idx, val, off = _flatten(streams)
+    idx, val, off = _flatten(streams, dtype)
     mask = np.zeros(N, np.uint8)
-    f32 = np.zeros(N, np.float32)
+    f32 = np.zeros(N, dtype)
     with op_scope(op):
-        lib().or_brute_force_op(len(streams), N, _ptr(idx), _ptr(val), _ptr(off), _ptr(mask), _ptr(f32))
+        lib(_is64(dtype)).or_brute_force_op(len(streams), N, _ptr(idx), _ptr(val), _ptr(off), _ptr(mask), _ptr(f32))
     return mask, f32
 
 
@@ -227,20 +247,20 @@ def _results(P, N, n_out, dense, n, oi, ov):
     return res
 
 
-def sparse_allgather(N, streams, delta=None, n_out=None):
+def sparse_allgather(N, streams, delta=None, n_out=None, dtype=np.float32):
     """Sparse allgather of streams with disjoint index ranges (R-27).
     Returns (results, stats); raises ValueError if two ranges overlap."""
     P = len(streams)
     if delta is None:
-        delta = switch_threshold(N)
+        delta = switch_threshold(N, isize=np.dtype(dtype).itemsize)
     n_out = P if n_out is None else n_out
-    idx, val, off = _flatten(streams)
+    idx, val, off = _flatten(streams, dtype)
     dense = np.zeros(P, np.int32)
     n = np.zeros(P, np.uint64)
     oi = np.zeros(max(n_out * N, 1), np.uint32)
-    ov = np.zeros(max(n_out * N, 1), np.float32)
+    ov = np.zeros(max(n_out * N, 1), dtype)
     st = (_RankStats * P)()
-    rc = lib().or_sparse_allgather(P, N, delta, _ptr(idx), _ptr(val), _ptr(off), n_out, _ptr(dense), _ptr(n),
+    rc = lib(_is64(dtype)).or_sparse_allgather(P, N, delta, _ptr(idx), _ptr(val), _ptr(off), n_out, _ptr(dense), _ptr(n),
                                    _ptr(oi), _ptr(ov), st)
     if rc == -2:
         raise ValueError("sparse allgather: index ranges of two ranks overlap")
@@ -249,18 +269,20 @@ def sparse_allgather(N, streams, delta=None, n_out=None):
     return _results(P, N, n_out, dense, n, oi, ov), _stats_list(st)
 
 
-def ssar_recursive_double(N, streams, delta=None, n_out=None):
+def ssar_recursive_double(N, streams, delta=None, n_out=None, dtype=np.float32):
+    """dtype float64: the fp64 build (values "single or double", P:470-471);
+    default delta then = floor(N*8/12) (P:488-491 with isize = 8)."""
     P = len(streams)
     if delta is None:
-        delta = switch_threshold(N)
+        delta = switch_threshold(N, isize=np.dtype(dtype).itemsize)
     n_out = P if n_out is None else n_out
-    idx, val, off = _flatten(streams)
+    idx, val, off = _flatten(streams, dtype)
     dense = np.zeros(P, np.int32)
     n = np.zeros(P, np.uint64)
     oi = np.zeros(max(n_out * N, 1), np.uint32)
-    ov = np.zeros(max(n_out * N, 1), np.float32)
+    ov = np.zeros(max(n_out * N, 1), dtype)
     st = (_RankStats * P)()
-    rc = lib().or_ssar_recursive_double(P, N, delta, _ptr(idx), _ptr(val), _ptr(off), n_out,
+    rc = lib(_is64(dtype)).or_ssar_recursive_double(P, N, delta, _ptr(idx), _ptr(val), _ptr(off), n_out,
                                         _ptr(dense), _ptr(n), _ptr(oi), _ptr(ov), st)
     if rc != 0:
         raise ValueError("or_ssar_recursive_double rejected its arguments")
@@ -268,19 +290,19 @@ def ssar_recursive_double(N, streams, delta=None, n_out=None):
 
 
 def split_allgather(N, streams, algo=ALGO_AUTO, delta=None, quant_bits=0, bucket=1024,
-                    seed=0, n_out=None):
+                    seed=0, n_out=None, dtype=np.float32):
     P = len(streams)
     if delta is None:
-        delta = switch_threshold(N)
+        delta = switch_threshold(N, isize=np.dtype(dtype).itemsize)
     n_out = P if n_out is None else n_out
-    idx, val, off = _flatten(streams)
+    idx, val, off = _flatten(streams, dtype)
     dense = np.zeros(P, np.int32)
     n = np.zeros(P, np.uint64)
     oi = np.zeros(max(n_out * N, 1), np.uint32)
-    ov = np.zeros(max(n_out * N, 1), np.float32)
+    ov = np.zeros(max(n_out * N, 1), dtype)
     st = (_RankStats * P)()
     used = C.c_int(0)
-    rc = lib().or_split_allgather(P, N, delta, algo, quant_bits, bucket, seed, _ptr(idx), _ptr(val),
+    rc = lib(_is64(dtype)).or_split_allgather(P, N, delta, algo, quant_bits, bucket, seed, _ptr(idx), _ptr(val),
                                   _ptr(off), n_out, _ptr(dense), _ptr(n), _ptr(oi), _ptr(ov), st,
                                   C.byref(used))
     if rc != 0:
@@ -387,13 +409,13 @@ def expected_nnz(k, N, P) -> float:
     return float(lib().or_expected_nnz(k, N, P))
 
 
-def result_to_dense(res, N):
-    """(dense, idx, val) -> (mask, fp32 vector) for comparisons."""
+def result_to_dense(res, N, dtype=np.float32):
+    """(dense, idx, val) -> (mask, vector of dtype) for comparisons."""
     d, i, v = res
     if d:
-        return np.ones(N, np.uint8), np.asarray(v, np.float32)
+        return np.ones(N, np.uint8), np.asarray(v, dtype)
     mask = np.zeros(N, np.uint8)
-    vec = np.zeros(N, np.float32)
+    vec = np.zeros(N, dtype)
     mask[i] = 1
     vec[i] = v
     return mask, vec

@@ -34,27 +34,33 @@ uint64_t or_switch_threshold(uint64_t N, int isize, int c, double scale) {
  * 2 MIN (neutral +inf).  Set with or_set_op; SUM by default. */
 static int g_op = 0;
 
+/* value and pair sizes on the wire: 4 / 8 bytes (fp32), 8 / 12 bytes (fp64) */
+#define VB ((uint64_t)sizeof(or_val))
+#define PB ((uint64_t)(4 + sizeof(or_val)))
+
+int or_val_bytes(void) { return (int)sizeof(or_val); }
+
 int or_set_op(int op) {
   if (op < 0 || op > 2) return -1;
   g_op = op;
   return 0;
 }
 
-static float op_combine(float a, float b) {
+static or_val op_combine(or_val a, or_val b) {
   if (g_op == 1) return a > b ? a : b;
   if (g_op == 2) return a < b ? a : b;
   return a + b;
 }
 
-static float op_neutral(void) {
+static or_val op_neutral(void) {
   if (g_op == 1) return -INFINITY;
   if (g_op == 2) return INFINITY;
-  return 0.0f;
+  return 0;
 }
 
-uint64_t or_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
-                      const uint32_t* ib, const float* vb, uint64_t nb,
-                      uint32_t* io, float* vo) {
+uint64_t or_merge_sum(const uint32_t* ia, const or_val* va, uint64_t na,
+                      const uint32_t* ib, const or_val* vb, uint64_t nb,
+                      uint32_t* io, or_val* vo) {
   /* P:516-527, overlapping indices, both sparse: union of the index sets,
    * values summed where the indices coincide.  Cancellation is ignored: an
    * index present in either input is present in the output even if the sum
@@ -76,9 +82,9 @@ uint64_t or_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
 }
 
 uint64_t or_stream_sum(uint64_t N, uint64_t delta,
-                       int a_dense, const uint32_t* ia, const float* va, uint64_t na,
-                       int b_dense, const uint32_t* ib, const float* vb, uint64_t nb,
-                       int* out_dense, uint32_t* out_idx, float* out_val) {
+                       int a_dense, const uint32_t* ia, const or_val* va, uint64_t na,
+                       int b_dense, const uint32_t* ib, const or_val* vb, uint64_t nb,
+                       int* out_dense, uint32_t* out_idx, or_val* out_val) {
   uint64_t j;
   if (!a_dense && !b_dense) {
     /* upper-bound |H1|+|H2|; if bigger than delta switch to dense. */
@@ -101,9 +107,9 @@ uint64_t or_stream_sum(uint64_t N, uint64_t delta,
   /* one dense, one sparse: iterate over the sparse pairs and
    * "set" (accumulate, reading R-12) the value at that position. */
   {
-    const float* dv = a_dense ? va : vb;
+    const or_val* dv = a_dense ? va : vb;
     const uint32_t* si = a_dense ? ib : ia;
-    const float* sv = a_dense ? vb : va;
+    const or_val* sv = a_dense ? vb : va;
     uint64_t sn = a_dense ? nb : na;
     for (j = 0; j < N; j++) out_val[j] = dv[j];
     for (j = 0; j < sn; j++) out_val[si[j]] = op_combine(out_val[si[j]], sv[j]);
@@ -112,8 +118,8 @@ uint64_t or_stream_sum(uint64_t N, uint64_t delta,
   return N;
 }
 
-uint64_t or_brute_force_op(int P, uint64_t N, const uint32_t* idx, const float* val,
-                           const uint64_t* off, uint8_t* mask, float* f32) {
+uint64_t or_brute_force_op(int P, uint64_t N, const uint32_t* idx, const or_val* val,
+                           const uint64_t* off, uint8_t* mask, or_val* f32) {
   /* The definition for any operator: every index of the union, reduced over
    * the ranks that hold it (rank order; MAX and MIN are order-free). */
   uint64_t j, K = 0;
@@ -157,18 +163,18 @@ typedef struct {
   int dense;
   uint64_t n;     /* pairs if sparse, N if dense */
   uint32_t* idx;  /* sparse only */
-  float* val;
+  or_val* val;
 } strm;
 
 static void strm_free(strm* s) { free(s->idx); free(s->val); s->idx = NULL; s->val = NULL; }
 
-static int strm_copy_in(strm* s, const uint32_t* idx, const float* val, uint64_t n) {
+static int strm_copy_in(strm* s, const uint32_t* idx, const or_val* val, uint64_t n) {
   s->dense = 0; s->n = n;
   s->idx = (uint32_t*)malloc((n ? n : 1) * sizeof(uint32_t));
-  s->val = (float*)malloc((n ? n : 1) * sizeof(float));
+  s->val = (or_val*)malloc((n ? n : 1) * sizeof(or_val));
   if (!s->idx || !s->val) return -1;
   memcpy(s->idx, idx, n * sizeof(uint32_t));
-  memcpy(s->val, val, n * sizeof(float));
+  memcpy(s->val, val, n * sizeof(or_val));
   return 0;
 }
 
@@ -177,7 +183,7 @@ static int strm_sum(uint64_t N, uint64_t delta, const strm* a, const strm* b, st
   uint64_t cap_pairs = a->n + b->n;
   uint64_t cap_vals = cap_pairs > N ? cap_pairs : N;
   r->idx = (uint32_t*)malloc((cap_pairs ? cap_pairs : 1) * sizeof(uint32_t));
-  r->val = (float*)malloc((cap_vals ? cap_vals : 1) * sizeof(float));
+  r->val = (or_val*)malloc((cap_vals ? cap_vals : 1) * sizeof(or_val));
   if (!r->idx || !r->val) return -1;
   r->n = or_stream_sum(N, delta, a->dense, a->idx, a->val, a->n,
                        b->dense, b->idx, b->val, b->n, &r->dense, r->idx, r->val);
@@ -185,19 +191,19 @@ static int strm_sum(uint64_t N, uint64_t delta, const strm* a, const strm* b, st
 }
 
 static uint64_t strm_bytes(const strm* s) {
-  /* payload bytes on the wire: 8 per (u32, f32) pair, 4 per dense word */
-  return s->dense ? 4 * s->n : 8 * s->n;
+  /* payload bytes on the wire: PB per (u32, value) pair, VB per dense word */
+  return s->dense ? VB * s->n : PB * s->n;
 }
 
 static void strm_out(const strm* s, uint64_t N, int r, int* out_dense, uint64_t* out_n,
-                     uint32_t* out_idx, float* out_val) {
+                     uint32_t* out_idx, or_val* out_val) {
   out_dense[r] = s->dense;
   out_n[r] = s->n;
   if (s->dense) {
-    memcpy(out_val + (uint64_t)r * N, s->val, N * sizeof(float));
+    memcpy(out_val + (uint64_t)r * N, s->val, N * sizeof(or_val));
   } else {
     memcpy(out_idx + (uint64_t)r * N, s->idx, s->n * sizeof(uint32_t));
-    memcpy(out_val + (uint64_t)r * N, s->val, s->n * sizeof(float));
+    memcpy(out_val + (uint64_t)r * N, s->val, s->n * sizeof(or_val));
   }
 }
 
@@ -206,9 +212,9 @@ static void strm_out(const strm* s, uint64_t N, int r, int* out_dense, uint64_t*
 /* ------------------------------------------------------------------------- */
 
 int or_ssar_recursive_double(int P, uint64_t N, uint64_t delta,
-                             const uint32_t* idx, const float* val, const uint64_t* off,
+                             const uint32_t* idx, const or_val* val, const uint64_t* off,
                              int n_out, int* out_dense, uint64_t* out_n,
-                             uint32_t* out_idx, float* out_val, or_rank_stats* stats) {
+                             uint32_t* out_idx, or_val* out_val, or_rank_stats* stats) {
   int r, t, L = 0, P2 = 1, e;
   strm *cur, *nxt;
   if (P < 1 || P > 256) return -1;
@@ -270,9 +276,9 @@ int or_ssar_recursive_double(int P, uint64_t N, uint64_t delta,
       memset(&cur[x], 0, sizeof(strm));
       cur[x].dense = 1;
       cur[x].n = N;
-      cur[x].val = (float*)malloc((N ? N : 1) * sizeof(float));
+      cur[x].val = (or_val*)malloc((N ? N : 1) * sizeof(or_val));
       if (!cur[x].val) return -1;
-      memcpy(cur[x].val, cur[r].val, N * sizeof(float));
+      memcpy(cur[x].val, cur[r].val, N * sizeof(or_val));
     } else if (strm_copy_in(&cur[x], cur[r].idx, cur[r].val, cur[r].n)) {
       return -1;
     }
@@ -317,9 +323,9 @@ static int tree_reduce(strm* slices, int lo, int hi, uint64_t part_n, strm* out)
 
 int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
                        int quant_bits, uint32_t bucket, uint64_t seed,
-                       const uint32_t* idx, const float* val, const uint64_t* off,
+                       const uint32_t* idx, const or_val* val, const uint64_t* off,
                        int n_out, int* out_dense, uint64_t* out_n,
-                       uint32_t* out_idx, float* out_val, or_rank_stats* stats,
+                       uint32_t* out_idx, or_val* out_val, or_rank_stats* stats,
                        int* dsar_used) {
   int i, j, r;
   uint64_t part, ksum = 0, K = 0, e;
@@ -331,6 +337,7 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
   if (quant_bits != 0 && quant_bits != 2 && quant_bits != 4 && quant_bits != 8) return -1;
   if (quant_bits && bucket == 0) return -1;
   if (quant_bits && g_op != 0) return -1;   /* QSGD needs the 0 neutral element (max-norm scale) */
+  if (quant_bits && sizeof(or_val) != sizeof(float)) return -1;   /* QSGD is defined on fp32 values here */
   part = N / (uint64_t)P;                         /* floor(N/P), App. A */
   bnd = (uint64_t*)malloc(((size_t)P + 1) * sizeof(uint64_t));
   slices = (strm*)calloc((size_t)P * (size_t)P, sizeof(strm));
@@ -344,7 +351,7 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
    * slice_ij directly to owner j */
   for (i = 0; i < P; i++) {
     const uint32_t* ii = idx + off[i];
-    const float* vv = val + off[i];
+    const or_val* vv = val + off[i];
     uint64_t n = off[i + 1] - off[i];
     ksum += n;
     for (j = 0; j < P; j++) {
@@ -355,10 +362,10 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
       if (strm_copy_in(s, ii + s0, vv + s0, s1 - s0)) return -1;
       for (t = 0; t < s->n; t++) s->idx[t] -= (uint32_t)bnd[j];  /* partition-local */
       if (stats && j != i) {
-        stats[i].bytes_sent += 8 * s->n;
+        stats[i].bytes_sent += PB * s->n;
         stats[i].pairs_sent += s->n;
         stats[i].msgs_sent += 1;
-        stats[j].bytes_recv += 8 * s->n;
+        stats[j].bytes_recv += PB * s->n;
       }
     }
   }
@@ -384,13 +391,13 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
       for (r = 0; r < P; r++)
         for (j = 0; j < P; j++)
           if (j != r) {
-            stats[j].bytes_sent += 8 * R[j].n; stats[j].pairs_sent += R[j].n;
-            stats[j].msgs_sent += 1; stats[r].bytes_recv += 8 * R[j].n;
+            stats[j].bytes_sent += PB * R[j].n; stats[j].pairs_sent += R[j].n;
+            stats[j].msgs_sent += 1; stats[r].bytes_recv += PB * R[j].n;
           }
     }
     if (K > delta) {
       res.dense = 1; res.n = N;
-      res.val = (float*)malloc((N ? N : 1) * sizeof(float));
+      res.val = (or_val*)malloc((N ? N : 1) * sizeof(or_val));
       if (!res.val) return -1;
       for (e = 0; e < N; e++) res.val[e] = op_neutral();
       for (j = 0; j < P; j++)
@@ -399,7 +406,7 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
       uint64_t o = 0;
       res.dense = 0; res.n = K;
       res.idx = (uint32_t*)malloc((K ? K : 1) * sizeof(uint32_t));
-      res.val = (float*)malloc((K ? K : 1) * sizeof(float));
+      res.val = (or_val*)malloc((K ? K : 1) * sizeof(or_val));
       if (!res.idx || !res.val) return -1;
       for (j = 0; j < P; j++)
         for (e = 0; e < R[j].n; e++) {
@@ -413,26 +420,26 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
   } else {
     /* DSAR: owner switches its reduced split to dense (neutral fill 0),
      * optionally QSGD-encodes it (§6), then dense allgather. */
-    float* dense = (float*)malloc((N ? N : 1) * sizeof(float));
+    or_val* dense = (or_val*)malloc((N ? N : 1) * sizeof(or_val));
     if (!dense) return -1;
     for (e = 0; e < N; e++) dense[e] = op_neutral();
     for (j = 0; j < P; j++) {
       uint64_t nj = bnd[j + 1] - bnd[j];
-      float* Dj = dense + bnd[j];
+      or_val* Dj = dense + bnd[j];
       uint64_t wire;
       for (e = 0; e < R[j].n; e++) Dj[R[j].idx[e]] = R[j].val[e];
-      if (quant_bits) {
+      if (quant_bits) {   /* fp32 build only (checked above) */
         uint64_t cb = (nj * (uint64_t)quant_bits + 7) / 8;
         uint64_t ns = (nj + bucket - 1) / bucket;
         uint8_t* codes = (uint8_t*)malloc(cb ? cb : 1);
         float* scales = (float*)malloc((ns ? ns : 1) * sizeof(float));
         if (!codes || !scales) return -1;
-        or_qsgd_quantize(Dj, nj, quant_bits, bucket, seed, bnd[j], codes, scales);
-        or_qsgd_dequantize(codes, scales, nj, quant_bits, bucket, Dj);
+        or_qsgd_quantize((const float*)Dj, nj, quant_bits, bucket, seed, bnd[j], codes, scales);
+        or_qsgd_dequantize(codes, scales, nj, quant_bits, bucket, (float*)Dj);
         free(codes); free(scales);
         wire = cb + 4 * ns;
       } else {
-        wire = 4 * nj;
+        wire = VB * nj;
       }
       if (stats)
         for (r = 0; r < P; r++)
@@ -443,7 +450,7 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
     }
     for (r = 0; r < P && r < n_out; r++) {
       out_dense[r] = 1; out_n[r] = N;
-      memcpy(out_val + (uint64_t)r * N, dense, N * sizeof(float));
+      memcpy(out_val + (uint64_t)r * N, dense, N * sizeof(or_val));
     }
     free(dense);
   }
@@ -474,9 +481,9 @@ static int cmp_u32(const void* pa, const void* pb) {
   return (a > b) - (a < b);
 }
 
-int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, const float* val,
+int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, const or_val* val,
                         const uint64_t* off, int n_out, int* out_dense, uint64_t* out_n,
-                        uint32_t* out_idx, float* out_val, or_rank_stats* stats) {
+                        uint32_t* out_idx, or_val* out_val, or_rank_stats* stats) {
   int r, i, j, order[256], m = 0;
   uint64_t K = 0, e, pos;
   if (P < 1 || P > 256 || N == 0 || n_out < 0 || n_out > P) return -1;
@@ -496,11 +503,11 @@ int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, 
   }
   for (r = 0; r < n_out; r++) {
     uint32_t* oi = out_idx + (uint64_t)r * N;
-    float* ov = out_val + (uint64_t)r * N;
+    or_val* ov = out_val + (uint64_t)r * N;
     if (K > delta) {   /* dense result: zeros, then every value at its index */
       out_dense[r] = 1;
       out_n[r] = N;
-      for (e = 0; e < N; e++) ov[e] = 0.0f;
+      for (e = 0; e < N; e++) ov[e] = 0;
       for (j = 0; j < m; j++)
         for (e = off[order[j]]; e < off[order[j] + 1]; e++) ov[idx[e]] = val[e];
     } else {           /* sparse: the concatenation in range order */
@@ -518,8 +525,8 @@ int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, 
     for (r = 0; r < P; r++) {
       const uint64_t n = off[r + 1] - off[r];
       memset(&stats[r], 0, sizeof(stats[r]));
-      stats[r].bytes_sent = 8 * n * (uint64_t)(P - 1);
-      stats[r].bytes_recv = 8 * (K - n);
+      stats[r].bytes_sent = PB * n * (uint64_t)(P - 1);
+      stats[r].bytes_recv = PB * (K - n);
       stats[r].msgs_sent = (uint64_t)(P - 1);
       stats[r].pairs_sent = n * (uint64_t)(P - 1);
     }

@@ -14,10 +14,14 @@
  * Representation: a stream is either
  *   sparse: n strictly increasing u32 indices < N with one fp32 value each, or
  *   dense:  N fp32 values.
- * Index type u32.  Values fp32: the paper works "with single or
- * double precision"; BASELINE.json fixes fp32 for every config,
- * so the algorithm simulators compute in fp32 exactly as the method would,
- * and the *definition* (or_brute_force) is additionally computed in fp64.
+ * Index type u32.  Values: the paper works "with single or double
+ * precision".  The collective simulators (or_merge_sum ..
+ * or_sparse_allgather, the functions taking `or_val`) are compiled twice:
+ * liboracle.so with or_val = float (BASELINE.json's fp32, computed in fp32
+ * exactly as the method would) and liboracle_f64.so with or_val = double
+ * (-DOR_VAL=double; every combine in fp64, pair = 12 bytes on the wire, QSGD
+ * not defined).  or_brute_force (the fp32 definition, additionally summed in
+ * fp64), top-k and QSGD are fp32 in both builds.
  *
  * Parity pins: see tests/test_oracle_*.py.  Every function below is pinned;
  * none is "parity unpinned".
@@ -29,6 +33,14 @@
 extern "C" {
 #endif
 
+#ifndef OR_VAL
+#define OR_VAL float
+#endif
+typedef OR_VAL or_val;   /* value type of the collective simulators (float or double) */
+
+/* sizeof(or_val) of this build: 4 (liboracle.so) or 8 (liboracle_f64.so). */
+int or_val_bytes(void);
+
 /* Dense-switch threshold δ = floor(scale * N*isize/(c+isize))  (§5.1 P:488-491,
  * symbol garbled to "0.0 cm"; reading R-1).  Sparse allowed while nnz <= δ. */
 uint64_t or_switch_threshold(uint64_t N, int isize, int c, double scale);
@@ -36,9 +48,9 @@ uint64_t or_switch_threshold(uint64_t N, int isize, int c, double scale);
 /* Two-pointer union merge with fp32 sum of two sparse streams (§5.1
  * "Efficient Summation", overlapping case, both sparse, no switch).
  * Output buffers must hold na+nb pairs.  Returns the output count. */
-uint64_t or_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
-                      const uint32_t* ib, const float* vb, uint64_t nb,
-                      uint32_t* io, float* vo);
+uint64_t or_merge_sum(const uint32_t* ia, const or_val* va, uint64_t na,
+                      const uint32_t* ib, const or_val* vb, uint64_t nb,
+                      uint32_t* io, or_val* vo);
 
 /* One stream summation u1+u2 with the paper's four cases:
  * both sparse & na+nb <= delta -> sparse union merge; both sparse & na+nb > delta
@@ -48,9 +60,9 @@ uint64_t or_merge_sum(const uint32_t* ia, const float* va, uint64_t na,
  * out_val must hold max(N, na+nb) floats, out_idx na+nb.  Returns out count
  * (N if dense). */
 uint64_t or_stream_sum(uint64_t N, uint64_t delta,
-                       int a_dense, const uint32_t* ia, const float* va, uint64_t na,
-                       int b_dense, const uint32_t* ib, const float* vb, uint64_t nb,
-                       int* out_dense, uint32_t* out_idx, float* out_val);
+                       int a_dense, const uint32_t* ia, const or_val* va, uint64_t na,
+                       int b_dense, const uint32_t* ib, const or_val* vb, uint64_t nb,
+                       int* out_dense, uint32_t* out_idx, or_val* out_val);
 
 /* THE DEFINITION (§5.3 problem statement P:576-579; union index set P:459-461):
  * result[j] = sum_i x_i[j] over ranks holding j.  Inputs: P streams
@@ -73,8 +85,8 @@ int or_set_op(int op);
 /* The definition for the current operator: mask = union of the index sets,
  * f32[j] = the operator over the ranks holding j (rank order), the neutral
  * element elsewhere.  Returns K. */
-uint64_t or_brute_force_op(int P, uint64_t N, const uint32_t* idx, const float* val,
-                           const uint64_t* off, uint8_t* mask, float* f32);
+uint64_t or_brute_force_op(int P, uint64_t N, const uint32_t* idx, const or_val* val,
+                           const uint64_t* off, uint8_t* mask, or_val* f32);
 
 /* Per-rank accounting of one simulated collective (the SPEC's TraceRecord,
  * S:172-179, reduced to what the tests check). */
@@ -103,9 +115,9 @@ typedef struct {
  * out_val + r*N (capacity N each).  stats: P entries (nullable).
  * Returns 0, or -1 on bad arguments. */
 int or_ssar_recursive_double(int P, uint64_t N, uint64_t delta,
-                             const uint32_t* idx, const float* val, const uint64_t* off,
+                             const uint32_t* idx, const or_val* val, const uint64_t* off,
                              int n_out, int* out_dense, uint64_t* out_n,
-                             uint32_t* out_idx, float* out_val, or_rank_stats* stats);
+                             uint32_t* out_idx, or_val* out_val, or_rank_stats* stats);
 
 /* Canonical balanced tree over ranks lo..hi-1 (reading R-8): hi-lo==1 -> x_lo,
  * else sum(tree(lo,mid), tree(mid,hi)) with mid = lo + (hi-lo)/2, absent
@@ -132,9 +144,9 @@ enum { OR_ALGO_AUTO = 0, OR_ALGO_SSAR_RD = 1, OR_ALGO_SSAR_SPLIT = 2, OR_ALGO_DS
  * path ran.  Returns 0, -1 on bad args. */
 int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
                        int quant_bits, uint32_t bucket, uint64_t seed,
-                       const uint32_t* idx, const float* val, const uint64_t* off,
+                       const uint32_t* idx, const or_val* val, const uint64_t* off,
                        int n_out, int* out_dense, uint64_t* out_n,
-                       uint32_t* out_idx, float* out_val, or_rank_stats* stats,
+                       uint32_t* out_idx, or_val* out_val, or_rank_stats* stats,
                        int* dsar_used);
 
 /* Sparse allgather for disjoint slices (§7 SCD: "the values
@@ -148,9 +160,9 @@ int or_split_allgather(int P, uint64_t N, uint64_t delta, int algo,
  * each of the P-1 others.  Returns 0, or -2 if two non-empty ranges overlap
  * (the precondition fails), -1 on bad arguments.  Outputs as in
  * or_split_allgather (all ranks get the same result). */
-int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, const float* val,
+int or_sparse_allgather(int P, uint64_t N, uint64_t delta, const uint32_t* idx, const or_val* val,
                         const uint64_t* off, int n_out, int* out_dense, uint64_t* out_n,
-                        uint32_t* out_idx, float* out_val, or_rank_stats* stats);
+                        uint32_t* out_idx, or_val* out_val, or_rank_stats* stats);
 
 /* Top-k by magnitude (§2.2; Algorithm 1).  Orders every
  * coordinate by (|x_j| descending, j ascending) — ties to the lower index,
