@@ -39,6 +39,7 @@ extern "C" {
 #define SPARCML_HEADER_BYTES 64       /* result header at out[0]              */
 #define SPARCML_IPC_HANDLE_BYTES 64   /* cudaIpcMemHandle_t                    */
 #define SPARCML_HEADER_MAGIC 0x4D435053u /* "SPCM" little-endian              */
+#define SPARCML_HEADER_MAGIC_F64 0x44435053u /* "SPCD": a result of the _f64 calls (double values) */
 
 typedef enum {
   SPARCML_OK = 0,
@@ -122,6 +123,12 @@ size_t sparcml_result_bytes(uint64_t N);
 /* Byte offset of val[] for a sparse result of dimension N. */
 size_t sparcml_result_val_offset(uint64_t N);
 
+/* The same for double values (the _f64 calls): delta = floor(N*8/12)
+ * (P:488-491 with isize = 8), H64 = ceil4(floor(2N/3)) sparse slots:
+ * 64 + max(8N, 12*H64) + 32 bytes, val[] (double) at 64 + 4*H64. */
+size_t sparcml_result_bytes_f64(uint64_t N);
+size_t sparcml_result_val_offset_f64(uint64_t N);
+
 /* ---------------------------- communicator ----------------------------- */
 
 typedef struct sparcml_comm sparcml_comm;
@@ -184,6 +191,22 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* comm,
                                               const uint64_t* nnz_host, uint64_t N, sparcml_op op,
                                               const sparcml_opts* opts_host,
                                               void* const* out_host, size_t out_bytes, void* stream);
+
+/* The sparse allreduce with fp64 values: the paper's streams carry "single
+ * or double precision floating point values" (§5.1).  Identical to
+ * the calls above with val[] double, every combine one fp64 rounding in the
+ * same canonical order, a pair = 12 bytes (so delta = floor(N*8/12)),
+ * the result laid out per sparcml_result_*_f64 with header magic
+ * SPARCML_HEADER_MAGIC_F64 and double payload values.  All algorithms and
+ * operators; QSGD (quant_bits != 0) is fp32-only -> SPARCML_ERR_INVALID_ARG. */
+sparcml_status sparcml_sparse_allreduce_f64(sparcml_comm* comm, const uint32_t* idx, const double* val,
+                                            uint64_t nnz, uint64_t N, sparcml_op op,
+                                            const sparcml_opts* opts_host, void* out, size_t out_bytes,
+                                            void* stream);
+sparcml_status sparcml_sparse_allreduce_local_f64(sparcml_comm* comm, const uint32_t* const* idx_host,
+                                                  const double* const* val_host, const uint64_t* nnz_host,
+                                                  uint64_t N, sparcml_op op, const sparcml_opts* opts_host,
+                                                  void* const* out_host, size_t out_bytes, void* stream);
 
 /* Device-side barrier of all ranks (one warp per rank spinning on flags its
  * peers store over NVLink).  Stream-ordered, no host synchronisation;

@@ -27,6 +27,9 @@ uint64_t half_cap(uint64_t N) {   // H = ceil4(floor(N/2)): sparse slots in a re
   return align_up(N / 2, 4);
 }
 
+// fp64 values: delta = floor(N*8/12) (P:488-491 with isize = 8)
+uint64_t cap64(uint64_t N) { return align_up(N * 8 / 12, 4); }
+
 // ---------------------------------------------------------------------------
 // canonical tree over ranks (reading R-8): tree(lo,hi) = tree(lo,mid) + tree(mid,hi)
 // ---------------------------------------------------------------------------
@@ -97,7 +100,7 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.max_N = max_N;
   L.max_nnz = max_nnz;
   L.part_cap = align_up(max_N / P + P, 64);
-  L.cap_s = std::min<uint64_t>(max_nnz, L.part_cap);
+  L.cap_s = align_up(std::min<uint64_t>(max_nnz, L.part_cap), 4);   // val[] 16-byte aligned (fp64 too)
   L.nwin = (L.part_cap + kWin - 1) / kWin;
   L.ntab = (L.part_cap + kTab - 1) / kTab;
   size_t off = align_up(sizeof(Ctrl), 256);
@@ -105,25 +108,29 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.n_status = max_N / 1024 + 2 * max_nnz / kMergeTile + 256;
   off = align_up(off + L.n_status * sizeof(TileStatus), 256);
   L.recv_off = off;
-  L.region_bytes = align_up(8 * L.cap_s, 256);
+  // receive regions, spill area, partition result and RD buffers are sized
+  // for 8-byte values (fp64 calls); fp32 calls use the same idx offsets
+  L.region_bytes = align_up(12 * L.cap_s, 256);
   off += (size_t)P * L.region_bytes;
   L.win_off = off;
   L.win_bytes = align_up(4 * (L.ntab + 1), 256);
   off += (size_t)P * L.win_bytes;
   L.stage_off = off;
-  off += align_up(8 * (size_t)P * L.cap_s, 256);
+  off += align_up(12 * (size_t)P * L.cap_s, 256);
   L.blk_off = off;
   off += align_up(8 * 8192, 256);
   L.part_off = off;
-  L.part_bytes = align_up(8 * L.part_cap + 256, 256);
+  L.part_bytes = align_up(12 * L.part_cap + 256, 256);
   L.scales_off = off + align_up(L.part_cap + 16, 256);   // codes <= part_cap bytes (8 bits)
   off += L.part_bytes;
   L.L = 0;   // stages of recursive doubling over P' = the largest power of two <= P (R-28)
   while ((2 << L.L) <= P) ++L.L;
   L.rd_off = off;
-  // sparse slots: stage outputs hold <= delta <= N/2 pairs, the stage-1 push a whole input
-  L.rd_val_off = align_up(4 * std::max<uint64_t>(half_cap(max_N), max_nnz) + 64, 256);
-  L.rd_bytes = align_up(std::max<size_t>(2 * L.rd_val_off, 4 * max_N) + 256, 256);
+  // sparse slots: stage outputs hold <= delta <= 2N/3 pairs (fp64; N/2 fp32),
+  // the stage-1 push a whole input
+  const uint64_t rd_pairs = std::max<uint64_t>(cap64(max_N), max_nnz);
+  L.rd_val_off = align_up(4 * rd_pairs + 64, 256);
+  L.rd_bytes = align_up(std::max<size_t>(L.rd_val_off + 8 * rd_pairs, 8 * max_N) + 256, 256);
   // cur x2 + recv[2 parities][stages 0..L+1] (0: fold in, L+1: result out, R-28)
   if (P > 1) off += (size_t)(2 + 2 * (L.L + 2)) * L.rd_bytes;
   L.ag_off = off;
@@ -190,10 +197,12 @@ inline StreamBuf rd_recv(const Layout& L, char* base, int par, int t) {   // t =
   return b;
 }
 
-uint64_t effective_delta(uint64_t N, const sparcml_opts& o) {
-  // delta = floor(scale * N*4/(c+4)), c = 4 -> N/2; never above the result capacity
-  const uint64_t d = (uint64_t)std::floor((double)o.switch_scale * (double)N * 4.0 / (double)(o.index_bytes + 4));
-  return std::min<uint64_t>(d, N / 2);
+uint64_t effective_delta(uint64_t N, const sparcml_opts& o, int vbytes = 4) {
+  // delta = floor(scale * N*isize/(c+isize)), c = 4: N/2 (fp32), 2N/3 (fp64);
+  // never above the result capacity
+  const uint64_t d =
+      (uint64_t)std::floor((double)o.switch_scale * (double)N * vbytes / (double)(o.index_bytes + vbytes));
+  return std::min<uint64_t>(d, vbytes == 8 ? N * 8 / 12 : N / 2);
 }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -215,6 +224,7 @@ sparcml_status check_opts(sparcml_comm* c, const sparcml_opts& o) {
 // per-call parameters shared by all local ranks
 struct CallCtx {
   uint64_t N, delta, val_offset;
+  int f64;             // values are double
   sparcml_opts o;
   int algo;            // resolved: RD, SPLIT (SSAR/DSAR/AUTO decided below)
   int host_dsar;       // -1 unknown (device decides), 0/1 known
@@ -235,7 +245,7 @@ BarrierArgs barrier_args(sparcml_comm* c, int r) {
 // ------------------------------------------------------------ RD schedule ---
 // push (stage-1 partner) ; stage 1 .. L, each waiting for its partner's flag
 sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
-                      const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
+                      const void* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
   const Layout& L = c->L;
   const int Lg = L.L;
   const int P2 = 1 << Lg, E = c->P - P2;   // R-28: extra ranks P2..P-1 fold into 0..E-1
@@ -256,6 +266,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     a.N = cc.N;
     a.validate = cc.o.validate;
     a.tgt = tgt;
+    a.f64 = cc.f64;
     CK(c, launch_rd_push(a, cc.s));
     return SPARCML_OK;
   };
@@ -296,6 +307,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     a.stage = t;
     a.ctr = &ctrl_of(base)->scan[0];
     a.status = status_of(L, base);
+    a.f64 = cc.f64;
     CK(c, launch_rd_stage(a, cc.s));
     return SPARCML_OK;
   };
@@ -329,6 +341,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     u.out = out[i];
     u.N = cc.N;
     u.val_offset = cc.val_offset;
+    u.f64 = cc.f64;
     CK(c, launch_rd_unfold(u, cc.s));
   }
   return SPARCML_OK;
@@ -338,7 +351,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
 // push (slices + window tables -> owners) ; owner reduction (waits for the P
 // slices) ; pull-concat (waits for the P owners)
 sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
-                         const float* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
+                         const void* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
   const Layout& L = c->L;
   const int P = c->P;
   const uint64_t part = cc.N / P;
@@ -363,6 +376,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     }
     a.ctl = ctrl_of(c->peer[r]);
     a.validate = cc.o.validate;
+    a.f64 = cc.f64;
     CK(c, launch_split_push(a, cc.s));
   }
   const TreeSched ts = make_sched(P);
@@ -384,8 +398,8 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     }
     w.sched = ts;
     w.r_idx = reinterpret_cast<uint32_t*>(base + L.part_off);
-    w.r_val = reinterpret_cast<float*>(base + L.part_off + 4 * L.part_cap);
-    w.dense = reinterpret_cast<float*>(base + L.part_off);
+    w.r_val = base + L.part_off + 4 * L.part_cap;
+    w.dense = base + L.part_off;
     w.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
     w.scales = reinterpret_cast<float*>(base + L.scales_off);
     w.bits = cc.o.quant_bits;
@@ -398,8 +412,9 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.qnorm = cc.o.quant_norm;
     w.ctl = ctrl_of(base);
     w.st_idx = reinterpret_cast<uint32_t*>(base + L.stage_off);
-    w.st_val = reinterpret_cast<float*>(base + L.stage_off + 4 * (size_t)P * L.cap_s);
+    w.st_val = base + L.stage_off + 4 * (size_t)P * L.cap_s;
     w.blk = reinterpret_cast<uint64_t*>(base + L.blk_off);
+    w.f64 = cc.f64;
     CK(c, launch_owner(w, cc.s));
   }
   for (size_t i = 0; i < R.size(); ++i) {
@@ -413,11 +428,11 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     for (int j = 0; j < P; ++j) {
       char* pb = c->peer[j];
       a.r_idx[j] = reinterpret_cast<const uint32_t*>(pb + L.part_off);
-      a.r_val[j] = reinterpret_cast<const float*>(pb + L.part_off + 4 * L.part_cap);
+      a.r_val[j] = pb + L.part_off + 4 * L.part_cap;
       a.r_n[j] = &ctrl_of(pb)->owner_K;
       a.r_codes[j] = reinterpret_cast<const uint8_t*>(pb + L.part_off);
       a.r_scales[j] = reinterpret_cast<const float*>(pb + L.scales_off);
-      a.r_dense[j] = reinterpret_cast<const float*>(pb + L.part_off);
+      a.r_dense[j] = pb + L.part_off;
     }
     a.ctl = ctrl_of(c->peer[r]);
     a.wait_owners = 1;
@@ -429,13 +444,14 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     a.status = status_of(L, c->peer[r]);
     a.host_dsar = cc.host_dsar;
     a.op = cc.op;
+    a.f64 = cc.f64;
     CK(c, launch_concat(a, cc.s));
   }
   return SPARCML_OK;
 }
 
 // ------------------------------------------------------------- P == 1 ---
-sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, uint64_t n, char* out,
+sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const void* val, uint64_t n, char* out,
                       const CallCtx& cc) {
   const Layout& L = c->L;
   char* base = c->peer[0];
@@ -449,6 +465,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   p.algo = cc.o.algo;
   p.ctl = my;
   p.validate = cc.o.validate;
+  p.f64 = cc.f64;
   const bool dsar = cc.o.algo == SPARCML_DSAR_SPLIT_ALLGATHER || (cc.o.algo == SPARCML_ALGO_AUTO && n > cc.delta);
   const bool inplace = reinterpret_cast<const char*>(idx) == out + SPARCML_HEADER_BYTES &&
                        reinterpret_cast<const char*>(val) == out + cc.val_offset;
@@ -486,13 +503,14 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
     w.src_val[0] = val;
     w.src_win[0] = win_table(L, base, 0);   // built by p1_prep
     w.sched = make_sched(1);
-    w.dense = reinterpret_cast<float*>(base + L.part_off);
+    w.dense = base + L.part_off;
     w.codes = reinterpret_cast<uint8_t*>(base + L.part_off);
     w.scales = reinterpret_cast<float*>(base + L.scales_off);
     w.bits = cc.o.quant_bits;
     w.bucket = cc.o.quant_bucket;
     w.seed_lo = (uint32_t)cc.o.seed;
     w.seed_hi = (uint32_t)(cc.o.seed >> 32);
+    w.f64 = cc.f64;
     w.host_dsar = 1;
     w.wait = 0;
     w.op = cc.op;
@@ -502,7 +520,7 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
     CK(c, launch_owner(w, cc.s));
     a.r_codes[0] = reinterpret_cast<const uint8_t*>(base + L.part_off);
     a.r_scales[0] = reinterpret_cast<const float*>(base + L.scales_off);
-    a.r_dense[0] = reinterpret_cast<const float*>(base + L.part_off);
+    a.r_dense[0] = base + L.part_off;
   }
   a.ctl = my;
   a.wait_owners = 0;
@@ -514,13 +532,14 @@ sparcml_status run_p1(sparcml_comm* c, const uint32_t* idx, const float* val, ui
   a.status = status_of(L, base);
   a.host_dsar = dsar ? 1 : 0;
   a.op = cc.op;
+  a.f64 = cc.f64;
   CK(c, launch_concat(a, cc.s));
   return SPARCML_OK;
 }
 
-sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
+sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const void* const* val,
                               const uint64_t* nnz, uint64_t N, sparcml_op op, const sparcml_opts* opts,
-                              void* const* out, size_t out_bytes, void* stream) {
+                              void* const* out, size_t out_bytes, void* stream, int f64 = 0) {
   if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
   if (!c->connected) return fail(c, SPARCML_ERR_STATE, "communicator not connected");
   if (op != SPARCML_OP_SUM && op != SPARCML_OP_MAX && op != SPARCML_OP_MIN)
@@ -535,7 +554,10 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   if (st != SPARCML_OK) return st;
   if (o.quant_bits && op != SPARCML_OP_SUM)
     return fail(c, SPARCML_ERR_INVALID_ARG, "QSGD (quant_bits) requires SPARCML_OP_SUM");
-  if (out_bytes < sparcml_result_bytes(N)) return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N)");
+  if (f64 && o.quant_bits)
+    return fail(c, SPARCML_ERR_INVALID_ARG, "QSGD (quant_bits) is defined on fp32 values only");
+  if (out_bytes < (f64 ? sparcml_result_bytes_f64(N) : sparcml_result_bytes(N)))
+    return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N) (_f64 for double values)");
   const int nl = c->local ? c->P : 1;
   uint64_t ksum_host = 0;
   for (int i = 0; i < nl; ++i) {
@@ -549,8 +571,9 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   CallCtx cc;
   cc.N = N;
   cc.o = o;
-  cc.delta = effective_delta(N, o);
-  cc.val_offset = sparcml_result_val_offset(N);
+  cc.f64 = f64;
+  cc.delta = effective_delta(N, o, f64 ? 8 : 4);
+  cc.val_offset = f64 ? sparcml_result_val_offset_f64(N) : sparcml_result_val_offset(N);
   cc.op = (int)op;
   cc.s = static_cast<cudaStream_t>(stream);
   CK(c, cudaSetDevice(c->device));
@@ -708,6 +731,12 @@ size_t sparcml_result_bytes(uint64_t N) {
   return SPARCML_HEADER_BYTES + std::max<size_t>(4 * N, 8 * half_cap(N)) + 32;
 }
 
+size_t sparcml_result_val_offset_f64(uint64_t N) { return SPARCML_HEADER_BYTES + 4 * cap64(N); }
+
+size_t sparcml_result_bytes_f64(uint64_t N) {
+  return SPARCML_HEADER_BYTES + std::max<size_t>(8 * N, 12 * cap64(N)) + 32;
+}
+
 sparcml_status sparcml_comm_create(sparcml_comm** out, int nranks, int rank, int dev, uint64_t max_N,
                                    uint64_t max_nnz) {
   if (!out) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null out");
@@ -834,11 +863,30 @@ const char* sparcml_last_error(const sparcml_comm* c) {
   return c ? c->err.c_str() : g_last_error.c_str();
 }
 
+sparcml_status sparcml_sparse_allreduce_f64(sparcml_comm* c, const uint32_t* idx, const double* val, uint64_t nnz,
+                                            uint64_t N, sparcml_op op, const sparcml_opts* opts, void* out,
+                                            size_t out_bytes, void* stream) {
+  if (c && c->local) return fail(c, SPARCML_ERR_STATE, "use sparcml_sparse_allreduce_local_f64 on a loopback world");
+  const void* v = val;
+  return allreduce_impl(c, &idx, &v, &nnz, N, op, opts, &out, out_bytes, stream, 1);
+}
+
+sparcml_status sparcml_sparse_allreduce_local_f64(sparcml_comm* c, const uint32_t* const* idx,
+                                                  const double* const* val, const uint64_t* nnz, uint64_t N,
+                                                  sparcml_op op, const sparcml_opts* opts, void* const* out,
+                                                  size_t out_bytes, void* stream) {
+  if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
+  if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
+  std::vector<const void*> v(val, val + c->P);
+  return allreduce_impl(c, idx, v.data(), nnz, N, op, opts, out, out_bytes, stream, 1);
+}
+
 sparcml_status sparcml_sparse_allreduce(sparcml_comm* c, const uint32_t* idx, const float* val, uint64_t nnz,
                                         uint64_t N, sparcml_op op, const sparcml_opts* opts, void* out,
                                         size_t out_bytes, void* stream) {
   if (c && c->local) return fail(c, SPARCML_ERR_STATE, "use sparcml_sparse_allreduce_local on a loopback world");
-  return allreduce_impl(c, &idx, &val, &nnz, N, op, opts, &out, out_bytes, stream);
+  const void* v = val;
+  return allreduce_impl(c, &idx, &v, &nnz, N, op, opts, &out, out_bytes, stream);
 }
 
 sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
@@ -847,7 +895,8 @@ sparcml_status sparcml_sparse_allreduce_local(sparcml_comm* c, const uint32_t* c
                                               void* stream) {
   if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
   if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
-  return allreduce_impl(c, idx, val, nnz, N, op, opts, out, out_bytes, stream);
+  std::vector<const void*> v(val, val + c->P);
+  return allreduce_impl(c, idx, v.data(), nnz, N, op, opts, out, out_bytes, stream);
 }
 
 sparcml_status sparcml_sparse_allgather(sparcml_comm* c, const uint32_t* idx, const float* val, uint64_t nnz,

@@ -287,6 +287,29 @@ __device__ __forceinline__ float op_combine(int op, float a, float b) {
 __device__ __forceinline__ float op_neutral(int op) {
   return op == 0 ? 0.0f : (op == 1 ? -__int_as_float(0x7f800000) : __int_as_float(0x7f800000));
 }
+// fp64 values ("single or double precision"): one rounding per combine
+__device__ __forceinline__ double op_combine(int op, double a, double b) {
+  return op == 0 ? __dadd_rn(a, b) : (op == 1 ? fmax(a, b) : fmin(a, b));
+}
+template <typename V>
+__device__ __forceinline__ V op_neutral_v(int op) { return (V)op_neutral(op); }   // 0, -inf, +inf exact
+
+// four consecutive values to d (16-byte vector stores when aligned)
+__device__ __forceinline__ void store4(float* d, const float r[4], int n) {
+  if (n == 4 && (reinterpret_cast<uintptr_t>(d) & 15u) == 0) {
+    *reinterpret_cast<float4*>(d) = make_float4(r[0], r[1], r[2], r[3]);
+  } else {
+    for (int i = 0; i < 4 && i < n; ++i) d[i] = r[i];
+  }
+}
+__device__ __forceinline__ void store4(double* d, const double r[4], int n) {
+  if (n == 4 && (reinterpret_cast<uintptr_t>(d) & 15u) == 0) {
+    reinterpret_cast<double2*>(d)[0] = make_double2(r[0], r[1]);
+    reinterpret_cast<double2*>(d)[1] = make_double2(r[2], r[3]);
+  } else {
+    for (int i = 0; i < 4 && i < n; ++i) d[i] = r[i];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // warp-cooperative searches (32 probes per step)

@@ -20,7 +20,7 @@ struct MergeJob {
   const float* b_val;
   const uint64_t* b_n_dev;
   uint64_t b_n;
-  MergeOutput out;
+  MergeOutput<float> out;
 };
 
 struct MergeJobsArgs {   // stand-alone sparcml_merge_sum
@@ -41,7 +41,7 @@ struct StreamBuf {
 // Stage-1 push: my input -> stage-1 partner's receive buffer [par][1] (+ flag).
 struct RdPushArgs {
   const uint32_t* idx;
-  const float* val;
+  const void* val;           // float or double (f64)
   uint64_t n;
   StreamBuf dst[2];          // by call parity
   Ctrl* peer;                // the stage-1 partner's control block (or my fold partner's)
@@ -49,12 +49,13 @@ struct RdPushArgs {
   uint64_t N;
   int validate;
   int tgt;                   // receiving stage: 1, or 0 = fold into rank i (R-28)
+  int f64;                   // values are double
 };
 
 struct RdStageArgs {
   // own stream (stage 1: the caller's input)
   const uint32_t* a_idx;
-  const float* a_val;
+  const void* a_val;
   uint64_t a_n;              // stage 1 only
   int a_from_cur;            // stages > 1: my cur[(t-1)%2]
   StreamBuf cur[2];          // my cur buffers
@@ -74,6 +75,7 @@ struct RdStageArgs {
   sparcml_header* hdr;       // last stage only
   ScanCounters* ctr;
   TileStatus* status;
+  int f64;
 };
 
 // Extra rank of a folded RD (R-28): wait for the result my fold partner
@@ -84,22 +86,24 @@ struct RdUnfoldArgs {
   Ctrl* ctl;
   char* out;
   uint64_t N, val_offset;
+  int f64;
 };
 
 // ---------------------------------------------------------- split phase ---
 struct PushArgs {
   const uint32_t* idx;
-  const float* val;
+  const void* val;
   uint64_t n;
   uint64_t N;
   int P, rank;
   uint64_t bnd[kMaxRanks + 1];
   uint32_t* dst_idx[kMaxRanks];    // owner j's receive region for source `rank`
-  float* dst_val[kMaxRanks];
+  void* dst_val[kMaxRanks];
   uint32_t* dst_win[kMaxRanks];    // owner j's window-offset table for source `rank` (ntab_j + 1)
   Ctrl* peer[kMaxRanks];           // every rank's control block
   Ctrl* ctl;                       // mine
   int validate;
+  int f64;
 };
 
 struct OwnerArgs {
@@ -108,14 +112,14 @@ struct OwnerArgs {
   uint64_t delta;
   uint64_t lo, hi;                 // my partition
   const uint32_t* src_idx[kMaxRanks];
-  const float* src_val[kMaxRanks];
+  const void* src_val[kMaxRanks];
   const uint32_t* src_win[kMaxRanks];
   TreeSched sched;
   // SSAR: compacted partition result
   uint32_t* r_idx;
-  float* r_val;
-  // DSAR: dense partition or QSGD codes + scales
-  float* dense;
+  void* r_val;
+  // DSAR: dense partition or QSGD codes + scales (fp32 only)
+  void* dense;
   uint8_t* codes;
   float* scales;
   int bits;
@@ -130,8 +134,9 @@ struct OwnerArgs {
   // SSAR merge path: spill area for dense block ranges (P * cap_s pairs, SoA)
   // and per-block output counts
   uint32_t* st_idx;
-  float* st_val;
+  void* st_val;
   uint64_t* blk;
+  int f64;
 };
 
 struct ConcatArgs {
@@ -140,11 +145,11 @@ struct ConcatArgs {
   uint64_t bnd[kMaxRanks + 1];
   // owner j's partition result (peer pointers)
   const uint32_t* r_idx[kMaxRanks];
-  const float* r_val[kMaxRanks];
+  const void* r_val[kMaxRanks];
   const uint64_t* r_n[kMaxRanks];
   const uint8_t* r_codes[kMaxRanks];
   const float* r_scales[kMaxRanks];
-  const float* r_dense[kMaxRanks];
+  const void* r_dense[kMaxRanks];
   Ctrl* ctl;                       // mine (dsar, k_sum, slice counts, owner flags, status)
   int wait_owners;                 // 1: wait for owner_done flags (P > 1)
   int bits;
@@ -155,6 +160,7 @@ struct ConcatArgs {
   TileStatus* status;
   int host_dsar;                   // -1: launch both concat variants (the device decides), else 0/1
   int op;                          // reduction operator (R-30): neutral fill when densifying
+  int f64;
 };
 
 struct BarrierArgs {
@@ -166,7 +172,7 @@ struct BarrierArgs {
 
 struct P1PrepArgs {                 // P == 1: validate, fill the control block, (DSAR) window table
   const uint32_t* idx;
-  const float* val;
+  const void* val;
   uint64_t n, N, delta;
   int algo;
   Ctrl* ctl;
@@ -177,6 +183,7 @@ struct P1PrepArgs {                 // P == 1: validate, fill the control block,
   uint64_t val_offset;
   uint32_t algo_used;
   int copy;                         // 0: the input already is out's payload (in place)
+  int f64;
 };
 
 // ------------------------------------------------------ sparse allgather --

@@ -78,14 +78,15 @@ __device__ __forceinline__ uint32_t next_ticket(ScanCounters* c, uint32_t* s_tic
 
 __device__ __forceinline__ void write_header(sparcml_header* h, uint32_t repr, uint64_t nnz, uint64_t N,
                                              uint64_t ksum, uint64_t sent, uint64_t recv, uint32_t algo,
-                                             uint32_t status_bits, uint64_t val_offset) {
+                                             uint32_t status_bits, uint64_t val_offset,
+                                             uint32_t magic = SPARCML_HEADER_MAGIC) {
   uint32_t st = 0;
   for (uint32_t b = 1; b < 32; ++b)
     if (status_bits & (1u << b)) {
       st = b;
       break;
     }
-  h->magic = SPARCML_HEADER_MAGIC;
+  h->magic = magic;
   h->repr = repr;
   h->nnz = nnz;
   h->N = N;
@@ -97,10 +98,40 @@ __device__ __forceinline__ void write_header(sparcml_header* h, uint32_t repr, u
   h->val_offset = val_offset;
 }
 
+template <typename V>
 __device__ __forceinline__ void check_input(const uint32_t* idx, uint64_t e, uint64_t n, uint64_t N, uint32_t x,
-                                            float v, uint32_t* status) {
+                                            V v, uint32_t* status) {
   if (x >= N || (e + 1 < n && idx[e + 1] <= x)) atomicOr(status, 1u << SPARCML_ERR_UNSORTED);
   if (!isfinite(v)) atomicOr(status, 1u << SPARCML_ERR_NONFINITE);
+}
+
+// value type traits: header magic, bytes of a (u32, value) pair and of a dense word
+template <typename V>
+__host__ __device__ constexpr uint32_t hdr_magic() {
+  return sizeof(V) == 8 ? SPARCML_HEADER_MAGIC_F64 : SPARCML_HEADER_MAGIC;
+}
+template <typename V>
+__host__ __device__ constexpr uint64_t pair_bytes() { return 4 + sizeof(V); }
+
+// four consecutive values from src (cnt of them valid; 16-byte loads when aligned)
+__device__ __forceinline__ void load4(const float* src, int cnt, float v[4]) {
+  if (cnt == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    const float4 q = *reinterpret_cast<const float4*>(src);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = i < cnt ? src[i] : 0.0f;
+  }
+}
+__device__ __forceinline__ void load4(const double* src, int cnt, double v[4]) {
+  if (cnt == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    const double2 q0 = reinterpret_cast<const double2*>(src)[0];
+    const double2 q1 = reinterpret_cast<const double2*>(src)[1];
+    v[0] = q0.x; v[1] = q0.y; v[2] = q1.x; v[3] = q1.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = i < cnt ? src[i] : 0.0;
+  }
 }
 
 // ===========================================================================
@@ -108,7 +139,7 @@ __device__ __forceinline__ void check_input(const uint32_t* idx, uint64_t e, uin
 // ===========================================================================
 __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem);
+  MergeSmem<float>& sm = *reinterpret_cast<MergeSmem<float>*>(smem);
   __shared__ uint64_t s_na[kMaxJobs], s_nb[kMaxJobs];
   __shared__ uint32_t s_base[kMaxJobs + 1];
   __shared__ uint32_t s_ticket, s_gen;
@@ -127,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
   }
   __syncthreads();
   if (blockIdx.x == 0 && tid < a.njobs && s_na[tid] + s_nb[tid] == 0) {
-    const MergeOutput& o = a.job[tid].out;
+    const MergeOutput<float>& o = a.job[tid].out;
     if (o.n) *o.n = 0;
     if (o.n2) *o.n2 = 0;
   }
@@ -146,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
 
 cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t s) {
   static bool attr = false;
-  const size_t smem = sizeof(MergeSmem);
+  const size_t smem = sizeof(MergeSmem<float>);
   if (!attr) {
     cudaFuncSetAttribute(merge_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
@@ -162,15 +193,17 @@ cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t
 // ===========================================================================
 // recursive doubling (§5.3.1): push of the input, one kernel per stage
 // ===========================================================================
+template <typename V>
 __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
   const uint32_t seq = a.ctl->seq;
   const int par = seq & 1;
   uint32_t* di = reinterpret_cast<uint32_t*>(a.dst[par].base);
-  float* dv = reinterpret_cast<float*>(a.dst[par].base + a.dst[par].val_off);
+  V* dv = reinterpret_cast<V*>(a.dst[par].base + a.dst[par].val_off);
+  const V* sv = static_cast<const V*>(a.val);
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride) {
     const uint32_t x = a.idx[e];
-    const float v = a.val[e];
+    const V v = sv[e];
     di[e] = x;
     dv[e] = v;
     if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
@@ -179,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
     a.peer->rd_n[par][a.tgt] = a.n;
     a.peer->rd_dense[par][a.tgt] = 0;
     a.peer->rd_ksum[par][a.tgt] = a.n;
-    a.ctl->rd_sent[0] = 8 * a.n;
+    a.ctl->rd_sent[0] = pair_bytes<V>() * a.n;
     st_release_sys(&a.peer->rd_flag[par][a.tgt], seq + 1);
   }
 }
@@ -188,15 +221,17 @@ cudaError_t launch_rd_push(const RdPushArgs& a, cudaStream_t s) {
   const uint64_t blocks =
       std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, (uint64_t)device_sm_count() * 8));
   SPARCML_PROF("rd_push", s);
-  rd_push_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  if (a.f64) rd_push_kernel<double><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  else rd_push_kernel<float><<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t s_ticket, s_gen;
-  __shared__ WinSource s_src[2];
+  __shared__ WinSource<V> s_src[2];
   const int tid = threadIdx.x;
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
@@ -205,7 +240,8 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   __syncthreads();
   const int cp = (t - 1) & 1;   // cur buffer holding my stage t-1 output
   const uint32_t* a_idx = a.a_from_cur ? reinterpret_cast<const uint32_t*>(a.cur[cp].base) : a.a_idx;
-  const float* a_val = a.a_from_cur ? reinterpret_cast<const float*>(a.cur[cp].base + a.cur[cp].val_off) : a.a_val;
+  const V* a_val = a.a_from_cur ? reinterpret_cast<const V*>(a.cur[cp].base + a.cur[cp].val_off)
+                                : static_cast<const V*>(a.a_val);
   const uint64_t an = a.a_from_cur ? *(volatile uint64_t*)&ctl->own_n[cp] : a.a_n;
   const uint32_t ad = a.a_from_cur ? *(volatile uint32_t*)&ctl->own_dense[cp] : 0u;
   const uint64_t aks = a.a_from_cur ? *(volatile uint64_t*)&ctl->own_ksum[cp] : a.a_n;
@@ -219,16 +255,16 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   const bool sparse_out = !ad && !bd && (an + bn <= a.delta);
   if (tid == 0) s_gen = a.ctr->gen;
   const uint32_t* b_idx = reinterpret_cast<const uint32_t*>(b.base);
-  const float* b_val = reinterpret_cast<const float*>(b.base + b.val_off);
+  const V* b_val = reinterpret_cast<const V*>(b.base + b.val_off);
   if (sparse_out) {
-    MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem);
-    MergeOutput mo;
+    MergeSmem<V>& sm = *reinterpret_cast<MergeSmem<V>*>(smem);
+    MergeOutput<V> mo;
     mo.op = a.op;
     mo.idx = reinterpret_cast<uint32_t*>(o.base);
-    mo.val = reinterpret_cast<float*>(o.base + o.val_off);
+    mo.val = reinterpret_cast<V*>(o.base + o.val_off);
     mo.n = &ctl->own_n[t & 1];
     mo.idx2 = m.base ? reinterpret_cast<uint32_t*>(m.base) : nullptr;
-    mo.val2 = m.base ? reinterpret_cast<float*>(m.base + m.val_off) : nullptr;
+    mo.val2 = m.base ? reinterpret_cast<V*>(m.base + m.val_off) : nullptr;
     mo.n2 = nullptr;
     __syncthreads();
     const uint32_t total = (uint32_t)ceil_div(an + bn, kMergeTile);
@@ -242,12 +278,12 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     // densify: window over [0, N) with the two streams (sparse or dense)
     if (tid == 0) {
       s_src[0].idx = a_idx;
-      s_src[0].val = ad ? reinterpret_cast<const float*>(a_idx) : a_val;
+      s_src[0].val = ad ? reinterpret_cast<const V*>(a_idx) : a_val;
       s_src[0].n = an;
       s_src[0].dense = (int)ad;
       s_src[0].dense_base = 0;
       s_src[1].idx = b_idx;
-      s_src[1].val = bd ? reinterpret_cast<const float*>(b.base) : b_val;
+      s_src[1].val = bd ? reinterpret_cast<const V*>(b.base) : b_val;
       s_src[1].n = bn;
       s_src[1].dense = (int)bd;
       s_src[1].dense_base = 0;
@@ -257,11 +293,11 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     ts.n = 1;
     ts.dst[0] = 0;
     ts.src[0] = 1;
-    WinOutput wo = {};
+    WinOutput<V> wo = {};
     wo.mode = WIN_DENSE;
     wo.op = a.op;
-    wo.dense = reinterpret_cast<float*>(o.base);
-    wo.dense2 = m.base ? reinterpret_cast<float*>(m.base) : nullptr;
+    wo.dense = reinterpret_cast<V*>(o.base);
+    wo.dense2 = m.base ? reinterpret_cast<V*>(m.base) : nullptr;
     wo.dense_base = 0;
     const uint32_t nwin = (uint32_t)ceil_div(a.N, kWin);
     while (true) {
@@ -279,8 +315,8 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     fence_acq_rel_gpu();
     const uint64_t on = sparse_out ? *(volatile uint64_t*)&ctl->own_n[t & 1] : a.N;
     const uint64_t ksum = aks + bks;
-    const uint64_t obytes = sparse_out ? 8 * on : 4 * a.N;
-    const uint64_t bbytes = bd ? 4 * a.N : 8 * bn;
+    const uint64_t obytes = sparse_out ? pair_bytes<V>() * on : sizeof(V) * a.N;
+    const uint64_t bbytes = bd ? sizeof(V) * a.N : pair_bytes<V>() * bn;
     ctl->own_n[t & 1] = on;
     ctl->own_dense[t & 1] = sparse_out ? 0u : 1u;
     ctl->own_ksum[t & 1] = ksum;
@@ -305,7 +341,8 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
       }
       write_header(a.hdr, sparse_out ? SPARCML_REPR_SPARSE : SPARCML_REPR_DENSE, on, a.N, ksum, sent, recv,
                    SPARCML_SSAR_RECURSIVE_DOUBLE, ctl->status,
-                   sparse_out ? (uint64_t)((char*)o.base + o.val_off - (char*)a.hdr) : (uint64_t)SPARCML_HEADER_BYTES);
+                   sparse_out ? (uint64_t)((char*)o.base + o.val_off - (char*)a.hdr) : (uint64_t)SPARCML_HEADER_BYTES,
+                   hdr_magic<V>());
       ctl->status = 0;
       __threadfence();
       ctl->seq = seq + 1;   // the call is complete on this rank
@@ -313,6 +350,7 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   }
 }
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads) rd_unfold_kernel(RdUnfoldArgs a) {
   __shared__ uint64_t s_n;
   __shared__ uint32_t s_d;
@@ -330,14 +368,14 @@ __global__ void __launch_bounds__(kThreads) rd_unfold_kernel(RdUnfoldArgs a) {
   const StreamBuf b = a.src[par];
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   if (dense) {
-    const float* src = reinterpret_cast<const float*>(b.base);
-    float* d = reinterpret_cast<float*>(a.out + SPARCML_HEADER_BYTES);
+    const V* src = reinterpret_cast<const V*>(b.base);
+    V* d = reinterpret_cast<V*>(a.out + SPARCML_HEADER_BYTES);
     for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.N; e += stride) d[e] = __ldcg(&src[e]);
   } else {
     const uint32_t* si = reinterpret_cast<const uint32_t*>(b.base);
-    const float* sv = reinterpret_cast<const float*>(b.base + b.val_off);
+    const V* sv = reinterpret_cast<const V*>(b.base + b.val_off);
     uint32_t* oi = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
-    float* ov = reinterpret_cast<float*>(a.out + a.val_offset);
+    V* ov = reinterpret_cast<V*>(a.out + a.val_offset);
     for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) {
       oi[e] = __ldcg(&si[e]);
       ov[e] = __ldcg(&sv[e]);
@@ -346,8 +384,9 @@ __global__ void __launch_bounds__(kThreads) rd_unfold_kernel(RdUnfoldArgs a) {
   if (last_block<false>(&ctl->done_ctr[1]) && threadIdx.x == 0) {
     const uint64_t ksum = *(volatile uint64_t*)&ctl->rd_ksum[par][t];
     write_header(reinterpret_cast<sparcml_header*>(a.out), dense ? SPARCML_REPR_DENSE : SPARCML_REPR_SPARSE,
-                 dense ? a.N : n, a.N, ksum, ctl->rd_sent[0], dense ? 4 * a.N : 8 * n, SPARCML_SSAR_RECURSIVE_DOUBLE,
-                 ctl->status, dense ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset);
+                 dense ? a.N : n, a.N, ksum, ctl->rd_sent[0], dense ? sizeof(V) * a.N : pair_bytes<V>() * n,
+                 SPARCML_SSAR_RECURSIVE_DOUBLE, ctl->status, dense ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset,
+                 hdr_magic<V>());
     ctl->status = 0;
     __threadfence();
     ctl->seq = seq + 1;   // the call is complete on this rank
@@ -356,21 +395,28 @@ __global__ void __launch_bounds__(kThreads) rd_unfold_kernel(RdUnfoldArgs a) {
 
 cudaError_t launch_rd_unfold(const RdUnfoldArgs& a, cudaStream_t s) {
   SPARCML_PROF("rd_unfold", s);
-  rd_unfold_kernel<<<device_sm_count() * 2, kThreads, 0, s>>>(a);
+  if (a.f64) rd_unfold_kernel<double><<<device_sm_count() * 2, kThreads, 0, s>>>(a);
+  else rd_unfold_kernel<float><<<device_sm_count() * 2, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
 
-cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
+template <typename V>
+static size_t rd_stage_smem() {
   static bool attr = false;
-  const size_t smem = std::max(sizeof(MergeSmem), win_smem_bytes(2));
+  const size_t smem = std::max(sizeof(MergeSmem<V>), win_smem_bytes(2, sizeof(V)));
   if (!attr) {
-    cudaFuncSetAttribute(rd_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(rd_stage_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  return smem;
+}
+
+cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
   const int grid = device_sm_count() * 4;
   SPARCML_PROF("rd_stage", s);
-  rd_stage_kernel<<<grid, kThreads, smem, s>>>(a);
+  if (a.f64) rd_stage_kernel<double><<<grid, kThreads, rd_stage_smem<double>(), s>>>(a);
+  else rd_stage_kernel<float><<<grid, kThreads, rd_stage_smem<float>(), s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -381,6 +427,7 @@ cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
 // ===========================================================================
 constexpr int kPushItems = 4;
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
   __shared__ uint64_t s_off[kMaxRanks + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -410,11 +457,11 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
     const uint64_t e = base + (uint64_t)i * kThreads + tid;
     if (e < a.n) {
       const uint32_t x = a.idx[e];
-      const float v = a.val[e];
+      const V v = static_cast<const V*>(a.val)[e];
       const int j = (int)std::min<uint64_t>(x / part, a.P - 1);
       const uint64_t p = e - s_off[j];
       a.dst_idx[j][p] = x;
-      a.dst_val[j][p] = v;
+      static_cast<V*>(a.dst_val[j])[p] = v;
       // window-offset table (kTab positions per entry): win[w] = first slice
     // position whose table window >= w
       const uint64_t lo = a.bnd[j];
@@ -457,7 +504,8 @@ cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s) {
   const uint64_t per = (uint64_t)kThreads * kPushItems;
   const uint64_t blocks = std::max<uint64_t>(1, (a.n + per - 1) / per);
   SPARCML_PROF("split_push", s);
-  split_push_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  if (a.f64) split_push_kernel<double><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  else split_push_kernel<float><<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -478,7 +526,9 @@ constexpr int kMT = 512;                  // merge tile capacity beyond one tabl
 constexpr uint32_t kDead = 0xFFFFFFFFu;   // never an index: N <= 2^32 - 1
 
 __host__ __device__ constexpr int mtile_cap(int P) { return kMT + kTab * P; }
-__host__ __device__ constexpr size_t owner_merge_smem_bytes(int P) { return 16 * (size_t)mtile_cap(P); }
+__host__ __device__ constexpr size_t owner_merge_smem_bytes(int P, size_t vbytes = 4) {
+  return (8 + 2 * vbytes) * (size_t)mtile_cap(P);   // xk, yk (u32) and xv, yv (values)
+}
 
 
 __device__ __forceinline__ uint32_t sm_lower_bound(const uint32_t* k, uint32_t n, uint32_t x) {
@@ -589,9 +639,9 @@ __device__ __forceinline__ void runs_prefix(MergeShared<P>& m, uint32_t len) {
 // most cap of them; s_c holds table entries, row = window, column = source).
 // The result (sorted, unique, canonical-tree sums) is left in xk/xv, or, if
 // oi != nullptr, written to oi/ov.  Returns its length.
-template <int P>
+template <int P, typename V>
 __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const uint32_t* s_c, int w0, int w1,
-                                   uint32_t* oi, float* ov_out, uint32_t* xk, float* xv, uint32_t* yk, float* yv) {
+                                   uint32_t* oi, V* ov_out, uint32_t* xk, V* xv, uint32_t* yk, V* yv) {
   constexpr int cap = mtile_cap(P);
   constexpr uint32_t kTop = pow2_floor(cap);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -611,7 +661,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
   {
     constexpr int Q = (cap + kThreads - 1) / kThreads;
     uint32_t kk[Q];
-    float vv[Q];
+    V vv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const uint32_t u = q * kThreads + tid;
@@ -621,7 +671,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
         for (int j = 1; j < P; ++j) s += m.off[j] <= u ? 1 : 0;
         const uint32_t e = m.ta[s] + (u - m.off[s]);
         kk[q] = __ldcg(&a.src_idx[s][e]);
-        vv[q] = __ldcg(&a.src_val[s][e]);
+        vv[q] = __ldcg(&static_cast<const V*>(a.src_val[s])[e]);
       }
     }
 #pragma unroll
@@ -646,7 +696,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
     for (uint32_t b0 = 0; b0 < n; b0 += 2 * kThreads) {
       constexpr int Q = 2;
       uint32_t key[Q], rank[Q], qoff[Q], qlen[Q], pos0[Q];
-      float v[Q];
+      V v[Q];
       int role[Q], part[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
@@ -656,7 +706,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
         for (int j = 1; j < P; ++j) s += off[j] <= u ? 1 : 0;
         const bool in = u < n;
         key[q] = in ? xk[u] : 0u;
-        v[q] = in ? xv[u] : 0.0f;
+        v[q] = in ? xv[u] : V(0);
         role[q] = in ? (int)role_h[s] : -1;
         const int pq = part_h[s];
         part[q] = pq;
@@ -671,7 +721,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
       for (int q = 0; q < Q; ++q) {
         if (role[q] < 0) continue;
         uint32_t k = key[q];
-        float val = v[q];
+        V val = v[q];
         const uint32_t pos = pos0[q] + rank[q];
         if (role[q] == 1) {   // left run (lower ranks): first on ties, fl(left + right)
           if (rank[q] < qlen[q] && xk[qoff[q] + rank[q]] == k) val = op_combine(a.op, val, xv[qoff[q] + rank[q]]);
@@ -711,7 +761,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
     uint32_t base = 0;
     for (int w = 0; w < warp; ++w) base += m.wtot[w];
     uint32_t* ok = last && oi ? oi : xk;
-    float* ov = last && oi ? ov_out : xv;
+    V* ov = last && oi ? ov_out : xv;
     for (uint32_t u = u0 + lane; u < u0 + seg; u += 32) {
       const uint32_t key = u < u1 ? yk[u] : kDead;
       const bool alive = key != kDead;
@@ -739,14 +789,16 @@ constexpr int kTabSmem = 2048;   // table entries staged per chunk (general path
 // staging area at the range's input offset.  After one grid sync every block
 // knows its output offset (sum of the block counts before it) and writes its
 // result contiguously; the last block to finish flags the P sources.
-template <int P>
+template <int P, typename V>
 __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int cap = mtile_cap(P);
   uint32_t* xk = reinterpret_cast<uint32_t*>(smem);
-  float* xv = reinterpret_cast<float*>(xk + cap);
-  uint32_t* yk = reinterpret_cast<uint32_t*>(xv + cap);
-  float* yv = reinterpret_cast<float*>(yk + cap);
+  uint32_t* yk = xk + cap;
+  V* xv = reinterpret_cast<V*>(yk + cap);   // 8-byte aligned: cap is even
+  V* yv = xv + cap;
+  V* const st_val = static_cast<V*>(a.st_val);
+  V* const r_val = static_cast<V*>(a.r_val);
   __shared__ MergeShared<P> m;
   __shared__ uint64_t s_ks[kMaxRanks], s_sc[kMaxRanks];
   __shared__ uint32_t s_c[kTabSmem];                 // table entries of the current chunk
@@ -785,7 +837,7 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
     }
     dbg_mark(ctl, 2);
     if (tot <= (uint32_t)cap) {
-      cnt = merge_subrange<P>(a, m, s_c, 0, 1, nullptr, nullptr, xk, xv, yk, yv);
+      cnt = merge_subrange<P, V>(a, m, s_c, 0, 1, nullptr, nullptr, xk, xv, yk, yv);
     } else {
       in_smem = false;
       const uint32_t wchunk = kTabSmem / P - 1;   // windows per chunk
@@ -808,8 +860,8 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
           uint32_t tsum;
           const uint32_t incl = block_exclusive_sum<uint32_t>(c, s_scan, &tsum) + c;
           const int take = __syncthreads_count(w < nw && incl <= (uint32_t)cap);
-          cnt += merge_subrange<P>(a, m, s_c, pos, pos + take, a.st_idx + ibase + cnt, a.st_val + ibase + cnt, xk,
-                                   xv, yk, yv);
+          cnt += merge_subrange<P, V>(a, m, s_c, pos, pos + take, a.st_idx + ibase + cnt, st_val + ibase + cnt, xk,
+                                      xv, yk, yv);
           pos += take;
         }
       }
@@ -834,12 +886,12 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
   if (in_smem) {
     for (uint32_t i = tid; i < cnt; i += kThreads) {
       a.r_idx[excl + i] = xk[i];
-      a.r_val[excl + i] = xv[i];
+      r_val[excl + i] = xv[i];
     }
   } else {
     for (uint32_t i = tid; i < cnt; i += kThreads) {
       a.r_idx[excl + i] = __ldcg(&a.st_idx[ibase + i]);
-      a.r_val[excl + i] = __ldcg(&a.st_val[ibase + i]);
+      r_val[excl + i] = __ldcg(&st_val[ibase + i]);
     }
   }
   dbg_mark(ctl, 5);
@@ -864,13 +916,16 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
 // max from a block reduction).  Every output lands at a fixed offset: no
 // prefix, no grid-wide sync; the last block to finish flags the P readers.
 // ===========================================================================
-__host__ __device__ constexpr size_t dsar_smem_bytes(int P) { return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)P; }
+__host__ __device__ constexpr size_t dsar_smem_bytes(int P, size_t vbytes = 4) {
+  return sizeof(uint32_t) * kWin + vbytes * kWin * (size_t)P;
+}
 
-template <int P>
+template <int P, typename V>
 __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
-  float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
+  V* vals = reinterpret_cast<V*>(smem + sizeof(uint32_t) * kWin);
+  V* const dense = static_cast<V*>(a.dense);
   __shared__ uint64_t s_ks[kMaxRanks];
   __shared__ uint32_t s_dsar, s_bmax[kWin / 8];
   __shared__ uint32_t s_e0[P], s_pre[P + 1];
@@ -911,7 +966,7 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
     const uint32_t tot = s_pre[P];
     for (uint32_t b0 = 0; b0 < tot; b0 += 4 * kThreads) {
       uint32_t xi[4];
-      float xv[4];
+      V xv[4];
       int xs[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -923,7 +978,7 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
           for (int j = 1; j < P; ++j) s += s_pre[j] <= u ? 1 : 0;
           const uint32_t e = s_e0[s] + (u - s_pre[s]);
           xi[q] = __ldcg(&a.src_idx[s][e]);
-          xv[q] = __ldcg(&a.src_val[s][e]);
+          xv[q] = __ldcg(&static_cast<const V*>(a.src_val[s])[e]);
           xs[q] = s;
         }
       }
@@ -938,7 +993,7 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
     __syncthreads();
     // (3) combine per position in the canonical tree order
     const int p0 = tid * kWinPerThread;
-    float r[kWinPerThread];
+    V r[kWinPerThread];
 #pragma unroll
     for (int q = 0; q < kWinPerThread; ++q) {
       const int p = p0 + q;
@@ -956,21 +1011,22 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
         }
         r[q] = vals[p];
       } else {
-        r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : op_neutral(a.op);
+        r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : op_neutral_v<V>(a.op);
       }
     }
     // (4) store: QSGD codes + scales, or dense
     const uint64_t e = w * kWin + p0;   // partition-relative
-    if (a.bits) {
-      const int rem = wn - p0;
-      const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
-      qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax,
-                        a.qnorm);
-    } else if (p0 + 4 <= wn) {
-      reinterpret_cast<float4*>(a.dense + e)[0] = make_float4(r[0], r[1], r[2], r[3]);
-    } else {
-      for (int q = 0; q < kWinPerThread && p0 + q < wn; ++q) a.dense[e + q] = r[q];
+    bool coded = false;
+    if constexpr (sizeof(V) == sizeof(float)) {   // QSGD is defined on fp32 values (the host rejects f64)
+      if (a.bits) {
+        const int rem = wn - p0;
+        const int valid = rem < 0 ? 0 : (rem > 4 ? 4 : rem);
+        qsgd_block_encode(r, valid, e, wlo + p0, a.bits, a.bucket, a.seed_lo, a.seed_hi, a.codes, a.scales, s_bmax,
+                          a.qnorm);
+        coded = true;
+      }
     }
+    if (!coded && p0 < wn) store4(dense + e, r, wn - p0);
     c0 = n0;
     c1 = n1;
     __syncthreads();   // vals / pres / s_pre reused by the next window
@@ -979,70 +1035,74 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
 }
 
 using DsarFn = void (*)(OwnerArgs);
-template <int... Ps>
+template <typename V, int... Ps>
 struct DsarTable {
   static DsarFn get(int P) {
     DsarFn f = nullptr;
-    ((P == Ps ? (f = dsar_owner_kernel<Ps>, 0) : 0), ...);
+    ((P == Ps ? (f = dsar_owner_kernel<Ps, V>, 0) : 0), ...);
     return f;
   }
 };
-static DsarFn dsar_fn(int P) { return DsarTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P); }
+static DsarFn dsar_fn(int P, bool f64) {
+  return f64 ? DsarTable<double, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P)
+             : DsarTable<float, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P);
+}
 
 using OwnerMergeFn = void (*)(OwnerArgs);
-template <int... Ps>
+template <typename V, int... Ps>
 struct OwnerMergeTable {
   static OwnerMergeFn get(int P) {
     OwnerMergeFn f = nullptr;
-    ((P == Ps ? (f = owner_merge_kernel<Ps>, 0) : 0), ...);
+    ((P == Ps ? (f = owner_merge_kernel<Ps, V>, 0) : 0), ...);
     return f;
   }
 };
-static OwnerMergeFn owner_merge_fn(int P) {
-  return OwnerMergeTable<1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P);
+static OwnerMergeFn owner_merge_fn(int P, bool f64) {
+  return f64 ? OwnerMergeTable<double, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P)
+             : OwnerMergeTable<float, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P);
 }
 
-static int owner_merge_occupancy(int P) {
-  static int cache[kMaxRanks + 1] = {0};
-  if (!cache[P]) {
-    const OwnerMergeFn f = owner_merge_fn(P);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)owner_merge_smem_bytes(P));
+static int owner_merge_occupancy(int P, bool f64) {
+  static int cache[2][kMaxRanks + 1] = {{0}};
+  if (!cache[f64][P]) {
+    const OwnerMergeFn f = owner_merge_fn(P, f64);
+    const size_t smem = owner_merge_smem_bytes(P, f64 ? 8 : 4);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kThreads, owner_merge_smem_bytes(P));
-    cache[P] = std::max(1, per);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kThreads, smem);
+    cache[f64][P] = std::max(1, per);
   }
-  return cache[P];
+  return cache[f64][P];
 }
 
 cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
+  const bool f64 = a.f64 != 0;
+  const size_t vb = f64 ? 8 : 4;
   if (a.host_dsar != 1) {   // SSAR (or undecided: the kernel exits if the device picks DSAR)
-    const uint64_t G = (uint64_t)owner_merge_occupancy(a.P) * device_sm_count();
+    const uint64_t G = (uint64_t)owner_merge_occupancy(a.P, f64) * device_sm_count();
     OwnerArgs ac = a;
     void* args[] = {(void*)&ac};
     SPARCML_PROF("owner", s);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_merge_fn(a.P), dim3((unsigned)G), dim3(kThreads),
-                                                args, owner_merge_smem_bytes(a.P), s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_merge_fn(a.P, f64), dim3((unsigned)G),
+                                                dim3(kThreads), args, owner_merge_smem_bytes(a.P, vb), s);
     ++g_launches;
     if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (a.host_dsar != 0) {   // DSAR (or undecided: the kernel exits if the device picks SSAR)
-    const DsarFn f = dsar_fn(a.P);
-    static bool dattr[kMaxRanks + 1] = {false};
-    if (!dattr[a.P]) {
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsar_smem_bytes(a.P));
-      dattr[a.P] = true;
-    }
-    static int occ[kMaxRanks + 1] = {0};
-    if (!occ[a.P]) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.P], f, kThreads, dsar_smem_bytes(a.P));
-      occ[a.P] = std::max(1, occ[a.P]);
+    const DsarFn f = dsar_fn(a.P, f64);
+    const size_t smem = dsar_smem_bytes(a.P, vb);
+    static int occ[2][kMaxRanks + 1] = {{0}};
+    if (!occ[f64][a.P]) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[f64][a.P], f, kThreads, smem);
+      occ[f64][a.P] = std::max(1, occ[f64][a.P]);
     }
     const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
-    const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)occ[a.P] * device_sm_count()));
+    const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)occ[f64][a.P] * device_sm_count()));
     SPARCML_PROF("owner_dsar", s);
-    f<<<(unsigned)G, kThreads, dsar_smem_bytes(a.P), s>>>(a);
+    f<<<(unsigned)G, kThreads, smem, s>>>(a);
     ++g_launches;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1059,18 +1119,26 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
 // MODE 0: sparse result paths only (SSAR concat, K > delta densify); MODE 1:
 // DSAR decode only.  Each instantiation returns at once unless the device's
 // SSAR/DSAR decision is its case (separate register budgets).
-template <int MODE>
+template <int MODE, typename V>
 __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint64_t s_pref[kMaxRanks + 1];
   __shared__ uint64_t s_upref[kMaxRanks + 1];
   __shared__ uint32_t s_dsar;
-  __shared__ WinSource s_src[1];
+  __shared__ WinSource<V> s_src[1];
   const int tid = threadIdx.x;
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
   __shared__ uint64_t s_k[kMaxRanks];
   dbg_mark(ctl, 12);
+  // SSAR or DSAR: decided by this rank's own owner kernel earlier on this
+  // stream.  The variant that is not the case returns before anything else:
+  // when both are launched (host_dsar == -1) the one running second must not
+  // wait for owner flags of a call the first has already completed (seq + 1).
+  if (tid == 0) s_dsar = *(volatile uint32_t*)&ctl->dsar;
+  __syncthreads();
+  const bool dsar = s_dsar != 0;
+  if (dsar != (MODE == 1)) return;
   if (tid < a.P) {   // one lane per owner: wait for its flag, read its result size
     if (a.wait_owners) {
       wait_flag_geq(&ctl->owner_done[tid], seq + 1);
@@ -1081,7 +1149,6 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    s_dsar = *(volatile uint32_t*)&ctl->dsar;
     s_pref[0] = 0;
     s_upref[0] = 0;
     for (int j = 0; j < a.P; ++j) {
@@ -1092,12 +1159,10 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   }
   __syncthreads();
   dbg_mark(ctl, 14);
-  const bool dsar = s_dsar != 0;
-  if (dsar != (MODE == 1)) return;
   const uint64_t K = s_pref[a.P];
-  float* out_dense = reinterpret_cast<float*>(a.out + SPARCML_HEADER_BYTES);
+  V* out_dense = reinterpret_cast<V*>(a.out + SPARCML_HEADER_BYTES);
   uint32_t* out_idx = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
-  float* out_val = reinterpret_cast<float*>(a.out + a.val_offset);
+  V* out_val = reinterpret_cast<V*>(a.out + a.val_offset);
   const uint64_t gstride = (uint64_t)gridDim.x * kThreads;
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + tid;
   bool dense_result = dsar;
@@ -1124,7 +1189,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     for (uint64_t u0 = gw; u0 < nunits; u0 += nw * U) {
       uint32_t word[U];
       float scl[U];   // a lane's 4 positions share one bucket (B >= 8, 4-aligned)
-      float4 dv[U];
+      V dv[U][4];
       int jj[U], cnt[U];
       uint64_t ee[U];
 #pragma unroll
@@ -1142,7 +1207,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
         ee[x] = e;
         cnt[x] = e >= nj ? 0 : (int)((nj - e) < 4 ? (nj - e) : 4);
         if (cnt[x] == 0) continue;
-        if (a.bits) {
+        if (sizeof(V) == sizeof(float) && a.bits) {   // QSGD: fp32 only (the host rejects f64)
           const uint8_t* cp = a.r_codes[j] + (e * a.bits) / 8;
           uint32_t w;
           if (cnt[x] == 4 && a.bits == 4) w = *reinterpret_cast<const uint16_t*>(cp);
@@ -1156,20 +1221,14 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
           word[x] = w;
           scl[x] = a.r_scales[j][e >> lgB];
         } else {
-          const float* src = a.r_dense[j] + e;
-          if (cnt[x] == 4 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0)) {
-            dv[x] = *reinterpret_cast<const float4*>(src);
-          } else {
-            dv[x] = make_float4(src[0], cnt[x] > 1 ? src[1] : 0.0f, cnt[x] > 2 ? src[2] : 0.0f,
-                                cnt[x] > 3 ? src[3] : 0.0f);
-          }
+          load4(static_cast<const V*>(a.r_dense[j]) + e, cnt[x], dv[x]);
         }
       }
 #pragma unroll
       for (int x = 0; x < U; ++x) {
         if (cnt[x] == 0) continue;
-        float v[4];
-        if (a.bits) {
+        V v[4];
+        if (sizeof(V) == sizeof(float) && a.bits) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint32_t code = (word[x] >> (i * a.bits)) & mask;
@@ -1177,16 +1236,10 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
             v[i] = (code >> (a.bits - 1)) ? -mag : mag;
           }
         } else {
-          v[0] = dv[x].x; v[1] = dv[x].y; v[2] = dv[x].z; v[3] = dv[x].w;
-        }
-        float* d = out_dense + a.bnd[jj[x]] + ee[x];
-        if (cnt[x] == 4 && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
-          *reinterpret_cast<float4*>(d) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (i < cnt[x]) d[i] = v[i];
+          for (int i = 0; i < 4; ++i) v[i] = dv[x][i];
         }
+        store4(out_dense + a.bnd[jj[x]] + ee[x], v, cnt[x]);
       }
     }
   } else if (K <= a.delta) {
@@ -1196,7 +1249,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     constexpr int U = 4;   // units per thread per iteration: all their NVLink loads in flight
     for (uint64_t u0 = gtid; u0 < units; u0 += gstride * U) {
       uint4 ix[U];
-      float4 vx[U];
+      V vx[U][4];
       uint64_t oo[U];
       int cnt[U];   // pairs in the unit (4, or an owner's short last unit; 0 = none)
 #pragma unroll
@@ -1209,18 +1262,15 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
         const uint64_t p = (u - s_upref[j]) * 4;
         const uint64_t kj = s_pref[j + 1] - s_pref[j];
         oo[x] = s_pref[j] + p;
-        if (p + 4 <= kj) {
+        const int n = (int)std::min<uint64_t>(4, kj - p);
+        if (n == 4) {
           ix[x] = *reinterpret_cast<const uint4*>(a.r_idx[j] + p);
-          vx[x] = *reinterpret_cast<const float4*>(a.r_val[j] + p);
-          cnt[x] = 4;
         } else {
           const uint32_t* si = a.r_idx[j] + p;
-          const float* sv = a.r_val[j] + p;
-          const int n = (int)(kj - p);
           ix[x] = make_uint4(si[0], n > 1 ? si[1] : 0u, n > 2 ? si[2] : 0u, 0u);
-          vx[x] = make_float4(sv[0], n > 1 ? sv[1] : 0.0f, n > 2 ? sv[2] : 0.0f, 0.0f);
-          cnt[x] = n;
         }
+        load4(static_cast<const V*>(a.r_val[j]) + p, n, vx[x]);
+        cnt[x] = n;
       }
 #pragma unroll
       for (int x = 0; x < U; ++x) {
@@ -1228,18 +1278,18 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
         if (n == 0) continue;
         const uint64_t o = oo[x];
         out_idx[o] = ix[x].x;
-        out_val[o] = vx[x].x;
+        out_val[o] = vx[x][0];
         if (n > 1) {
           out_idx[o + 1] = ix[x].y;
-          out_val[o + 1] = vx[x].y;
+          out_val[o + 1] = vx[x][1];
         }
         if (n > 2) {
           out_idx[o + 2] = ix[x].z;
-          out_val[o + 2] = vx[x].z;
+          out_val[o + 2] = vx[x][2];
         }
         if (n > 3) {
           out_idx[o + 3] = ix[x].w;
-          out_val[o + 3] = vx[x].w;
+          out_val[o + 3] = vx[x][3];
         }
       }
     }
@@ -1248,7 +1298,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     dense_result = true;
     TreeSched ts;
     ts.n = 0;
-    WinOutput wo = {};
+    WinOutput<V> wo = {};
     wo.mode = WIN_DENSE;
     wo.op = a.op;
     wo.dense = out_dense;
@@ -1256,7 +1306,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     for (int j = 0; j < a.P; ++j) {
       if (tid == 0) {
         s_src[0].idx = a.r_idx[j];
-        s_src[0].val = a.r_val[j];
+        s_src[0].val = static_cast<const V*>(a.r_val[j]);
         s_src[0].n = s_pref[j + 1] - s_pref[j];
         s_src[0].dense = 0;
         s_src[0].dense_base = 0;
@@ -1274,20 +1324,20 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     uint64_t sent = 0, recv = 0;
     for (int j = 0; j < a.P; ++j) {
       if (j == a.rank) continue;
-      sent += 8 * ctl->slice_out[j];
-      recv += 8 * ctl->slice_cnt[j];
+      sent += pair_bytes<V>() * ctl->slice_out[j];
+      recv += pair_bytes<V>() * ctl->slice_cnt[j];
     }
     for (int j = 0; j < a.P; ++j) {
       uint64_t w;
       const uint64_t nj = a.bnd[j + 1] - a.bnd[j];
-      if (dsar) w = a.bits ? (nj * a.bits + 7) / 8 + 4 * ceil_div(nj, a.bucket) : 4 * nj;
-      else w = 8 * (s_pref[j + 1] - s_pref[j]);
+      if (dsar) w = a.bits ? (nj * a.bits + 7) / 8 + 4 * ceil_div(nj, a.bucket) : sizeof(V) * nj;
+      else w = pair_bytes<V>() * (s_pref[j + 1] - s_pref[j]);
       if (j == a.rank) sent += (uint64_t)(a.P - 1) * w;
       else recv += w;
     }
     write_header(reinterpret_cast<sparcml_header*>(a.out), dense_result ? SPARCML_REPR_DENSE : SPARCML_REPR_SPARSE,
                  dense_result ? a.N : K, a.N, ctl->k_sum, sent, recv, dsar ? SPARCML_DSAR_SPLIT_ALLGATHER : a.algo,
-                 ctl->status, dense_result ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset);
+                 ctl->status, dense_result ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset, hdr_magic<V>());
     ctl->status = 0;
     __threadfence();
     ctl->seq = seq + 1;   // the call is complete on this rank
@@ -1295,26 +1345,32 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   dbg_mark(ctl, 13);
 }
 
-cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
+template <typename V>
+static void launch_concat_t(const ConcatArgs& a, cudaStream_t s) {
   static bool attr = false;
-  const size_t smem = win_smem_bytes(1);
+  const size_t smem = win_smem_bytes(1, sizeof(V));
   if (!attr) {
-    cudaFuncSetAttribute(concat_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(concat_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(concat_kernel<0, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(concat_kernel<1, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   // one block per SM for the sparse concatenation (fewer flag pollers and a
   // shorter completion count), four for the dense decode
   const int grid = device_sm_count() * (a.host_dsar == 0 ? 1 : 4);
-  SPARCML_PROF("concat", s);
   if (a.host_dsar != 1) {
-    concat_kernel<0><<<grid, kThreads, smem, s>>>(a);
+    concat_kernel<0, V><<<grid, kThreads, smem, s>>>(a);
     ++g_launches;
   }
   if (a.host_dsar != 0) {
-    concat_kernel<1><<<grid, kThreads, smem, s>>>(a);
+    concat_kernel<1, V><<<grid, kThreads, smem, s>>>(a);
     ++g_launches;
   }
+}
+
+cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s) {
+  SPARCML_PROF("concat", s);
+  if (a.f64) launch_concat_t<double>(a, s);
+  else launch_concat_t<float>(a, s);
   return cudaGetLastError();
 }
 
@@ -1348,12 +1404,13 @@ cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s) {
 
 // P == 1: the collective is the identity on the stream (or its densified /
 // QSGD-coded form); validate and fill the control block the concat reads.
+template <typename V>
 __global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   if (a.validate || a.win) {
     for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += stride) {
       const uint32_t x = a.idx[e];
-      if (a.validate) check_input(a.idx, e, a.n, a.N, x, a.val[e], &a.ctl->status);
+      if (a.validate) check_input(a.idx, e, a.n, a.N, x, static_cast<const V*>(a.val)[e], &a.ctl->status);
       if (a.win) {   // window-offset table of the one partition (as split_push builds for owners)
         const int64_t w = (int64_t)(x / kTab);
         const int64_t wprev = e == 0 ? -1 : (int64_t)(a.idx[e - 1] / kTab);
@@ -1382,32 +1439,33 @@ __global__ void __launch_bounds__(kThreads) p1_prep_kernel(P1PrepArgs a) {
 
 // P == 1, sparse result (nnz <= delta): one kernel copies the input into out
 // (16-byte vectors where aligned) and writes the header -- the whole call.
+template <typename V>
 __global__ void __launch_bounds__(kThreads) p1_sparse_kernel(P1PrepArgs a) {
   uint32_t* oi = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
-  float* ov = reinterpret_cast<float*>(a.out + a.val_offset);
+  V* ov = reinterpret_cast<V*>(a.out + a.val_offset);
+  const V* iv = static_cast<const V*>(a.val);
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   const uint64_t gt = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
   const bool vec = ((reinterpret_cast<uintptr_t>(a.idx) | reinterpret_cast<uintptr_t>(a.val)) & 15u) == 0;
   if (!a.copy) {
     // in place: the payload is already there
-  } else if (vec) {
-    const uint64_t n4 = a.n / 4;
-    for (uint64_t u = gt; u < n4; u += stride) {
+  } else if (vec) {   // 16-byte units: 4 indices, 16 / sizeof(V) values
+    constexpr uint64_t kv = 16 / sizeof(V);
+    const uint64_t n4 = a.n / 4, nv = a.n / kv;
+    for (uint64_t u = gt; u < n4; u += stride)
       reinterpret_cast<uint4*>(oi)[u] = ld_stream_u4(reinterpret_cast<const uint4*>(a.idx) + u);
-      reinterpret_cast<float4*>(ov)[u] = ld_stream_f4(reinterpret_cast<const float4*>(a.val) + u);
-    }
-    for (uint64_t e = 4 * n4 + gt; e < a.n; e += stride) {
-      oi[e] = a.idx[e];
-      ov[e] = a.val[e];
-    }
+    for (uint64_t u = gt; u < nv; u += stride)
+      reinterpret_cast<uint4*>(ov)[u] = ld_stream_u4(reinterpret_cast<const uint4*>(iv) + u);
+    for (uint64_t e = 4 * n4 + gt; e < a.n; e += stride) oi[e] = a.idx[e];
+    for (uint64_t e = kv * nv + gt; e < a.n; e += stride) ov[e] = iv[e];
   } else {
     for (uint64_t e = gt; e < a.n; e += stride) {
       oi[e] = a.idx[e];
-      ov[e] = a.val[e];
+      ov[e] = iv[e];
     }
   }
   if (a.validate)
-    for (uint64_t e = gt; e < a.n; e += stride) check_input(a.idx, e, a.n, a.N, a.idx[e], a.val[e], &a.ctl->status);
+    for (uint64_t e = gt; e < a.n; e += stride) check_input(a.idx, e, a.n, a.N, a.idx[e], iv[e], &a.ctl->status);
   if (last_block<false>(&a.ctl->done_ctr[2]) && threadIdx.x == 0) {
     Ctrl* c = a.ctl;
     c->k_in[0] = a.n;
@@ -1417,7 +1475,7 @@ __global__ void __launch_bounds__(kThreads) p1_sparse_kernel(P1PrepArgs a) {
     c->k_sum = a.n;
     c->dsar = 0;
     write_header(reinterpret_cast<sparcml_header*>(a.out), SPARCML_REPR_SPARSE, a.n, a.N, a.n, 0, 0, a.algo_used,
-                 c->status, a.val_offset);
+                 c->status, a.val_offset, hdr_magic<V>());
     c->status = 0;
     __threadfence();
     c->seq = c->seq + 1;   // the call is complete
@@ -1429,7 +1487,8 @@ cudaError_t launch_p1_sparse(const P1PrepArgs& a, cudaStream_t s) {
   const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((work + kThreads - 1) / kThreads,
                                                                    (uint64_t)device_sm_count() * 4));
   SPARCML_PROF("p1_sparse", s);
-  p1_sparse_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  if (a.f64) p1_sparse_kernel<double><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  else p1_sparse_kernel<float><<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -1439,7 +1498,8 @@ cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s) {
                               ? std::max<uint64_t>(1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, 4096))
                               : 1;
   SPARCML_PROF("p1_prep", s);
-  p1_prep_kernel<<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  if (a.f64) p1_prep_kernel<double><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+  else p1_prep_kernel<float><<<(unsigned)blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -17,23 +17,25 @@ namespace sparcml {
 // ---------------------------------------------------------------------------
 // merge tile
 // ---------------------------------------------------------------------------
+template <typename V = float>
 struct MergeSmem {
   uint32_t ak[kMergeTile + 1];   // ak[0] = A[a0-1] (look-behind), ak[1+i] = A[a0+i]
-  float av[kMergeTile + 1];
   uint32_t bk[kMergeTile + 1];   // bk[i] = B[b0+i], bk[lb] = B[b1] (look-ahead)
-  float bv[kMergeTile + 1];
+  V av[kMergeTile + 1];
+  V bv[kMergeTile + 1];
   uint64_t split[2];
   uint32_t scan[kWarps + 1];
   uint64_t excl;
   int has_prev_a, has_next_b;
 };
 
+template <typename V = float>
 struct MergeOutput {
   uint32_t* idx;
-  float* val;
+  V* val;
   uint64_t* n;          // receives the output count (written by the last tile)
   uint32_t* idx2;       // optional mirror (a peer's receive buffer over NVLink)
-  float* val2;
+  V* val2;
   uint64_t* n2;
   int op;               // reduction operator (R-30)
 };
@@ -42,13 +44,14 @@ struct MergeOutput {
 // writes its outputs at the exclusive prefix found by look-back.  Must be
 // called by all kThreads threads.  gtile/gfirst: global tile ids for the
 // look-back chain of this job.
+template <typename V>
 __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
-                                           const float* __restrict__ Av, uint64_t na,
+                                           const V* __restrict__ Av, uint64_t na,
                                            const uint32_t* __restrict__ B,
-                                           const float* __restrict__ Bv, uint64_t nb,
-                                           uint64_t d0, MergeSmem& sm, TileStatus* st,
+                                           const V* __restrict__ Bv, uint64_t nb,
+                                           uint64_t d0, MergeSmem<V>& sm, TileStatus* st,
                                            uint32_t gtile, uint32_t gfirst, uint32_t gen,
-                                           const MergeOutput& out) {
+                                           const MergeOutput<V>& out) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t total_in = na + nb;
   const uint64_t d1 = (d0 + kMergeTile < total_in) ? d0 + kMergeTile : total_in;
@@ -91,17 +94,17 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
   int ia = lo, ib = dt - lo;
   const bool has_prev_a = sm.has_prev_a, has_next_b = sm.has_next_b;
   uint32_t ok[kMergeItems];
-  float ov[kMergeItems];
+  V ov[kMergeItems];
   uint32_t emit = 0;
 #pragma unroll
   for (int s = 0; s < kMergeItems; ++s) {
     ok[s] = 0;
-    ov[s] = 0.0f;
+    ov[s] = 0;
     if (dt + s < L) {
       const bool takeA = ib >= lb || (ia < la && sm.ak[ia + 1] <= sm.bk[ib]);
       if (takeA) {
         const uint32_t key = sm.ak[ia + 1];
-        float v = sm.av[ia + 1];
+        V v = sm.av[ia + 1];
         // the element following A[ia] in merged order is B[ib] (or the look-ahead)
         if ((ib < lb || has_next_b) && sm.bk[ib] == key) v = op_combine(out.op, v, sm.bv[ib]);
         ok[s] = key;
@@ -156,9 +159,10 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
 // ---------------------------------------------------------------------------
 // window tile
 // ---------------------------------------------------------------------------
+template <typename V = float>
 struct WinSource {
   const uint32_t* idx;   // sparse: global indices
-  const float* val;      // sparse values, or dense values indexed by (g - dense_base)
+  const V* val;          // sparse values, or dense values indexed by (g - dense_base)
   uint64_t n;            // sparse count
   uint64_t dense_base;   // dense: global index of val[0]
   int dense;
@@ -166,20 +170,21 @@ struct WinSource {
 
 enum WinMode : int { WIN_DENSE = 0, WIN_SPARSE = 1, WIN_QUANT = 2 };
 
+template <typename V = float>
 struct WinOutput {
   int mode;
   // WIN_DENSE: out[g - dense_base] (and mirror)
-  float* dense;
-  float* dense2;
+  V* dense;
+  V* dense2;
   uint64_t dense_base;
   // WIN_SPARSE: compacted (g, v); count to *n (and mirrors)
   uint32_t* idx;
-  float* val;
+  V* val;
   uint64_t* n;
   uint32_t* idx2;
-  float* val2;
+  V* val2;
   uint64_t* n2;
-  // WIN_QUANT: QSGD of the window, positions relative to qbase (= partition start)
+  // WIN_QUANT (fp32 only): QSGD of the window, positions relative to qbase (= partition start)
   uint8_t* codes;
   float* scales;
   uint64_t qbase;
@@ -198,8 +203,8 @@ struct WinMisc {
   uint32_t bmax[kWin / 8];
 };
 
-__host__ __device__ constexpr size_t win_smem_bytes(int nsrc) {
-  return sizeof(uint32_t) * kWin + sizeof(float) * kWin * (size_t)nsrc + sizeof(WinMisc);
+__host__ __device__ constexpr size_t win_smem_bytes(int nsrc, size_t vbytes = 4) {
+  return sizeof(uint32_t) * kWin + vbytes * kWin * (size_t)nsrc + sizeof(WinMisc);
 }
 
 // Canonical tree schedule (reading R-8): post-order list of (dst, src) slot
@@ -303,14 +308,15 @@ __device__ __forceinline__ void qsgd_block_encode(const float r[4], int valid, u
 
 // Processes window w of [lo, hi): positions [lo + w*kWin, min(lo+(w+1)*kWin, hi)).
 // ticket order == window order (required for WIN_SPARSE's look-back).
-__device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, const TreeSched& ts,
+template <typename V>
+__device__ __forceinline__ void window_tile(const WinSource<V>* src, int nsrc, const TreeSched& ts,
                                             uint64_t lo, uint64_t hi, uint32_t w,
                                             unsigned char* smem, TileStatus* st, uint32_t gen,
-                                            uint32_t nwin, const WinOutput& out) {
+                                            uint32_t nwin, const WinOutput<V>& out) {
   const int tid = threadIdx.x, warp = tid >> 5;
   uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
-  float* vals = reinterpret_cast<float*>(smem + sizeof(uint32_t) * kWin);
-  WinMisc& mc = *reinterpret_cast<WinMisc*>(smem + sizeof(uint32_t) * kWin + sizeof(float) * kWin * nsrc);
+  V* vals = reinterpret_cast<V*>(smem + sizeof(uint32_t) * kWin);
+  WinMisc& mc = *reinterpret_cast<WinMisc*>(smem + sizeof(uint32_t) * kWin + sizeof(V) * kWin * nsrc);
   const uint64_t wlo = lo + (uint64_t)w * kWin;
   const uint64_t whi = (wlo + kWin < hi) ? wlo + kWin : hi;
   const int wn = (int)(whi - wlo);
@@ -332,7 +338,7 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
   // sources at once (one load latency for the window, not one per source)
   for (int s = 0; s < nsrc; ++s) {
     if (src[s].dense) {
-      const float* dv = src[s].val + (wlo - src[s].dense_base);
+      const V* dv = src[s].val + (wlo - src[s].dense_base);
       for (int p = tid; p < wn; p += kThreads) vals[s * kWin + p] = dv[p];
       for (int p = tid; p < wn; p += kThreads) atomicOr(&pres[p], 1u << s);
     }
@@ -360,7 +366,7 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
 
   // each thread: 4 consecutive positions
   const int p0 = tid * kWinPerThread;
-  float r[kWinPerThread];
+  V r[kWinPerThread];
   uint32_t present = 0;
 #pragma unroll
   for (int i = 0; i < kWinPerThread; ++i) {
@@ -377,23 +383,15 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
         }
       }
     }
-    r[i] = (m & 1u) ? vals[p] : op_neutral(out.op);
+    r[i] = (m & 1u) ? vals[p] : op_neutral_v<V>(out.op);
     if (m & 1u) present |= 1u << i;
   }
 
   if (out.mode == WIN_DENSE) {
     const uint64_t g0 = wlo + p0;
     if (p0 < wn) {
-      float* d = out.dense + (g0 - out.dense_base);
-      if (p0 + 4 <= wn && ((reinterpret_cast<uintptr_t>(d) & 15u) == 0)) {
-        *reinterpret_cast<float4*>(d) = make_float4(r[0], r[1], r[2], r[3]);
-        if (out.dense2) *reinterpret_cast<float4*>(out.dense2 + (g0 - out.dense_base)) = make_float4(r[0], r[1], r[2], r[3]);
-      } else {
-        for (int i = 0; i < kWinPerThread && p0 + i < wn; ++i) {
-          d[i] = r[i];
-          if (out.dense2) out.dense2[g0 - out.dense_base + i] = r[i];
-        }
-      }
+      store4(out.dense + (g0 - out.dense_base), r, wn - p0);
+      if (out.dense2) store4(out.dense2 + (g0 - out.dense_base), r, wn - p0);
     }
   } else if (out.mode == WIN_SPARSE) {
     uint32_t total;
@@ -421,7 +419,7 @@ __device__ __forceinline__ void window_tile(const WinSource* src, int nsrc, cons
       if (out.n) *out.n = mc.excl + total;
       if (out.n2) *out.n2 = mc.excl + total;
     }
-  } else {
+  } else if constexpr (sizeof(V) == sizeof(float)) {
     const uint64_t e = (wlo - out.qbase) + p0;   // partition-relative position
     const int valid = max(0, min(kWinPerThread, wn - p0));
     qsgd_block_encode(r, valid, e, wlo + p0, out.bits, out.bucket, out.seed_lo, out.seed_hi, out.codes,

@@ -37,6 +37,7 @@ HEADER_BYTES = 64
 IPC_HANDLE_BYTES = 64
 MAX_RANKS = 16
 HEADER_MAGIC = 0x4D435053
+HEADER_MAGIC_F64 = 0x44435053   # results of the fp64 calls (double values)
 
 EXPORTED = [
     "sparcml_version", "sparcml_status_string", "sparcml_opts_default", "sparcml_switch_threshold",
@@ -49,6 +50,8 @@ EXPORTED = [
     "sparcml_kernel_launches", "sparcml_profile_enable", "sparcml_profile_only", "sparcml_profile_reset",
     "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges", "sparcml_sparse_allgather",
     "sparcml_sparse_allgather_local", "sparcml_apply_update", "sparcml_quantize_norm",
+    "sparcml_sparse_allreduce_f64", "sparcml_sparse_allreduce_local_f64", "sparcml_result_bytes_f64",
+    "sparcml_result_val_offset_f64",
 ]
 
 
@@ -86,6 +89,10 @@ _sig = {
     "sparcml_last_error": (C.c_char_p, [_p]),
     "sparcml_sparse_allreduce": (_i32, [_p, _p, _p, _u64, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_sparse_allreduce_local": (_i32, [_p, _p, _p, _p, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_sparse_allreduce_f64": (_i32, [_p, _p, _p, _u64, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_sparse_allreduce_local_f64": (_i32, [_p, _p, _p, _p, _u64, _i32, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_result_bytes_f64": (_sz, [_u64]),
+    "sparcml_result_val_offset_f64": (_sz, [_u64]),
     "sparcml_read_header": (_i32, [_p, C.POINTER(Header), _p]),
     "sparcml_barrier": (_i32, [_p, _p]),
     "sparcml_ops_workspace_bytes": (_sz, [_u64]),
@@ -171,12 +178,23 @@ def expected_nnz(k: int, N: int, P: int) -> float:
     return float(_lib.sparcml_expected_nnz(k, N, P))
 
 
-def result_bytes(N: int) -> int:
+def result_bytes(N: int, dtype=torch.float32) -> int:
+    if dtype == torch.float64:
+        return int(_lib.sparcml_result_bytes_f64(N))
     return int(_lib.sparcml_result_bytes(N))
 
 
-def result_val_offset(N: int) -> int:
+def result_val_offset(N: int, dtype=torch.float32) -> int:
+    if dtype == torch.float64:
+        return int(_lib.sparcml_result_val_offset_f64(N))
     return int(_lib.sparcml_result_val_offset(N))
+
+
+def _val_dtype(t: torch.Tensor):
+    """float32, or float64 for the fp64 calls (values "single or double")."""
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ValueError("val must be float32 or float64")
+    return t.dtype
 
 
 def make_opts(algo: int = ALGO_AUTO, switch_scale: float = 1.0, quant_bits: int = 0, quant_bucket: int = 1024,
@@ -209,19 +227,20 @@ class Result:
     header: Header
     dense: bool
     idx: Optional[torch.Tensor]   # int32 [nnz] (sparse) or None
-    val: torch.Tensor             # float32 [nnz] or [N]
+    val: torch.Tensor             # float32 (float64 for the fp64 calls) [nnz] or [N]
 
 
-def new_out(N: int, device=None) -> torch.Tensor:
-    return torch.empty(result_bytes(N), dtype=torch.uint8, device=device or "cuda")
+def new_out(N: int, device=None, dtype=torch.float32) -> torch.Tensor:
+    return torch.empty(result_bytes(N, dtype), dtype=torch.uint8, device=device or "cuda")
 
 
-def payload_views(out: torch.Tensor, N: int, n: int):
-    """(idx int32[n], val float32[n]) views of out's sparse payload slots: a stream
+def payload_views(out: torch.Tensor, N: int, n: int, dtype=torch.float32):
+    """(idx int32[n], val[n]) views of out's sparse payload slots: a stream
     written there (e.g. by the top-k) is an in-place allreduce input."""
-    vo = result_val_offset(N)
+    vo = result_val_offset(N, dtype)
+    w = torch.empty(0, dtype=dtype).element_size()
     idx = out[HEADER_BYTES:HEADER_BYTES + 4 * n].view(torch.int32)
-    val = out[vo:vo + 4 * n].view(torch.float32)
+    val = out[vo:vo + w * n].view(dtype)
     return idx, val
 
 
@@ -229,15 +248,16 @@ def read_result(out: torch.Tensor, stream=None) -> Result:
     """Synchronises `stream`, reads the header and returns views of the payload."""
     h = Header()
     _check(_lib.sparcml_read_header(out.data_ptr(), C.byref(h), _stream(stream)))
-    if h.magic != HEADER_MAGIC:
+    if h.magic not in (HEADER_MAGIC, HEADER_MAGIC_F64):
         raise SparcmlError(ERR_STATE, "output header not written")
+    dt, w = (torch.float64, 8) if h.magic == HEADER_MAGIC_F64 else (torch.float32, 4)
     N = int(h.N)
     if h.repr == REPR_DENSE:
-        val = out[HEADER_BYTES:HEADER_BYTES + 4 * N].view(torch.float32)
+        val = out[HEADER_BYTES:HEADER_BYTES + w * N].view(dt)
         return Result(h, True, None, val)
     n = int(h.nnz)
     idx = out[HEADER_BYTES:HEADER_BYTES + 4 * n].view(torch.int32)
-    val = out[h.val_offset:h.val_offset + 4 * n].view(torch.float32)
+    val = out[h.val_offset:h.val_offset + w * n].view(dt)
     return Result(h, False, idx, val)
 
 
@@ -267,21 +287,22 @@ class LocalWorld:
 
     def allreduce(self, streams: Sequence, N: int, outs: Optional[Sequence[torch.Tensor]] = None,
                   opts: Optional[Opts] = None, stream=None, op: int = OP_SUM):
-        """streams: P pairs (idx int32 cuda, val float32 cuda).  Returns the P out buffers."""
+        """streams: P pairs (idx int32 cuda, val float32 or float64 cuda).  Returns the P out buffers."""
         P = self.P
         assert len(streams) == P
+        dt = _val_dtype(streams[0][1])
         for i, v in streams:
             _need(i, torch.int32, "idx")
-            _need(v, torch.float32, "val")
+            _need(v, dt, "val")
         if outs is None:
-            outs = [new_out(N, i.device) for i, _ in streams]
+            outs = [new_out(N, i.device, dt) for i, _ in streams]
         ia = (C.c_void_p * P)(*[_ptr(i) for i, _ in streams])
         va = (C.c_void_p * P)(*[_ptr(v) for _, v in streams])
         na = (C.c_uint64 * P)(*[int(i.numel()) for i, _ in streams])
         oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
         o = opts if opts is not None else make_opts()
-        _check(_lib.sparcml_sparse_allreduce_local(self._h, ia, va, na, N, op, C.byref(o), oa,
-                                                   int(outs[0].numel()), _stream(stream)), self._h)
+        fn = _lib.sparcml_sparse_allreduce_local_f64 if dt == torch.float64 else _lib.sparcml_sparse_allreduce_local
+        _check(fn(self._h, ia, va, na, N, op, C.byref(o), oa, int(outs[0].numel()), _stream(stream)), self._h)
         return list(outs)
 
     def allgather(self, streams: Sequence, N: int, outs: Optional[Sequence[torch.Tensor]] = None,
@@ -344,12 +365,14 @@ class Comm:
     def allreduce(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,
                   opts: Optional[Opts] = None, stream=None, op: int = OP_SUM) -> torch.Tensor:
         _need(idx, torch.int32, "idx")
-        _need(val, torch.float32, "val")
+        dt = _val_dtype(val)
+        _need(val, dt, "val")
         if out is None:
-            out = new_out(N, idx.device)
+            out = new_out(N, idx.device, dt)
         o = opts if opts is not None else make_opts()
-        _check(_lib.sparcml_sparse_allreduce(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, op, C.byref(o),
-                                             out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
+        fn = _lib.sparcml_sparse_allreduce_f64 if dt == torch.float64 else _lib.sparcml_sparse_allreduce
+        _check(fn(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, op, C.byref(o), out.data_ptr(),
+                  int(out.numel()), _stream(stream)), self._h)
         return out
 
     def allgather(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,

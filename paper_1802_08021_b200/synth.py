@@ -60,6 +60,8 @@ def _distinct_sorted(rng: np.random.Generator, N: int, k: int) -> np.ndarray:
 def values(rng: np.random.Generator, n: int, kind: str = "normal") -> np.ndarray:
     if kind == "normal":
         return rng.standard_normal(n, dtype=np.float32)
+    if kind == "normal64":   # fp64 values: full 53-bit mantissas
+        return rng.standard_normal(n, dtype=np.float64)
     if kind == "int":
         v = rng.integers(1, 1025, size=n)
         s = rng.integers(0, 2, size=n) * 2 - 1

@@ -16,6 +16,9 @@ from paper_1802_08021_b200 import synth  # noqa: E402
 
 
 def main():
+    if os.environ.get("SPARCML_MP_VERBOSE"):
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["SPARCML_MP_VERBOSE"]), exit=True)
     dist.init_process_group("gloo")
     rank, P = dist.get_rank(), dist.get_world_size()
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -27,7 +30,13 @@ def main():
         ("dsar", 1 << 20, 200_000, S.DSAR_SPLIT_ALLGATHER, 0),
         ("dsar4", 1 << 20, 200_000, S.DSAR_SPLIT_ALLGATHER, 4),
         ("auto", 1 << 20, 300_000, S.ALGO_AUTO, 2),
+        ("auto-ssar", 1 << 20, 100_000, S.ALGO_AUTO, 0),   # device decides SSAR (both concat variants launched)
         ("ssar-big", 1 << 24, 167_772, S.SSAR_SPLIT_ALLGATHER, 0),
+        # fp64 values: the _f64 entry points, oracle's fp64 build
+        ("f64-rd", 200_003, 3000, S.SSAR_RECURSIVE_DOUBLE, 0),
+        ("f64-ssar", 1 << 20, 10_000, S.SSAR_SPLIT_ALLGATHER, 0),
+        ("f64-dsar", 1 << 20, 200_000, S.DSAR_SPLIT_ALLGATHER, 0),
+        ("f64-auto", 1 << 20, 300_000, S.ALGO_AUTO, 0),
     ]
     max_N = max(c[1] for c in cases)
     max_k = max(c[2] for c in cases)
@@ -35,7 +44,11 @@ def main():
     fails = 0
     for rep in range(2):
         for name, N, k, algo, bits in cases:
-            streams = synth.uniform_streams(P, N, k, seed=rep * 10 + len(name), kind="normal")
+            if os.environ.get("SPARCML_MP_VERBOSE"):
+                print(f"rank {rank}: rep {rep} case {name}", flush=True)
+            f64 = name.startswith("f64")
+            dt = np.float64 if f64 else np.float32
+            streams = synth.uniform_streams(P, N, k, seed=rep * 10 + len(name), kind="normal64" if f64 else "normal")
             i, v = streams[rank]
             it = torch.from_numpy(i.view(np.int32)).cuda()
             vt = torch.from_numpy(v).cuda()
@@ -43,11 +56,11 @@ def main():
             out = comm.allreduce(it, vt, N, opts=opts)
             res = S.read_result(out)
             if algo == S.SSAR_RECURSIVE_DOUBLE:
-                ref, st = oracle.ssar_recursive_double(N, streams)
+                ref, st = oracle.ssar_recursive_double(N, streams, dtype=dt)
             else:
                 oa = {S.SSAR_SPLIT_ALLGATHER: oracle.ALGO_SSAR_SPLIT, S.DSAR_SPLIT_ALLGATHER: oracle.ALGO_DSAR_SPLIT,
                       S.ALGO_AUTO: oracle.ALGO_AUTO}[algo]
-                ref, st, _ = oracle.split_allgather(N, streams, algo=oa, quant_bits=bits, seed=3)
+                ref, st, _ = oracle.split_allgather(N, streams, algo=oa, quant_bits=bits, seed=3, dtype=dt)
             d, ei, ev = ref[rank]
             ok = res.header.status == 0 and res.dense == d and res.header.k_sum == P * k
             if ok and d:
