@@ -392,8 +392,9 @@ def main():
                 "frac": (achieved / hbm_peak) if achieved else None,
                 "traffic": ncu_traffic("topk_bucketed" if bucket else "topk"),
                 "alg_bytes_per_launch": alg_bytes, "avg_launch_us": t_filter * 1e6, "peak_source": peak_src,
-                "share_of_step": (prof.get("topk_bucketed" if bucket else "topk", (0, 0.0))[1] / total_prof_ms)
-                if total_prof_ms else None}
+                # share of the step on the device, from the split graph (its event node sits in the
+                # allreduce part, so this under-states the top-k share a little)
+                "share_of_step": t_topk_kernel / (t_topk_kernel + t_ar) if t_topk_kernel + t_ar > 0 else None}
 
     # ---------------- e2e through the C ABI with host buffers ----------------
     e2e = None
