@@ -32,6 +32,8 @@ namespace sparcml {
 
 constexpr int kTopkTile = 4096;           // elements per filter tile (16 per thread)
 constexpr int kBins = 4096;
+constexpr int kCoarse = 64;                   // coarse bins of 64 fine bins each, stored after the fine ones
+constexpr int kHist = kBins + kCoarse;
 constexpr uint64_t kSampleMinN = 1u << 16;   // below this: tau = 0 (all candidates)
 constexpr uint32_t kSampleChunks = 8192;     // 8-value chunks sampled
 constexpr int kMaxGrid = 4096;
@@ -40,8 +42,8 @@ constexpr int kLevels = 4;                   // histogram levels (12 + 12 + 7 ke
 
 struct TopkCtl {
   uint64_t t_phase[16];     // %globaltimer at phase ends (block 0), diagnostics only
-  uint32_t hist_s[kBins];   // sample histogram (key >> 19)
-  uint32_t hist[kLevels][kBins];   // candidate histogram per refinement level
+  uint32_t hist_s[kHist];   // sample histogram (key >> 19), then its 64 coarse sums
+  uint32_t hist[kLevels][kHist];   // candidate histogram per refinement level (+ coarse sums)
   uint64_t blk[kMaxGrid];   // per-block (gt | eq << 32) selected counts
   uint32_t status, passes;
   uint32_t smax;            // largest sampled key
@@ -127,65 +129,67 @@ struct BinFind {
   bool reached;
 };
 
-// Up to two targets from one staging of h and one scan.
-__device__ void find_bins(const uint32_t* h, uint64_t above0, const uint64_t* target, int ntarget, uint32_t* sm,
-                          BinFind* out, uint32_t nbins = kBins) {
-  __shared__ uint64_t scan[kWarps + 1];
-  __shared__ uint32_t s_bin[2];
-  __shared__ uint64_t s_above[2];
+// Up to two targets.  Two small reads instead of one 16 KB one (every block
+// runs this on the same histogram right after a grid barrier, so the read is
+// the contended part): warp 0 scans the 64 coarse sums from the top, then warp
+// q scans the 64 fine bins of target q's coarse bin.  Same result as a scan of
+// the fine bins (the coarse sums are their exact sums).
+__device__ __forceinline__ bool pair_find(uint32_t hi, uint32_t lo, uint64_t base, uint64_t tg, uint32_t* which,
+                                          uint64_t* above) {
+  // lane holds bins (hi, lo) of a descending scan; base = count above them
+  if (!(base < tg && base + hi + lo >= tg)) return false;
+  if (base + hi >= tg) {
+    *which = 0;
+    *above = base;
+  } else {
+    *which = 1;
+    *above = base + hi;
+  }
+  return true;
+}
+
+__device__ void find_bins(const uint32_t* h, uint64_t above0, const uint64_t* target, int ntarget, uint32_t* /*sm*/,
+                          BinFind* out) {
+  __shared__ uint32_t s_cb[2];
+  __shared__ uint64_t s_ca[2];
   __shared__ int s_ok[2];
-  const int tid = threadIdx.x;
-  constexpr int per = kBins / kThreads;   // 16
-  // stage: 16 independent coalesced loads in flight per thread; bin j at
-  // sm[j + j/16] so that each thread's 16 consecutive bins are bank-conflict free
-  uint32_t v[per];
-#pragma unroll
-  for (int i = 0; i < per; ++i) v[i] = (uint32_t)(i * kThreads + tid) < nbins ? __ldcg(&h[i * kThreads + tid]) : 0u;
-#pragma unroll
-  for (int i = 0; i < per; ++i) {
-    const int j = i * kThreads + tid;
-    sm[j + (j >> 4)] = v[i];
-  }
-  if (tid < 2) {
-    s_bin[tid] = 0;
-    s_above[tid] = above0;
-    s_ok[tid] = 0;
-  }
-  __syncthreads();
-  const int hiB = kBins - tid * per;     // this thread: bins [hiB - per, hiB), scanned downwards
-  uint32_t loc[per];
-  uint64_t local = 0;
-#pragma unroll
-  for (int i = 0; i < per; ++i) {
-    const int j = hiB - 1 - i;
-    loc[i] = sm[j + (j >> 4)];
-    local += loc[i];
-  }
-  uint64_t total;
-  const uint64_t before = above0 + block_exclusive_sum<uint64_t>(local, scan, &total);
-  for (int q = 0; q < ntarget; ++q) {
-    const uint64_t tg = target[q];
-    if (before < tg && before + local >= tg) {
-      uint64_t cum = before;
-      bool found = false;
-#pragma unroll
-      for (int i = 0; i < per; ++i) {
-        if (!found && cum + loc[i] >= tg) {
-          s_bin[q] = (uint32_t)(hiB - 1 - i);
-          s_above[q] = cum;
-          s_ok[q] = 1;
-          found = true;
-        }
-        cum += loc[i];
+  __shared__ BinFind s_res[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    const uint32_t* hc = h + kBins;
+    const uint32_t chi = __ldcg(&hc[63 - 2 * lane]), clo = __ldcg(&hc[62 - 2 * lane]);
+    const uint32_t s = chi + clo;
+    const uint64_t excl = warp_inclusive_sum<uint64_t>(s) - s;
+    for (int q = 0; q < ntarget; ++q) {
+      uint32_t which = 0;
+      uint64_t ab = 0;
+      const bool hit = pair_find(chi, clo, above0 + excl, target[q], &which, &ab);
+      const uint32_t m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) s_ok[q] = m != 0;
+      if (hit) {
+        s_cb[q] = 63 - 2 * lane - which;
+        s_ca[q] = ab;
       }
     }
   }
   __syncthreads();
-  for (int q = 0; q < ntarget; ++q) {
-    out[q].bin = s_bin[q];
-    out[q].above = s_above[q];
-    out[q].reached = s_ok[q] != 0;
+  if (warp < ntarget) {
+    const int q = warp;
+    if (!s_ok[q]) {
+      if (lane == 0) s_res[q] = BinFind{0u, above0, false};
+    } else {
+      const uint32_t* hf = h + (size_t)s_cb[q] * 64;
+      const uint32_t fhi = __ldcg(&hf[63 - 2 * lane]), flo = __ldcg(&hf[62 - 2 * lane]);
+      const uint32_t s = fhi + flo;
+      const uint64_t excl = warp_inclusive_sum<uint64_t>(s) - s;
+      uint32_t which = 0;
+      uint64_t ab = 0;
+      if (pair_find(fhi, flo, s_ca[q] + excl, target[q], &which, &ab))
+        s_res[q] = BinFind{s_cb[q] * 64 + 63 - 2 * lane - which, ab, true};
+    }
   }
+  __syncthreads();
+  for (int q = 0; q < ntarget; ++q) out[q] = s_res[q];
   __syncthreads();
 }
 
@@ -312,7 +316,9 @@ __device__ __forceinline__ void filter_tile(const float* __restrict__ x, const f
           ks->ci[kb + pos] = (uint32_t)(p + q);
           ks->cv[kb + pos] = v[j][q];
         }
-        atomicAdd(&sh[bin_of(abs_key(v[j][q]), tau, split, shift)], 1u);
+        const uint32_t bn = bin_of(abs_key(v[j][q]), tau, split, shift);
+        atomicAdd(&sh[bn], 1u);
+        atomicAdd(&sh[kBins + (bn >> 6)], 1u);
         ++pos;
       }
     }
@@ -385,7 +391,7 @@ __device__ __forceinline__ void load4(const float* cv, uint32_t n, uint32_t i0, 
 
 __device__ __forceinline__ void flush_hist(const uint32_t* sh, uint32_t* gh) {
   __syncthreads();
-  for (int i = threadIdx.x; i < kBins; i += kThreads) {
+  for (int i = threadIdx.x; i < kHist; i += kThreads) {
     const uint32_t v = sh[i];
     if (v) atomicAdd(&gh[i], v);
   }
@@ -414,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const uint32_t gwarp = b * kWarps + warp, nwarps = G * kWarps;
   const uint64_t t0 = L.ntiles * b / G, t1 = L.ntiles * (b + 1) / G;   // this block's tiles in C
-  for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+  for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
   if (tid == 0) {
     s_status = 0;
     ks.ntl = 0;
@@ -455,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
         const uint32_t key = abs_key(v[i]);
         mx = max(mx, key);
         atomicAdd(&sh[key >> 19], 1u);
+        atomicAdd(&sh[kBins + (key >> 25)], 1u);
       }
     }
 #pragma unroll
@@ -462,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
     if (lane == 0 && mx) atomicMax(&c->smax, mx);
     flush_hist(sh, c->hist_s);
     __syncthreads();
-    for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+    for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
   }
   mark(c, 1);
   grid.sync();
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
     lv.split = split;
     lv.shift = shift_for(split - tau, kBins - 1);
   }
-  for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+  for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
   __syncthreads();
   mark(c, 2);
   const uint32_t tau = (uint32_t)lv.lo;
@@ -525,13 +532,13 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
     if (!f0.reached) {   // fewer than k candidates: the sample under-estimated; exact re-filter with tau = 0 (rare)
       grid.sync();   // every block has read hist[0]
       if (b == 0) {
-        for (int i = tid; i < kBins; i += kThreads) c->hist[0][i] = 0;
+        for (int i = tid; i < kHist; i += kThreads) c->hist[0][i] = 0;
         if (tid == 0) {
           c->tile_ticket = 0;
           c->passes = 2;
         }
       }
-      for (int i = tid; i < kBins; i += kThreads) sh[i] = 0;
+      for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
       if (tid == 0) s_fast = 0;   // the re-filtered candidates live in global memory only
       grid.sync();
       lv.lo = 0;
@@ -563,7 +570,11 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
     if (s_fast) {
       for (uint32_t i = tid; i < ks.nc; i += kThreads) {
         const uint32_t key = abs_key(ks.cv[i]);
-        if (key >= lv.lo && key < lv.hi) atomicAdd(&gh[bin_of(key, lv.lo, lv.split, lv.shift)], 1u);
+        if (key >= lv.lo && key < lv.hi) {
+          const uint32_t bn = bin_of(key, lv.lo, lv.split, lv.shift);
+          atomicAdd(&gh[bn], 1u);
+          atomicAdd(&gh[kBins + (bn >> 6)], 1u);
+        }
       }
     } else
     for (uint64_t t = gwarp; t < L.ntiles; t += nwarps) {
@@ -575,8 +586,11 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const uint32_t key = abs_key(v[r]);
-          if (i0 + r * 32 + lane < n && key >= lv.lo && key < lv.hi)
-            atomicAdd(&gh[bin_of(key, lv.lo, lv.split, lv.shift)], 1u);
+          if (i0 + r * 32 + lane < n && key >= lv.lo && key < lv.hi) {
+            const uint32_t bn = bin_of(key, lv.lo, lv.split, lv.shift);
+            atomicAdd(&gh[bn], 1u);
+            atomicAdd(&gh[kBins + (bn >> 6)], 1u);
+          }
         }
       }
     }
@@ -642,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel
   // every histogram has been read by every block: clear them for the next call
   if (b < (uint32_t)(kLevels + 1)) {
     uint32_t* h = b == 0 ? c->hist_s : c->hist[b - 1];
-    for (int i = tid; i < kBins; i += kThreads) h[i] = 0;
+    for (int i = tid; i < kHist; i += kThreads) h[i] = 0;
     if (b == 0 && tid == 0) c->smax = 0;
   }
   if (s_fast) {
