@@ -235,7 +235,9 @@ sparcml_status sparcml_sparse_allgather_local(sparcml_comm* comm, const uint32_t
 /* Algorithm 1's update ("v_t <- v_{t-1} - g_t"): v[j] -= g[j] for the
  * allreduce result g in `out` (sparse: its pairs; dense: all N values),
  * read from the device header -- no host synchronisation.  v: N floats
- * (N = the result's N).  Errors: null arguments -> SPARCML_ERR_INVALID_ARG. */
+ * (N = the result's N).  fp32 results only: a result whose header magic is
+ * not SPARCML_HEADER_MAGIC (e.g. an _f64 result) leaves v unchanged.
+ * Errors: null arguments -> SPARCML_ERR_INVALID_ARG. */
 sparcml_status sparcml_apply_update(float* v, const void* out, void* stream);
 
 /* ---------------------- layer-wise tensor fusion ------------------------ */

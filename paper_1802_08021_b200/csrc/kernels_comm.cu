@@ -1724,6 +1724,7 @@ cudaError_t launch_ag_gather(const AgGatherArgs& a, cudaStream_t s) {
 // ===========================================================================
 __global__ void __launch_bounds__(kThreads) apply_update_kernel(float* v, const char* out) {
   const sparcml_header* h = reinterpret_cast<const sparcml_header*>(out);
+  if (h->magic != SPARCML_HEADER_MAGIC) return;   // not an fp32 result
   const bool dense = h->repr == SPARCML_REPR_DENSE;
   const uint64_t n = dense ? h->N : h->nnz;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;

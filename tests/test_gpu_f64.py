@@ -143,3 +143,13 @@ def test_f64_rejects_qsgd_and_small_out():
     small = [S.new_out(1000, "cuda", torch.float32) for _ in range(2)]   # sized for fp32 values
     with pytest.raises(S.SparcmlError):
         w.allreduce(s, 1000, outs=small)
+
+
+def test_apply_update_ignores_f64_results():
+    w = S.LocalWorld(2, 1000, 10)
+    s = [(torch.tensor([3], dtype=torch.int32, device="cuda"), torch.ones(1, dtype=torch.float64, device="cuda"))] * 2
+    outs = w.allreduce(s, 1000)
+    v = torch.ones(1000, device="cuda")
+    S.apply_update(v, outs[0])
+    torch.cuda.synchronize()
+    assert torch.all(v == 1.0)
