@@ -231,6 +231,16 @@ sparcml_status sparcml_sparse_allgather_local(sparcml_comm* comm, const uint32_t
                                               const float* const* val_host, const uint64_t* nnz_host,
                                               uint64_t N, const sparcml_opts* opts_host,
                                               void* const* out_host, size_t out_bytes, void* stream);
+/* The same with fp64 values: result laid out per
+ * sparcml_result_*_f64 (magic SPARCML_HEADER_MAGIC_F64), dense when
+ * K > floor(N*8/12), header byte counts at 12 bytes per pair. */
+sparcml_status sparcml_sparse_allgather_f64(sparcml_comm* comm, const uint32_t* idx, const double* val,
+                                            uint64_t nnz, uint64_t N, const sparcml_opts* opts_host,
+                                            void* out, size_t out_bytes, void* stream);
+sparcml_status sparcml_sparse_allgather_local_f64(sparcml_comm* comm, const uint32_t* const* idx_host,
+                                                  const double* const* val_host, const uint64_t* nnz_host,
+                                                  uint64_t N, const sparcml_opts* opts_host,
+                                                  void* const* out_host, size_t out_bytes, void* stream);
 
 /* Algorithm 1's update ("v_t <- v_{t-1} - g_t"): v[j] -= g[j] for the
  * allreduce result g in `out` (sparse: its pairs; dense: all N values),

@@ -135,7 +135,7 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   if (P > 1) off += (size_t)(2 + 2 * (L.L + 2)) * L.rd_bytes;
   L.ag_off = off;
   L.ag_val_off = align_up(4 * max_nnz, 256);
-  off += align_up(L.ag_val_off + 4 * max_nnz, 256);
+  off += align_up(L.ag_val_off + 8 * max_nnz, 256);   // values up to 8 bytes (fp64)
   L.total = align_up(off, 1 << 20);
   return L;
 }
@@ -605,9 +605,9 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
 }
 
 // ------------------------------------------------------ sparse allgather ---
-sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
+sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const void* const* val,
                               const uint64_t* nnz, uint64_t N, const sparcml_opts* opts, void* const* out,
-                              size_t out_bytes, void* stream) {
+                              size_t out_bytes, void* stream, int f64 = 0) {
   if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
   if (!c->connected) return fail(c, SPARCML_ERR_STATE, "communicator not connected");
   if (N == 0 || N > c->L.max_N) return fail(c, SPARCML_ERR_INVALID_ARG, "N must be in [1, max_N]");
@@ -617,7 +617,8 @@ sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const
   if (opts) o = *opts;
   if (!(o.switch_scale > 0.0f) || o.switch_scale > 1.0f)
     return fail(c, SPARCML_ERR_INVALID_ARG, "switch_scale must be in (0, 1]");
-  if (out_bytes < sparcml_result_bytes(N)) return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N)");
+  if (out_bytes < (f64 ? sparcml_result_bytes_f64(N) : sparcml_result_bytes(N)))
+    return fail(c, SPARCML_ERR_INVALID_ARG, "out_bytes < sparcml_result_bytes(N) (_f64 for double values)");
   const int nl = c->local ? c->P : 1;
   for (int i = 0; i < nl; ++i) {
     if (nnz[i] > c->L.max_nnz) return fail(c, SPARCML_ERR_INVALID_ARG, "nnz > max_nnz");
@@ -645,7 +646,8 @@ sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const
     a.P = P;
     a.rank = r;
     a.my_idx = reinterpret_cast<uint32_t*>(c->peer[r] + L.ag_off);
-    a.my_val = reinterpret_cast<float*>(c->peer[r] + L.ag_off + L.ag_val_off);
+    a.my_val = c->peer[r] + L.ag_off + L.ag_val_off;
+    a.f64 = f64;
     for (int j = 0; j < P; ++j) a.peer[j] = ctrl_of(c->peer[j]);
     a.ctl = ctrl_of(c->peer[r]);
     a.validate = o.validate;
@@ -657,14 +659,15 @@ sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const
     g.P = P;
     g.rank = r;
     g.N = N;
-    g.delta = effective_delta(N, o);
+    g.delta = effective_delta(N, o, f64 ? 8 : 4);
     for (int j = 0; j < P; ++j) {
       g.src_idx[j] = reinterpret_cast<const uint32_t*>(c->peer[j] + L.ag_off);
-      g.src_val[j] = reinterpret_cast<const float*>(c->peer[j] + L.ag_off + L.ag_val_off);
+      g.src_val[j] = c->peer[j] + L.ag_off + L.ag_val_off;
     }
     g.ctl = ctrl_of(c->peer[r]);
     g.out = static_cast<char*>(out[i]);
-    g.val_offset = sparcml_result_val_offset(N);
+    g.val_offset = f64 ? sparcml_result_val_offset_f64(N) : sparcml_result_val_offset(N);
+    g.f64 = f64;
     CK(c, launch_ag_gather(g, s));
   }
   return SPARCML_OK;
@@ -903,7 +906,8 @@ sparcml_status sparcml_sparse_allgather(sparcml_comm* c, const uint32_t* idx, co
                                         uint64_t N, const sparcml_opts* opts, void* out, size_t out_bytes,
                                         void* stream) {
   if (c && c->local) return fail(c, SPARCML_ERR_STATE, "use sparcml_sparse_allgather_local on a loopback world");
-  return allgather_impl(c, &idx, &val, &nnz, N, opts, &out, out_bytes, stream);
+  const void* v = val;
+  return allgather_impl(c, &idx, &v, &nnz, N, opts, &out, out_bytes, stream);
 }
 
 sparcml_status sparcml_sparse_allgather_local(sparcml_comm* c, const uint32_t* const* idx, const float* const* val,
@@ -911,7 +915,25 @@ sparcml_status sparcml_sparse_allgather_local(sparcml_comm* c, const uint32_t* c
                                               void* const* out, size_t out_bytes, void* stream) {
   if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
   if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
-  return allgather_impl(c, idx, val, nnz, N, opts, out, out_bytes, stream);
+  std::vector<const void*> v(val, val + c->P);
+  return allgather_impl(c, idx, v.data(), nnz, N, opts, out, out_bytes, stream);
+}
+
+sparcml_status sparcml_sparse_allgather_f64(sparcml_comm* c, const uint32_t* idx, const double* val, uint64_t nnz,
+                                        uint64_t N, const sparcml_opts* opts, void* out, size_t out_bytes,
+                                        void* stream) {
+  if (c && c->local) return fail(c, SPARCML_ERR_STATE, "use sparcml_sparse_allgather_local_f64 on a loopback world");
+  const void* v = val;
+  return allgather_impl(c, &idx, &v, &nnz, N, opts, &out, out_bytes, stream, 1);
+}
+
+sparcml_status sparcml_sparse_allgather_local_f64(sparcml_comm* c, const uint32_t* const* idx, const double* const* val,
+                                              const uint64_t* nnz, uint64_t N, const sparcml_opts* opts,
+                                              void* const* out, size_t out_bytes, void* stream) {
+  if (!c || !idx || !val || !nnz || !out) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
+  if (!c->local) return fail(c, SPARCML_ERR_STATE, "not a loopback world");
+  std::vector<const void*> v(val, val + c->P);
+  return allgather_impl(c, idx, v.data(), nnz, N, opts, out, out_bytes, stream, 1);
 }
 
 sparcml_status sparcml_barrier(sparcml_comm* c, void* stream) {

@@ -189,23 +189,25 @@ struct P1PrepArgs {                 // P == 1: validate, fill the control block,
 // ------------------------------------------------------ sparse allgather --
 struct AgPublishArgs {
   const uint32_t* idx;
-  const float* val;
+  const void* val;                 // float or double (f64)
   uint64_t n, N;
   int P, rank;
   uint32_t* my_idx;                // my published copy (my workspace)
-  float* my_val;
+  void* my_val;
   Ctrl* peer[kMaxRanks];
   Ctrl* ctl;
   int validate;
+  int f64;
 };
 struct AgGatherArgs {
   int P, rank;
   uint64_t N, delta;
   const uint32_t* src_idx[kMaxRanks];   // every rank's published stream (peer pointers)
-  const float* src_val[kMaxRanks];
+  const void* src_val[kMaxRanks];
   Ctrl* ctl;
   char* out;
   uint64_t val_offset;
+  int f64;
 };
 
 // -------------------------------------------------- layer-wise fusion ------

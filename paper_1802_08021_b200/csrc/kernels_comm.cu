@@ -1553,12 +1553,13 @@ cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off,
 // sparse allgather for disjoint slices (§7 SCD; reading R-27):
 // publish (local copy + announce to every peer), then one pull-concatenation
 // ===========================================================================
+template <typename V>
 __global__ void __launch_bounds__(kThreads) ag_publish_kernel(AgPublishArgs a) {
   for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += (uint64_t)gridDim.x * kThreads) {
     const uint32_t x = a.idx[e];
-    const float v = a.val[e];
+    const V v = static_cast<const V*>(a.val)[e];
     a.my_idx[e] = x;
-    a.my_val[e] = v;
+    static_cast<V*>(a.my_val)[e] = v;
     if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
   }
   if (last_block<false>(&a.ctl->done_ctr[0]) && threadIdx.x < a.P) {   // local copies only: gpu scope
@@ -1575,11 +1576,13 @@ cudaError_t launch_ag_publish(const AgPublishArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)std::max<uint64_t>(
       1, std::min<uint64_t>((a.n + kThreads - 1) / kThreads, (uint64_t)device_sm_count() * 4));
   SPARCML_PROF("ag_publish", s);
-  ag_publish_kernel<<<blocks, kThreads, 0, s>>>(a);
+  if (a.f64) ag_publish_kernel<double><<<blocks, kThreads, 0, s>>>(a);
+  else ag_publish_kernel<float><<<blocks, kThreads, 0, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
   __shared__ uint64_t s_n[kMaxRanks], s_pref[kMaxRanks + 1], s_upref[kMaxRanks + 1];
   __shared__ uint32_t s_first[kMaxRanks], s_last[kMaxRanks];
@@ -1626,12 +1629,12 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
   const uint64_t gtid = (uint64_t)blockIdx.x * kThreads + tid;
   if (!dense) {   // concatenation in range order, units of 4 pairs, four units' NVLink loads in flight
     uint32_t* out_idx = reinterpret_cast<uint32_t*>(a.out + SPARCML_HEADER_BYTES);
-    float* out_val = reinterpret_cast<float*>(a.out + a.val_offset);
+    V* out_val = reinterpret_cast<V*>(a.out + a.val_offset);
     const uint64_t units = s_upref[m];
     constexpr int U = 4;
     for (uint64_t u0 = gtid; u0 < units; u0 += gstride * U) {
       uint4 ix[U];
-      float4 vx[U];
+      V vx[U][4];
       uint64_t oo[U];
       int cnt[U];
 #pragma unroll
@@ -1645,18 +1648,15 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
         const uint64_t p = (u - s_upref[i]) * 4;
         const uint64_t nr = s_n[r];
         oo[x] = s_pref[i] + p;
-        if (p + 4 <= nr) {
+        const int n = (int)std::min<uint64_t>(4, nr - p);
+        if (n == 4) {
           ix[x] = *reinterpret_cast<const uint4*>(a.src_idx[r] + p);
-          vx[x] = *reinterpret_cast<const float4*>(a.src_val[r] + p);
-          cnt[x] = 4;
         } else {
           const uint32_t* si = a.src_idx[r] + p;
-          const float* sv = a.src_val[r] + p;
-          const int n = (int)(nr - p);
           ix[x] = make_uint4(si[0], n > 1 ? si[1] : 0u, n > 2 ? si[2] : 0u, 0u);
-          vx[x] = make_float4(sv[0], n > 1 ? sv[1] : 0.0f, n > 2 ? sv[2] : 0.0f, 0.0f);
-          cnt[x] = n;
         }
+        load4(static_cast<const V*>(a.src_val[r]) + p, n, vx[x]);
+        cnt[x] = n;
       }
 #pragma unroll
       for (int x = 0; x < U; ++x) {
@@ -1664,39 +1664,40 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
         if (n == 0) continue;
         const uint64_t o = oo[x];
         out_idx[o] = ix[x].x;
-        out_val[o] = vx[x].x;
+        out_val[o] = vx[x][0];
         if (n > 1) {
           out_idx[o + 1] = ix[x].y;
-          out_val[o + 1] = vx[x].y;
+          out_val[o + 1] = vx[x][1];
         }
         if (n > 2) {
           out_idx[o + 2] = ix[x].z;
-          out_val[o + 2] = vx[x].z;
+          out_val[o + 2] = vx[x][2];
         }
         if (n > 3) {
           out_idx[o + 3] = ix[x].w;
-          out_val[o + 3] = vx[x].w;
+          out_val[o + 3] = vx[x][3];
         }
       }
     }
   } else {        // K > delta: zeros, then every value at its index
-    float* d = reinterpret_cast<float*>(a.out + SPARCML_HEADER_BYTES);
-    for (uint64_t e = gtid; e < a.N; e += gstride) d[e] = 0.0f;
+    V* d = reinterpret_cast<V*>(a.out + SPARCML_HEADER_BYTES);
+    for (uint64_t e = gtid; e < a.N; e += gstride) d[e] = V(0);
     grid.sync();
     for (uint64_t e = gtid; e < K; e += gstride) {
       int i = 0;
       while (e >= s_pref[i + 1]) ++i;
       const int r = s_ord[i];
       const uint64_t q = e - s_pref[i];
-      d[a.src_idx[r][q]] = a.src_val[r][q];
+      d[a.src_idx[r][q]] = static_cast<const V*>(a.src_val[r])[q];
     }
   }
   grid.sync();
   if (blockIdx.x == 0 && tid == 0) {
     const uint64_t mine = s_n[a.rank];
     write_header(reinterpret_cast<sparcml_header*>(a.out), dense ? SPARCML_REPR_DENSE : SPARCML_REPR_SPARSE,
-                 dense ? a.N : K, a.N, K, 8 * mine * (uint64_t)(a.P - 1), 8 * (K - mine), SPARCML_SPARSE_ALLGATHER,
-                 ctl->status, dense ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset);
+                 dense ? a.N : K, a.N, K, pair_bytes<V>() * mine * (uint64_t)(a.P - 1), pair_bytes<V>() * (K - mine),
+                 SPARCML_SPARSE_ALLGATHER, ctl->status, dense ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset,
+                 hdr_magic<V>());
     ctl->status = 0;
     __threadfence();
     ctl->seq = seq + 1;   // the call is complete on this rank
@@ -1704,16 +1705,17 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
 }
 
 cudaError_t launch_ag_gather(const AgGatherArgs& a, cudaStream_t s) {
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ag_gather_kernel, kThreads, 0);
-    occ = std::max(1, std::min(occ, 2));
+  static int occ[2] = {0, 0};
+  const int f = a.f64 ? 1 : 0;
+  const void* fn = a.f64 ? (const void*)ag_gather_kernel<double> : (const void*)ag_gather_kernel<float>;
+  if (!occ[f]) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[f], fn, kThreads, 0);
+    occ[f] = std::max(1, std::min(occ[f], 2));
   }
   AgGatherArgs ac = a;
   void* args[] = {(void*)&ac};
   SPARCML_PROF("ag_gather", s);
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)ag_gather_kernel, dim3(device_sm_count() * occ),
-                                                    dim3(kThreads), args, 0, s);
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(device_sm_count() * occ[f]), dim3(kThreads), args, 0, s);
   ++g_launches;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -51,7 +51,7 @@ EXPORTED = [
     "sparcml_profile_read", "sparcml_fuse_streams", "sparcml_layer_ranges", "sparcml_sparse_allgather",
     "sparcml_sparse_allgather_local", "sparcml_apply_update", "sparcml_quantize_norm",
     "sparcml_sparse_allreduce_f64", "sparcml_sparse_allreduce_local_f64", "sparcml_result_bytes_f64",
-    "sparcml_result_val_offset_f64",
+    "sparcml_result_val_offset_f64", "sparcml_sparse_allgather_f64", "sparcml_sparse_allgather_local_f64",
 ]
 
 
@@ -110,6 +110,8 @@ _sig = {
     "sparcml_quantize_norm": (_i32, [_p, _u64, _i32, C.c_uint32, _i32, _u64, _u64, _p, _p, _p]),
     "sparcml_sparse_allgather": (_i32, [_p, _p, _p, _u64, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_sparse_allgather_local": (_i32, [_p, _p, _p, _p, _u64, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_sparse_allgather_f64": (_i32, [_p, _p, _p, _u64, _u64, C.POINTER(Opts), _p, _sz, _p]),
+    "sparcml_sparse_allgather_local_f64": (_i32, [_p, _p, _p, _p, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_layer_ranges": (_i32, [_p, _i32, _p, _p, _p]),
     "sparcml_kernel_launches": (_u64, []),
     "sparcml_profile_enable": (None, [_i32]),
@@ -310,15 +312,19 @@ class LocalWorld:
         """Sparse allgather (§7 SCD, reading R-27): streams with disjoint index ranges.
         Returns the P out buffers (all hold the union)."""
         P = self.P
+        dt = _val_dtype(streams[0][1])
+        for i, v in streams:
+            _need(i, torch.int32, "idx")
+            _need(v, dt, "val")
         if outs is None:
-            outs = [new_out(N, streams[0][0].device) for _ in range(P)]
+            outs = [new_out(N, streams[0][0].device, dt) for _ in range(P)]
         ia = (C.c_void_p * P)(*[_ptr(i) for i, _ in streams])
         va = (C.c_void_p * P)(*[_ptr(v) for _, v in streams])
         na = (C.c_uint64 * P)(*[int(i.numel()) for i, _ in streams])
         oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
         o = opts if opts is not None else make_opts()
-        _check(_lib.sparcml_sparse_allgather_local(self._h, ia, va, na, N, C.byref(o), oa, int(outs[0].numel()),
-                                                   _stream(stream)), self._h)
+        fn = _lib.sparcml_sparse_allgather_local_f64 if dt == torch.float64 else _lib.sparcml_sparse_allgather_local
+        _check(fn(self._h, ia, va, na, N, C.byref(o), oa, int(outs[0].numel()), _stream(stream)), self._h)
         return outs
 
     def close(self):
@@ -379,12 +385,14 @@ class Comm:
                   opts: Optional[Opts] = None, stream=None) -> torch.Tensor:
         """Sparse allgather of streams with disjoint index ranges (§7 SCD, reading R-27)."""
         _need(idx, torch.int32, "idx")
-        _need(val, torch.float32, "val")
+        dt = _val_dtype(val)
+        _need(val, dt, "val")
         if out is None:
-            out = new_out(N, idx.device)
+            out = new_out(N, idx.device, dt)
         o = opts if opts is not None else make_opts()
-        _check(_lib.sparcml_sparse_allgather(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, C.byref(o),
-                                             out.data_ptr(), int(out.numel()), _stream(stream)), self._h)
+        fn = _lib.sparcml_sparse_allgather_f64 if dt == torch.float64 else _lib.sparcml_sparse_allgather
+        _check(fn(self._h, _ptr(idx), _ptr(val), int(idx.numel()), N, C.byref(o), out.data_ptr(), int(out.numel()),
+                  _stream(stream)), self._h)
         return out
 
     def allreduce_async(self, idx: torch.Tensor, val: torch.Tensor, N: int, out: Optional[torch.Tensor] = None,

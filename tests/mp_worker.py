@@ -150,7 +150,8 @@ def layerwise(comm, rank, P):
 def allgather(comm, rank, P):
     """§7 SCD sparse allgather over the IPC world: slices owned in shuffled order."""
     fails = 0
-    for N, per in [(1 << 20, 100), (1 << 16, 30_000)]:   # sparse, then K > delta (dense)
+    for N, per, dt in [(1 << 20, 100, np.float32), (1 << 16, 30_000, np.float32), (1 << 20, 300, np.float64),
+                       (1 << 16, 32_000, np.float64)]:   # sparse, then K > delta (dense); fp32 and fp64
         rng = np.random.default_rng(N + per)
         bounds = np.linspace(0, N, P + 1).astype(np.int64)
         order = rng.permutation(P)
@@ -159,11 +160,11 @@ def allgather(comm, rank, P):
             lo, hi = bounds[order[r]], bounds[order[r] + 1]
             n = min(per, hi - lo)
             i = np.sort(rng.choice(np.arange(lo, hi), n, replace=False)).astype(np.uint32)
-            streams.append((i, rng.standard_normal(n).astype(np.float32)))
+            streams.append((i, rng.standard_normal(n).astype(dt)))
         i, v = streams[rank]
         out = comm.allgather(torch.from_numpy(i.view(np.int32)).cuda(), torch.from_numpy(v).cuda(), N)
         g = S.read_result(out)
-        ref, st = oracle.sparse_allgather(N, streams)
+        ref, st = oracle.sparse_allgather(N, streams, dtype=dt)
         d, ei, ev = ref[rank]
         ok = g.header.status == 0 and g.dense == d
         if ok and d:

@@ -153,3 +153,34 @@ def test_apply_update_ignores_f64_results():
     S.apply_update(v, outs[0])
     torch.cuda.synchronize()
     assert torch.all(v == 1.0)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("frac", [0.01, 0.3, 0.8])
+def test_f64_sparse_allgather(orc, P, frac):
+    # disjoint slices (SCD, R-27) with double values; dense past floor(N*8/12)
+    N = 30_011
+    bounds = np.linspace(0, N, P + 1).astype(np.int64)
+    g = np.random.default_rng(P)
+    streams = []
+    for r in range(P):
+        lo, hi = bounds[P - 1 - r], bounds[P - r]   # ranks in reverse range order
+        n = int(frac * (hi - lo))
+        streams.append((np.sort(g.choice(np.arange(lo, hi), n, replace=False)).astype(np.uint32),
+                        g.standard_normal(n)))
+    w = S.LocalWorld(P, N, max(1, max(len(s[0]) for s in streams)))
+    outs = w.allgather(to_cuda(streams), N)
+    torch.cuda.synchronize()
+    ref, st = orc.sparse_allgather(N, streams, dtype=F64)
+    for r in range(P):
+        gr = S.read_result(outs[r])
+        d, ei, ev = ref[r]
+        assert gr.header.magic == S.HEADER_MAGIC_F64 and gr.header.status == 0
+        assert gr.dense == bool(d)
+        if d:
+            np.testing.assert_array_equal(gr.val.cpu().numpy(), ev)
+        else:
+            np.testing.assert_array_equal(gr.idx.cpu().numpy().view(np.uint32), ei)
+            np.testing.assert_array_equal(gr.val.cpu().numpy(), ev)
+        if P > 1:
+            assert gr.header.bytes_sent == st[r]["bytes_sent"] and gr.header.bytes_recv == st[r]["bytes_recv"]
