@@ -133,3 +133,26 @@ def lr_gradient_streams(P: int, N: int = 3_231_961, samples: int = 1000, feats: 
         np.add.at(gsum, inv, contrib)
         out.append((uniq.astype(np.uint32), gsum.astype(np.float32)))
     return out
+
+
+def lr_dataset(P: int, N: int, samples: int = 1000, feats: int = 100, seed: int = 0, block: int = 256,
+               zipf_a: float = 1.1):
+    """Per-rank synthetic sparse logistic-regression data with config 5's structure:
+    `samples` samples of `feats` binary features, feature blocks of `block` drawn
+    Zipf(zipf_a) over a random block permutation, labels y in {0, 1} from a hidden
+    sparse model (so the problem is learnable).  Returns [(feat int64[samples, feats], y float32[samples])]."""
+    nblocks = (N + block - 1) // block
+    perm = rng_for(seed, 10_000).permutation(nblocks)
+    w_true = np.zeros(N, np.float64)
+    gt = rng_for(seed, 20_000)
+    hot = gt.choice(N, size=max(1, N // 50), replace=False)
+    w_true[hot] = gt.standard_normal(len(hot)) * 2.0
+    out = []
+    for r in range(P):
+        g = rng_for(seed, r)
+        ranks = np.minimum(g.zipf(zipf_a, size=(samples, feats)) - 1, nblocks - 1)
+        feat = np.minimum(perm[ranks] * block + g.integers(0, block, size=(samples, feats)), N - 1)
+        margin = np.array([w_true[np.unique(f)].sum() for f in feat])
+        y = (g.random(samples) < 1.0 / (1.0 + np.exp(-margin))).astype(np.float32)
+        out.append((feat.astype(np.int64), y))
+    return out
