@@ -249,6 +249,9 @@ sparcml_status sparcml_sparse_allgather_local_f64(sparcml_comm* comm, const uint
  * not SPARCML_HEADER_MAGIC (e.g. an _f64 result) leaves v unchanged.
  * Errors: null arguments -> SPARCML_ERR_INVALID_ARG. */
 sparcml_status sparcml_apply_update(float* v, const void* out, void* stream);
+/* The same for an _f64 result (v: N doubles, one fp64 rounding per element);
+ * a result that is not fp64 (magic != SPARCML_HEADER_MAGIC_F64) leaves v unchanged. */
+sparcml_status sparcml_apply_update_f64(double* v, const void* out, void* stream);
 
 /* ---------------------- layer-wise tensor fusion ------------------------ */
 /* (the paper's deployment mode: "communication is

@@ -1060,6 +1060,12 @@ sparcml_status sparcml_apply_update(float* v, const void* out, void* stream) {
   return SPARCML_OK;
 }
 
+sparcml_status sparcml_apply_update_f64(double* v, const void* out, void* stream) {
+  if (!v || !out) return fail(nullptr, SPARCML_ERR_INVALID_ARG, "null argument");
+  CK(nullptr, launch_apply_update_f64(v, static_cast<const char*>(out), static_cast<cudaStream_t>(stream)));
+  return SPARCML_OK;
+}
+
 sparcml_status sparcml_layer_ranges(const void* out, int L, const uint64_t* off, uint64_t* starts, void* stream) {
   if (!out || !off || !starts || L <= 0 || L > kMaxLayers)
     return fail(nullptr, SPARCML_ERR_INVALID_ARG, "need 1..64 layers and non-null arguments");

@@ -254,6 +254,7 @@ cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);
 cudaError_t launch_p1_sparse(const P1PrepArgs& a, cudaStream_t s);
 cudaError_t launch_fuse_streams(const FuseArgs& a, cudaStream_t s);
 cudaError_t launch_apply_update(float* v, const char* out, cudaStream_t s);
+cudaError_t launch_apply_update_f64(double* v, const char* out, cudaStream_t s);
 cudaError_t launch_ag_publish(const AgPublishArgs& a, cudaStream_t s);
 cudaError_t launch_ag_gather(const AgGatherArgs& a, cudaStream_t s);
 cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off, uint64_t* starts, cudaStream_t s);

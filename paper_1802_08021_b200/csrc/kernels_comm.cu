@@ -1724,26 +1724,34 @@ cudaError_t launch_ag_gather(const AgGatherArgs& a, cudaStream_t s) {
 // ===========================================================================
 // Algorithm 1's update v <- v - g, g read from an allreduce result
 // ===========================================================================
-__global__ void __launch_bounds__(kThreads) apply_update_kernel(float* v, const char* out) {
+template <typename V>
+__global__ void __launch_bounds__(kThreads) apply_update_kernel(V* v, const char* out) {
   const sparcml_header* h = reinterpret_cast<const sparcml_header*>(out);
-  if (h->magic != SPARCML_HEADER_MAGIC) return;   // not an fp32 result
+  if (h->magic != hdr_magic<V>()) return;   // a result of the other value type
   const bool dense = h->repr == SPARCML_REPR_DENSE;
   const uint64_t n = dense ? h->N : h->nnz;
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   if (dense) {
-    const float* g = reinterpret_cast<const float*>(out + SPARCML_HEADER_BYTES);
-    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) v[e] = __fsub_rn(v[e], g[e]);
+    const V* g = reinterpret_cast<const V*>(out + SPARCML_HEADER_BYTES);
+    for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride) v[e] = v[e] - g[e];
   } else {
     const uint32_t* gi = reinterpret_cast<const uint32_t*>(out + SPARCML_HEADER_BYTES);
-    const float* gv = reinterpret_cast<const float*>(out + h->val_offset);
+    const V* gv = reinterpret_cast<const V*>(out + h->val_offset);
     for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < n; e += stride)
-      v[gi[e]] = __fsub_rn(v[gi[e]], gv[e]);
+      v[gi[e]] = v[gi[e]] - gv[e];
   }
 }
 
 cudaError_t launch_apply_update(float* v, const char* out, cudaStream_t s) {
   SPARCML_PROF("apply_update", s);
-  apply_update_kernel<<<device_sm_count() * 4, kThreads, 0, s>>>(v, out);
+  apply_update_kernel<float><<<device_sm_count() * 4, kThreads, 0, s>>>(v, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_update_f64(double* v, const char* out, cudaStream_t s) {
+  SPARCML_PROF("apply_update", s);
+  apply_update_kernel<double><<<device_sm_count() * 4, kThreads, 0, s>>>(v, out);
   ++g_launches;
   return cudaGetLastError();
 }

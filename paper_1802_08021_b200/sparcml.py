@@ -52,6 +52,7 @@ EXPORTED = [
     "sparcml_sparse_allgather_local", "sparcml_apply_update", "sparcml_quantize_norm",
     "sparcml_sparse_allreduce_f64", "sparcml_sparse_allreduce_local_f64", "sparcml_result_bytes_f64",
     "sparcml_result_val_offset_f64", "sparcml_sparse_allgather_f64", "sparcml_sparse_allgather_local_f64",
+    "sparcml_apply_update_f64",
 ]
 
 
@@ -107,6 +108,7 @@ _sig = {
     "sparcml_dequantize": (_i32, [_p, _p, _u64, _i32, C.c_uint32, _p, _p]),
     "sparcml_fuse_streams": (_i32, [_i32, _p, _p, _p, _p, _p, _p, _p]),
     "sparcml_apply_update": (_i32, [_p, _p, _p]),
+    "sparcml_apply_update_f64": (_i32, [_p, _p, _p]),
     "sparcml_quantize_norm": (_i32, [_p, _u64, _i32, C.c_uint32, _i32, _u64, _u64, _p, _p, _p]),
     "sparcml_sparse_allgather": (_i32, [_p, _p, _p, _u64, _u64, C.POINTER(Opts), _p, _sz, _p]),
     "sparcml_sparse_allgather_local": (_i32, [_p, _p, _p, _p, _u64, C.POINTER(Opts), _p, _sz, _p]),
@@ -533,6 +535,10 @@ def split_result(out: torch.Tensor, offsets: Sequence[int], stream=None):
 
 def apply_update(v: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
     """Algorithm 1's update v <- v - g from an allreduce result, on the device."""
+    if v.dtype == torch.float64:   # for an _f64 result
+        _need(v, torch.float64, "v")
+        _check(_lib.sparcml_apply_update_f64(v.data_ptr(), out.data_ptr(), _stream(stream)))
+        return v
     _need(v, torch.float32, "v")
     _check(_lib.sparcml_apply_update(v.data_ptr(), out.data_ptr(), _stream(stream)))
     return v

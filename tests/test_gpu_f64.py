@@ -184,3 +184,21 @@ def test_f64_sparse_allgather(orc, P, frac):
             np.testing.assert_array_equal(gr.val.cpu().numpy(), ev)
         if P > 1:
             assert gr.header.bytes_sent == st[r]["bytes_sent"] and gr.header.bytes_recv == st[r]["bytes_recv"]
+
+
+@pytest.mark.parametrize("k", [50, 4000])   # sparse and dense (K > floor(8N/12)) results
+def test_apply_update_f64(orc, k):
+    P, N = 2, 5000
+    streams = synth.uniform_streams(P, N, k, seed=k, kind="normal64")
+    w = S.LocalWorld(P, N, k)
+    outs = w.allreduce(to_cuda(streams), N)
+    v0 = np.random.default_rng(1).standard_normal(N)
+    v = torch.from_numpy(v0.copy()).cuda()
+    S.apply_update(v, outs[0])
+    v32 = torch.ones(N, device="cuda")
+    S.apply_update(v32, outs[0])   # an fp64 result leaves an fp32 vector unchanged
+    torch.cuda.synchronize()
+    ref, _, _ = orc.split_allgather(N, streams, dtype=F64)
+    _, g = orc.result_to_dense(ref[0], N, dtype=F64)
+    np.testing.assert_array_equal(v.cpu().numpy(), v0 - g)
+    assert torch.all(v32 == 1.0)
