@@ -425,7 +425,10 @@ cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
 // split phase (§5.3.2): slice by partition, push every slice and its
 // window-offset table into the owner's receive region over NVLink, then flag
 // ===========================================================================
-constexpr int kPushItems = 4;
+#ifndef SPARCML_PUSH_ITEMS
+#define SPARCML_PUSH_ITEMS 4
+#endif
+constexpr int kPushItems = SPARCML_PUSH_ITEMS;   // pairs per thread in the split push
 
 template <typename V>
 __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
@@ -1246,7 +1249,10 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     // sparse concatenation: disjoint ranges, globally sorted by construction
     // (P:511-515).  Units of 4 pairs of one owner: 16-byte loads over NVLink.
     const uint64_t units = s_upref[a.P];
-    constexpr int U = 4;   // units per thread per iteration: all their NVLink loads in flight
+#ifndef SPARCML_CONCAT_U
+#define SPARCML_CONCAT_U 4
+#endif
+    constexpr int U = SPARCML_CONCAT_U;   // units per thread per iteration: all their NVLink loads in flight
     for (uint64_t u0 = gtid; u0 < units; u0 += gstride * U) {
       uint4 ix[U];
       V vx[U][4];
@@ -1354,9 +1360,12 @@ static void launch_concat_t(const ConcatArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(concat_kernel<1, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  // one block per SM for the sparse concatenation (fewer flag pollers and a
-  // shorter completion count), four for the dense decode
-  const int grid = device_sm_count() * (a.host_dsar == 0 ? 1 : 4);
+  // two blocks per SM for the sparse concatenation (A/B at P = 2 and 4: 1 and
+  // 2 blocks per SM beat 4; 2 beats 1 by ~2 us at P = 4), four for the dense decode
+#ifndef SPARCML_CONCAT_BPSM
+#define SPARCML_CONCAT_BPSM 2
+#endif
+  const int grid = device_sm_count() * (a.host_dsar == 0 ? SPARCML_CONCAT_BPSM : 4);
   if (a.host_dsar != 1) {
     concat_kernel<0, V><<<grid, kThreads, smem, s>>>(a);
     ++g_launches;
