@@ -1082,7 +1082,11 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
   const bool f64 = a.f64 != 0;
   const size_t vb = f64 ? 8 : 4;
   if (a.host_dsar != 1) {   // SSAR (or undecided: the kernel exits if the device picks DSAR)
-    const uint64_t G = (uint64_t)owner_merge_occupancy(a.P, f64) * device_sm_count();
+#ifndef SPARCML_OWNER_BPSM
+#define SPARCML_OWNER_BPSM 0   // 0: as many blocks per SM as fit
+#endif
+    const int occ = owner_merge_occupancy(a.P, f64);
+    const uint64_t G = (uint64_t)(SPARCML_OWNER_BPSM > 0 ? std::min(occ, SPARCML_OWNER_BPSM) : occ) * device_sm_count();
     OwnerArgs ac = a;
     void* args[] = {(void*)&ac};
     SPARCML_PROF("owner", s);
