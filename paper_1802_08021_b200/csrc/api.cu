@@ -249,6 +249,8 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
   const Layout& L = c->L;
   const int Lg = L.L;
   const int P2 = 1 << Lg, E = c->P - P2;   // R-28: extra ranks P2..P-1 fold into 0..E-1
+  uint64_t max_in = L.max_nnz;             // bound on every rank's input (the comm's capacity)
+  for (size_t i = 0; i < R.size(); ++i) max_in = std::max<uint64_t>(max_in, nnz[i]);
   auto pos = [&](int r) -> int {           // R's slot of rank r (loopback: every rank)
     for (size_t i = 0; i < R.size(); ++i)
       if (R[i] == r) return (int)i;
@@ -305,6 +307,13 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     }
     a.ctl = ctrl_of(base);
     a.stage = t;
+    // the stage's input is at most 2^t inputs of <= max_nnz pairs (t = 0: two); if
+    // that cannot pass delta the output is sparse for sure: launch only the merge
+    // tiles it can need instead of a grid sized for a dense window pass
+    {
+      const uint64_t ub = std::min<uint64_t>(cc.N, (uint64_t)max_in << (t == 0 ? 1 : t + (E > 0 ? 1 : 0)));
+      a.grid = ub <= cc.delta ? (int)std::max<uint64_t>(1, (ub + kMergeTile - 1) / kMergeTile) : 0;
+    }
     a.ctr = &ctrl_of(base)->scan[0];
     a.status = status_of(L, base);
     a.f64 = cc.f64;

@@ -72,6 +72,7 @@ struct RdStageArgs {
   int last;
   int fold;                  // this rank folded an extra rank in (and sends it the result)
   int op;                    // reduction operator (R-30)
+  int grid;                  // blocks to launch (0: the default, enough for a dense window pass)
   sparcml_header* hdr;       // last stage only
   ScanCounters* ctr;
   TileStatus* status;

@@ -413,7 +413,7 @@ static size_t rd_stage_smem() {
 }
 
 cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s) {
-  const int grid = device_sm_count() * 4;
+  const int grid = a.grid > 0 ? std::min(a.grid, device_sm_count() * 4) : device_sm_count() * 4;
   SPARCML_PROF("rd_stage", s);
   if (a.f64) rd_stage_kernel<double><<<grid, kThreads, rd_stage_smem<double>(), s>>>(a);
   else rd_stage_kernel<float><<<grid, kThreads, rd_stage_smem<float>(), s>>>(a);
