@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -206,6 +207,19 @@ uint64_t effective_delta(uint64_t N, const sparcml_opts& o, int vbytes = 4) {
 }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// Programmatic dependent launch of the owner and concat kernels: opt-in
+// (SPARCML_PDL=1).  Correct (same tests, stress), but measured slower: +1 us at
+// P = 2 and +5 us at P = 4 per allreduce (profiles/r01_ab_pdl.log) -- the early
+// blocks spin on flags on SMs the push / owner still needs.
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("SPARCML_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
 
 sparcml_status check_opts(sparcml_comm* c, const sparcml_opts& o) {
   if (o.index_bytes != 4) return fail(c, SPARCML_ERR_INVALID_ARG, "index_bytes must be 4 (u32 indices, P:931)");
@@ -424,6 +438,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.st_val = base + L.stage_off + 4 * (size_t)P * L.cap_s;
     w.blk = reinterpret_cast<uint64_t*>(base + L.blk_off);
     w.f64 = cc.f64;
+    w.pdl = cc.host_dsar >= 0 && pdl_enabled() ? 1 : 0;   // one owner kernel: it may start during the push
     CK(c, launch_owner(w, cc.s));
   }
   for (size_t i = 0; i < R.size(); ++i) {
@@ -454,6 +469,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     a.host_dsar = cc.host_dsar;
     a.op = cc.op;
     a.f64 = cc.f64;
+    a.pdl = cc.host_dsar >= 0 && pdl_enabled() ? 1 : 0;
     CK(c, launch_concat(a, cc.s));
   }
   return SPARCML_OK;

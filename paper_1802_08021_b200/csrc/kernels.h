@@ -138,6 +138,7 @@ struct OwnerArgs {
   void* st_val;
   uint64_t* blk;
   int f64;
+  int pdl;                         // launch as a programmatic dependent of the push (host_dsar known)
 };
 
 struct ConcatArgs {
@@ -162,6 +163,7 @@ struct ConcatArgs {
   int host_dsar;                   // -1: launch both concat variants (the device decides), else 0/1
   int op;                          // reduction operator (R-30): neutral fill when densifying
   int f64;
+  int pdl;                         // launch as a programmatic dependent of the owner (host_dsar known)
 };
 
 struct BarrierArgs {

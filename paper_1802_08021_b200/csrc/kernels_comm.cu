@@ -105,6 +105,33 @@ __device__ __forceinline__ void check_input(const uint32_t* idx, uint64_t e, uin
   if (!isfinite(v)) atomicOr(status, 1u << SPARCML_ERR_NONFINITE);
 }
 
+// Programmatic dependent launch: the next kernel of the call (owner after the
+// push, concat after the owner) may be scheduled as soon as every block of
+// this one has started; it orders itself on device flags, not on stream order.
+__device__ __forceinline__ void allow_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch with the programmatic-stream-serialization attribute (and cooperative if asked).
+static cudaError_t launch_pdl(const void* fn, dim3 grid, size_t smem, cudaStream_t s, void** args, bool coop) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 // value type traits: header magic, bytes of a (u32, value) pair and of a dense word
 template <typename V>
 __host__ __device__ constexpr uint32_t hdr_magic() {
@@ -437,6 +464,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
   const uint64_t base = (uint64_t)blockIdx.x * kThreads * kPushItems;
   const uint64_t last = std::min<uint64_t>(a.n, base + (uint64_t)kThreads * kPushItems) - 1;
   const uint64_t part = a.bnd[1];   // floor(N/P); owner(x) = min(x / part, P - 1)
+  allow_dependents();
   // slice boundaries s_off[j] = first position with idx >= b_j: block 0 needs
   // all of them (counts, empty slices), the others only those of the owners
   // their element range touches (usually two searches)
@@ -811,6 +839,7 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
   const int tid = threadIdx.x;
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
+  allow_dependents();
   dbg_mark(ctl, 0);
   for (int q = tid; q < kMaxTreeH * P; q += kThreads) {
     const int hh = q / P, sl = q - hh * P;
@@ -935,6 +964,7 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
+  allow_dependents();
   if (!owner_prologue(a, seq, s_ks, &s_dsar)) return;   // SSAR: the merge kernel reduces
   const uint64_t nwin = ceil_div(a.hi - a.lo, kWin);
   const uint64_t ntab = ceil_div(a.hi - a.lo, kTab);
@@ -1090,8 +1120,11 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
     OwnerArgs ac = a;
     void* args[] = {(void*)&ac};
     SPARCML_PROF("owner", s);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)owner_merge_fn(a.P, f64), dim3((unsigned)G),
-                                                dim3(kThreads), args, owner_merge_smem_bytes(a.P, vb), s);
+    cudaError_t e =
+        a.pdl ? launch_pdl((const void*)owner_merge_fn(a.P, f64), dim3((unsigned)G), owner_merge_smem_bytes(a.P, vb),
+                           s, args, true)
+              : cudaLaunchCooperativeKernel((const void*)owner_merge_fn(a.P, f64), dim3((unsigned)G), dim3(kThreads),
+                                            args, owner_merge_smem_bytes(a.P, vb), s);
     ++g_launches;
     if (e != cudaSuccess) return e;
     e = cudaGetLastError();
@@ -1109,7 +1142,14 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
     const uint64_t nwin = (a.hi - a.lo + kWin - 1) / kWin;
     const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(nwin, (uint64_t)occ[f64][a.P] * device_sm_count()));
     SPARCML_PROF("owner_dsar", s);
-    f<<<(unsigned)G, kThreads, smem, s>>>(a);
+    if (a.pdl) {
+      OwnerArgs ac = a;
+      void* args[] = {(void*)&ac};
+      const cudaError_t e = launch_pdl((const void*)f, dim3((unsigned)G), smem, s, args, false);
+      if (e != cudaSuccess) return e;
+    } else {
+      f<<<(unsigned)G, kThreads, smem, s>>>(a);
+    }
     ++g_launches;
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1142,7 +1182,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   // stream.  The variant that is not the case returns before anything else:
   // when both are launched (host_dsar == -1) the one running second must not
   // wait for owner flags of a call the first has already completed (seq + 1).
-  if (tid == 0) s_dsar = *(volatile uint32_t*)&ctl->dsar;
+  if (tid == 0) s_dsar = a.host_dsar >= 0 ? (uint32_t)a.host_dsar : *(volatile uint32_t*)&ctl->dsar;
   __syncthreads();
   const bool dsar = s_dsar != 0;
   if (dsar != (MODE == 1)) return;
@@ -1370,12 +1410,16 @@ static void launch_concat_t(const ConcatArgs& a, cudaStream_t s) {
 #define SPARCML_CONCAT_BPSM 2
 #endif
   const int grid = device_sm_count() * (a.host_dsar == 0 ? SPARCML_CONCAT_BPSM : 4);
+  ConcatArgs ac = a;
+  void* args[] = {(void*)&ac};
   if (a.host_dsar != 1) {
-    concat_kernel<0, V><<<grid, kThreads, smem, s>>>(a);
+    if (a.pdl) launch_pdl((const void*)concat_kernel<0, V>, dim3(grid), smem, s, args, false);
+    else concat_kernel<0, V><<<grid, kThreads, smem, s>>>(a);
     ++g_launches;
   }
   if (a.host_dsar != 0) {
-    concat_kernel<1, V><<<grid, kThreads, smem, s>>>(a);
+    if (a.pdl) launch_pdl((const void*)concat_kernel<1, V>, dim3(grid), smem, s, args, false);
+    else concat_kernel<1, V><<<grid, kThreads, smem, s>>>(a);
     ++g_launches;
   }
 }
