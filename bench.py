@@ -70,10 +70,10 @@ def parse():
     return ap.parse_args()
 
 
-# A ~100 us spin kernel ahead of each timed step: the start event then fires
+# A ~0.5 ms spin kernel ahead of each timed step: the start event then fires
 # when the GPU reaches the step, not while it idles waiting for the host to
 # finish enqueueing (host launch latency is not kernel time; e2e keeps it).
-HOLD_CYCLES = 200_000
+HOLD_CYCLES = 1_000_000   # ~0.5 ms: covers host jitter (e.g. the clock sampler) while the step is enqueued
 
 
 def load_peaks():
