@@ -77,6 +77,8 @@ def lib(f64: bool = False):
         _lib.or_set_op.argtypes = [i32]
         _lib.or_brute_force_op.restype = u64
         _lib.or_brute_force_op.argtypes = [i32, u64, p, p, p, p, p]
+        _lib.or_apply_update.restype = i32
+        _lib.or_apply_update.argtypes = [p, u64, i32, u64, p, p]
         _lib.or_topk.restype = u64
         _lib.or_topk.argtypes = [p, u64, u64, p, p, p]
         _lib.or_ef_topk.restype = u64
@@ -403,6 +405,22 @@ def qsgd_dequantize(codes, scales, n, bits, bucket=1024):
     if rc != 0:
         raise ValueError("bad quantizer arguments")
     return out[:n]
+
+
+def apply_update(v, res, N, dtype=np.float32):
+    """Algorithm 1's v <- v - g (P:239) with g an allreduce result (dense, idx, val);
+    returns the updated copy of v."""
+    d, i, g = res
+    v = _fv(v, dtype).copy()
+    if len(v) != N:
+        raise ValueError("v must hold N values")
+    gi = _u32(i if not d else np.zeros(0, np.uint32))
+    gv = _fv(g, dtype)
+    n = N if d else len(gi)
+    rc = lib(_is64(dtype)).or_apply_update(_ptr(v), N, 1 if d else 0, n, _ptr(gi), _ptr(gv))
+    if rc != 0:
+        raise ValueError("index out of range")
+    return v
 
 
 def expected_nnz(k, N, P) -> float:

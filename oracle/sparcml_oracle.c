@@ -707,6 +707,24 @@ int or_qsgd_dequantize(const uint8_t* codes, const float* scales, uint64_t n,
 }
 
 /* ------------------------------------------------------------------------- */
+/* Algorithm 1, last line: v <- v - g                                 */
+/* ------------------------------------------------------------------------- */
+
+int or_apply_update(or_val* v, uint64_t N, int dense, uint64_t n,
+                    const uint32_t* idx, const or_val* val) {
+  uint64_t e;
+  if (dense) {
+    for (e = 0; e < N; e++) v[e] = v[e] - val[e];
+    return 0;
+  }
+  for (e = 0; e < n; e++) {
+    if (idx[e] >= N) return -1;
+    v[idx[e]] = v[idx[e]] - val[e];
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* App. B: expected result size for uniform supports                          */
 /* ------------------------------------------------------------------------- */
 

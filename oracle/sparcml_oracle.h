@@ -221,6 +221,15 @@ int or_qsgd_quantize(const float* x, uint64_t n, int bits, uint32_t B,
 int or_qsgd_dequantize(const uint8_t* codes, const float* scales, uint64_t n,
                        int bits, uint32_t B, float* out);
 
+/* Algorithm 1's model update v <- v - g ("v_{t+1} = v_t - g_t"):
+ * g is an allreduce result, dense (N values) or sparse (n strictly
+ * increasing indices with one value each; absent coordinates are the neutral
+ * 0 and leave v unchanged).  Every touched coordinate is one or_val
+ * round-to-nearest subtraction fl(v_j - g_j).  Returns 0, or -1 on a sparse
+ * index >= N. */
+int or_apply_update(or_val* v, uint64_t N, int dense, uint64_t n,
+                    const uint32_t* idx, const or_val* val);
+
 /* E[K] for uniform supports (App. B), the paper's
  * inclusion-exclusion sum N * sum_{i=1..P} (-1)^(i-1) C(P,i) (k/N)^i,
  * evaluated term by term in long double. */

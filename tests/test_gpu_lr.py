@@ -60,8 +60,7 @@ def test_lr_training_matches_oracle_and_learns(orc, P, bucket):
             hs.append((i, v))
         ref, _, _ = orc.split_allgather(N, hs, algo=orc.ALGO_SSAR_SPLIT)
         for r in range(P):
-            _, g = orc.result_to_dense(ref[r], N)
-            v_h[r] = (v_h[r] - g).astype(np.float32)
+            v_h[r] = orc.apply_update(v_h[r], ref[r], N)   # v <- v - g
             np.testing.assert_array_equal(e_d[r].cpu().numpy(), e_h[r])
             np.testing.assert_array_equal(v_d[r].cpu().numpy(), v_h[r])
         for r in range(1, P):   # every rank applies the same g: the replicas stay identical

@@ -356,3 +356,33 @@ def test_quantization_requires_sum(orc):
     with orc.op_scope(1):
         with pytest.raises(ValueError):
             orc.split_allgather(4096, streams, algo=orc.ALGO_DSAR_SPLIT, quant_bits=4)
+
+
+# ---- DSAR + QSGD: every element of the N-vector draws its own Philox counter ----------
+
+@pytest.mark.parametrize("P,N,B", [(2, 4096, 256), (4, 8192, 1024), (8, 8192, 512)])
+def test_dsar_qsgd_counter_is_the_global_index(orc, P, N, B):
+    """partition j's QSGD draws use ctr_base = b_j, so the
+    element at global index g draws u(seed, g).  Input: the dense sum is 1 at
+    every bucket start and 1/2 elsewhere (integer-free but exact: 1/4 + 1/4),
+    at 2 bits (s = 1) a 1/2 decodes to 1 iff u >= 1/2 iff bit 31 of Philox
+    word g%4 of counter g/4 is set -- computed from the KAT-pinned Philox
+    block, not from the quantizer.  A counter base of 0 per partition (every
+    owner reusing one stream) fails for every partition j >= 1."""
+    seed = 12345
+    idx = np.arange(N, dtype=np.uint32)
+    v = np.full(N, 0.25, np.float32)
+    v[::B] = 0.5
+    streams = [(idx, v), (idx, v)] + [(np.zeros(0, np.uint32), np.zeros(0, np.float32))] * (P - 2)
+    res, _, used = orc.split_allgather(N, streams, algo=orc.ALGO_DSAR_SPLIT, quant_bits=2, bucket=B, seed=seed)
+    out = res[0][2]
+    key = np.array([seed & 0xFFFFFFFF, seed >> 32], np.uint32)
+    expect = np.empty(N, np.float32)
+    for c in range(N // 4):
+        w = orc.philox4x32_10(np.array([c, 0, 0, 0], np.uint32), key)
+        for q in range(4):
+            expect[4 * c + q] = 1.0 if (w[q] >> 31) else 0.0
+    expect[::B] = 1.0            # |v| = scale decodes exactly (level s)
+    np.testing.assert_array_equal(out, expect)
+    for r in range(1, P):
+        np.testing.assert_array_equal(res[r][2], out)

@@ -152,3 +152,23 @@ def test_l2_needs_power_of_two_bucket(orc):
     with orc.qsgd_norm_scope(1):
         with pytest.raises(ValueError):
             orc.qsgd_quantize(np.ones(10, np.float32), 4, bucket=100)
+
+
+def test_l2_scale_summation_order_is_the_adjacent_pair_tree(orc):
+    """Pins the ORDER of R-31's sum of squares, not only its value: hand-derived
+    inputs on which the balanced adjacent-pair tree, a sequential fold, a
+    reversed fold and a strided tree all round differently (tests/golden)."""
+    g = _load("qsgd_examples.json")["l2_tree_order"]
+    ulp = np.float32(2.0 ** -23)
+    small = np.float32(2.0 ** -12)
+    for case in g["cases"]:
+        B = case["B"]
+        x = np.zeros(B, np.float32)
+        x[0] = 1.0
+        if B == 64:
+            x[1:] = small
+        else:
+            x[4:] = small
+        with orc.qsgd_norm_scope(1):
+            _, s = orc.qsgd_quantize(x, 8, bucket=B, seed=0)
+        assert s[0] == np.float32(1.0) + np.float32(case["scale_minus_1_in_ulps"]) * ulp, (B, s[0])
