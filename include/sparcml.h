@@ -327,6 +327,14 @@ sparcml_status sparcml_ef_topk(float* eps, const float* grad, float alpha, uint6
                                uint64_t k, uint64_t bucket, uint32_t* idx_out, float* val_out,
                                void* ws, size_t ws_bytes, void* stream);
 
+/* Diagnostics: the positions of the float4 granules the global top-k samples
+ * (4 values each) to set its candidate threshold on the current device, for a
+ * vector of N values; writes min(count, cap) of them to pos_host and returns
+ * the count (0 when N < 65536: no sampling).  The selection never depends on
+ * them for correctness -- an input that defeats the sample takes the exact
+ * re-filter path (passes == 2); tests use this to build such an input. */
+size_t sparcml_topk_sample_positions(uint64_t N, uint64_t* pos_host, size_t cap);
+
 /* Synchronous: device status of the last top-k run on `ws` (0 or
  * SPARCML_ERR_NONFINITE) and how many filter passes it needed. */
 sparcml_status sparcml_topk_status(const void* ws, uint32_t* status_host, uint32_t* passes_host,

@@ -1019,6 +1019,10 @@ sparcml_status sparcml_merge_sum(const uint32_t* ia, const float* va, uint64_t n
 
 size_t sparcml_topk_workspace_bytes(uint64_t N, uint64_t k) { return topk_workspace_bytes(N, k); }
 
+size_t sparcml_topk_sample_positions(uint64_t N, uint64_t* pos_host, size_t cap) {
+  return topk_sample_positions(N, pos_host, pos_host ? cap : 0);
+}
+
 static sparcml_status topk_common(const float* x, const float* grad, float alpha, int ef, float* xout, uint64_t N,
                                   uint64_t k, uint64_t bucket, uint32_t* io, float* vo, float* resid, void* ws,
                                   size_t ws_bytes, void* stream) {

@@ -264,6 +264,7 @@ cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off,
 
 // top-k / QSGD (kernels_topk.cu, kernels_qsgd.cu)
 size_t topk_workspace_bytes(uint64_t N, uint64_t k);
+size_t topk_sample_positions(uint64_t N, uint64_t* pos, size_t cap);   // diagnostics (tests)
 cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, float* x_out,
                         uint64_t N, uint64_t k, uint32_t* idx_out, float* val_out, float* residual,
                         void* ws, cudaStream_t s);

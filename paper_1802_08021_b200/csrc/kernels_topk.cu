@@ -1,114 +1,122 @@
 // kernels_topk.cu — top-k sparsification with error feedback (§2.2 P:216-224,
-// Algorithm 1) in one HBM pass over the N-vector, as ONE persistent
-// cooperative kernel (grid = SMs x resident blocks).  Between phases the grid
-// meets at a barrier whose LAST arriving block computes the next decision
-// (threshold, bin, prefix) and publishes it before releasing the others.
+// Algorithm 1).
 //
-//   S  sample : 8192 chunks of 8 values (one 32-byte sector every N/8192) ->
-//               magnitude histogram -> conservative candidate threshold tau
-//               (expected candidates ~ k + 4 sigma + 16 of the sample)
-//   F  filter : the streaming pass over the block's contiguous 4096-tiles:
-//               (EF) acc = fmaf(alpha, g, eps), eps <- acc; values with
-//               |x| >= tau compacted per tile in index order; histogram of
-//               candidate magnitudes in 4096 bins of width 2^s above tau
-//   R  refine : histogram the candidates of the crossing bin until the bin is a
-//               single magnitude: the exact k-th magnitude `kth` and how many
-//               of its ties to keep (usually one refine level)
-//   C  place  : per-block (gt, eq) counts -> grid prefix -> ordered placement of
-//               |x| > kth and the first `need` ties (lower index wins, R-18);
-//               the residual at the selected indices is zeroed.
-// If the sample under-estimates (fewer than k candidates) every block
-// re-filters with tau = 0 (exact; rare slow path, counted in `passes`).
+// Global top-k: ONE persistent cooperative kernel, one CTA of 16 warps per SM.
+// Every warp owns a contiguous run of 256-element chunks and streams it
+// through its own 4-stage TMA ring (cp.async.bulk global -> shared, mbarrier
+// completion), so HBM reads are in flight continuously and no block barrier
+// sits in the streaming loop.
+//
+//   S  sample : every CTA reads the SAME 4096 values (1024 float4 granules,
+//               one in the last chunk of every W/1024-th warp) and derives the
+//               same candidate threshold tau and histogram range [tau, split)
+//               -- no grid barrier.  (EF: a warp overwrites its last chunk only
+//               after every CTA has sampled: a counter, checked once per warp.)
+//   F  filter : (EF) acc = fmaf(alpha, g, eps), eps <- acc (st.global.v4);
+//               |acc| >= tau -> appended to the warp's candidate list in index
+//               order (shared memory, spilling to its global region) and
+//               binned into a 4096-bin shared histogram -> flushed to global.
+//   -- grid barrier A --
+//   R  every CTA reads the global histogram and finds the bin holding the
+//               k-th magnitude.  Width 1: exact.  At most 4096 candidates in
+//               it: LIST.  Otherwise refine (histogram those candidates, grid
+//               barrier, again).  Fewer than k candidates in all (the sample
+//               over-estimated tau): exact re-filter with tau = 0.
+//   L  each CTA publishes (#candidates above the bin, #in it) and appends the
+//               bin's candidates to a global list.
+//   -- grid barrier B --
+//   P  every CTA resolves the exact k-th magnitude and the number of its ties
+//               to take (lower index first, R-18) from the list, its own
+//               output offset from the per-CTA counts, then writes its
+//               selected pairs in index order and zeroes them in the residual.
+// Two grid barriers in the common case; all histogram slots are cleared after
+// barrier B (so a workspace can be reused at any N <= its size).
 #include <algorithm>
 #include <cmath>
 
-#include <cooperative_groups.h>
-
 #include "kernels.h"
-
-namespace cg = cooperative_groups;
 
 namespace sparcml {
 
-constexpr int kTopkTile = 4096;           // elements per filter tile (16 per thread)
-constexpr int kBins = 4096;
-constexpr int kCoarse = 64;                   // coarse bins of 64 fine bins each, stored after the fine ones
-constexpr int kHist = kBins + kCoarse;
-constexpr uint64_t kSampleMinN = 1u << 16;   // below this: tau = 0 (all candidates)
-constexpr uint32_t kSampleChunks = 8192;     // 8-value chunks sampled
-constexpr int kMaxGrid = 4096;
-#define kKeyEnd 0x80000000ull  // one past the largest |x| key (NaN included)
-constexpr int kLevels = 4;                   // histogram levels (12 + 12 + 7 key bits worst case)
+constexpr int kTkWarps = 16;
+constexpr int kTkThreads = kTkWarps * 32;
+constexpr int kChunk = 256;                   // elements per pipeline chunk (1 KB per array)
+#ifndef SPARCML_TOPK_RING_KB
+#define SPARCML_TOPK_RING_KB 8               // TMA ring bytes per warp (x, or eps and grad)
+#endif
+#ifndef SPARCML_TOPK_LATE_PRO
+#define SPARCML_TOPK_LATE_PRO 0              // 1: issue the TMA prologue after the sample (A/B diagnostics)
+#endif
+#ifndef SPARCML_TOPK_EPS_EF
+#define SPARCML_TOPK_EPS_EF 0                // 1: eps / residual stores with an L2 evict-first hint (A/B)
+#endif
+#ifndef SPARCML_TOPK_FENCE
+#define SPARCML_TOPK_FENCE 0                 // 1: proxy fence before every ring refill (A/B diagnostics)
+#endif
+constexpr int kBins = 4096;                   // bins per histogram level (last one: overflow [split, hi))
+constexpr int kLevels = 6;                    // histogram slots per call (filter, re-filter, refinements)
+constexpr int kListCap = 4096;                // crossing-bin candidates resolved in shared memory
+constexpr int kSampleGran = 1024;             // sampled float4 granules (4096 values)
+constexpr uint64_t kSampleMinN = 1u << 16;    // below this: tau = 0 (every value is a candidate)
+constexpr int kMaxGrid = 1024;
+constexpr uint64_t kKeyEnd = 0x80000000ull;   // one past the largest |x| key (NaN included)
+
+template <bool EF>
+struct TkCfg {
+  static constexpr int kArr = EF ? 2 : 1;               // eps and grad, or x
+  static constexpr int kStages = SPARCML_TOPK_RING_KB * 1024 / (kArr * kChunk * 4);   // chunks in flight per warp
+  static constexpr int kCap = 512;                      // candidates per warp kept in shared memory
+  static constexpr size_t kRing = (size_t)kTkWarps * kStages * kArr * kChunk * 4;
+  static constexpr size_t kBar = (size_t)kTkWarps * kStages * 8;
+  static constexpr size_t kSmem = kRing + kBar + (size_t)kBins * 4 + (size_t)kTkWarps * kCap * 8;
+  static_assert(kRing >= (size_t)kListCap * 8 + 2 * kMaxGrid * 4, "list staging reuses the ring");
+};
 
 struct TopkCtl {
-  uint64_t t_phase[16];     // %globaltimer at phase ends (block 0), diagnostics only
-  uint32_t hist_s[kHist];   // sample histogram (key >> 19), then its 64 coarse sums
-  uint32_t hist[kLevels][kHist];   // candidate histogram per refinement level (+ coarse sums)
-  uint64_t blk[kMaxGrid];   // per-block (gt | eq << 32) selected counts
-  uint32_t status, passes;
-  uint32_t smax;            // largest sampled key
-  uint32_t tile_ticket;     // filter tiles handed out dynamically
-  uint32_t spill;           // some block could not keep its candidates in shared memory
-  uint64_t t_blk[kMaxGrid][8];   // %globaltimer per block at phase ends (diagnostics)
+  uint32_t arrive;          // arrivals at the current grid barrier (reset by the last arriver)
+  uint32_t flag;            // grid barriers released so far (wrapping)
+  uint32_t calls;           // completed calls; parity p = calls & 1 selects the per-call slots below
+  uint32_t status, passes;  // last call: non-finite input seen, filter passes (1, or 2 after a re-filter)
+  uint32_t bad[2];          // per call parity: a non-finite value was seen
+  uint32_t sampled[2];      // per call parity: CTAs done sampling (EF write guard)
+  uint32_t list_n[2];       // per call parity: length of the crossing-bin list
+  uint32_t nofast[2];       // per call parity: some CTA could not sort its candidates (slow path)
+  uint32_t pad[1];
+  uint64_t t_phase[16];     // %globaltimer phase ends (SPARCML_DEBUG_MARKS); [15] = bucketed status
+  uint64_t dbg[32];         // CTA 0's fine-grained %globaltimer marks (SPARCML_DEBUG_MARKS)
+  alignas(16) uint32_t hist[2][kLevels][kBins];   // [call parity][slot]; 16-byte aligned (uint4 reads)
+  uint32_t cta_a[kMaxGrid];  // per CTA: candidates with key >= hi of the final range
+  uint32_t cta_e[kMaxGrid];  // per CTA: candidates in [lo, hi) of the final range
+  uint64_t t_cta[2][kMaxGrid];   // per CTA: %globaltimer at start and filter end (SPARCML_DEBUG_MARKS)
 };
 
 struct TopkLayout {
   TopkCtl* ctl;
-  uint64_t* tile_sel;       // per-tile (gt | eq << 32) selected counts
-  uint32_t* tile_count;
-  uint32_t* cand_idx;
-  float* cand_val;
-  uint64_t* gsum;           // per 64-tile group: sum of tile_sel (fast placement path)
-  uint64_t ntiles, ngroups;
+  uint4* list;              // (index, key, cta, 0) of the crossing bin's candidates
+  uint32_t* sp_idx;         // per-warp candidate spill regions (the warp's element range)
+  float* sp_val;
 };
-
-constexpr int kGroupTiles = 64;
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static TopkLayout topk_layout(void* ws, uint64_t N) {
   TopkLayout L;
   char* p = static_cast<char*>(ws);
-  L.ntiles = (N + kTopkTile - 1) / kTopkTile;
   L.ctl = reinterpret_cast<TopkCtl*>(p);
   p += align256(sizeof(TopkCtl));
-  L.tile_sel = reinterpret_cast<uint64_t*>(p);
-  p += align256(L.ntiles * sizeof(uint64_t));
-  L.tile_count = reinterpret_cast<uint32_t*>(p);
-  p += align256(L.ntiles * sizeof(uint32_t));
-  L.cand_idx = reinterpret_cast<uint32_t*>(p);
-  p += align256(L.ntiles * kTopkTile * sizeof(uint32_t));
-  L.cand_val = reinterpret_cast<float*>(p);
-  p += align256(L.ntiles * kTopkTile * sizeof(float));
-  L.ngroups = (L.ntiles + kGroupTiles - 1) / kGroupTiles;
-  L.gsum = reinterpret_cast<uint64_t*>(p);
+  L.list = reinterpret_cast<uint4*>(p);
+  p += align256((size_t)kListCap * sizeof(uint4));
+  L.sp_idx = reinterpret_cast<uint32_t*>(p);
+  p += align256(N * sizeof(uint32_t));
+  L.sp_val = reinterpret_cast<float*>(p);
   return L;
 }
 
 size_t topk_workspace_bytes(uint64_t N, uint64_t /*k*/) {
-  const uint64_t nt = (N + kTopkTile - 1) / kTopkTile;
-  return align256(sizeof(TopkCtl)) + align256(nt * sizeof(uint64_t)) + align256(nt * sizeof(uint32_t)) +
-         2 * align256(nt * kTopkTile * sizeof(uint32_t)) + align256(((nt + 63) / 64) * sizeof(uint64_t));
+  return align256(sizeof(TopkCtl)) + align256((size_t)kListCap * sizeof(uint4)) + 2 * align256(N * sizeof(uint32_t));
 }
 
 __device__ __forceinline__ uint32_t abs_key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
-
-__device__ __forceinline__ void mark(TopkCtl* c, int i) {
-  if (threadIdx.x == 0) {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (blockIdx.x == 0) c->t_phase[i] = t;
-    if (i < 8) c->t_blk[blockIdx.x][i] = t;
-  }
-}
-
-// level binning: bins 0..kBins-2 cover [lo, split) in steps of 2^shift (the
-// shift is chosen so that they do), bin kBins-1 collects every key >= split
-__device__ __forceinline__ uint32_t bin_of(uint32_t key, uint64_t lo, uint64_t split, uint32_t shift) {
-  if ((uint64_t)key >= split) return kBins - 1;
-  const uint64_t b = ((uint64_t)key - lo) >> shift;
-  return b < (uint64_t)(kBins - 1) ? (uint32_t)b : (uint32_t)(kBins - 2);
-}
 
 __host__ __device__ __forceinline__ uint32_t shift_for(uint64_t span, uint64_t nbins) {
   uint32_t s = 0;
@@ -116,642 +124,1107 @@ __host__ __device__ __forceinline__ uint32_t shift_for(uint64_t span, uint64_t n
   return s;
 }
 
-// Grid-wide barrier of a cooperative launch.  The last block to arrive runs
-// f() (whole block) before releasing the others; f's global writes are
-// visible to every block after the barrier.
-// Whole block: the highest bin b with above0 + (count in bins > b) < target
-// <= above0 + (count in bins >= b).  h is staged through shared memory
-// (coalesced).  Returns b and the count strictly above it (including above0).
-// If the histogram cannot reach the target: b = 0 and *reached = false.
-struct BinFind {
-  uint32_t bin;
-  uint64_t above;
-  bool reached;
+// bins 0..kBins-2 cover [lo, split) in steps of 2^shift; kBins-1 holds keys >= split
+__device__ __forceinline__ uint32_t bin_of(uint32_t key, uint32_t lo, uint64_t split, uint32_t shift) {
+  if ((uint64_t)key >= split) return kBins - 1;
+  const uint32_t b = (key - lo) >> shift;
+  return b < (uint32_t)(kBins - 1) ? b : (uint32_t)(kBins - 2);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---- TMA bulk copies and mbarriers (PTX) ---------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "TK_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TK_DONE;\n\t"
+      "bra TK_WAIT;\n"
+      "TK_DONE:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ float4 lds_f4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// ---- diagnostics (compiled in only with -DSPARCML_DEBUG_MARKS) -------------------
+__device__ __forceinline__ void tk_mark(TopkCtl* c, int i) {
+  // [0] CTA 0's start, [1..7] the latest CTA's end of phase i, [8] the latest
+  // CTA's start, [9..14] CTA 0's end of phases 1..6
+#ifdef SPARCML_DEBUG_MARKS
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (i == 0) {
+      if (blockIdx.x == 0) c->t_phase[0] = t;
+      atomicMax(reinterpret_cast<unsigned long long*>(&c->t_phase[8]), (unsigned long long)t);
+    } else {
+      atomicMax(reinterpret_cast<unsigned long long*>(&c->t_phase[i]), (unsigned long long)t);
+      if (blockIdx.x == 0 && i <= 6) c->t_phase[8 + i] = t;
+    }
+  }
+#else
+  (void)c;
+  (void)i;
+#endif
+}
+
+#ifdef SPARCML_DEBUG_MARKS
+#define TK_D(i)                                                        \
+  do {                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                         \
+      uint64_t t_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));           \
+      c->dbg[i] = t_;                                                  \
+    }                                                                  \
+  } while (0)
+#define TK_C(j)                                                        \
+  do {                                                                 \
+    if (threadIdx.x == 0) {                                            \
+      uint64_t t_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));           \
+      c->t_cta[j][blockIdx.x] = t_;                                    \
+    }                                                                  \
+  } while (0)
+#define TK_V(i, v)                                                     \
+  do {                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->dbg[i] = (uint64_t)(v); \
+  } while (0)
+#else
+#define TK_D(i) \
+  do {          \
+  } while (0)
+#define TK_V(i, v) \
+  do {             \
+  } while (0)
+#define TK_C(j) \
+  do {          \
+  } while (0)
+#endif
+
+// ---- block primitives (kTkThreads) ------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T blk_excl_sum(T x, T* sc, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T inc = warp_inclusive_sum(x);
+  if (lane == 31) sc[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const T w = lane < kTkWarps ? sc[lane] : T(0);
+    const T wi = warp_inclusive_sum(w);
+    if (lane < kTkWarps) sc[lane] = wi - w;
+    if (lane == kTkWarps - 1) sc[kTkWarps] = wi;
+  }
+  __syncthreads();
+  const T r = sc[warp] + inc - x;
+  *total = sc[kTkWarps];
+  __syncthreads();
+  return r;
+}
+
+// two exclusive block sums with one set of barriers
+__device__ __forceinline__ void blk_excl_sum2(uint64_t x, uint64_t y, uint64_t* sc /*2*(kTkWarps+1)*/, uint64_t* ex,
+                                              uint64_t* ey) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t ix = warp_inclusive_sum(x), iy = warp_inclusive_sum(y);
+  if (lane == 31) {
+    sc[warp] = ix;
+    sc[kTkWarps + 1 + warp] = iy;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t wx = lane < kTkWarps ? sc[lane] : 0, wy = lane < kTkWarps ? sc[kTkWarps + 1 + lane] : 0;
+    const uint64_t jx = warp_inclusive_sum(wx), jy = warp_inclusive_sum(wy);
+    if (lane < kTkWarps) {
+      sc[lane] = jx - wx;
+      sc[kTkWarps + 1 + lane] = jy - wy;
+    }
+  }
+  __syncthreads();
+  *ex = sc[warp] + ix - x;
+  *ey = sc[kTkWarps + 1 + warp] + iy - y;
+  __syncthreads();
+}
+
+struct Cross {
+  uint32_t bin;    // crossing bin
+  uint32_t cnt;    // its count
+  uint64_t above;  // count in the bins above it (or the histogram total if !ok)
+  int ok;          // the histogram reaches the target
 };
 
-// Up to two targets.  Two small reads instead of one 16 KB one (every block
-// runs this on the same histogram right after a grid barrier, so the read is
-// the contended part): warp 0 scans the 64 coarse sums from the top, then warp
-// q scans the 64 fine bins of target q's coarse bin.  Same result as a scan of
-// the fine bins (the coarse sums are their exact sums).
-__device__ __forceinline__ bool pair_find(uint32_t hi, uint32_t lo, uint64_t base, uint64_t tg, uint32_t* which,
-                                          uint64_t* above) {
-  // lane holds bins (hi, lo) of a descending scan; base = count above them
-  if (!(base < tg && base + hi + lo >= tg)) return false;
-  if (base + hi >= tg) {
-    *which = 0;
-    *above = base;
-  } else {
-    *which = 1;
-    *above = base + hi;
+// Whole block, shared histogram h[NB] (NB = 512 * per): for each target t, the
+// highest bin b with sum_{bins > b} < t <= sum_{bins >= b}.  Thread i scans bins
+// NB-1-per*i down to NB-per*(i+1).  Results in s_out[0..1].
+template <int NB>
+__device__ __forceinline__ void find2(const uint32_t* h, uint64_t t0, uint64_t t1, uint64_t* sc, Cross* s_out) {
+  constexpr int per = NB / kTkThreads;
+  static_assert(per % 4 == 0, "uint4 reads");
+  const int tid = threadIdx.x;
+  const int base = NB - per * (tid + 1);
+  uint32_t v[per];   // v[i] = bin base+i
+#pragma unroll
+  for (int q = 0; q < per; q += 4) {
+    const uint4 u = *reinterpret_cast<const uint4*>(h + base + q);
+    v[q] = u.x;
+    v[q + 1] = u.y;
+    v[q + 2] = u.z;
+    v[q + 3] = u.w;
   }
+  uint64_t loc = 0;
+#pragma unroll
+  for (int i = 0; i < per; ++i) loc += v[i];
+  uint64_t tot;
+  const uint64_t ex = blk_excl_sum<uint64_t>(loc, sc, &tot);
+  const uint64_t tg[2] = {t0, t1};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (tid == 0 && tot < tg[q]) s_out[q] = Cross{0u, 0u, tot, 0};
+    if (ex < tg[q] && ex + loc >= tg[q]) {
+      uint64_t cum = ex;
+#pragma unroll
+      for (int i = per - 1; i >= 0; --i) {
+        if (cum < tg[q] && cum + v[i] >= tg[q]) s_out[q] = Cross{(uint32_t)(base + i), v[i], cum, 1};
+        cum += v[i];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ Cross find_desc(const uint32_t* h, uint64_t t, uint64_t* sc, Cross* s_out) {
+  find2<kBins>(h, t, t, sc, s_out);
+  const Cross r = s_out[0];
+  __syncthreads();
+  return r;
+}
+
+// Grid barrier of a cooperative launch: arrivals on a counter (the last
+// arriver resets it) and a wrapping release flag; `target` = the flag value
+// that releases this barrier.
+__device__ __forceinline__ void tk_grid_barrier(TopkCtl* c, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t old = atomicAdd(&c->arrive, 1u);
+    if (old == gridDim.x - 1) {
+      atomicExch(&c->arrive, 0u);
+      __threadfence();
+      st_release_gpu(&c->flag, target);
+    } else {
+      while ((int)(ld_relaxed_gpu_u32(&c->flag) - target) < 0) {
+      }
+      (void)ld_acquire_gpu(&c->flag);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Chunk split: C chunks over W warps, warp w owns [wstart(w), wstart(w) + wcount(w))
+// (32-bit: C < 2^24 for N < 2^32, W <= 16384).
+struct WSplit {
+  uint32_t base, rem;
+};
+__host__ __device__ __forceinline__ uint32_t wstart(const WSplit& s, uint32_t w) {
+  return w * s.base + (w < s.rem ? w : s.rem);
+}
+__host__ __device__ __forceinline__ uint32_t wcount(const WSplit& s, uint32_t w) { return s.base + (w < s.rem ? 1u : 0u); }
+
+// The float4 granule of sample q: in the last chunk of warp q*W/1024 (so EF can
+// guard its overwrite with one check per warp).  False if the granule does not
+// exist (the ragged final chunk of the vector holding < 4 values).
+__host__ __device__ __forceinline__ bool sample_pos(uint32_t q, uint64_t N, uint32_t C, uint32_t W, const WSplit& sp,
+                                                    uint64_t* pos) {
+  const uint32_t wq = (q * W) / kSampleGran;
+  const uint32_t cl = wstart(sp, wq) + wcount(sp, wq) - 1;
+  uint32_t gr = (q * 17u) & 63u;
+  if (cl + 1 == C) {
+    const uint32_t nval = (uint32_t)((N - (uint64_t)cl * kChunk < (uint64_t)kChunk ? N - (uint64_t)cl * kChunk
+                                                                                    : (uint64_t)kChunk) / 4);
+    if (nval == 0) return false;
+    gr %= nval;
+  }
+  *pos = (uint64_t)cl * kChunk + gr * 4;
   return true;
 }
 
-__device__ void find_bins(const uint32_t* h, uint64_t above0, const uint64_t* target, int ntarget, uint32_t* /*sm*/,
-                          BinFind* out) {
-  __shared__ uint32_t s_cb[2];
-  __shared__ uint64_t s_ca[2];
-  __shared__ int s_ok[2];
-  __shared__ BinFind s_res[2];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) {
-    const uint32_t* hc = h + kBins;
-    const uint32_t chi = __ldcg(&hc[63 - 2 * lane]), clo = __ldcg(&hc[62 - 2 * lane]);
-    const uint32_t s = chi + clo;
-    const uint64_t excl = warp_inclusive_sum<uint64_t>(s) - s;
-    for (int q = 0; q < ntarget; ++q) {
-      uint32_t which = 0;
-      uint64_t ab = 0;
-      const bool hit = pair_find(chi, clo, above0 + excl, target[q], &which, &ab);
-      const uint32_t m = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) s_ok[q] = m != 0;
-      if (hit) {
-        s_cb[q] = 63 - 2 * lane - which;
-        s_ca[q] = ab;
-      }
-    }
-  }
-  __syncthreads();
-  if (warp < ntarget) {
-    const int q = warp;
-    if (!s_ok[q]) {
-      if (lane == 0) s_res[q] = BinFind{0u, above0, false};
-    } else {
-      const uint32_t* hf = h + (size_t)s_cb[q] * 64;
-      const uint32_t fhi = __ldcg(&hf[63 - 2 * lane]), flo = __ldcg(&hf[62 - 2 * lane]);
-      const uint32_t s = fhi + flo;
-      const uint64_t excl = warp_inclusive_sum<uint64_t>(s) - s;
-      uint32_t which = 0;
-      uint64_t ab = 0;
-      if (pair_find(fhi, flo, s_ca[q] + excl, target[q], &which, &ab))
-        s_res[q] = BinFind{s_cb[q] * 64 + 63 - 2 * lane - which, ab, true};
-    }
-  }
-  __syncthreads();
-  for (int q = 0; q < ntarget; ++q) out[q] = s_res[q];
-  __syncthreads();
-}
-
-// One tile: 16 values per thread (4 coalesced float4 rows).  Candidates are
-// written in index order to the tile's region and binned into `sh`.
-#ifndef SPARCML_TOPK_KEEP
-#define SPARCML_TOPK_KEEP 1      // 0: always take the global-memory path (A/B diagnostics)
-#endif
-#ifndef SPARCML_TOPK_CANDCAP
-#define SPARCML_TOPK_CANDCAP 2048
-#endif
-#ifndef SPARCML_TOPK_MINB
-#define SPARCML_TOPK_MINB 3      // blocks per SM (A/B at N = 2^24: 3 beats 4 by 1.5 us, 2 loses 2.5 us)
-#endif
-constexpr int kCandCap = SPARCML_TOPK_CANDCAP;   // candidates a block keeps in shared memory
-constexpr int kTileCap = 32;     // tiles a block tracks
-
-// The block's filtered tiles and their candidates, kept in shared memory for
-// the refine / count / place phases (no global re-reads).  spill = some tile
-// did not fit: the whole grid then takes the global-memory path.
-struct KeepSmem {
-  uint32_t ci[kCandCap];
-  float cv[kCandCap];
-  uint32_t tl[kTileCap], tn[kTileCap], to[kTileCap];
-  uint64_t tp[kTileCap];
-  uint32_t ntl, nc, spill;
+struct TkArgs {
+  const float* x;   // EF: eps (read, then overwritten by acc through dst); else the input
+  const float* g;   // EF: the gradient
+  float alpha;
+  float* dst;       // STORE: EF -> eps (== x), sparsify -> residual (!= x)
+  float* zero_at;   // selected coordinates zeroed here (EF: eps; residual; x in place; or null)
+  uint64_t N, k;
+  uint32_t* idx_out;
+  float* val_out;
+  TopkLayout L;
 };
 
-template <bool EF, bool RESID, bool STORE>
-__device__ __forceinline__ void filter_tile(const float* __restrict__ x, const float* __restrict__ g, float alpha,
-                                            float* __restrict__ xout, float* __restrict__ resid, uint64_t N, uint64_t t,
-                                            uint32_t tau, uint64_t split, uint32_t shift, const TopkLayout& L,
-                                            uint32_t* sh, uint32_t* s_wt, uint32_t* s_status, KeepSmem* ks) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t base = t * kTopkTile;
-  const uint64_t pol = l2_evict_first_policy();
-  float v[4][4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
-    if (p + 4 <= N) {
-      const float4 a = ld_stream_f4_ef(reinterpret_cast<const float4*>(x + p), pol);
-      v[j][0] = a.x; v[j][1] = a.y; v[j][2] = a.z; v[j][3] = a.w;
+// Per-warp candidate storage: the first kCap in shared memory, the rest in the
+// warp's global spill region (its element range, so it never overflows).
+template <bool EF>
+struct CandStore {
+  uint32_t* si;
+  float* sv;
+  uint32_t* gi;
+  float* gv;
+  __device__ __forceinline__ void put(uint32_t pos, uint32_t idx, float v) const {
+    if (pos < (uint32_t)TkCfg<EF>::kCap) {
+      si[pos] = idx;
+      sv[pos] = v;
+    } else {
+      gi[pos - TkCfg<EF>::kCap] = idx;
+      gv[pos - TkCfg<EF>::kCap] = v;
+    }
+  }
+  __device__ __forceinline__ void get(uint32_t pos, uint32_t* idx, float* v) const {
+    if (pos < (uint32_t)TkCfg<EF>::kCap) {
+      *idx = si[pos];
+      *v = sv[pos];
+    } else {
+      *idx = gi[pos - TkCfg<EF>::kCap];
+      *v = gv[pos - TkCfg<EF>::kCap];
+    }
+  }
+};
+
+// One 128-element row of a chunk (4 consecutive values per lane): optional
+// store, non-finite check, in-order compaction of |v| >= tau, histogram.
+template <bool EF, bool STORE>
+__device__ __forceinline__ void consume_row(const float v[4], uint64_t gp, bool full, uint64_t N, float* dst,
+                                            uint32_t tau, uint64_t split, uint32_t shift, uint32_t* sh,
+                                            const CandStore<EF>& cs, uint32_t& nw, uint32_t& bad) {
+  if (STORE) {
+    if (full) {
+      *reinterpret_cast<float4*>(dst + gp) = make_float4(v[0], v[1], v[2], v[3]);
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[j][q] = (p + q < N) ? x[p + q] : 0.0f;
+      for (int j = 0; j < 4; ++j)
+        if (gp + j < N) dst[gp + j] = v[j];
     }
   }
-  if (EF) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
-      if (p + 4 <= N) {
-        const float4 a = ld_stream_f4_ef(reinterpret_cast<const float4*>(g + p), pol);
-        v[j][0] = __fmaf_rn(alpha, a.x, v[j][0]);
-        v[j][1] = __fmaf_rn(alpha, a.y, v[j][1]);
-        v[j][2] = __fmaf_rn(alpha, a.z, v[j][2]);
-        v[j][3] = __fmaf_rn(alpha, a.w, v[j][3]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (p + q < N) v[j][q] = __fmaf_rn(alpha, g[p + q], v[j][q]);
-      }
-    }
-  }
-  if (STORE) {   // EF: eps <- acc ; sparsify: residual <- x
-    float* dst = EF ? xout : resid;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
-      if (p + 4 <= N) {
-        st_stream_f4_ef(reinterpret_cast<float4*>(dst + p), make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), pol);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (p + q < N) dst[p + q] = v[j][q];
-      }
-    }
-  }
-  // candidate flags and in-order compaction over (row j, warp, lane, q)
-  uint32_t flags[4];
-  uint32_t bad = 0;
+  uint32_t fl = 0;
+  uint32_t key[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    flags[j] = 0;
-    const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t key = abs_key(v[j][q]);
-      if (p + q < N) {
-        bad |= key >= 0x7F800000u;
-        if (key >= tau) flags[j] |= 1u << q;
-      }
+    key[j] = abs_key(v[j]);
+    const bool valid = full || gp + j < N;
+    if (valid) {
+      bad |= key[j] >= 0x7F800000u ? 1u : 0u;
+      if (key[j] >= tau) fl |= 1u << j;
     }
   }
-  if (bad) *s_status = 1;
-  uint32_t incl[4];
+  const uint32_t lt = lanemask_lt();
+  uint32_t before = 0, tot = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    incl[j] = warp_inclusive_sum<uint32_t>(__popc(flags[j]));
-    if (lane == 31) s_wt[j * kWarps + warp] = incl[j];
+    const uint32_t bj = __ballot_sync(0xffffffffu, (fl >> j) & 1u);
+    before += __popc(bj & lt);
+    tot += __popc(bj);
   }
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = s_wt[lane];   // 4 * 8 = 32 entries, (j, warp) order
-    const uint32_t wi = warp_inclusive_sum<uint32_t>(w);
-    s_wt[32 + lane] = wi - w;
-    if (lane == 31) s_wt[64] = wi;
-  }
-  __syncthreads();
-  const uint32_t tcount = s_wt[64];
-  const uint32_t kb = ks ? ks->nc : 0u;
-  const bool keep = ks && kb + tcount <= (uint32_t)kCandCap && ks->ntl < (uint32_t)kTileCap;
+  if (fl) {
+    uint32_t pos = nw + before;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    uint32_t pos = s_wt[32 + j * kWarps + warp] + incl[j] - __popc(flags[j]);
-    const uint64_t p = base + (uint64_t)(j * kThreads + tid) * 4;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (flags[j] & (1u << q)) {
-        L.cand_idx[base + pos] = (uint32_t)(p + q);
-        L.cand_val[base + pos] = v[j][q];
-        if (keep) {
-          ks->ci[kb + pos] = (uint32_t)(p + q);
-          ks->cv[kb + pos] = v[j][q];
-        }
-        const uint32_t bn = bin_of(abs_key(v[j][q]), tau, split, shift);
-        atomicAdd(&sh[bn], 1u);
-        atomicAdd(&sh[kBins + (bn >> 6)], 1u);
+    for (int j = 0; j < 4; ++j)
+      if ((fl >> j) & 1u) {
+        cs.put(pos, (uint32_t)(gp + j), v[j]);
+        atomicAdd(&sh[bin_of(key[j], tau, split, shift)], 1u);
         ++pos;
       }
-    }
   }
-  if (tid == 0) L.tile_count[t] = tcount;
-  __syncthreads();
-  if (ks && tid == 0) {   // read by every thread only after the next tile's first barrier
-    if (keep) {
-      ks->tl[ks->ntl] = (uint32_t)t;
-      ks->tn[ks->ntl] = tcount;
-      ks->to[ks->ntl] = kb;
-      ks->ntl = ks->ntl + 1;
-      ks->nc = kb + tcount;
-    } else {
-      ks->spill = 1;
-    }
-  }
+  nw += tot;
 }
 
-// A refinement level: bins 0..kBins-2 cover [lo, split) in steps of 2^shift,
-// bin kBins-1 is [split, hi); `above` counts candidates with key >= hi.
-struct Level {
-  uint64_t lo, split, hi, above;
-  uint32_t shift;
-  int exact;
-  uint32_t kth;
-  uint64_t need;
-};
-
-// Narrow the level to the crossing bin f (found in this level's histogram).
-__device__ __forceinline__ void apply_narrow(Level& lv, const BinFind& f, uint64_t k) {
-  uint64_t nlo, nhi;
-  if (f.bin == kBins - 1) {
-    nlo = lv.split;
-    nhi = lv.hi;
-  } else {
-    nlo = lv.lo + ((uint64_t)f.bin << lv.shift);
-    nhi = min(lv.split, lv.lo + ((uint64_t)(f.bin + 1) << lv.shift));
-  }
-  lv.above = f.above;
-  lv.lo = nlo;
-  lv.split = nhi;
-  lv.hi = nhi;
-  if (nhi - nlo <= 1) {
-    lv.exact = 1;
-    lv.kth = (uint32_t)nlo;
-    lv.need = k - f.above;
-  } else {
-    lv.shift = shift_for(nhi - nlo, kBins - 1);
-  }
+// bins for the hot loop (32-bit: split <= 2^31)
+__device__ __forceinline__ uint32_t bin_of32(uint32_t key, uint32_t lo, uint32_t split, uint32_t shift) {
+  if (key >= split) return kBins - 1;
+  return min((key - lo) >> shift, (uint32_t)(kBins - 2));
 }
 
-// Whole block (every block computes the same result from the same global
-// histogram): locate the crossing bin of `h` and narrow the level.
-__device__ __forceinline__ void narrow(Level& lv, const uint32_t* h, uint64_t k, uint32_t* sm) {
-  BinFind f;
-  find_bins(h, lv.above, &k, 1, sm, &f);
-  apply_narrow(lv, f, k);
-}
-
-// Warp: load the (up to 128) candidates [i0, i0+128) of a tile, 4 per lane in flight.
-__device__ __forceinline__ void load4(const float* cv, uint32_t n, uint32_t i0, float v[4]) {
+// One full chunk from the TMA ring (the hot loop, kept short: it is issue-bound
+// otherwise).  Lane l holds elements 4l..4l+3 (row 0) and 128+4l..128+4l+3
+// (row 1).  Candidates (|v| >= tau, or unordered: NaN) are rare; their
+// in-order positions come from one packed warp scan of the per-row counts,
+// and each lane walks only its own set bits, re-reading the value from the
+// stage (EF: recomputing the same fma) instead of indexing registers.
+template <bool EF, bool STORE>
+__device__ __forceinline__ void hot_chunk(const float* sx, uint32_t e0, float alpha, float* dst, float tauf,
+                                          uint32_t lo, uint32_t split, uint32_t shift, uint32_t* sh,
+                                          const CandStore<EF>& cs, uint32_t& nw, uint32_t& bad) {
   const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const uint32_t i = i0 + r * 32 + lane;
-    v[r] = i < n ? __ldcg(&cv[i]) : 0.0f;
+  float4 r0 = lds_f4(sx + lane * 4), r1 = lds_f4(sx + 128 + lane * 4);
+  if (EF) {
+    const float4 g0 = lds_f4(sx + kChunk + lane * 4), g1 = lds_f4(sx + kChunk + 128 + lane * 4);
+    r0 = make_float4(__fmaf_rn(alpha, g0.x, r0.x), __fmaf_rn(alpha, g0.y, r0.y), __fmaf_rn(alpha, g0.z, r0.z),
+                     __fmaf_rn(alpha, g0.w, r0.w));
+    r1 = make_float4(__fmaf_rn(alpha, g1.x, r1.x), __fmaf_rn(alpha, g1.y, r1.y), __fmaf_rn(alpha, g1.z, r1.z),
+                     __fmaf_rn(alpha, g1.w, r1.w));
   }
+  if (STORE) {
+    if (SPARCML_TOPK_EPS_EF) {
+      const uint64_t pol = l2_evict_first_policy();
+      st_stream_f4_ef(reinterpret_cast<float4*>(dst + e0 + lane * 4), r0, pol);
+      st_stream_f4_ef(reinterpret_cast<float4*>(dst + e0 + 128 + lane * 4), r1, pol);
+    } else {
+      *reinterpret_cast<float4*>(dst + e0 + lane * 4) = r0;
+      *reinterpret_cast<float4*>(dst + e0 + 128 + lane * 4) = r1;
+    }
+  }
+  uint32_t m = 0;
+  m |= !(fabsf(r0.x) < tauf) ? 0x01u : 0u;
+  m |= !(fabsf(r0.y) < tauf) ? 0x02u : 0u;
+  m |= !(fabsf(r0.z) < tauf) ? 0x04u : 0u;
+  m |= !(fabsf(r0.w) < tauf) ? 0x08u : 0u;
+  m |= !(fabsf(r1.x) < tauf) ? 0x10u : 0u;
+  m |= !(fabsf(r1.y) < tauf) ? 0x20u : 0u;
+  m |= !(fabsf(r1.z) < tauf) ? 0x40u : 0u;
+  m |= !(fabsf(r1.w) < tauf) ? 0x80u : 0u;
+  if (!__any_sync(0xffffffffu, m)) return;
+  const uint32_t pk = (uint32_t)__popc(m & 0xFu) | ((uint32_t)__popc(m >> 4) << 16);
+  const uint32_t inc = warp_inclusive_sum<uint32_t>(pk);
+  const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+  const uint32_t ex = inc - pk;
+  uint32_t pos0 = nw + (ex & 0xFFFFu), pos1 = nw + (tot & 0xFFFFu) + (ex >> 16);
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const uint32_t el = (j < 4 ? 0u : 124u) + lane * 4 + j;   // j >= 4: 128 + 4l + (j - 4)
+    const float v = EF ? __fmaf_rn(alpha, sx[kChunk + el], sx[el]) : sx[el];
+    const uint32_t pos = j < 4 ? pos0++ : pos1++;
+    cs.put(pos, e0 + el, v);
+    const uint32_t key = abs_key(v);
+    bad |= key >= 0x7F800000u ? 1u : 0u;
+    atomicAdd(&sh[bin_of32(key, lo, split, shift)], 1u);
+  }
+  nw += (tot & 0xFFFFu) + (tot >> 16);
 }
 
-__device__ __forceinline__ void flush_hist(const uint32_t* sh, uint32_t* gh) {
-  __syncthreads();
-  for (int i = threadIdx.x; i < kHist; i += kThreads) {
-    const uint32_t v = sh[i];
-    if (v) atomicAdd(&gh[i], v);
-  }
-}
+template <bool EF, bool STORE>
+__global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
+  using Cfg = TkCfg<EF>;
+  constexpr int kCap = Cfg::kCap;
+  constexpr int kStages = Cfg::kStages;
+  extern __shared__ __align__(128) unsigned char tk_smem[];
+  float* ring = reinterpret_cast<float*>(tk_smem);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tk_smem + Cfg::kRing);
+  uint32_t* sh = reinterpret_cast<uint32_t*>(tk_smem + Cfg::kRing + Cfg::kBar);
+  uint32_t* cidx = sh + kBins;
+  float* cval = reinterpret_cast<float*>(cidx + kTkWarps * kCap);
+  __shared__ uint64_t s_sc[2 * (kTkWarps + 1)];
+  __shared__ Cross s_cross[2];
+  __shared__ uint32_t s_w[kTkWarps][2];
+  __shared__ uint32_t s_wn[kTkWarps];
+  __shared__ uint32_t s_bad, s_spill, s_nofast, s_lbase, s_quota;
+  __shared__ uint64_t s_off;
 
-constexpr int kGroup = 32;   // tiles per placement group (one warp scans their prefix)
-
-template <bool EF, bool RESID>
-__global__ void __launch_bounds__(kThreads, SPARCML_TOPK_MINB) topk_fused_kernel(const float* __restrict__ x,
-                                                                 const float* __restrict__ g, float alpha,
-                                                                 float* __restrict__ xout, float* __restrict__ resid,
-                                                                 uint64_t N, uint64_t k, uint32_t* __restrict__ idx_out,
-                                                                 float* __restrict__ val_out, float* zero_at,
-                                                                 TopkLayout L) {
-  __shared__ uint32_t sh[kBins + kBins / 16];   // histogram; find_bin staging (padded)
-  __shared__ uint32_t s_wt[65];
-  __shared__ uint32_t s_status, s_ticket;
-  __shared__ uint64_t s_sum[kWarps + 1];
-  __shared__ uint64_t s_pref[kGroup];
-  __shared__ uint64_t s_base;
-  __shared__ KeepSmem ks;
-  __shared__ uint32_t s_fast;
-  cg::grid_group grid = cg::this_grid();
-  TopkCtl* c = L.ctl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t G = gridDim.x, b = blockIdx.x;
-  const uint32_t gwarp = b * kWarps + warp, nwarps = G * kWarps;
-  const uint64_t t0 = L.ntiles * b / G, t1 = L.ntiles * (b + 1) / G;   // this block's tiles in C
-  for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
-  if (tid == 0) {
-    s_status = 0;
-    ks.ntl = 0;
-    ks.nc = 0;
-    ks.spill = SPARCML_TOPK_KEEP ? 0u : 1u;
-  }
-  if (b == 0 && tid == 0) {
-    c->tile_ticket = 0;
-    c->status = 0;
-    c->spill = 0;
-  }
-  for (uint64_t i = (uint64_t)b * kThreads + tid; i < L.ngroups; i += (uint64_t)G * kThreads) L.gsum[i] = 0;
-  mark(c, 0);
+  TopkCtl* c = a.L.ctl;
+  const uint64_t N = a.N, k = a.k;
+  const uint32_t C = (uint32_t)((N + kChunk - 1) / kChunk);
+  const uint32_t W = G * kTkWarps, gw = b * kTkWarps + warp;
+  const WSplit sp{C / W, C % W};
+  const uint32_t c0 = wstart(sp, gw), nch = wcount(sp, gw);
+  const uint64_t wbase = (uint64_t)c0 * kChunk;
+  const uint32_t p = ld_relaxed_gpu_u32(&c->calls) & 1u;
+  uint32_t bar_t = ld_relaxed_gpu_u32(&c->flag);
+  const CandStore<EF> cs{cidx + warp * kCap, cval + warp * kCap, a.L.sp_idx + wbase, a.L.sp_val + wbase};
+  tk_mark(c, 0);
+  TK_C(0);
 
-  // ---- S: sample ----------------------------------------------------------------
-  const uint64_t nchunk = N >= kSampleMinN ? std::min<uint64_t>(kSampleChunks, N / 8) : 0;
-  const uint32_t sblocks = (uint32_t)std::min<uint64_t>(G, (nchunk + kThreads - 1) / kThreads);
-  __syncthreads();
-  if (b < sblocks) {
-    const uint64_t ch = (uint64_t)b * kThreads + tid;
-    uint32_t mx = 0;
-    if (ch < nchunk) {
-      const uint64_t pos = (ch * (N / 8) / nchunk) * 8;
-      float v[8];
-      const float4 a0 = *reinterpret_cast<const float4*>(x + pos);
-      const float4 a1 = *reinterpret_cast<const float4*>(x + pos + 4);
-      v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w;
-      v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+  // ---- S: the shared sample (loads issued first, ahead of the ring's) --------------
+  const bool sampling = N >= kSampleMinN;
+  constexpr int kSPer = kSampleGran / kTkThreads;   // granules per thread
+  float4 smp[kSPer];
+  bool sok[kSPer];
+#pragma unroll
+  for (int j = 0; j < kSPer; ++j) {
+    uint64_t pos = 0;
+    sok[j] = sampling && sample_pos((uint32_t)(tid + j * kTkThreads), N, C, W, sp, &pos);
+    smp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sok[j]) {
+      smp[j] = __ldcg(reinterpret_cast<const float4*>(a.x + pos));
       if (EF) {
-        const float4 g0 = *reinterpret_cast<const float4*>(g + pos);
-        const float4 g1 = *reinterpret_cast<const float4*>(g + pos + 4);
-        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = __fmaf_rn(alpha, gg[i], v[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t key = abs_key(v[i]);
-        mx = max(mx, key);
-        atomicAdd(&sh[key >> 19], 1u);
-        atomicAdd(&sh[kBins + (key >> 25)], 1u);
+        const float4 gv = __ldcg(reinterpret_cast<const float4*>(a.g + pos));
+        smp[j] = make_float4(__fmaf_rn(a.alpha, gv.x, smp[j].x), __fmaf_rn(a.alpha, gv.y, smp[j].y),
+                             __fmaf_rn(a.alpha, gv.z, smp[j].z), __fmaf_rn(a.alpha, gv.w, smp[j].w));
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0 && mx) atomicMax(&c->smax, mx);
-    flush_hist(sh, c->hist_s);
-    __syncthreads();
-    for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
   }
-  mark(c, 1);
-  grid.sync();
-  // tau: where the sample's count from the top reaches mean + 4 sigma + 16;
-  // split: where it reaches mean - 4 sigma - 16.  The k-th magnitude lies in
-  // [tau, split) with overwhelming probability: level-1 bins cover that range
-  // finely, everything above it is one bin.  (Same result in every block.)
-  Level lv;
-  lv.lo = 0;
-  lv.split = kKeyEnd;
-  lv.hi = kKeyEnd;
-  lv.above = 0;
-  lv.shift = shift_for(kKeyEnd, kBins - 1);
-  lv.exact = 0;
-  lv.kth = 0;
-  lv.need = 0;
-  if (nchunk) {
-    const double S = (double)nchunk * 8.0;
-    const double mean = (double)k * S / (double)N;
-    const uint64_t t_lo = (uint64_t)ceil(mean + 4.0 * sqrt(mean) + 16.0);
-    const double th = mean - 4.0 * sqrt(mean) - 16.0;
-    const uint64_t t_hi = th > 1.0 ? (uint64_t)th : 1;
-    const uint64_t tg[2] = {t_lo, t_hi};
-    BinFind fb[2];
-    find_bins(c->hist_s, 0, tg, 2, sh, fb);
-    const bool ok = fb[0].reached, okh = fb[1].reached;
-    const uint32_t bn = fb[0].bin, bh = fb[1].bin;
-    const uint64_t tau = ok ? ((uint64_t)bn << 19) : 0ull;
-    const uint64_t top = (uint64_t)__ldcg(&c->smax) + (1ull << 23);   // 2 x the largest sample
-    uint64_t split = okh ? min((uint64_t)(bh + 1) << 19, (uint64_t)kKeyEnd) : min(top, (uint64_t)kKeyEnd);
-    if (split <= tau) split = tau + 1;
-    lv.lo = tau;
-    lv.split = split;
-    lv.shift = shift_for(split - tau, kBins - 1);
+
+  // ---- ring set-up and prologue: the first kStages chunks of every warp ---------
+  uint64_t* wbar = mbar + warp * kStages;
+  float* wring = ring + (size_t)warp * kStages * Cfg::kArr * kChunk;
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](uint32_t cc, int s) {
+    if ((uint64_t)(cc + 1) * kChunk > N) return;   // the ragged final chunk is read directly
+    float* d = wring + (size_t)s * Cfg::kArr * kChunk;
+    mbar_expect_tx(&wbar[s], Cfg::kArr * kChunk * 4);
+    bulk_g2s(d, a.x + (uint64_t)cc * kChunk, kChunk * 4, &wbar[s], pol);
+    if (EF) bulk_g2s(d + kChunk, a.g + (uint64_t)cc * kChunk, kChunk * 4, &wbar[s], pol);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&wbar[s], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+    if (!SPARCML_TOPK_LATE_PRO)
+      for (int s = 0; s < kStages && (uint32_t)s < nch; ++s) issue(c0 + s, s);
   }
-  for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
+  constexpr int kSBins = 4096;    // sample histogram: key >> 19 (1/16 octave), in the candidate area
+  static_assert(kSBins * 4 <= kTkWarps * kCap * 8, "sample histogram fits the candidate area");
+  uint32_t* shs = cidx;
+  for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
+  if (sampling)
+    for (int i = tid; i < kSBins / 4; i += kTkThreads) reinterpret_cast<uint4*>(shs)[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) {
+    s_bad = 0;
+    s_spill = 0;
+  }
   __syncthreads();
-  mark(c, 2);
-  const uint32_t tau = (uint32_t)lv.lo;
+  TK_D(0);
 
-  // ---- F: the streaming pass (tiles handed out dynamically for balance) ------
-  while (true) {
-    if (tid == 0) s_ticket = atomicAdd(&c->tile_ticket, 1u);
-    __syncthreads();
-    const uint64_t t = s_ticket;
-    if (t >= L.ntiles) break;
-    filter_tile<EF, RESID, EF || RESID>(x, g, alpha, xout, resid, N, t, tau, lv.split, lv.shift, L, sh, s_wt,
-                                        &s_status, SPARCML_TOPK_KEEP ? &ks : nullptr);
+  uint32_t tau = 0;
+  uint64_t split = kKeyEnd;
+  if (sampling) {
+    uint32_t ns = 0;
+#pragma unroll
+    for (int j = 0; j < kSPer; ++j) {
+      if (sok[j]) {
+        atomicAdd(&shs[abs_key(smp[j].x) >> 19], 1u);
+        atomicAdd(&shs[abs_key(smp[j].y) >> 19], 1u);
+        atomicAdd(&shs[abs_key(smp[j].z) >> 19], 1u);
+        atomicAdd(&shs[abs_key(smp[j].w) >> 19], 1u);
+      }
+      ns += sok[j] ? 4u : 0u;
+    }
+    TK_D(1);
+    uint64_t S;
+    (void)blk_excl_sum<uint64_t>(ns, s_sc, &S);   // (syncs: the sample histogram is complete)
+    TK_D(2);
+    // tau where the sample count from the top reaches t_lo = mean + 5 sigma + 4
+    // (to 1/16 octave): the k-th magnitude is >= tau unless the sample holds >=
+    // t_lo values above it (a 5.6-sigma event; then the exact re-filter runs).
+    // split where the count reaches mean - 4 sigma - 16: the level-0 bins cover
+    // [tau, split) finely.  Same result in every CTA.
+    const float mean = (float)((double)k * (double)S / (double)N);
+    const float sd = sqrtf(mean);
+    const uint64_t t_lo = (uint64_t)ceilf(mean + 5.0f * sd + 4.0f);
+    const float th = mean - 4.0f * sd - 16.0f;
+    const uint64_t t_hi = th > 1.0f ? (uint64_t)th : 1;
+    find2<kSBins>(shs, t_lo, t_hi, s_sc, s_cross);
+    const Cross f0 = s_cross[0], f1 = s_cross[1];
+    if (EF && tid == 0) atomicAdd(&c->sampled[p], 1u);   // this CTA's sample reads are complete
+    tau = f0.ok ? (f0.bin << 19) : 0u;
+    split = f1.ok ? (uint64_t)(f1.bin + 1) << 19 : kKeyEnd;
+    if (split <= tau) split = (uint64_t)tau + 1;
+    TK_D(3);
   }
-  mark(c, 3);
-  flush_hist(sh, c->hist[0]);
-  if (tid == 0 && s_status) atomicOr(&c->status, 1u);
-  if (tid == 0 && ks.spill) atomicOr(&c->spill, 1u);
-  grid.sync();
-  if (tid == 0) s_fast = __ldcg(&c->spill) == 0u;
-  mark(c, 4);
+  uint32_t shift = shift_for(split - tau, kBins - 1);
+  if (SPARCML_TOPK_LATE_PRO && lane == 0)
+    for (int s = 0; s < kStages && (uint32_t)s < nch; ++s) issue(c0 + s, s);
+  tk_mark(c, 1);
+
+  // ---- F: the streaming pass ---------------------------------------------------------
+  if (tau > 0x7F800000u) tau = 0x7F800000u;   // a sample holding NaN: Inf must stay a candidate
+  const float tauf = __uint_as_float(tau);
+  const uint32_t split32 = (uint32_t)split;
+  uint32_t nw = 0, bad = 0;
+  const bool ragged = nch > 0 && (uint64_t)(c0 + nch) * kChunk > N;   // this warp owns the vector's partial last chunk
+  const uint32_t nfull = ragged ? nch - 1 : nch;
+  auto guard = [&](uint32_t i) {   // EF: the warp's last chunk may hold sampled values
+    if (EF && STORE && sampling && i + 1 == nch) {
+      if (lane == 0) {
+        while ((int)(ld_relaxed_gpu_u32(&c->sampled[p]) - G) < 0) {
+        }
+        (void)ld_acquire_gpu(&c->sampled[p]);
+      }
+      __syncwarp();
+    }
+  };
+  for (uint32_t i = 0; i < nfull; ++i) {
+    const int s = (int)(i % kStages);
+    const float* sx = wring + (size_t)s * Cfg::kArr * kChunk;
+    mbar_wait(&wbar[s], (i / kStages) & 1u);
+    guard(i);
+    hot_chunk<EF, STORE>(sx, (c0 + i) * kChunk, a.alpha, a.dst, tauf, tau, split32, shift, sh, cs, nw, bad);
+    __syncwarp();
+    if (lane == 0 && i + kStages < nch) {
+      // every lane has consumed stage s (its values fed the vote above the
+      // __syncwarp), so the async refill cannot overwrite unread data
+      if (SPARCML_TOPK_FENCE) fence_proxy_async_smem();
+      issue(c0 + i + kStages, s);
+    }
+  }
+  if (ragged) {   // the partial final chunk of the vector, read directly
+    const uint64_t cc = c0 + nch - 1;
+    guard(nch - 1);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint64_t gp = cc * kChunk + r * 128 + lane * 4;
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[j] = 0.0f;
+        if (gp + j < N) v[j] = EF ? __fmaf_rn(a.alpha, a.g[gp + j], a.x[gp + j]) : a.x[gp + j];
+      }
+      consume_row<EF, STORE>(v, gp, false, N, a.dst, tau, split, shift, sh, cs, nw, bad);
+    }
+  }
+  TK_D(5);
+  bad = __any_sync(0xffffffffu, bad) ? 1u : 0u;
+  if (lane == 0) {
+    s_wn[warp] = nw;
+    if (nw > (uint32_t)kCap) s_spill = 1u;
+    if (bad) s_bad = 1u;
+  }
+  __syncthreads();
+  TK_D(4);
+  TK_C(1);
+
+  // ---- counting sort of this CTA's candidates by bin (fast path) -------------------
+  // The CTA's element range [r0, r1) doubles as its sorted region: sp_idx[r0 ..
+  // r0+kBins) = per-bin counts ABOVE the bin (descending exclusive scan),
+  // sp_idx/sp_val[r0+kBins + i] = the candidates in descending bin order.  After
+  // barrier A any CTA reads the crossing bin's segment of every CTA directly.
+  uint32_t cta_n = 0;
+#pragma unroll
+  for (int w = 0; w < kTkWarps; ++w) cta_n += s_wn[w];
+  const uint64_t r0 = (uint64_t)wstart(sp, b * kTkWarps) * kChunk;
+  const uint64_t r1 = std::min<uint64_t>(N, (uint64_t)(wstart(sp, b * kTkWarps + kTkWarps - 1) +
+                                                         wcount(sp, b * kTkWarps + kTkWarps - 1)) * kChunk);
+  const bool fast_ok = !s_spill && (uint64_t)cta_n + kBins <= r1 - r0;
+  TK_V(20, tau);
+  TK_V(21, split);
+  TK_V(22, cta_n);
+  TK_V(23, fast_ok);
+  if (fast_ok) {
+    uint32_t* ab = reinterpret_cast<uint32_t*>(ring);   // per-bin cursors (the ring is drained)
+    {
+      constexpr int per = kBins / kTkThreads;
+      const int base = kBins - per * (tid + 1);
+      const uint4 lo4 = *reinterpret_cast<const uint4*>(sh + base);
+      const uint4 hi4 = *reinterpret_cast<const uint4*>(sh + base + 4);
+      const uint32_t v[per] = {hi4.w, hi4.z, hi4.y, hi4.x, lo4.w, lo4.z, lo4.y, lo4.x};
+      uint32_t loc = 0;
+#pragma unroll
+      for (int i = 0; i < per; ++i) loc += v[i];
+      uint64_t tot;
+      uint32_t cum = (uint32_t)blk_excl_sum<uint64_t>(loc, s_sc, &tot);
+      uint32_t o[per];
+#pragma unroll
+      for (int i = 0; i < per; ++i) {
+        o[i] = cum;
+        cum += v[i];
+      }
+      const uint4 olo = make_uint4(o[7], o[6], o[5], o[4]), ohi = make_uint4(o[3], o[2], o[1], o[0]);
+      *reinterpret_cast<uint4*>(ab + base) = olo;
+      *reinterpret_cast<uint4*>(ab + base + 4) = ohi;
+      *reinterpret_cast<uint4*>(a.L.sp_idx + r0 + base) = olo;
+      *reinterpret_cast<uint4*>(a.L.sp_idx + r0 + base + 4) = ohi;
+    }
+    __syncthreads();
+    TK_D(12);
+    uint32_t* si = a.L.sp_idx + r0 + kBins;
+    float* sv = a.L.sp_val + r0 + kBins;
+    for (uint32_t i = lane; i < nw; i += 32) {
+      uint32_t idx;
+      float v;
+      cs.get(i, &idx, &v);
+      const uint32_t key = abs_key(v);
+      const uint32_t at = atomicAdd(&ab[bin_of(key, tau, split, shift)], 1u);
+      si[at] = idx;
+      sv[at] = v;
+    }
+    TK_D(13);
+  }
+  // the level-0 histogram to global; per-call flags
+  for (int i = tid; i < kBins; i += kTkThreads) {
+    const uint32_t v = sh[i];
+    if (v) atomicAdd(&c->hist[p][0][i], v);
+    sh[i] = 0;
+  }
+  if (tid == 0) {
+    if (s_bad) atomicOr(&c->bad[p], 1u);
+    if (!fast_ok) atomicOr(&c->nofast[p], 1u);
+    c->cta_a[b] = cta_n;
+  }
+  TK_D(6);
+  tk_mark(c, 2);
+  tk_grid_barrier(c, ++bar_t);   // ---- A
+  TK_D(7);
+  tk_mark(c, 3);
+  if (b == 0 && tid == 0) {
+    c->status = __ldcg(&c->bad[p]) ? 1u : 0u;
+    c->bad[p ^ 1u] = 0;       // the next call's slots (the previous call has ended)
+    c->sampled[p ^ 1u] = 0;
+    c->list_n[p ^ 1u] = 0;
+    c->nofast[p ^ 1u] = 0;
+  }
+  {   // the previous call's histogram slots, for the next call (every CTA has read them)
+    uint4* hz = reinterpret_cast<uint4*>(&c->hist[p ^ 1u][0][0]);
+    for (uint32_t i = b * kTkThreads + tid; i < (uint32_t)(kLevels * kBins / 4); i += G * kTkThreads)
+      hz[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+
+  // ---- R: locate the k-th magnitude -------------------------------------------------
+  uint32_t slot = 0;
+  uint32_t lo = tau;
+  uint64_t spl = split, hi = kKeyEnd, above = 0;
+  uint32_t passes = 1;
+  bool exact = false, fast = false;
+  uint32_t kth = 0;
+  uint64_t need = 0;
   {
-    BinFind f0;
-    find_bins(c->hist[0], lv.above, &k, 1, sh, &f0);
-    if (!f0.reached) {   // fewer than k candidates: the sample under-estimated; exact re-filter with tau = 0 (rare)
-      grid.sync();   // every block has read hist[0]
-      if (b == 0) {
-        for (int i = tid; i < kHist; i += kThreads) c->hist[0][i] = 0;
-        if (tid == 0) {
-          c->tile_ticket = 0;
-          c->passes = 2;
-        }
-      }
-      for (int i = tid; i < kHist; i += kThreads) sh[i] = 0;
-      if (tid == 0) s_fast = 0;   // the re-filtered candidates live in global memory only
-      grid.sync();
-      lv.lo = 0;
-      lv.split = kKeyEnd;
-      lv.shift = shift_for(kKeyEnd, kBins - 1);
-      const float* src = EF ? xout : x;
-      while (true) {
-        if (tid == 0) s_ticket = atomicAdd(&c->tile_ticket, 1u);
-        __syncthreads();
-        const uint64_t t = s_ticket;
-        if (t >= L.ntiles) break;
-        filter_tile<false, false, false>(src, nullptr, 0.0f, nullptr, nullptr, N, t, 0u, lv.split, lv.shift, L, sh,
-                                         s_wt, &s_status, nullptr);
-      }
-      flush_hist(sh, c->hist[0]);
-      grid.sync();
-      narrow(lv, c->hist[0], k, sh);
-    } else {
-      if (b == 0 && tid == 0) c->passes = 1;
-      apply_narrow(lv, f0, k);
-    }
-  }
-  mark(c, 5);
-
-  // ---- R: refine the crossing bin until it is one magnitude ------------------
-  int level = 1;
-  while (!lv.exact) {
-    uint32_t* gh = c->hist[level < kLevels ? level : kLevels - 1];
-    if (s_fast) {
-      for (uint32_t i = tid; i < ks.nc; i += kThreads) {
-        const uint32_t key = abs_key(ks.cv[i]);
-        if (key >= lv.lo && key < lv.hi) {
-          const uint32_t bn = bin_of(key, lv.lo, lv.split, lv.shift);
-          atomicAdd(&gh[bn], 1u);
-          atomicAdd(&gh[kBins + (bn >> 6)], 1u);
-        }
-      }
-    } else
-    for (uint64_t t = gwarp; t < L.ntiles; t += nwarps) {
-      const uint32_t n = __ldcg(&L.tile_count[t]);
-      const float* cv = L.cand_val + t * kTopkTile;
-      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
-        float v[4];
-        load4(cv, n, i0, v);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint32_t key = abs_key(v[r]);
-          if (i0 + r * 32 + lane < n && key >= lv.lo && key < lv.hi) {
-            const uint32_t bn = bin_of(key, lv.lo, lv.split, lv.shift);
-            atomicAdd(&gh[bn], 1u);
-            atomicAdd(&gh[kBins + (bn >> 6)], 1u);
-          }
-        }
-      }
-    }
-    grid.sync();
-    narrow(lv, gh, k, sh);
-    ++level;
-  }
-  mark(c, 6);
-  const uint32_t kth = lv.kth;
-  const uint64_t need = lv.need;
-
-  // ---- C: ordered placement (index order = tile order, then in-tile order) --
-  if (s_fast) {
-    // per kept tile: (#|v| > kth) | (#|v| == kth) << 32, from shared memory
-    for (uint32_t j = warp; j < ks.ntl; j += kWarps) {
-      const uint32_t n = ks.tn[j], o = ks.to[j];
-      uint32_t ng = 0, ne = 0;
-      for (uint32_t i = lane; i < n; i += 32) {
-        const uint32_t key = abs_key(ks.cv[o + i]);
-        ng += key > kth;
-        ne += key == kth;
-      }
-      ng = warp_sum<uint32_t>(ng);
-      ne = warp_sum<uint32_t>(ne);
-      if (lane == 0) {
-        const uint64_t sel = (uint64_t)ng | ((uint64_t)ne << 32);
-        L.tile_sel[ks.tl[j]] = sel;
-        if (sel) atomicAdd(reinterpret_cast<unsigned long long*>(&L.gsum[ks.tl[j] / kGroupTiles]), sel);
-      }
-    }
-    mark(c, 10);
-  } else {
-    uint64_t bsum = 0;
-    for (uint64_t t = t0 + warp; t < t1; t += kWarps) {
-      const uint32_t n = __ldcg(&L.tile_count[t]);
-      const float* cv = L.cand_val + t * kTopkTile;
-      uint32_t ng = 0, ne = 0;
-      for (uint32_t i0 = 0; i0 < n; i0 += 128) {
-        float v[4];
-        load4(cv, n, i0, v);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const bool in = i0 + r * 32 + lane < n;
-          const uint32_t key = abs_key(v[r]);
-          ng += __popc(__ballot_sync(0xffffffffu, in && key > kth));
-          ne += __popc(__ballot_sync(0xffffffffu, in && key == kth));
-        }
-      }
-      const uint64_t sel = (uint64_t)ng | ((uint64_t)ne << 32);
-      if (lane == 0) {
-        L.tile_sel[t] = sel;
-        bsum += sel;
-      }
-    }
-    {
-      uint64_t tot;
-      block_exclusive_sum<uint64_t>(bsum, s_sum, &tot);
-      if (tid == 0) c->blk[b] = tot;
-    }
-  }
-  grid.sync();
-  mark(c, 8);
-  // every histogram has been read by every block: clear them for the next call
-  if (b < (uint32_t)(kLevels + 1)) {
-    uint32_t* h = b == 0 ? c->hist_s : c->hist[b - 1];
-    for (int i = tid; i < kHist; i += kThreads) h[i] = 0;
-    if (b == 0 && tid == 0) c->smax = 0;
-  }
-  if (s_fast) {
-    // exclusive prefix of tile_sel at each kept tile: the group sums before
-    // its 64-tile group plus the tiles before it in the group (one warp per tile)
-    for (uint32_t j = warp; j < ks.ntl; j += kWarps) {
-      const uint64_t t = ks.tl[j], g0 = t / kGroupTiles;
-      uint64_t v = 0;
-      for (uint64_t i = lane; i < g0; i += 32) v += __ldcg(reinterpret_cast<const unsigned long long*>(&L.gsum[i]));
-#pragma unroll
-      for (int q = 0; q < kGroupTiles / 32; ++q) {
-        const uint64_t tt = g0 * kGroupTiles + q * 32 + lane;
-        if (tt < t) v += __ldcg(reinterpret_cast<const unsigned long long*>(&L.tile_sel[tt]));
-      }
-      v = warp_sum<uint64_t>(v);
-      if (lane == 0) ks.tp[j] = v;
-    }
+    const uint4* gh = reinterpret_cast<const uint4*>(c->hist[p][0]);
+    if (tid == 0) s_nofast = __ldcg(&c->nofast[p]);
+    for (int i = tid; i < kBins / 4; i += kTkThreads) reinterpret_cast<uint4*>(sh)[i] = __ldcg(gh + i);
     __syncthreads();
-    mark(c, 9);
-    for (uint32_t j = warp; j < ks.ntl; j += kWarps) {
-      const uint32_t n = ks.tn[j], o = ks.to[j];
-      uint64_t gt_run = ks.tp[j] & 0xFFFFFFFFull, eq_run = ks.tp[j] >> 32;
-      for (uint32_t i0 = 0; i0 < n; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const float vv = i < n ? ks.cv[o + i] : 0.0f;
-        const uint32_t key = abs_key(vv);
-        const bool gsel = i < n && key > kth, esel = i < n && key == kth;
-        const uint32_t gbal = __ballot_sync(0xffffffffu, gsel), ebal = __ballot_sync(0xffffffffu, esel);
-        const uint32_t lower = (1u << lane) - 1u;
-        const uint64_t gt_before = gt_run + __popc(gbal & lower);
-        const uint64_t eq_before = eq_run + __popc(ebal & lower);
-        if (gsel || (esel && eq_before < need)) {
-          const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
-          const uint32_t j2 = ks.ci[o + i];
-          idx_out[pos] = j2;
-          val_out[pos] = vv;
-          if (zero_at) zero_at[j2] = 0.0f;   // acc - TopK(acc)
-        }
-        gt_run += __popc(gbal);
-        eq_run += __popc(ebal);
-      }
-    }
-  } else {
-    {
-      uint64_t v = 0;
-      for (uint32_t j = tid; j < b; j += kThreads) v += __ldcg(reinterpret_cast<const unsigned long long*>(&c->blk[j]));
-      uint64_t tot;
-      block_exclusive_sum<uint64_t>(v, s_sum, &tot);
-      if (tid == 0) s_base = tot;
-    }
+    const Cross f = find_desc(sh, k, s_sc, &s_cross[0]);
+    for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
     __syncthreads();
-    for (uint64_t gs = t0; gs < t1; gs += kGroup) {
-      const int nt = (int)std::min<uint64_t>(kGroup, t1 - gs);
-      if (warp == 0) {
-        const uint64_t v = lane < nt ? __ldcg(reinterpret_cast<const unsigned long long*>(&L.tile_sel[gs + lane])) : 0ull;
-        const uint64_t inc = warp_inclusive_sum<uint64_t>(v);
-        s_pref[lane] = s_base + inc - v;
-        __syncwarp();
-        if (lane == 31) s_base += inc;
+    TK_D(8);
+    if (f.ok && !s_nofast) {
+      const uint32_t B = f.bin;
+      TK_V(24, f.cnt);
+      TK_V(25, B);
+      uint64_t blo, bhi;
+      if (B == kBins - 1) {
+        blo = split;
+        bhi = kKeyEnd;
+      } else {
+        blo = (uint64_t)tau + ((uint64_t)B << shift);
+        bhi = std::min<uint64_t>(split, (uint64_t)tau + ((uint64_t)(B + 1) << shift));
       }
-      __syncthreads();
-      for (int j = warp; j < nt; j += kWarps) {
-        const uint64_t t = gs + j;
-        const uint32_t n = __ldcg(&L.tile_count[t]);
-        const uint32_t* ci = L.cand_idx + t * kTopkTile;
-        const float* cv = L.cand_val + t * kTopkTile;
-        uint64_t gt_run = s_pref[j] & 0xFFFFFFFFull, eq_run = s_pref[j] >> 32;
-        for (uint32_t i0 = 0; i0 < n; i0 += 128) {
-          float v[4];
-          load4(cv, n, i0, v);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const uint32_t i = i0 + r * 32 + lane;
-            const uint32_t key = abs_key(v[r]);
-            const bool gsel = i < n && key > kth, esel = i < n && key == kth;
-            const uint32_t gbal = __ballot_sync(0xffffffffu, gsel), ebal = __ballot_sync(0xffffffffu, esel);
-            const uint32_t lower = (1u << lane) - 1u;
-            const uint64_t gt_before = gt_run + __popc(gbal & lower);
-            const uint64_t eq_before = eq_run + __popc(ebal & lower);
-            if (gsel || (esel && eq_before < need)) {
-              const uint64_t pos = gt_before + (eq_before < need ? eq_before : need);
-              const uint32_t j2 = ci[i];
-              idx_out[pos] = j2;
-              val_out[pos] = v[r];
-              if (zero_at) zero_at[j2] = 0.0f;   // acc - TopK(acc)
+      if (bhi - blo == 1 || f.cnt <= (uint32_t)kListCap) {
+        // ---- fast path: the crossing bin's entries of every CTA, straight from
+        // their sorted regions (no second barrier) ----
+        fast = true;
+        uint32_t* lk = reinterpret_cast<uint32_t*>(ring);   // crossing-bin keys
+        uint32_t* lc = lk + kListCap;                        // their CTAs
+        uint32_t* abh = lc + kListCap;                       // per CTA: candidates above the bin
+        uint32_t* cnb = abh + kMaxGrid;                      // per CTA: candidates in the bin
+        uint32_t* sof = cnb + kMaxGrid;                      // per CTA: offset of its entries in lk
+        uint32_t* gtl = sof + kMaxGrid;                      // per CTA: bin entries > kth
+        uint32_t* eql = gtl + kMaxGrid;                      // per CTA: bin entries == kth
+        const uint32_t bb0 = 2 * tid, bb1 = 2 * tid + 1;
+        auto cta_r0 = [&](uint32_t bq) { return (uint64_t)wstart(sp, bq * kTkWarps) * kChunk; };
+        uint32_t ah0 = 0, al0 = 0, ah1 = 0, al1 = 0;
+        if (bb0 < G) {
+          const uint32_t* g0 = a.L.sp_idx + cta_r0(bb0);
+          ah0 = __ldcg(g0 + B);
+          al0 = B == 0 ? __ldcg(&c->cta_a[bb0]) : __ldcg(g0 + B - 1);
+        }
+        if (bb1 < G) {
+          const uint32_t* g1 = a.L.sp_idx + cta_r0(bb1);
+          ah1 = __ldcg(g1 + B);
+          al1 = B == 0 ? __ldcg(&c->cta_a[bb1]) : __ldcg(g1 + B - 1);
+        }
+        const uint32_t n0 = al0 - ah0, n1 = al1 - ah1;
+        uint64_t ntot;
+        const uint32_t so0 = (uint32_t)blk_excl_sum<uint64_t>((uint64_t)n0 + n1, s_sc, &ntot);
+        if (bb0 < G) {
+          abh[bb0] = ah0;
+          cnb[bb0] = n0;
+          sof[bb0] = so0;
+          gtl[bb0] = 0;
+          eql[bb0] = 0;
+        }
+        if (bb1 < G) {
+          abh[bb1] = ah1;
+          cnb[bb1] = n1;
+          sof[bb1] = so0 + n0;
+          gtl[bb1] = 0;
+          eql[bb1] = 0;
+        }
+        above = f.above;
+        if (bhi - blo == 1) {   // the bin is one magnitude: every entry is a tie
+          kth = (uint32_t)blo;
+          need = k - above;
+          __syncthreads();
+          if (bb0 < G) eql[bb0] = n0;
+          if (bb1 < G) eql[bb1] = n1;
+          exact = true;
+        } else {
+          // gather every CTA's segment in one round of loads: entry e belongs to
+          // the CTA bq with sof[bq] <= e < sof[bq + 1] (binary search)
+          __syncthreads();
+          for (uint32_t e = tid; e < (uint32_t)ntot; e += kTkThreads) {
+            uint32_t lo_b = 0, hi_b = G;   // largest bq with sof[bq] <= e and cnb[bq] > 0
+            while (hi_b - lo_b > 1) {
+              const uint32_t mid = (lo_b + hi_b) >> 1;
+              if (sof[mid] <= e) lo_b = mid;
+              else hi_b = mid;
             }
-            gt_run += __popc(gbal);
-            eq_run += __popc(ebal);
+            while (cnb[lo_b] == 0 || sof[lo_b] + cnb[lo_b] <= e) ++lo_b;   // skip empty segments
+            lk[e] = abs_key(__ldcg(a.L.sp_val + cta_r0(lo_b) + kBins + abh[lo_b] + (e - sof[lo_b])));
+            lc[e] = lo_b;
+          }
+          __syncthreads();
+          TK_D(9);
+          const uint32_t n = (uint32_t)ntot;
+          uint64_t t = k - above;
+          {
+            uint64_t rlo = blo, rhi = bhi;
+            while (rhi - rlo > 1) {
+              const uint32_t s = shift_for(rhi - rlo, kBins);
+              for (uint32_t i = tid; i < n; i += kTkThreads) {
+                const uint32_t key = lk[i];
+                if (key >= rlo && key < rhi) atomicAdd(&sh[(uint32_t)(key - rlo) >> s], 1u);
+              }
+              __syncthreads();
+              const Cross fr = find_desc(sh, t, s_sc, &s_cross[0]);
+              for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
+              __syncthreads();
+              t -= fr.above;
+              const uint64_t nlo = rlo + ((uint64_t)fr.bin << s);
+              rhi = std::min<uint64_t>(rhi, rlo + ((uint64_t)(fr.bin + 1) << s));
+              rlo = nlo;
+            }
+            kth = (uint32_t)rlo;
+            need = t;
+          }
+          for (uint32_t i = tid; i < n; i += kTkThreads) {
+            if (lk[i] > kth) atomicAdd(&gtl[lc[i]], 1u);
+            else if (lk[i] == kth) atomicAdd(&eql[lc[i]], 1u);
           }
         }
+        __syncthreads();
+        TK_D(10);
+        // per CTA (index order): ties are taken in CTA order, so the ties taken
+        // before CTA b' are min(E_b', need) with E the prefix of the tie counts:
+        // offset(b') = prefix(above-bin + above-kth) + min(E_b', need)
+        const uint32_t e0 = bb0 < G ? eql[bb0] : 0u, e1 = bb1 < G ? eql[bb1] : 0u;
+        const uint64_t g0 = bb0 < G ? (uint64_t)ah0 + gtl[bb0] : 0, g1 = bb1 < G ? (uint64_t)ah1 + gtl[bb1] : 0;
+        uint64_t AG0, E0;
+        blk_excl_sum2(g0 + g1, (uint64_t)e0 + e1, s_sc, &AG0, &E0);
+        const uint64_t E1 = E0 + e0;
+        if (bb0 == b) {
+          s_off = AG0 + std::min<uint64_t>(E0, need);
+          s_quota = (uint32_t)std::min<uint64_t>(e0, need > E0 ? need - E0 : 0);
+        }
+        if (bb1 == b) {
+          s_off = AG0 + g0 + std::min<uint64_t>(E1, need);
+          s_quota = (uint32_t)std::min<uint64_t>(e1, need > E1 ? need - E1 : 0);
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  if (!fast) {
+    // ---- slow path: refinement levels / exact re-filter, then the list + barrier B --
+    while (true) {
+      {
+        const uint4* gh = reinterpret_cast<const uint4*>(c->hist[p][slot]);
+        for (int i = tid; i < kBins / 4; i += kTkThreads) reinterpret_cast<uint4*>(sh)[i] = __ldcg(gh + i);
+      }
+      __syncthreads();
+      const Cross f = find_desc(sh, k - above, s_sc, &s_cross[0]);
+      for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
+      __syncthreads();
+      if (!f.ok) {
+        // fewer than k candidates: the sample over-estimated tau.  Exact re-filter
+        // of every value (tau = 0) from the current vector (EF: acc, now in eps).
+        passes = 2;
+        ++slot;
+        lo = 0;
+        spl = kKeyEnd;
+        hi = kKeyEnd;
+        above = 0;
+        shift = shift_for(kKeyEnd, kBins - 1);
+        nw = 0;
+        const float* src = EF ? a.dst : a.x;
+        for (uint32_t i = 0; i < nch; ++i) {
+          const uint64_t cc = c0 + i;
+          const bool full = (cc + 1) * kChunk <= N;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const uint64_t gp = cc * kChunk + r * 128 + lane * 4;
+            float v[4];
+            if (full) {
+              const float4 xv = __ldcg(reinterpret_cast<const float4*>(src + gp));
+              v[0] = xv.x; v[1] = xv.y; v[2] = xv.z; v[3] = xv.w;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[j] = gp + j < N ? __ldcg(src + gp + j) : 0.0f;
+            }
+            uint32_t dummy = 0;
+            consume_row<EF, false>(v, gp, full, N, nullptr, 0u, spl, shift, sh, cs, nw, dummy);
+          }
+        }
+        __syncthreads();
+        for (int i = tid; i < kBins; i += kTkThreads) {
+          const uint32_t v = sh[i];
+          if (v) atomicAdd(&c->hist[p][slot][i], v);
+          sh[i] = 0;
+        }
+        tk_grid_barrier(c, ++bar_t);
+        continue;
+      }
+      uint64_t blo, bhi;
+      if (f.bin == kBins - 1) {
+        blo = spl;
+        bhi = hi;
+      } else {
+        blo = (uint64_t)lo + ((uint64_t)f.bin << shift);
+        bhi = std::min<uint64_t>(spl, (uint64_t)lo + ((uint64_t)(f.bin + 1) << shift));
+      }
+      above += f.above;
+      lo = (uint32_t)blo;
+      hi = bhi;
+      if (bhi - blo == 1) {
+        exact = true;
+        break;
+      }
+      if (f.cnt <= (uint32_t)kListCap) break;
+      // refine: histogram the candidates in [lo, hi) at a finer step
+      ++slot;
+      spl = hi;
+      shift = shift_for(hi - lo, kBins - 1);
+      for (uint32_t i0 = 0; i0 < nw; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        if (i < nw) {
+          uint32_t idx;
+          float v;
+          cs.get(i, &idx, &v);
+          const uint32_t key = abs_key(v);
+          if (key >= lo && (uint64_t)key < hi) atomicAdd(&sh[bin_of(key, lo, spl, shift)], 1u);
+        }
+      }
+      __syncthreads();
+      for (int i = tid; i < kBins; i += kTkThreads) {
+        const uint32_t v = sh[i];
+        if (v) atomicAdd(&c->hist[p][slot][i], v);
+        sh[i] = 0;
+      }
+      tk_grid_barrier(c, ++bar_t);
+    }
+    tk_mark(c, 4);
+
+    // ---- L: per-CTA counts above / in [lo, hi); the bin's candidates to the list --
+    {
+      uint32_t aw = 0, ew = 0;
+      for (uint32_t i0 = 0; i0 < nw; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        uint32_t key = 0;
+        const bool in = i < nw;
+        if (in) {
+          uint32_t idx;
+          float v;
+          cs.get(i, &idx, &v);
+          key = abs_key(v);
+        }
+        aw += __popc(__ballot_sync(0xffffffffu, in && (uint64_t)key >= hi));
+        ew += __popc(__ballot_sync(0xffffffffu, in && key >= lo && (uint64_t)key < hi));
+      }
+      if (lane == 0) {
+        s_w[warp][0] = aw;
+        s_w[warp][1] = ew;
+      }
+      __syncthreads();
+      if (tid == 0) {   // one list reservation per CTA; warp w's entries follow warps < w
+        uint32_t sa = 0, se = 0;
+        for (int w = 0; w < kTkWarps; ++w) {
+          sa += s_w[w][0];
+          const uint32_t e = s_w[w][1];
+          s_w[w][1] = se;
+          se += e;
+        }
+        c->cta_a[b] = sa;
+        c->cta_e[b] = se;
+        s_lbase = (!exact && se) ? atomicAdd(&c->list_n[p], se) : 0u;
+      }
+      __syncthreads();
+      if (!exact && ew) {
+        const uint32_t lt = lanemask_lt();
+        uint32_t at = s_lbase + s_w[warp][1];
+        for (uint32_t i0 = 0; i0 < nw; i0 += 32) {
+          const uint32_t i = i0 + lane;
+          uint32_t idx = 0, key = 0;
+          float v = 0.0f;
+          const bool in = i < nw;
+          if (in) {
+            cs.get(i, &idx, &v);
+            key = abs_key(v);
+          }
+          const bool e = in && key >= lo && (uint64_t)key < hi;
+          const uint32_t eb = __ballot_sync(0xffffffffu, e);
+          if (e && at + __popc(eb & lt) < (uint32_t)kListCap)
+            a.L.list[at + __popc(eb & lt)] = make_uint4(idx, key, b, 0u);
+          at += __popc(eb);
+        }
+      }
+    }
+    tk_grid_barrier(c, ++bar_t);   // ---- B
+    tk_mark(c, 5);
+
+    // ---- exact k-th magnitude, ties, this CTA's offset ---------------------------
+    {
+      uint32_t* lk = reinterpret_cast<uint32_t*>(ring);       // list keys
+      uint32_t* lc = lk + kListCap;                            // list CTAs
+      uint32_t* gtl = lc + kListCap;                           // per CTA: list entries > kth
+      uint32_t* eql = gtl + kMaxGrid;                          // per CTA: entries == kth (ties)
+      const uint32_t b0 = 2 * tid, b1 = 2 * tid + 1;
+      const uint32_t a0 = b0 < G ? __ldcg(&c->cta_a[b0]) : 0u, a1 = b1 < G ? __ldcg(&c->cta_a[b1]) : 0u;
+      uint32_t ce0 = 0, ce1 = 0;
+      if (exact) {
+        ce0 = b0 < G ? __ldcg(&c->cta_e[b0]) : 0u;
+        ce1 = b1 < G ? __ldcg(&c->cta_e[b1]) : 0u;
+      }
+      const uint32_t n = exact ? 0u : std::min<uint32_t>(__ldcg(&c->list_n[p]), (uint32_t)kListCap);
+      for (uint32_t i = tid; i < G; i += kTkThreads) {
+        gtl[i] = 0;
+        eql[i] = 0;
+      }
+      for (uint32_t i = tid; i < n; i += kTkThreads) {
+        const uint4 e = __ldcg(&a.L.list[i]);
+        lk[i] = e.y;
+        lc[i] = e.z;
+      }
+      __syncthreads();
+      if (!exact) {
+        uint64_t t = k - above;
+        uint64_t rlo = lo, rhi = hi;
+        while (rhi - rlo > 1) {
+          const uint32_t s = shift_for(rhi - rlo, kBins);
+          for (uint32_t i = tid; i < n; i += kTkThreads) {
+            const uint32_t key = lk[i];
+            if (key >= rlo && key < rhi) atomicAdd(&sh[(uint32_t)(key - rlo) >> s], 1u);
+          }
+          __syncthreads();
+          const Cross fr = find_desc(sh, t, s_sc, &s_cross[0]);
+          for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
+          __syncthreads();
+          t -= fr.above;
+          const uint64_t nlo = rlo + ((uint64_t)fr.bin << s);
+          rhi = std::min<uint64_t>(rhi, rlo + ((uint64_t)(fr.bin + 1) << s));
+          rlo = nlo;
+        }
+        kth = (uint32_t)rlo;
+        need = t;
+        for (uint32_t i = tid; i < n; i += kTkThreads) {
+          if (lk[i] > kth) atomicAdd(&gtl[lc[i]], 1u);
+          else if (lk[i] == kth) atomicAdd(&eql[lc[i]], 1u);
+        }
+        __syncthreads();
+      } else {
+        kth = lo;
+        need = k - above;
+      }
+      const uint32_t e0 = exact ? ce0 : (b0 < G ? eql[b0] : 0u), e1 = exact ? ce1 : (b1 < G ? eql[b1] : 0u);
+      const uint32_t g0 = exact ? 0u : (b0 < G ? gtl[b0] : 0u), g1 = exact ? 0u : (b1 < G ? gtl[b1] : 0u);
+      uint64_t etot;
+      const uint64_t E0 = blk_excl_sum<uint64_t>((uint64_t)e0 + e1, s_sc, &etot);
+      const uint64_t E1 = E0 + e0;
+      const uint32_t q0 = (uint32_t)std::min<uint64_t>(e0, need > E0 ? need - E0 : 0);
+      const uint32_t q1 = (uint32_t)std::min<uint64_t>(e1, need > E1 ? need - E1 : 0);
+      const uint64_t s0 = (uint64_t)a0 + g0 + q0;
+      const uint64_t s1 = (uint64_t)a1 + g1 + q1;
+      uint64_t stot;
+      const uint64_t O0 = blk_excl_sum<uint64_t>(s0 + s1, s_sc, &stot);
+      if (b0 == b) {
+        s_off = O0;
+        s_quota = q0;
+      }
+      if (b1 == b) {
+        s_off = O0 + s0;
+        s_quota = q1;
       }
       __syncthreads();
     }
   }
-  mark(c, 7);
+  TK_D(11);
+  TK_V(26, fast);
+  TK_V(27, kth);
+  if (b == 0 && tid == 0) {
+    c->passes = passes;
+    c->calls = c->calls + 1u;
+  }
+  // ---- placement: per warp, pass 1 counts (> kth, == kth), every warp scans the
+  // 16 pairs (offsets, tie quotas), pass 2 writes in index order.  Compact loops:
+  // this code runs once per call, so its instruction footprint is its cost.
+  tk_mark(c, 6);
+  TK_D(16);
+  {
+    uint32_t gtw = 0, eqw = 0;
+#pragma unroll 1
+    for (uint32_t i0 = 0; i0 < nw; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint32_t idx = 0, key = 0;
+      float v = 0.0f;
+      if (i < nw) {
+        cs.get(i, &idx, &v);
+        key = abs_key(v);
+      }
+      gtw += __popc(__ballot_sync(0xffffffffu, i < nw && key > kth));
+      eqw += __popc(__ballot_sync(0xffffffffu, i < nw && key == kth));
+    }
+    if (lane == 0) {
+      s_w[warp][0] = gtw;
+      s_w[warp][1] = eqw;
+    }
+    __syncthreads();
+    uint64_t o;
+    uint32_t tq;
+    {   // every warp scans the 16 (gt, eq) pairs itself: no second barrier
+      const uint32_t gv = lane < kTkWarps ? s_w[lane][0] : 0u, ev = lane < kTkWarps ? s_w[lane][1] : 0u;
+      const uint32_t E = warp_inclusive_sum<uint32_t>(ev) - ev;
+      const uint32_t q = s_quota;
+      const uint32_t t = q > E ? std::min(q - E, ev) : 0u;
+      const uint32_t sel = gv + t;
+      const uint32_t Sx = warp_inclusive_sum<uint32_t>(sel) - sel;
+      o = s_off + __shfl_sync(0xffffffffu, Sx, warp);
+      tq = __shfl_sync(0xffffffffu, t, warp);
+    }
+    const uint32_t lt = lanemask_lt();
+    uint32_t run = 0, eq_run = 0;
+#pragma unroll 1
+    for (uint32_t i0 = 0; i0 < nw; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint32_t idx = 0, key = 0;
+      float v = 0.0f;
+      if (i < nw) {
+        cs.get(i, &idx, &v);
+        key = abs_key(v);
+      }
+      const bool gsel = i < nw && key > kth, esel = i < nw && key == kth;
+      const uint32_t eb = __ballot_sync(0xffffffffu, esel);
+      const uint32_t eq_before = eq_run + __popc(eb & lt);
+      const bool take = gsel || (esel && eq_before < tq);
+      const uint32_t tb = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const uint64_t pos = o + run + __popc(tb & lt);
+        a.idx_out[pos] = idx;
+        a.val_out[pos] = v;
+        if (a.zero_at) a.zero_at[idx] = 0.0f;   // acc - TopK(acc)
+      }
+      run += __popc(tb);
+      eq_run += __popc(eb);
+    }
+  }
+  TK_D(17);
+  tk_mark(c, 7);
 }
 
 // ------------------------------------------------------- bucketed ---------
@@ -1002,8 +1475,8 @@ cudaError_t launch_topk_bucketed(const float* x, const float* grad, float alpha,
 
 // --------------------------------------------------------- k >= N ---------
 template <bool EF>
-__global__ void topk_all_kernel(const float* __restrict__ x, const float* __restrict__ g, float alpha,
-                                float* __restrict__ xout, float* __restrict__ resid, uint64_t N,
+__global__ void topk_all_kernel(const float* x, const float* __restrict__ g, float alpha,
+                                float* xout, float* __restrict__ resid, uint64_t N,   // EF: x == xout
                                 uint32_t* __restrict__ idx_out, float* __restrict__ val_out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
     float v = x[i];
@@ -1017,23 +1490,28 @@ __global__ void topk_all_kernel(const float* __restrict__ x, const float* __rest
   }
 }
 
+
 // ------------------------------------------------------------ launcher -----
-template <bool EF, bool RESID>
-static cudaError_t launch_fused(const float* x, const float* grad, float alpha, float* x_out, float* residual,
-                                uint64_t N, uint64_t k, uint32_t* idx_out, float* val_out, float* zero_at,
-                                const TopkLayout& L, cudaStream_t s) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_fused_kernel<EF, RESID>, kThreads, 0);
-    if (per_sm < 1) per_sm = 1;
+static uint64_t topk_grid(uint64_t N) {
+  const uint64_t C = (N + kChunk - 1) / kChunk;
+  return std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)device_sm_count(), C / kTkWarps, (uint64_t)kMaxGrid}));
+}
+
+template <bool EF, bool STORE>
+static cudaError_t launch_stream(const TkArgs& a, cudaStream_t s) {
+  static unsigned attr_set = 0;   // per device: dynamic shared memory opt-in done
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 32 && !(attr_set & (1u << dev))) {
+    const cudaError_t e = cudaFuncSetAttribute(topk_stream_kernel<EF, STORE>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TkCfg<EF>::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set |= 1u << dev;
   }
-  const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>({(uint64_t)per_sm * device_sm_count(), L.ntiles,
-                                                                (uint64_t)kMaxGrid}));
-  TopkLayout Lc = L;
-  void* args[] = {(void*)&x,      (void*)&grad,    (void*)&alpha,   (void*)&x_out,   (void*)&residual, (void*)&N,
-                  (void*)&k,      (void*)&idx_out, (void*)&val_out, (void*)&zero_at, (void*)&Lc};
-  return cudaLaunchCooperativeKernel((const void*)topk_fused_kernel<EF, RESID>, dim3((unsigned)G), dim3(kThreads), args,
-                                     0, s);
+  TkArgs ac = a;
+  void* args[] = {(void*)&ac};
+  return cudaLaunchCooperativeKernel((const void*)topk_stream_kernel<EF, STORE>, dim3((unsigned)topk_grid(a.N)),
+                                     dim3(kTkThreads), args, TkCfg<EF>::kSmem, s);
 }
 
 cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, float* x_out, uint64_t N,
@@ -1048,19 +1526,51 @@ cudaError_t launch_topk(const float* x, const float* grad, float alpha, int ef, 
     ++g_launches;
     return cudaGetLastError();
   }
-  TopkLayout L = topk_layout(ws, N);
+  TkArgs a;
+  a.x = x;
+  a.g = grad;
+  a.alpha = alpha;
+  a.N = N;
+  a.k = k;
+  a.idx_out = idx_out;
+  a.val_out = val_out;
+  a.L = topk_layout(ws, N);
   cudaError_t e;
   {
     SPARCML_PROF("topk", s);
-    if (ef) e = launch_fused<true, false>(x, grad, alpha, x_out, nullptr, N, k, idx_out, val_out, x_out, L, s);
-    else if (residual && residual != x)
-      e = launch_fused<false, true>(x, nullptr, 0.0f, nullptr, residual, N, k, idx_out, val_out, residual, L, s);
-    else   // no residual, or residual aliasing x (in place)
-      e = launch_fused<false, false>(x, nullptr, 0.0f, nullptr, nullptr, N, k, idx_out, val_out, residual, L, s);
+    if (ef) {   // eps is read through x and overwritten with acc, then zeroed at the selection
+      a.dst = x_out;
+      a.zero_at = x_out;
+      e = launch_stream<true, true>(a, s);
+    } else if (residual && residual != x) {
+      a.dst = residual;
+      a.zero_at = residual;
+      e = launch_stream<false, true>(a, s);
+    } else {    // no residual, or the residual is x itself (zeroed in place at the selection)
+      a.dst = nullptr;
+      a.zero_at = residual;
+      e = launch_stream<false, false>(a, s);
+    }
   }
   ++g_launches;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// host replica of sample_pos (diagnostics: lets a test build an input that
+// defeats the sample and so exercises the exact re-filter)
+size_t topk_sample_positions(uint64_t N, uint64_t* pos, size_t cap) {
+  if (N < kSampleMinN) return 0;
+  const uint32_t C = (uint32_t)((N + kChunk - 1) / kChunk), W = (uint32_t)topk_grid(N) * kTkWarps;
+  const WSplit sp{C / W, C % W};
+  size_t n = 0;
+  for (uint32_t q = 0; q < (uint32_t)kSampleGran; ++q) {
+    uint64_t p;
+    if (!sample_pos(q, N, C, W, sp, &p)) continue;
+    if (n < cap) pos[n] = p;
+    ++n;
+  }
+  return n;
 }
 
 // status readback helper for the API

@@ -52,7 +52,7 @@ EXPORTED = [
     "sparcml_sparse_allgather_local", "sparcml_apply_update", "sparcml_quantize_norm",
     "sparcml_sparse_allreduce_f64", "sparcml_sparse_allreduce_local_f64", "sparcml_result_bytes_f64",
     "sparcml_result_val_offset_f64", "sparcml_sparse_allgather_f64", "sparcml_sparse_allgather_local_f64",
-    "sparcml_apply_update_f64",
+    "sparcml_apply_update_f64", "sparcml_topk_sample_positions",
 ]
 
 
@@ -100,6 +100,7 @@ _sig = {
     "sparcml_ops_workspace_init": (_i32, [_p, _sz, _p]),
     "sparcml_merge_sum": (_i32, [_p, _p, _u64, _p, _p, _u64, _p, _p, _p, _p, _sz, _p]),
     "sparcml_topk_workspace_bytes": (_sz, [_u64, _u64]),
+    "sparcml_topk_sample_positions": (_sz, [_u64, _p, _sz]),
     "sparcml_topk_sparsify": (_i32, [_p, _u64, _u64, _u64, _p, _p, _p, _p, _sz, _p]),
     "sparcml_ef_topk": (_i32, [_p, _p, _f32, _u64, _u64, _u64, _p, _p, _p, _sz, _p]),
     "sparcml_topk_status": (_i32, [_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), _p]),
@@ -462,6 +463,15 @@ class TopkWorkspace:
         st, ps = C.c_uint32(), C.c_uint32()
         _check(_lib.sparcml_topk_status(self.buf.data_ptr(), C.byref(st), C.byref(ps), _stream(stream)))
         return int(st.value), int(ps.value)
+
+
+def topk_sample_positions(N: int):
+    """Diagnostics: start positions of the float4 granules the global top-k samples (current device)."""
+    import numpy as np
+    n = int(_lib.sparcml_topk_sample_positions(N, None, 0))
+    buf = np.zeros(max(n, 1), np.uint64)
+    _lib.sparcml_topk_sample_positions(N, buf.ctypes.data_as(C.c_void_p), n)
+    return buf[:n]
 
 
 class Request:

@@ -97,23 +97,88 @@ def test_topk_sparse_input_and_in_place_residual(orc):
     np.testing.assert_array_equal(xt.cpu().numpy(), er)
 
 
+def _defeat_sample(N, rng, small, large):
+    """Large values at exactly the granules the kernel samples, small ones elsewhere."""
+    x = small(N)
+    pos = S.topk_sample_positions(N).astype(np.int64)
+    assert len(pos) > 1000
+    for q in range(4):
+        x[pos + q] = large(len(pos))
+    return x, 4 * len(pos)
+
+
 def test_topk_fallback_when_sample_underestimates(orc):
-    """Adversarial input: every sampled chunk (8 values every N/16384) holds a
-    large value, the rest are small, and k exceeds the number of large values.
-    The sampled threshold then admits fewer than k candidates and the kernel
-    must take its exact re-filter path (passes == 2) and still be exact."""
+    """Adversarial input: every sampled granule holds large values, the rest are
+    small, and k exceeds the number of large values.  The sampled threshold then
+    admits fewer than k candidates and the kernel must take its exact re-filter
+    path (passes == 2) and still be exact."""
     N, k = 1 << 20, 1 << 18
     rng = np.random.default_rng(5)
-    x = rng.random(N, dtype=np.float32)
-    pos = (np.arange(16384, dtype=np.int64) * (N // 8) // 16384) * 8
-    for q in range(8):
-        x[pos + q] = 100.0 + rng.random(16384, dtype=np.float32) * 100.0
+    x, nl = _defeat_sample(N, rng, lambda n: rng.random(n, dtype=np.float32),
+                           lambda n: 100.0 + rng.random(n, dtype=np.float32) * 100.0)
+    assert nl < k
     ws = S.TopkWorkspace(N, k)
-    io, vo = S.topk_sparsify(cu(x, torch.float32), k, ws=ws)
-    ei, ev = orc.topk(x, k)
+    res = torch.empty(N, device="cuda")
+    io, vo = S.topk_sparsify(cu(x, torch.float32), k, residual=res, ws=ws)
+    ei, ev, er = orc.topk(x, k, residual=True)
     np.testing.assert_array_equal(host_idx(io), ei)
     np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    np.testing.assert_array_equal(res.cpu().numpy(), er)
     assert ws.status() == (0, 2)
+
+
+def test_ef_topk_fallback_when_sample_underestimates(orc):
+    """The same with error feedback: the re-filter reads acc back from eps (which
+    the kernel has already overwritten) and must still be exact."""
+    N, k = 1 << 20, 1 << 17
+    rng = np.random.default_rng(6)
+    eps = (rng.random(N, dtype=np.float32) * np.float32(0.01)).astype(np.float32)
+    g, nl = _defeat_sample(N, rng, lambda n: rng.standard_normal(n).astype(np.float32) * np.float32(0.1),
+                           lambda n: np.float32(1000.0) + rng.random(n, dtype=np.float32))
+    assert nl < k
+    ws = S.TopkWorkspace(N, k)
+    et = cu(eps, torch.float32)
+    io, vo = S.ef_topk(et, cu(g, torch.float32), 0.5, k, ws=ws)
+    ei, ev, ee = orc.ef_topk(eps, g, 0.5, k)
+    np.testing.assert_array_equal(host_idx(io), ei)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    np.testing.assert_array_equal(et.cpu().numpy(), ee)
+    assert ws.status() == (0, 2)
+
+
+def test_topk_workspace_reused_across_sizes(orc):
+    """One workspace, zeroed once, serves calls at any N up to its size, in any
+    order (every histogram slot is cleared by the call that used it)."""
+    ws = S.TopkWorkspace(300_000, 3000)
+    rng = np.random.default_rng(8)
+    for it, (N, k, ef) in enumerate([(1000, 10, False), (10_000, 100, True), (300_000, 3000, False),
+                                     (1000, 999, True), (70_000, 700, True), (10_000, 1, False),
+                                     (1000, 10, False), (300_000, 2999, True), (4096, 4095, False)]):
+        x = rng.standard_normal(N).astype(np.float32)
+        if ef:
+            g = rng.standard_normal(N).astype(np.float32)
+            et = cu(x, torch.float32)
+            io, vo = S.ef_topk(et, cu(g, torch.float32), 0.25, k, ws=ws)
+            ei, ev, ee = orc.ef_topk(x, g, 0.25, k)
+            np.testing.assert_array_equal(et.cpu().numpy(), ee)
+        else:
+            io, vo = S.topk_sparsify(cu(x, torch.float32), k, ws=ws)
+            ei, ev = orc.topk(x, k)
+        np.testing.assert_array_equal(host_idx(io), ei, err_msg=f"call {it}")
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev, err_msg=f"call {it}")
+        assert ws.status() == (0, 1)
+
+
+def test_topk_heavy_ties_refine_levels(orc):
+    """Half-integer values (config 5's gradients) give crossing bins of one
+    magnitude with far more than the list capacity: exact-bin and refine paths."""
+    rng = np.random.default_rng(11)
+    for N, k in [(1 << 20, 100_000), (3_231_961, 32_319), (1 << 22, 1_000_000)]:
+        x = (rng.integers(-40, 41, size=N) * 0.5).astype(np.float32)
+        io, vo = S.topk_sparsify(cu(x, torch.float32), k)
+        ei, ev = orc.topk(x, k)
+        np.testing.assert_array_equal(host_idx(io), ei)
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev)
 
 
 def test_topk_nonfinite_reported():
@@ -235,9 +300,10 @@ def test_qsgd_l2_parity(orc, n, bits, B):
     np.testing.assert_array_equal(c.cpu().numpy(), ec)
 
 
-@pytest.mark.parametrize("N,k,bucket", [(1 << 24, 167_772, 0), (25_557_032, 25_557, 0), (25_557_032, 4, 512)])
+@pytest.mark.parametrize("N,k,bucket", [(1 << 24, 167_772, 0), (25_557_032, 25_557, 0), (25_557_032, 4, 512),
+                                         (1 << 24, 1_677_721, 0)])
 def test_topk_bench_sizes(orc, N, k, bucket):
-    """The bench's top-k launches at full size (cfg2, cfg3, bucket512): EF over
+    """The bench's top-k launches at full size (cfg2, cfg3, bucket512, cfg4's 10 %): EF over
     two steps, bit-exact indices, values and residual against the oracle."""
     g = synth.gaussian_vector(N, seed=0)
     eps = np.zeros(N, np.float32)
