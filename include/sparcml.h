@@ -37,7 +37,7 @@ extern "C" {
 
 #define SPARCML_MAX_RANKS 16          /* one 8-GPU box; 16 for loopback worlds */
 #define SPARCML_HEADER_BYTES 64       /* result header at out[0]              */
-#define SPARCML_IPC_HANDLE_BYTES 64   /* cudaIpcMemHandle_t                    */
+#define SPARCML_IPC_HANDLE_BYTES 128  /* cudaIpcMemHandle_t + workspace descriptor */
 #define SPARCML_HEADER_MAGIC 0x4D435053u /* "SPCM" little-endian              */
 #define SPARCML_HEADER_MAGIC_F64 0x44435053u /* "SPCD": a result of the _f64 calls (double values) */
 
@@ -46,10 +46,19 @@ typedef enum {
   SPARCML_ERR_INVALID_ARG = 1,  /* bad size, null pointer, unsupported option */
   SPARCML_ERR_UNSORTED = 2,     /* input indices not strictly increasing or >= N */
   SPARCML_ERR_NONFINITE = 3,    /* NaN/Inf value where the method needs finite */
-  SPARCML_ERR_MISMATCH = 4,     /* ranks disagree on a collective argument     */
+  SPARCML_ERR_MISMATCH = 4,     /* ranks disagree on a collective argument: the
+                                   call signature (N, op, algo, options, value
+                                   type) travels with every exchange and a rank
+                                   receiving another one reports this in its
+                                   header; connect reports mismatched limits */
   SPARCML_ERR_CUDA = 5,         /* a CUDA runtime call failed (see last_error) */
   SPARCML_ERR_OOM = 7,          /* device allocation failed                    */
-  SPARCML_ERR_STATE = 8         /* communicator not connected / wrong mode     */
+  SPARCML_ERR_STATE = 8,        /* communicator not connected / wrong mode     */
+  SPARCML_ERR_TIMEOUT = 9       /* a peer's flag did not arrive within the comm's
+                                   timeout (dead, hung or mismatched rank); the
+                                   call completed without it, its result is
+                                   undefined and the communicator must be
+                                   destroyed (device-reported, header.status) */
 } sparcml_status;
 
 /* Reduction operator (§5: "arbitrary coordinate-wise associative
@@ -138,12 +147,36 @@ typedef struct sparcml_comm sparcml_comm;
  * per-rank nnz <= max_nnz.  Then every rank exports its handle, the caller
  * gathers the nranks handles in rank order (any host transport; the Python
  * binding uses torch.distributed) and passes them to sparcml_comm_connect,
- * which maps the peers' workspaces over NVLink (CUDA IPC). */
+ * which maps the peers' workspaces over NVLink (CUDA IPC).  A handle is the
+ * CUDA IPC handle (64 B) followed by a descriptor of the workspace layout
+ * (nranks, rank, max_N, max_nnz, layout size): connect returns
+ * SPARCML_ERR_MISMATCH, mapping nothing, unless every peer's descriptor matches
+ * this rank's (ranks built with different limits would address each other's
+ * memory at different offsets). */
 sparcml_status sparcml_comm_create(sparcml_comm** comm_out_host, int nranks, int rank,
                                    int cuda_device, uint64_t max_N, uint64_t max_nnz);
-sparcml_status sparcml_comm_export_handle(sparcml_comm* comm, uint8_t* handle_host /* 64 B */);
+sparcml_status sparcml_comm_export_handle(sparcml_comm* comm,
+                                          uint8_t* handle_host /* SPARCML_IPC_HANDLE_BYTES */);
 sparcml_status sparcml_comm_connect(sparcml_comm* comm,
-                                    const uint8_t* all_handles_host /* nranks*64 B, rank order */);
+                                    const uint8_t* all_handles_host /* nranks*SPARCML_IPC_HANDLE_BYTES, rank order */);
+
+/* Failure handling ("watchdog").  Every wait of a collective
+ * for a peer's flag gives up after timeout_ms (default 10000; 0 = wait
+ * forever): the call then completes with header.status = SPARCML_ERR_TIMEOUT
+ * on the ranks that waited, instead of hanging every GPU of the world.  After a
+ * timeout the communicator's flag protocol is out of step: destroy it.
+ * Synchronous (writes the value into the workspaces this process owns). */
+sparcml_status sparcml_comm_set_timeout(sparcml_comm* comm, uint64_t timeout_ms);
+
+/* Failure injection for tests, loopback worlds only:
+ *   what = SPARCML_INJECT_SKIP_RANKS: value = bit mask of ranks whose kernels
+ *          are not launched (dead ranks; the others must time out);
+ *   what = SPARCML_INJECT_PERTURB_SIG: value = r + 1 makes rank r call with a
+ *          different signature (N/op/algo/options; the others must report
+ *          SPARCML_ERR_MISMATCH), 0 = off.                                  */
+#define SPARCML_INJECT_SKIP_RANKS 1
+#define SPARCML_INJECT_PERTURB_SIG 2
+sparcml_status sparcml_comm_inject(sparcml_comm* comm, int what, uint64_t value);
 
 /* Loopback world: all nranks ranks live in this process on one device and
  * run the same kernels and exchanges through local memory.  Used for tests

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -91,9 +92,11 @@ struct Layout {
   size_t blk_off;                       // owner per-block output counts
   size_t part_off, part_bytes, scales_off;
   size_t rd_off, rd_bytes, rd_val_off;  // cur[2] + recv[2 parities][L stages]
-  size_t ag_off, ag_val_off;            // sparse allgather: my published stream (max_nnz pairs)
+  size_t ag_off, ag_val_off, ag_bytes;  // sparse allgather: my published stream (max_nnz pairs) x 2 call parities
   size_t total;
 };
+
+constexpr uint64_t kDefaultTimeoutNs = 10ull * 1000 * 1000 * 1000;   // flag waits give up after 10 s
 
 Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   Layout L;
@@ -136,7 +139,8 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   if (P > 1) off += (size_t)(2 + 2 * (L.L + 2)) * L.rd_bytes;
   L.ag_off = off;
   L.ag_val_off = align_up(4 * max_nnz, 256);
-  off += align_up(L.ag_val_off + 8 * max_nnz, 256);   // values up to 8 bytes (fp64)
+  L.ag_bytes = align_up(L.ag_val_off + 8 * max_nnz, 256);   // values up to 8 bytes (fp64)
+  off += 2 * L.ag_bytes;
   L.total = align_up(off, 1 << 20);
   return L;
 }
@@ -152,6 +156,8 @@ struct sparcml_comm {
   std::vector<bool> opened;  // peer[p] came from cudaIpcOpenMemHandle
   cudaIpcMemHandle_t handle;
   std::string err;
+  uint64_t inject_skip = 0;  // loopback failure injection: ranks whose kernels are not launched
+  uint64_t inject_sig = 0;   // r + 1: rank r calls with a perturbed signature
 };
 
 namespace {
@@ -244,7 +250,30 @@ struct CallCtx {
   int host_dsar;       // -1 unknown (device decides), 0/1 known
   int op;              // reduction operator (R-30)
   cudaStream_t s;
+  uint64_t sig;        // call signature: every rank's must agree
 };
+
+// FNV-1a over the arguments every rank must pass identically
+uint64_t call_signature(uint64_t N, int op, const sparcml_opts& o, int f64, int kind) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xFFu;
+      h *= 0x100000001b3ull;
+    }
+  };
+  uint32_t sc;
+  std::memcpy(&sc, &o.switch_scale, 4);
+  mix(N); mix((uint64_t)op); mix((uint64_t)o.algo); mix(sc); mix((uint64_t)o.index_bytes);
+  mix((uint64_t)o.quant_bits); mix(o.quant_bucket); mix(o.seed); mix(o.k_sum_hint); mix((uint64_t)o.quant_norm);
+  mix((uint64_t)f64); mix((uint64_t)kind);
+  return h;
+}
+
+inline uint64_t rank_sig(const sparcml_comm* c, uint64_t sig, int r) {
+  return c->inject_sig == (uint64_t)r + 1 ? sig ^ 0x9E3779B97F4A7C15ull : sig;
+}
+inline bool skipped(const sparcml_comm* c, int r) { return c->local && ((c->inject_skip >> r) & 1u); }
 
 BarrierArgs barrier_args(sparcml_comm* c, int r) {
   BarrierArgs b = {};
@@ -266,6 +295,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
   uint64_t max_in = L.max_nnz;             // bound on every rank's input (the comm's capacity)
   for (size_t i = 0; i < R.size(); ++i) max_in = std::max<uint64_t>(max_in, nnz[i]);
   auto pos = [&](int r) -> int {           // R's slot of rank r (loopback: every rank)
+    if (skipped(c, r)) return -1;          // failure injection: a dead rank launches nothing
     for (size_t i = 0; i < R.size(); ++i)
       if (R[i] == r) return (int)i;
     return -1;
@@ -283,6 +313,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     a.validate = cc.o.validate;
     a.tgt = tgt;
     a.f64 = cc.f64;
+    a.sig = rank_sig(c, cc.sig, r);
     CK(c, launch_rd_push(a, cc.s));
     return SPARCML_OK;
   };
@@ -331,6 +362,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     a.ctr = &ctrl_of(base)->scan[0];
     a.status = status_of(L, base);
     a.f64 = cc.f64;
+    a.sig = rank_sig(c, cc.sig, r);
     CK(c, launch_rd_stage(a, cc.s));
     return SPARCML_OK;
   };
@@ -365,6 +397,7 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
     u.N = cc.N;
     u.val_offset = cc.val_offset;
     u.f64 = cc.f64;
+    u.sig = rank_sig(c, cc.sig, r);
     CK(c, launch_rd_unfold(u, cc.s));
   }
   return SPARCML_OK;
@@ -383,6 +416,7 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
   bnd[P] = cc.N;
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
+    if (skipped(c, r)) continue;
     PushArgs a = {};
     a.idx = idx[i];
     a.val = val[i];
@@ -400,11 +434,13 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     a.ctl = ctrl_of(c->peer[r]);
     a.validate = cc.o.validate;
     a.f64 = cc.f64;
+    a.sig = rank_sig(c, cc.sig, r);
     CK(c, launch_split_push(a, cc.s));
   }
   const TreeSched ts = make_sched(P);
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
+    if (skipped(c, r)) continue;
     char* base = c->peer[r];
     OwnerArgs w = {};
     w.P = P;
@@ -439,10 +475,12 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
     w.blk = reinterpret_cast<uint64_t*>(base + L.blk_off);
     w.f64 = cc.f64;
     w.pdl = cc.host_dsar >= 0 && pdl_enabled() ? 1 : 0;   // one owner kernel: it may start during the push
+    w.sig = rank_sig(c, cc.sig, r);
     CK(c, launch_owner(w, cc.s));
   }
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
+    if (skipped(c, r)) continue;
     ConcatArgs a = {};
     a.P = P;
     a.rank = r;
@@ -601,6 +639,7 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   cc.val_offset = f64 ? sparcml_result_val_offset_f64(N) : sparcml_result_val_offset(N);
   cc.op = (int)op;
   cc.s = static_cast<cudaStream_t>(stream);
+  cc.sig = call_signature(N, (int)op, o, f64, 0);
   CK(c, cudaSetDevice(c->device));
   // algorithm: AUTO -> recursive doubling for small data (latency-bound,
   // P:635-650), split-allgather otherwise; RD needs P = 2^m
@@ -661,8 +700,10 @@ sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const
     for (int r = 0; r < P; ++r) R.push_back(r);
   else
     R.push_back(c->rank);
+  const uint64_t sig = call_signature(N, 0, o, f64, 1);
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
+    if (skipped(c, r)) continue;
     AgPublishArgs a = {};
     a.idx = idx[i];
     a.val = val[i];
@@ -670,9 +711,12 @@ sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const
     a.N = N;
     a.P = P;
     a.rank = r;
-    a.my_idx = reinterpret_cast<uint32_t*>(c->peer[r] + L.ag_off);
-    a.my_val = c->peer[r] + L.ag_off + L.ag_val_off;
+    for (int q = 0; q < 2; ++q) {
+      a.my_idx[q] = reinterpret_cast<uint32_t*>(c->peer[r] + L.ag_off + q * L.ag_bytes);
+      a.my_val[q] = c->peer[r] + L.ag_off + q * L.ag_bytes + L.ag_val_off;
+    }
     a.f64 = f64;
+    a.sig = rank_sig(c, sig, r);
     for (int j = 0; j < P; ++j) a.peer[j] = ctrl_of(c->peer[j]);
     a.ctl = ctrl_of(c->peer[r]);
     a.validate = o.validate;
@@ -680,15 +724,18 @@ sparcml_status allgather_impl(sparcml_comm* c, const uint32_t* const* idx, const
   }
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
+    if (skipped(c, r)) continue;
     AgGatherArgs g = {};
     g.P = P;
     g.rank = r;
     g.N = N;
     g.delta = effective_delta(N, o, f64 ? 8 : 4);
-    for (int j = 0; j < P; ++j) {
-      g.src_idx[j] = reinterpret_cast<const uint32_t*>(c->peer[j] + L.ag_off);
-      g.src_val[j] = c->peer[j] + L.ag_off + L.ag_val_off;
-    }
+    g.sig = rank_sig(c, sig, r);
+    for (int q = 0; q < 2; ++q)
+      for (int j = 0; j < P; ++j) {
+        g.src_idx[q][j] = reinterpret_cast<const uint32_t*>(c->peer[j] + L.ag_off + q * L.ag_bytes);
+        g.src_val[q][j] = c->peer[j] + L.ag_off + q * L.ag_bytes + L.ag_val_off;
+      }
     g.ctl = ctrl_of(c->peer[r]);
     g.out = static_cast<char*>(out[i]);
     g.val_offset = f64 ? sparcml_result_val_offset_f64(N) : sparcml_result_val_offset(N);
@@ -704,8 +751,23 @@ sparcml_status alloc_ws(sparcml_comm* c, char** p) {
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc");
   e = cudaMemset(*p, 0, c->L.total);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset");
+  const uint64_t t = kDefaultTimeoutNs;
+  e = cudaMemcpy(*p + offsetof(Ctrl, timeout_ns), &t, sizeof(t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemcpy");
   return SPARCML_OK;
 }
+
+// the workspace descriptor exported after the IPC handle (connect checks it)
+struct WsDesc {
+  uint32_t magic, version;
+  int32_t P, rank;
+  uint64_t max_N, max_nnz, total;
+  uint8_t pad[SPARCML_IPC_HANDLE_BYTES - 64 - 40];
+};
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+static_assert(sizeof(WsDesc) == SPARCML_IPC_HANDLE_BYTES - 64, "descriptor size");
+constexpr uint32_t kDescMagic = 0x53445053u;   // "SPDS"
+
 
 }  // namespace
 
@@ -724,6 +786,7 @@ const char* sparcml_status_string(sparcml_status s) {
     case SPARCML_ERR_CUDA: return "CUDA error";
     case SPARCML_ERR_OOM: return "out of device memory";
     case SPARCML_ERR_STATE: return "communicator in the wrong state";
+    case SPARCML_ERR_TIMEOUT: return "a peer did not arrive within the timeout (destroy the communicator)";
   }
   return "unknown status";
 }
@@ -811,8 +874,16 @@ sparcml_status sparcml_comm_create(sparcml_comm** out, int nranks, int rank, int
 sparcml_status sparcml_comm_export_handle(sparcml_comm* c, uint8_t* h) {
   if (!c || !h) return fail(c, SPARCML_ERR_INVALID_ARG, "null argument");
   if (c->local) return fail(c, SPARCML_ERR_STATE, "loopback worlds have no handle");
-  static_assert(sizeof(cudaIpcMemHandle_t) == SPARCML_IPC_HANDLE_BYTES, "IPC handle size");
-  std::memcpy(h, &c->handle, SPARCML_IPC_HANDLE_BYTES);
+  std::memcpy(h, &c->handle, 64);
+  WsDesc d = {};
+  d.magic = kDescMagic;
+  d.version = 1;
+  d.P = c->P;
+  d.rank = c->rank;
+  d.max_N = c->L.max_N;
+  d.max_nnz = c->L.max_nnz;
+  d.total = c->L.total;
+  std::memcpy(h + 64, &d, sizeof(d));
   return SPARCML_OK;
 }
 
@@ -821,10 +892,19 @@ sparcml_status sparcml_comm_connect(sparcml_comm* c, const uint8_t* all) {
   if (c->local) return fail(c, SPARCML_ERR_STATE, "loopback worlds are connected at creation");
   if (c->connected) return SPARCML_OK;
   CK(c, cudaSetDevice(c->device));
+  for (int p = 0; p < c->P; ++p) {   // every rank must have built the same layout
+    WsDesc d;
+    std::memcpy(&d, all + (size_t)p * SPARCML_IPC_HANDLE_BYTES + 64, sizeof(d));
+    if (d.magic != kDescMagic || d.version != 1 || d.P != c->P || d.rank != p || d.max_N != c->L.max_N ||
+        d.max_nnz != c->L.max_nnz || d.total != c->L.total)
+      return fail(c, SPARCML_ERR_MISMATCH,
+                  "rank " + std::to_string(p) + "'s workspace descriptor (nranks, rank, max_N, max_nnz, layout) "
+                  "does not match this rank's: every rank must create the communicator with the same limits");
+  }
   for (int p = 0; p < c->P; ++p) {
     if (p == c->rank) continue;
     cudaIpcMemHandle_t h;
-    std::memcpy(&h, all + (size_t)p * SPARCML_IPC_HANDLE_BYTES, SPARCML_IPC_HANDLE_BYTES);
+    std::memcpy(&h, all + (size_t)p * SPARCML_IPC_HANDLE_BYTES, 64);
     void* ptr = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaIpcOpenMemHandle");
@@ -867,6 +947,23 @@ sparcml_status sparcml_comm_create_local(sparcml_comm** out, int nranks, int dev
   c->opened.assign(nranks, false);
   c->connected = true;
   *out = c;
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_comm_set_timeout(sparcml_comm* c, uint64_t timeout_ms) {
+  if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
+  CK(c, cudaSetDevice(c->device));
+  const uint64_t t = timeout_ms * 1000ull * 1000ull;
+  for (char* p : c->own) CK(c, cudaMemcpy(p + offsetof(Ctrl, timeout_ns), &t, sizeof(t), cudaMemcpyHostToDevice));
+  return SPARCML_OK;
+}
+
+sparcml_status sparcml_comm_inject(sparcml_comm* c, int what, uint64_t value) {
+  if (!c) return fail(c, SPARCML_ERR_INVALID_ARG, "null communicator");
+  if (!c->local) return fail(c, SPARCML_ERR_STATE, "failure injection is for loopback worlds");
+  if (what == SPARCML_INJECT_SKIP_RANKS) c->inject_skip = value;
+  else if (what == SPARCML_INJECT_PERTURB_SIG) c->inject_sig = value;
+  else return fail(c, SPARCML_ERR_INVALID_ARG, "unknown injection");
   return SPARCML_OK;
 }
 

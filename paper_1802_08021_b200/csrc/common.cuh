@@ -363,20 +363,6 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
   return lo + __popc(__ballot_sync(0xffffffffu, pred));
 }
 
-// ---------------------------------------------------------------------------
-// cross-GPU signalling: a flag holds the sequence number of the call that set
-// it; waiters compare wrap-safely against seq + 1 of their own call
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void wait_flag_geq(const uint32_t* f, uint32_t target) {
-  // relaxed polling, then one acquire load of the (already satisfied) flag:
-  // synchronizes-with the producer's release without a full system fence
-  if ((int)(ld_acquire_sys(f) - target) >= 0) return;
-  int spins = 0;
-  while ((int)(ld_relaxed_sys_u32(f) - target) < 0)
-    if (++spins > 64) __nanosleep(32);   // tight polling first: a flag is usually microseconds away
-  (void)ld_acquire_sys(f);
-}
-
 constexpr int kMaxStages = 5;   // recursive doubling: log2(16) stages (+1)
 
 // ---------------------------------------------------------------------------
@@ -412,11 +398,66 @@ struct alignas(128) Ctrl {
   uint64_t dbg[2][16];            // %globaltimer phase marks (diagnostics): block 0, last block
   uint64_t owner_k[16];           // K_j of owner j's sparse partition result, stored by owner j with its flag
   // sparse allgather: rank i's published stream (count, index range) and its flag
-  uint64_t ag_n[16];
-  uint32_t ag_first[16], ag_last[16];
-  uint32_t ag_done[16];
+  // sparse allgather, per call parity (seq & 1): rank i's published stream
+  // (count, index range, call signature) and its flag.  Two slots: a rank that
+  // has finished call s may publish s+1 while a slower peer still pulls s.
+  uint64_t ag_n[2][16];
+  uint32_t ag_first[2][16], ag_last[2][16];
+  uint32_t ag_done[2][16];
+  uint64_t ag_sig[2][16];
   uint64_t fold_recv;             // RD folding (R-28): bytes received from my extra rank
+  // collective discipline: every rank's call signature (N, op, algo,
+  // options) travels with its data; a consumer that sees another signature sets
+  // SPARCML_ERR_MISMATCH.  RD stage inputs carry the sender's signature, xor 1
+  // once the sender has seen a mismatch (so it propagates to every rank).
+  uint64_t sig_in[kMaxRanks];     // split: source i's signature (with its slice)
+  uint64_t rd_sig[2][kMaxStages + 2];
+  uint64_t slice_rx[2][kMaxRanks];   // split owner: pairs received from source i in call parity p
+  uint64_t timeout_ns;            // flag waits give up after this long (SPARCML_ERR_TIMEOUT)
 };
+
+// ---------------------------------------------------------------------------
+// cross-GPU signalling: a flag holds the sequence number of the call that set
+// it; waiters compare wrap-safely against seq + 1 of their own call.  A wait
+// gives up after ctl->timeout_ns (a dead, hung or mismatched peer), sets
+// SPARCML_ERR_TIMEOUT in the rank's status and returns false; once that bit is
+// set, later waits of the call return at once, so the call completes (its
+// header reports the timeout) instead of hanging the GPU.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ bool wait_flag_geq(const uint32_t* f, uint32_t target, Ctrl* ctl) {
+  // relaxed polling, then one acquire load of the (already satisfied) flag:
+  // synchronizes-with the producer's release without a full system fence
+  if ((int)(ld_acquire_sys(f) - target) >= 0) return true;
+  if (ld_relaxed_gpu_u32(&ctl->status) & (1u << SPARCML_ERR_TIMEOUT)) return false;
+  const uint64_t limit = *(volatile uint64_t*)&ctl->timeout_ns;
+  const uint64_t t0 = global_ns();
+  uint32_t spins = 0;
+  while ((int)(ld_relaxed_sys_u32(f) - target) < 0) {
+    if (++spins > 64) {   // tight polling first: a flag is usually microseconds away
+      __nanosleep(32);
+      if ((spins & 255u) == 0 && limit && global_ns() - t0 > limit) {
+        atomicOr(&ctl->status, 1u << SPARCML_ERR_TIMEOUT);
+        return false;
+      }
+    }
+  }
+  (void)ld_acquire_sys(f);
+  return true;
+}
+
+// signature checks (see Ctrl::sig_in)
+__device__ __forceinline__ void check_sig(Ctrl* ctl, uint64_t got, uint64_t mine) {
+  if (got != mine) atomicOr(&ctl->status, 1u << SPARCML_ERR_MISMATCH);
+}
+__device__ __forceinline__ uint64_t sig_out(const Ctrl* ctl, uint64_t mine) {
+  return mine ^ ((*(volatile const uint32_t*)&ctl->status >> SPARCML_ERR_MISMATCH) & 1u);
+}
 
 __device__ __forceinline__ void dbg_mark(Ctrl* c, int slot) {
   // dbg[0][slot] = %globaltimer (ns) of block 0, dbg[1][slot] = the latest

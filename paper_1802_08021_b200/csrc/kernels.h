@@ -50,6 +50,7 @@ struct RdPushArgs {
   int validate;
   int tgt;                   // receiving stage: 1, or 0 = fold into rank i (R-28)
   int f64;                   // values are double
+  uint64_t sig;              // this rank's call signature (sent with the stream)
 };
 
 struct RdStageArgs {
@@ -77,6 +78,7 @@ struct RdStageArgs {
   ScanCounters* ctr;
   TileStatus* status;
   int f64;
+  uint64_t sig;              // this rank's call signature (checked, and mirrored on)
 };
 
 // Extra rank of a folded RD (R-28): wait for the result my fold partner
@@ -88,6 +90,7 @@ struct RdUnfoldArgs {
   char* out;
   uint64_t N, val_offset;
   int f64;
+  uint64_t sig;
 };
 
 // ---------------------------------------------------------- split phase ---
@@ -105,6 +108,7 @@ struct PushArgs {
   Ctrl* ctl;                       // mine
   int validate;
   int f64;
+  uint64_t sig;                    // this rank's call signature (sent with the slices)
 };
 
 struct OwnerArgs {
@@ -139,6 +143,7 @@ struct OwnerArgs {
   uint64_t* blk;
   int f64;
   int pdl;                         // launch as a programmatic dependent of the push (host_dsar known)
+  uint64_t sig;                    // this rank's call signature (every source's must match)
 };
 
 struct ConcatArgs {
@@ -195,22 +200,24 @@ struct AgPublishArgs {
   const void* val;                 // float or double (f64)
   uint64_t n, N;
   int P, rank;
-  uint32_t* my_idx;                // my published copy (my workspace)
-  void* my_val;
+  uint32_t* my_idx[2];             // my published copy (my workspace), by call parity
+  void* my_val[2];
   Ctrl* peer[kMaxRanks];
   Ctrl* ctl;
   int validate;
   int f64;
+  uint64_t sig;
 };
 struct AgGatherArgs {
   int P, rank;
   uint64_t N, delta;
-  const uint32_t* src_idx[kMaxRanks];   // every rank's published stream (peer pointers)
-  const void* src_val[kMaxRanks];
+  const uint32_t* src_idx[2][kMaxRanks];   // every rank's published stream (peer pointers), by call parity
+  const void* src_val[2][kMaxRanks];
   Ctrl* ctl;
   char* out;
   uint64_t val_offset;
   int f64;
+  uint64_t sig;
 };
 
 // -------------------------------------------------- layer-wise fusion ------

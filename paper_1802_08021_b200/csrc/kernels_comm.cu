@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(kThreads) rd_push_kernel(RdPushArgs a) {
     a.peer->rd_n[par][a.tgt] = a.n;
     a.peer->rd_dense[par][a.tgt] = 0;
     a.peer->rd_ksum[par][a.tgt] = a.n;
+    a.peer->rd_sig[par][a.tgt] = sig_out(a.ctl, a.sig);
     a.ctl->rd_sent[0] = pair_bytes<V>() * a.n;
     st_release_sys(&a.peer->rd_flag[par][a.tgt], seq + 1);
   }
@@ -263,8 +264,13 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
   const int par = seq & 1, t = a.stage;
-  if (tid == 0) wait_flag_geq(&ctl->rd_flag[par][t], seq + 1);   // the partner's stream is in place
+  __shared__ uint32_t s_ok;
+  if (tid == 0) {   // the partner's stream is in place (or it timed out: then treat it as empty)
+    s_ok = wait_flag_geq(&ctl->rd_flag[par][t], seq + 1, ctl) ? 1u : 0u;
+    if (s_ok) check_sig(ctl, *(volatile uint64_t*)&ctl->rd_sig[par][t], a.sig);
+  }
   __syncthreads();
+  const bool got = s_ok != 0;
   const int cp = (t - 1) & 1;   // cur buffer holding my stage t-1 output
   const uint32_t* a_idx = a.a_from_cur ? reinterpret_cast<const uint32_t*>(a.cur[cp].base) : a.a_idx;
   const V* a_val = a.a_from_cur ? reinterpret_cast<const V*>(a.cur[cp].base + a.cur[cp].val_off)
@@ -272,9 +278,9 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
   const uint64_t an = a.a_from_cur ? *(volatile uint64_t*)&ctl->own_n[cp] : a.a_n;
   const uint32_t ad = a.a_from_cur ? *(volatile uint32_t*)&ctl->own_dense[cp] : 0u;
   const uint64_t aks = a.a_from_cur ? *(volatile uint64_t*)&ctl->own_ksum[cp] : a.a_n;
-  const uint64_t bn = *(volatile uint64_t*)&ctl->rd_n[par][t];
-  const uint32_t bd = *(volatile uint32_t*)&ctl->rd_dense[par][t];
-  const uint64_t bks = *(volatile uint64_t*)&ctl->rd_ksum[par][t];
+  const uint64_t bn = got ? *(volatile uint64_t*)&ctl->rd_n[par][t] : 0;
+  const uint32_t bd = got ? *(volatile uint32_t*)&ctl->rd_dense[par][t] : 0u;
+  const uint64_t bks = got ? *(volatile uint64_t*)&ctl->rd_ksum[par][t] : 0;
   const StreamBuf b = a.b[par];
   const StreamBuf o = a.o_cur ? a.cur[t & 1] : a.o;
   const StreamBuf m = a.mpeer ? a.m[par] : StreamBuf{nullptr, 0};
@@ -353,6 +359,7 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
       a.mpeer->rd_n[par][t + 1] = on;
       a.mpeer->rd_dense[par][t + 1] = sparse_out ? 0u : 1u;
       a.mpeer->rd_ksum[par][t + 1] = ksum;
+      a.mpeer->rd_sig[par][t + 1] = sig_out(ctl, a.sig);
       ctl->rd_sent[t] = obytes;
       st_release_sys(&a.mpeer->rd_flag[par][t + 1], seq + 1);
     }
@@ -385,9 +392,10 @@ __global__ void __launch_bounds__(kThreads) rd_unfold_kernel(RdUnfoldArgs a) {
   const uint32_t seq = ctl->seq;
   const int par = seq & 1, t = a.stage;
   if (threadIdx.x == 0) {
-    wait_flag_geq(&ctl->rd_flag[par][t], seq + 1);
-    s_n = *(volatile uint64_t*)&ctl->rd_n[par][t];
-    s_d = *(volatile uint32_t*)&ctl->rd_dense[par][t];
+    const bool ok = wait_flag_geq(&ctl->rd_flag[par][t], seq + 1, ctl);
+    if (ok) check_sig(ctl, *(volatile uint64_t*)&ctl->rd_sig[par][t], a.sig);
+    s_n = ok ? *(volatile uint64_t*)&ctl->rd_n[par][t] : 0;
+    s_d = ok ? *(volatile uint32_t*)&ctl->rd_dense[par][t] : 0u;
   }
   __syncthreads();
   const uint64_t n = s_n;
@@ -517,6 +525,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
       const uint64_t c = s_off[tid + 1] - s_off[tid];
       a.peer[tid]->slice_cnt[a.rank] = c;
       a.peer[tid]->k_in[a.rank] = a.n;
+      a.peer[tid]->sig_in[a.rank] = sig_out(a.ctl, a.sig);
       a.ctl->slice_out[tid] = c;
     }
   }
@@ -597,9 +606,13 @@ __device__ __forceinline__ bool owner_prologue(const OwnerArgs& a, uint32_t seq,
   const int tid = threadIdx.x, P = a.P;
   Ctrl* ctl = a.ctl;
   if (tid < P) {
-    if (a.wait) wait_flag_geq(&ctl->src_done[tid], seq + 1);
-    s_ks[tid] = *(volatile uint64_t*)&ctl->k_in[tid];
-    if (s_sc) s_sc[tid] = *(volatile uint64_t*)&ctl->slice_cnt[tid];
+    bool ok = true;
+    if (a.wait) ok = wait_flag_geq(&ctl->src_done[tid], seq + 1, ctl);
+    if (ok && a.wait) check_sig(ctl, *(volatile uint64_t*)&ctl->sig_in[tid], a.sig);
+    s_ks[tid] = ok ? *(volatile uint64_t*)&ctl->k_in[tid] : 0;   // a timed-out source counts as empty
+    const uint64_t sc = ok ? *(volatile uint64_t*)&ctl->slice_cnt[tid] : 0;
+    if (s_sc) s_sc[tid] = sc;
+    if (blockIdx.x == 0) ctl->slice_rx[seq & 1][tid] = sc;   // this call's counts (the concat's header)
   }
   __syncthreads();
   if (tid == 0) {
@@ -1188,8 +1201,8 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
   if (dsar != (MODE == 1)) return;
   if (tid < a.P) {   // one lane per owner: wait for its flag, read its result size
     if (a.wait_owners) {
-      wait_flag_geq(&ctl->owner_done[tid], seq + 1);
-      s_k[tid] = *(volatile const uint64_t*)&ctl->owner_k[tid];   // stored by owner tid with its flag
+      const bool ok = wait_flag_geq(&ctl->owner_done[tid], seq + 1, ctl);
+      s_k[tid] = ok ? *(volatile const uint64_t*)&ctl->owner_k[tid] : 0;   // stored by owner tid with its flag
     } else {
       s_k[tid] = *(volatile const uint64_t*)a.r_n[tid];
     }
@@ -1375,7 +1388,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(ConcatArgs a) {
     for (int j = 0; j < a.P; ++j) {
       if (j == a.rank) continue;
       sent += pair_bytes<V>() * ctl->slice_out[j];
-      recv += pair_bytes<V>() * ctl->slice_cnt[j];
+      recv += pair_bytes<V>() * ctl->slice_rx[seq & 1][j];
     }
     for (int j = 0; j < a.P; ++j) {
       uint64_t w;
@@ -1445,8 +1458,7 @@ __global__ void barrier_kernel(BarrierArgs a) {
   fence_acq_rel_sys();
   if (!a.loopback && lane < a.P && lane != a.rank) {
     st_release_sys(a.peer_flags[lane], e);
-    while ((int)(ld_relaxed_sys_u32(&a.my->flags[lane]) - e) < 0) {
-    }
+    wait_flag_geq(&a.my->flags[lane], e, a.my);   // gives up after the comm's timeout (status bit)
   }
   __syncwarp();
   fence_acq_rel_sys();
@@ -1610,22 +1622,30 @@ cudaError_t launch_layer_ranges(const char* out, int L, const LayerOffsets& off,
 // sparse allgather for disjoint slices (§7 SCD; reading R-27):
 // publish (local copy + announce to every peer), then one pull-concatenation
 // ===========================================================================
+// Published streams and their metadata alternate by call parity: a rank that
+// has finished call s may publish s+1 (the other slot) while a slower peer
+// still pulls s; it can publish s+2 (this slot again) only after every peer
+// has published s+1, i.e. finished pulling s.
 template <typename V>
 __global__ void __launch_bounds__(kThreads) ag_publish_kernel(AgPublishArgs a) {
+  const uint32_t seq = a.ctl->seq;
+  const int par = seq & 1;
+  uint32_t* my_idx = a.my_idx[par];
+  V* my_val = static_cast<V*>(a.my_val[par]);
   for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < a.n; e += (uint64_t)gridDim.x * kThreads) {
     const uint32_t x = a.idx[e];
     const V v = static_cast<const V*>(a.val)[e];
-    a.my_idx[e] = x;
-    static_cast<V*>(a.my_val)[e] = v;
+    my_idx[e] = x;
+    my_val[e] = v;
     if (a.validate) check_input(a.idx, e, a.n, a.N, x, v, &a.ctl->status);
   }
   if (last_block<false>(&a.ctl->done_ctr[0]) && threadIdx.x < a.P) {   // local copies only: gpu scope
-    const uint32_t seq = a.ctl->seq;
     Ctrl* p = a.peer[threadIdx.x];
-    p->ag_n[a.rank] = a.n;
-    p->ag_first[a.rank] = a.n ? a.idx[0] : 0u;
-    p->ag_last[a.rank] = a.n ? a.idx[a.n - 1] : 0u;
-    st_release_sys(&p->ag_done[a.rank], seq + 1);
+    p->ag_n[par][a.rank] = a.n;
+    p->ag_first[par][a.rank] = a.n ? a.idx[0] : 0u;
+    p->ag_last[par][a.rank] = a.n ? a.idx[a.n - 1] : 0u;
+    p->ag_sig[par][a.rank] = sig_out(a.ctl, a.sig);
+    st_release_sys(&p->ag_done[par][a.rank], seq + 1);
   }
 }
 
@@ -1648,11 +1668,13 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
   const int tid = threadIdx.x;
   Ctrl* ctl = a.ctl;
   const uint32_t seq = ctl->seq;
+  const int par = seq & 1;
   if (tid < a.P) {   // one lane per rank: its stream is published
-    wait_flag_geq(&ctl->ag_done[tid], seq + 1);
-    s_n[tid] = *(volatile uint64_t*)&ctl->ag_n[tid];
-    s_first[tid] = *(volatile uint32_t*)&ctl->ag_first[tid];
-    s_last[tid] = *(volatile uint32_t*)&ctl->ag_last[tid];
+    const bool ok = wait_flag_geq(&ctl->ag_done[par][tid], seq + 1, ctl);
+    if (ok && blockIdx.x == 0) check_sig(ctl, *(volatile uint64_t*)&ctl->ag_sig[par][tid], a.sig);
+    s_n[tid] = ok ? *(volatile uint64_t*)&ctl->ag_n[par][tid] : 0;
+    s_first[tid] = *(volatile uint32_t*)&ctl->ag_first[par][tid];
+    s_last[tid] = *(volatile uint32_t*)&ctl->ag_last[par][tid];
   }
   __syncthreads();
   if (tid == 0) {   // non-empty ranks in range order; the ranges must not overlap
@@ -1707,12 +1729,12 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
         oo[x] = s_pref[i] + p;
         const int n = (int)std::min<uint64_t>(4, nr - p);
         if (n == 4) {
-          ix[x] = *reinterpret_cast<const uint4*>(a.src_idx[r] + p);
+          ix[x] = *reinterpret_cast<const uint4*>(a.src_idx[par][r] + p);
         } else {
-          const uint32_t* si = a.src_idx[r] + p;
+          const uint32_t* si = a.src_idx[par][r] + p;
           ix[x] = make_uint4(si[0], n > 1 ? si[1] : 0u, n > 2 ? si[2] : 0u, 0u);
         }
-        load4(static_cast<const V*>(a.src_val[r]) + p, n, vx[x]);
+        load4(static_cast<const V*>(a.src_val[par][r]) + p, n, vx[x]);
         cnt[x] = n;
       }
 #pragma unroll
@@ -1745,7 +1767,7 @@ __global__ void __launch_bounds__(kThreads) ag_gather_kernel(AgGatherArgs a) {
       while (e >= s_pref[i + 1]) ++i;
       const int r = s_ord[i];
       const uint64_t q = e - s_pref[i];
-      d[a.src_idx[r][q]] = static_cast<const V*>(a.src_val[r])[q];
+      d[a.src_idx[par][r][q]] = static_cast<const V*>(a.src_val[par][r])[q];
     }
   }
   grid.sync();

@@ -29,12 +29,14 @@ _lib = C.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants --
 OK, ERR_INVALID_ARG, ERR_UNSORTED, ERR_NONFINITE, ERR_MISMATCH, ERR_CUDA, ERR_OOM, ERR_STATE = 0, 1, 2, 3, 4, 5, 7, 8
+ERR_TIMEOUT = 9                 # a peer's flag did not arrive within the comm's timeout
+INJECT_SKIP_RANKS, INJECT_PERTURB_SIG = 1, 2   # loopback failure injection (tests)
 ALGO_AUTO, SSAR_RECURSIVE_DOUBLE, SSAR_SPLIT_ALLGATHER, DSAR_SPLIT_ALLGATHER = 0, 1, 2, 3
 SPARSE_ALLGATHER = 4   # header algo_used of sparcml_sparse_allgather
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
 REPR_SPARSE, REPR_DENSE = 0, 1
 HEADER_BYTES = 64
-IPC_HANDLE_BYTES = 64
+IPC_HANDLE_BYTES = 128          # CUDA IPC handle + workspace descriptor
 MAX_RANKS = 16
 HEADER_MAGIC = 0x4D435053
 HEADER_MAGIC_F64 = 0x44435053   # results of the fp64 calls (double values)
@@ -52,7 +54,7 @@ EXPORTED = [
     "sparcml_sparse_allgather_local", "sparcml_apply_update", "sparcml_quantize_norm",
     "sparcml_sparse_allreduce_f64", "sparcml_sparse_allreduce_local_f64", "sparcml_result_bytes_f64",
     "sparcml_result_val_offset_f64", "sparcml_sparse_allgather_f64", "sparcml_sparse_allgather_local_f64",
-    "sparcml_apply_update_f64", "sparcml_topk_sample_positions",
+    "sparcml_apply_update_f64", "sparcml_topk_sample_positions", "sparcml_comm_set_timeout", "sparcml_comm_inject",
 ]
 
 
@@ -101,6 +103,8 @@ _sig = {
     "sparcml_merge_sum": (_i32, [_p, _p, _u64, _p, _p, _u64, _p, _p, _p, _p, _sz, _p]),
     "sparcml_topk_workspace_bytes": (_sz, [_u64, _u64]),
     "sparcml_topk_sample_positions": (_sz, [_u64, _p, _sz]),
+    "sparcml_comm_set_timeout": (_i32, [_p, _u64]),
+    "sparcml_comm_inject": (_i32, [_p, _i32, _u64]),
     "sparcml_topk_sparsify": (_i32, [_p, _u64, _u64, _u64, _p, _p, _p, _p, _sz, _p]),
     "sparcml_ef_topk": (_i32, [_p, _p, _f32, _u64, _u64, _u64, _p, _p, _p, _sz, _p]),
     "sparcml_topk_status": (_i32, [_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), _p]),
@@ -268,17 +272,26 @@ def read_result(out: torch.Tensor, stream=None) -> Result:
 
 # -------------------------------------------------------------- communicators --
 def exchange_handles(mine: bytes, group=None) -> bytes:
-    """All-gather every rank's 64-byte workspace handle over the process group
-    (host-side bootstrap; any backend) and return them concatenated in rank order."""
+    """All-gather every rank's workspace handle (CUDA IPC handle + layout descriptor,
+    IPC_HANDLE_BYTES) over the process group (host-side bootstrap; any backend) and
+    return them concatenated in rank order."""
     import torch.distributed as dist
     if len(mine) != IPC_HANDLE_BYTES:
-        raise ValueError("handle must be 64 bytes")
+        raise ValueError(f"handle must be {IPC_HANDLE_BYTES} bytes")
     P = dist.get_world_size(group)
     allh = [None] * P
     dist.all_gather_object(allh, mine, group=group)
     if any(h is None or len(h) != IPC_HANDLE_BYTES for h in allh):
         raise SparcmlError(ERR_MISMATCH, "a rank sent a malformed handle")
     return b"".join(allh)
+
+
+def _outs_bytes(outs) -> int:
+    """The byte capacity every out buffer offers (uint8, contiguous, on the device)."""
+    for o in outs:
+        if o.dtype != torch.uint8 or not o.is_contiguous() or not o.is_cuda:
+            raise ValueError("out buffers must be contiguous uint8 CUDA tensors (new_out)")
+    return min(int(o.numel()) for o in outs)
 
 
 class LocalWorld:
@@ -307,7 +320,7 @@ class LocalWorld:
         oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
         o = opts if opts is not None else make_opts()
         fn = _lib.sparcml_sparse_allreduce_local_f64 if dt == torch.float64 else _lib.sparcml_sparse_allreduce_local
-        _check(fn(self._h, ia, va, na, N, op, C.byref(o), oa, int(outs[0].numel()), _stream(stream)), self._h)
+        _check(fn(self._h, ia, va, na, N, op, C.byref(o), oa, _outs_bytes(outs), _stream(stream)), self._h)
         return list(outs)
 
     def allgather(self, streams: Sequence, N: int, outs: Optional[Sequence[torch.Tensor]] = None,
@@ -327,8 +340,16 @@ class LocalWorld:
         oa = (C.c_void_p * P)(*[o.data_ptr() for o in outs])
         o = opts if opts is not None else make_opts()
         fn = _lib.sparcml_sparse_allgather_local_f64 if dt == torch.float64 else _lib.sparcml_sparse_allgather_local
-        _check(fn(self._h, ia, va, na, N, C.byref(o), oa, int(outs[0].numel()), _stream(stream)), self._h)
+        _check(fn(self._h, ia, va, na, N, C.byref(o), oa, _outs_bytes(outs), _stream(stream)), self._h)
         return outs
+
+    def set_timeout(self, ms: int):
+        """Flag waits give up after `ms` milliseconds (header status ERR_TIMEOUT); 0 = never."""
+        _check(_lib.sparcml_comm_set_timeout(self._h, int(ms)), self._h)
+
+    def inject(self, what: int, value: int):
+        """Failure injection (tests): INJECT_SKIP_RANKS mask, INJECT_PERTURB_SIG rank + 1."""
+        _check(_lib.sparcml_comm_inject(self._h, int(what), int(value)), self._h)
 
     def close(self):
         if self._h:
@@ -413,6 +434,10 @@ class Comm:
     def barrier(self, stream=None):
         """Device-side barrier of all ranks (stream-ordered, over NVLink flags)."""
         _check(_lib.sparcml_barrier(self._h, _stream(stream)), self._h)
+
+    def set_timeout(self, ms: int):
+        """Flag waits give up after `ms` milliseconds (header status ERR_TIMEOUT); 0 = never."""
+        _check(_lib.sparcml_comm_set_timeout(self._h, int(ms)), self._h)
 
     def allreduce_host(self, idx_host, val_host, N: int, out_host=None, opts: Optional[Opts] = None, stream=None):
         """End-to-end path through the C ABI with HOST buffers: H2D of the input,

@@ -48,7 +48,8 @@ def test_handle_exchange_and_max_reduce():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    from paper_1802_08021_b200 import sparcml as S
     for rank, blob, tmax, bad in got:
-        assert blob == bytes([1]) * 64 + bytes([2]) * 64     # rank order
+        assert blob == bytes([1]) * S.IPC_HANDLE_BYTES + bytes([2]) * S.IPC_HANDLE_BYTES   # rank order
         assert tmax == 11.0
         assert bad == "rejected"
