@@ -109,7 +109,7 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.ntab = (L.part_cap + kTab - 1) / kTab;
   size_t off = align_up(sizeof(Ctrl), 256);
   L.status_off = off;
-  L.n_status = max_N / 1024 + 2 * max_nnz / kMergeTile + 256;
+  L.n_status = max_N / 1024 + 2 * max_nnz / kMergeTile + 2048;   // >= any stage grid (merge_span block counts)
   off = align_up(off + L.n_status * sizeof(TileStatus), 256);
   L.recv_off = off;
   // receive regions, spill area, partition result and RD buffers are sized

@@ -189,15 +189,13 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
     if (o.n) *o.n = 0;
     if (o.n2) *o.n2 = 0;
   }
-  const uint32_t total = s_base[a.njobs];
-  while (true) {
-    const uint32_t t = next_ticket(a.ctr, &s_ticket);
-    if (t >= total) break;
-    int j = 0;
-    while (t >= s_base[j + 1]) ++j;
+  (void)s_ticket;
+  // jobs one after another, each a merge span over the whole grid (the block
+  // counts of job j live at status[j * gridDim.x ..])
+  for (int j = 0; j < a.njobs; ++j) {
     const MergeJob& jb = a.job[j];
-    merge_tile(jb.a_idx, jb.a_val, s_na[j], jb.b_idx, jb.b_val, s_nb[j], (uint64_t)(t - s_base[j]) * kMergeTile, sm,
-               a.status, t, s_base[j], s_gen, jb.out);
+    merge_span(jb.a_idx, jb.a_val, s_na[j], jb.b_idx, jb.b_val, s_nb[j], sm, a.status + (size_t)j * gridDim.x, s_gen,
+               jb.out);
   }
   scan_block_exit_last(a.ctr);
 }
@@ -300,13 +298,7 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     mo.val2 = m.base ? reinterpret_cast<V*>(m.base + m.val_off) : nullptr;
     mo.n2 = nullptr;
     __syncthreads();
-    const uint32_t total = (uint32_t)ceil_div(an + bn, kMergeTile);
-    if (total == 0 && blockIdx.x == 0 && tid == 0) ctl->own_n[t & 1] = 0;
-    while (true) {
-      const uint32_t tk = next_ticket(a.ctr, &s_ticket);
-      if (tk >= total) break;
-      merge_tile(a_idx, a_val, an, b_idx, b_val, bn, (uint64_t)tk * kMergeTile, sm, a.status, tk, 0, s_gen, mo);
-    }
+    merge_span(a_idx, a_val, an, b_idx, b_val, bn, sm, a.status, s_gen, mo);
   } else {
     // densify: window over [0, N) with the two streams (sparse or dense)
     if (tid == 0) {

@@ -157,6 +157,193 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
 }
 
 // ---------------------------------------------------------------------------
+// merge span: the whole union-merge-with-sum on the grid without a per-tile
+// look-back chain.  Block b owns the contiguous diagonal range of tiles
+// [T*b/G, T*(b+1)/G); two global merge-path searches locate its ends, after
+// which every tile boundary inside the range follows from the previous tile's
+// merge (each tile stages the next kMergeTile elements of A and B from where
+// the previous one stopped -- a superset window -- and its local merge path
+// says how many of each it consumed).  Pass 1 counts the block's output;
+// the block publishes the count and adds up its predecessors' (one load per
+// predecessor, all in flight: no serial look-back); pass 2 re-merges the same
+// tiles (their inputs now hit L2) and writes at the final offsets.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t umin64(uint64_t x, uint64_t y) { return x < y ? x : y; }
+
+template <typename V>
+struct SpanTile {
+  uint32_t ok[kMergeItems];
+  V ov[kMergeItems];
+  uint32_t emit;
+  uint32_t la;   // A elements the tile consumed
+};
+
+// Stage the windows at (a, b) and merge the tile's first L outputs.  All kThreads threads.
+template <typename V>
+__device__ __forceinline__ void span_tile(const uint32_t* __restrict__ A, const V* __restrict__ Av, uint64_t na,
+                                          const uint32_t* __restrict__ B, const V* __restrict__ Bv, uint64_t nb,
+                                          uint64_t a, uint64_t b, int L, int op, MergeSmem<V>& sm, SpanTile<V>& t) {
+  const int tid = threadIdx.x;
+  const int wa = (int)umin64((uint64_t)L, na - a);          // A window
+  const int wbL = (int)umin64((uint64_t)L, nb - b);         // B window for the merge
+  const int wb = (int)umin64((uint64_t)L + 1, nb - b);      // + the look-ahead element
+  __syncthreads();   // the previous tile's readers are done with sm
+#pragma unroll 4
+  for (int i = tid; i < wa; i += kThreads) {
+    sm.ak[i + 1] = __ldcg(&A[a + i]);
+    sm.av[i + 1] = __ldcg(&Av[a + i]);
+  }
+#pragma unroll 4
+  for (int i = tid; i < wb; i += kThreads) {
+    sm.bk[i] = __ldcg(&B[b + i]);
+    sm.bv[i] = __ldcg(&Bv[b + i]);
+  }
+  if (tid == 0) {
+    sm.has_prev_a = a > 0;
+    if (a > 0) sm.ak[0] = __ldcg(&A[a - 1]);
+  }
+  __syncthreads();
+  // the tile's consumption: merge path of the windows at diagonal L (warp 0, lane 0)
+  if (tid == 0) {
+    int lo = max(0, L - wbL), hi = min(L, wa);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sm.ak[mid + 1] <= sm.bk[L - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    sm.split[0] = (uint64_t)lo;
+  }
+  const int dt = min(tid * kMergeItems, L);
+  int lo = max(0, dt - wbL), hi = min(dt, wa);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sm.ak[mid + 1] <= sm.bk[dt - 1 - mid]) lo = mid + 1; else hi = mid;
+  }
+  int ia = lo, ib = dt - lo;
+  const bool has_prev_a = sm.has_prev_a;
+  t.emit = 0;
+#pragma unroll
+  for (int s = 0; s < kMergeItems; ++s) {
+    t.ok[s] = 0;
+    t.ov[s] = V(0);
+    if (dt + s < L) {
+      const bool takeA = ib >= wbL || (ia < wa && sm.ak[ia + 1] <= sm.bk[ib]);
+      if (takeA) {
+        const uint32_t key = sm.ak[ia + 1];
+        V v = sm.av[ia + 1];
+        // the element following A[ia] in merged order is B[ib] (in the window or the look-ahead)
+        if (ib < wb && sm.bk[ib] == key) v = op_combine(op, v, sm.bv[ib]);
+        t.ok[s] = key;
+        t.ov[s] = v;
+        t.emit |= 1u << s;
+        ++ia;
+      } else {
+        const uint32_t key = sm.bk[ib];
+        // a B element equal to the preceding A element was already summed into it
+        const bool dup = (ia > 0 || has_prev_a) && sm.ak[ia] == key;
+        if (!dup) {
+          t.ok[s] = key;
+          t.ov[s] = sm.bv[ib];
+          t.emit |= 1u << s;
+        }
+        ++ib;
+      }
+    }
+  }
+  __syncthreads();
+  t.la = (uint32_t)sm.split[0];
+}
+
+template <typename V>
+__device__ void merge_span(const uint32_t* __restrict__ A, const V* __restrict__ Av, uint64_t na,
+                           const uint32_t* __restrict__ B, const V* __restrict__ Bv, uint64_t nb, MergeSmem<V>& sm,
+                           TileStatus* st, uint32_t gen, const MergeOutput<V>& out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t G = gridDim.x, blk = blockIdx.x;
+  const uint64_t total = na + nb;
+  const uint64_t T = (total + kMergeTile - 1) / kMergeTile;
+  const uint64_t D0 = umin64(T * blk / G * kMergeTile, total);
+  const uint64_t D1 = umin64(T * (blk + 1) / G * kMergeTile, total);
+  __shared__ uint64_t s_a0, s_off;
+  if (warp == 0 && D0 < D1) {
+    const uint64_t s0 = warp_merge_path(A, na, B, nb, D0);
+    if (lane == 0) s_a0 = s0;
+  }
+  __syncthreads();
+  SpanTile<V> t;
+  // pass 1: count
+  uint32_t cnt = 0;
+  if (D0 < D1) {
+    uint64_t a = s_a0, b = D0 - s_a0;
+    for (uint64_t d = D0; d < D1; d += kMergeTile) {
+      const int L = (int)umin64(kMergeTile, D1 - d);
+      span_tile(A, Av, na, B, Bv, nb, a, b, L, out.op, sm, t);
+      cnt += __popc(t.emit);
+      a += t.la;
+      b += (uint64_t)L - t.la;
+    }
+  }
+  uint32_t ctot;
+  (void)block_exclusive_sum<uint32_t>(cnt, sm.scan, &ctot);
+  // publish this block's count, then add up the predecessors' (all loads in flight)
+  if (tid == 0) {
+    st[blk].agg = ctot;
+    __threadfence();
+    st_release_gpu(&st[blk].flag, (gen << 2) | 1u);
+  }
+  uint64_t before = 0;
+  for (uint32_t j = tid; j < blk; j += kThreads) {
+    uint32_t f = ld_acquire_gpu(&st[j].flag);
+    while (f != ((gen << 2) | 1u)) {
+      __nanosleep(20);
+      f = ld_acquire_gpu(&st[j].flag);
+    }
+    before += ld_relaxed_gpu(&st[j].agg);
+  }
+  uint64_t btot;
+  __shared__ uint64_t s_red[kWarps + 1];
+  (void)block_exclusive_sum<uint64_t>(before, s_red, &btot);
+  if (tid == 0) s_off = btot;
+  __syncthreads();
+  // pass 2: the same tiles, written at the final offsets
+  uint64_t o = s_off;
+  if (D0 < D1) {
+    uint64_t a = s_a0, b = D0 - s_a0;
+    for (uint64_t d = D0; d < D1; d += kMergeTile) {
+      const int L = (int)umin64(kMergeTile, D1 - d);
+      span_tile(A, Av, na, B, Bv, nb, a, b, L, out.op, sm, t);
+      uint32_t tt;
+      const uint32_t my = block_exclusive_sum<uint32_t>(__popc(t.emit), sm.scan, &tt);
+      uint32_t pos = my;
+#pragma unroll
+      for (int s = 0; s < kMergeItems; ++s)   // compact through shared memory (the windows are consumed)
+        if (t.emit & (1u << s)) {
+          sm.ak[pos] = t.ok[s];
+          sm.av[pos] = t.ov[s];
+          ++pos;
+        }
+      __syncthreads();
+      for (uint32_t i = tid; i < tt; i += kThreads) {   // coalesced
+        const uint32_t k = sm.ak[i];
+        const V v = sm.av[i];
+        out.idx[o + i] = k;
+        out.val[o + i] = v;
+        if (out.idx2) {
+          out.idx2[o + i] = k;
+          out.val2[o + i] = v;
+        }
+      }
+      o += tt;
+      a += t.la;
+      b += (uint64_t)L - t.la;
+    }
+  }
+  if (blk == G - 1 && tid == 0) {
+    if (out.n) *out.n = o;
+    if (out.n2) *out.n2 = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // window tile
 // ---------------------------------------------------------------------------
 template <typename V = float>
