@@ -67,9 +67,12 @@ typedef enum {
  * 0 (SUM), -inf (MAX), +inf (MIN).  QSGD (quant_bits) requires SUM. */
 typedef enum { SPARCML_OP_SUM = 0, SPARCML_OP_MAX = 1, SPARCML_OP_MIN = 2 } sparcml_op;
 
-/* Allreduce algorithms (§5.3).  AUTO: recursive doubling for the
- * small-data case, split-allgather otherwise; inside split-
- * allgather SSAR vs DSAR follows the dense-switch rule (R-5). */
+/* Allreduce algorithms (§5.3).  AUTO: recursive doubling only
+ * while sum_i k_i * 8 bytes stays under the crossover measured on this box
+ * (the paper's small-data rule; on 2 and 4 B200 over
+ * NVSwitch split-allgather won at every size measured, so AUTO picks it),
+ * otherwise split-allgather; inside split-allgather SSAR vs DSAR follows the
+ * dense-switch rule (R-5). */
 typedef enum {
   SPARCML_ALGO_AUTO = 0,
   SPARCML_SSAR_RECURSIVE_DOUBLE = 1,   /* §5.3.1                 */

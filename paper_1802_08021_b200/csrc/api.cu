@@ -214,6 +214,23 @@ uint64_t effective_delta(uint64_t N, const sparcml_opts& o, int vbytes = 4) {
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 
+// AUTO's recursive-doubling vs split-allgather crossover (RD for
+// small data), MEASURED on this box by tools/auto_crossover.py
+// (profiles/r02_auto_crossover_p2.log, _p4.log): the largest sum_i k_i * 8
+// bytes at which recursive doubling still beat split-allgather, per P.  On 2
+// and 4 B200 over NVSwitch it never did (N = 2^12 .. 2^24, densities 1/16 ..
+// 1/256: split 35-82 us vs RD 39-94 us at P = 2, 37-139 vs 74-225 us at P = 4):
+// every exchange is one hop, so RD's fewer alpha terms buy nothing and its
+// log2(P) dependent stages cost more.  P = 8 is unmeasured and takes P = 4's
+// entry.  0 = AUTO never picks RD.
+constexpr uint64_t kRdMaxBytes[SPARCML_MAX_RANKS + 1] = {0};
+
+bool auto_picks_rd(int P, uint64_t ksum_bytes) {
+  if (!is_pow2(P) || P > SPARCML_MAX_RANKS) return false;
+  const uint64_t lim = kRdMaxBytes[P];
+  return lim > 0 && ksum_bytes <= lim;
+}
+
 // Programmatic dependent launch of the owner and concat kernels: opt-in
 // (SPARCML_PDL=1).  Correct (same tests, stress), but measured slower: +1 us at
 // P = 2 and +5 us at P = 4 per allreduce (profiles/r01_ab_pdl.log) -- the early
@@ -644,8 +661,11 @@ sparcml_status allreduce_impl(sparcml_comm* c, const uint32_t* const* idx, const
   // algorithm: AUTO -> recursive doubling for small data (latency-bound,
   // P:635-650), split-allgather otherwise; RD needs P = 2^m
   int algo = o.algo;
-  if (algo == SPARCML_ALGO_AUTO && c->P > 1)
-    algo = (is_pow2(c->P) && 4 * N <= (256u << 10)) ? SPARCML_SSAR_RECURSIVE_DOUBLE : SPARCML_ALGO_AUTO;
+  if (algo == SPARCML_ALGO_AUTO && c->P > 1) {
+    // the data volume every rank agrees on: the exact sum (loopback), the hint, or the bound P*N
+    const uint64_t ksum = c->local ? ksum_host : (o.k_sum_hint ? o.k_sum_hint : (uint64_t)c->P * N);
+    algo = auto_picks_rd(c->P, 8 * ksum) ? SPARCML_SSAR_RECURSIVE_DOUBLE : SPARCML_ALGO_AUTO;
+  }
   cc.algo = algo;
   if (algo == SPARCML_SSAR_RECURSIVE_DOUBLE && c->P > 1)
     for (int i = 0; i < nl; ++i)

@@ -553,27 +553,9 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
   tk_mark(c, 0);
   TK_C(0);
 
-  // ---- S: the shared sample (loads issued first, ahead of the ring's) --------------
-  const bool sampling = N >= kSampleMinN;
-  constexpr int kSPer = kSampleGran / kTkThreads;   // granules per thread
-  float4 smp[kSPer];
-  bool sok[kSPer];
-#pragma unroll
-  for (int j = 0; j < kSPer; ++j) {
-    uint64_t pos = 0;
-    sok[j] = sampling && sample_pos((uint32_t)(tid + j * kTkThreads), N, C, W, sp, &pos);
-    smp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (sok[j]) {
-      smp[j] = __ldcg(reinterpret_cast<const float4*>(a.x + pos));
-      if (EF) {
-        const float4 gv = __ldcg(reinterpret_cast<const float4*>(a.g + pos));
-        smp[j] = make_float4(__fmaf_rn(a.alpha, gv.x, smp[j].x), __fmaf_rn(a.alpha, gv.y, smp[j].y),
-                             __fmaf_rn(a.alpha, gv.z, smp[j].z), __fmaf_rn(a.alpha, gv.w, smp[j].w));
-      }
-    }
-  }
-
   // ---- ring set-up and prologue: the first kStages chunks of every warp ---------
+  // (issued before the sample's loads: a fence after outstanding loads would
+  // wait for them, and the ring is what the filter needs first)
   uint64_t* wbar = mbar + warp * kStages;
   float* wring = ring + (size_t)warp * kStages * Cfg::kArr * kChunk;
   const uint64_t pol = l2_evict_first_policy();
@@ -588,10 +570,15 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     for (int s = 0; s < kStages; ++s) mbar_init(&wbar[s], 1);
     fence_mbar_init();
     fence_proxy_async_smem();
+    TK_D(18);
     if (!SPARCML_TOPK_LATE_PRO)
       for (int s = 0; s < kStages && (uint32_t)s < nch; ++s) issue(c0 + s, s);
+    TK_D(19);
   }
-  constexpr int kSBins = 4096;    // sample histogram: key >> 19 (1/16 octave), in the candidate area
+  __syncwarp();
+
+  const bool sampling = N >= kSampleMinN;
+  constexpr int kSBins = 8192;    // sample histogram: key >> 18 (1/32 octave), in the candidate area
   static_assert(kSBins * 4 <= kTkWarps * kCap * 8, "sample histogram fits the candidate area");
   uint32_t* shs = cidx;
   for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
@@ -603,6 +590,21 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
   }
   __syncthreads();
   TK_D(0);
+  // ---- S: the shared sample (its loads in flight with the ring's) ----------------------
+  constexpr int kSPer = kSampleGran / kTkThreads;   // granules per thread
+  float4 smp[kSPer], smg[kSPer];
+  bool sok[kSPer];
+#pragma unroll
+  for (int j = 0; j < kSPer; ++j) {
+    uint64_t pos = 0;
+    sok[j] = sampling && sample_pos((uint32_t)(tid + j * kTkThreads), N, C, W, sp, &pos);
+    smp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smg[j] = smp[j];
+    if (sok[j]) {
+      smp[j] = __ldcg(reinterpret_cast<const float4*>(a.x + pos));
+      if (EF) smg[j] = __ldcg(reinterpret_cast<const float4*>(a.g + pos));
+    }
+  }
 
   uint32_t tau = 0;
   uint64_t split = kKeyEnd;
@@ -610,11 +612,14 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     uint32_t ns = 0;
 #pragma unroll
     for (int j = 0; j < kSPer; ++j) {
+      if (EF)   // acc = fmaf(alpha, g, eps) at the sampled positions
+        smp[j] = make_float4(__fmaf_rn(a.alpha, smg[j].x, smp[j].x), __fmaf_rn(a.alpha, smg[j].y, smp[j].y),
+                             __fmaf_rn(a.alpha, smg[j].z, smp[j].z), __fmaf_rn(a.alpha, smg[j].w, smp[j].w));
       if (sok[j]) {
-        atomicAdd(&shs[abs_key(smp[j].x) >> 19], 1u);
-        atomicAdd(&shs[abs_key(smp[j].y) >> 19], 1u);
-        atomicAdd(&shs[abs_key(smp[j].z) >> 19], 1u);
-        atomicAdd(&shs[abs_key(smp[j].w) >> 19], 1u);
+        atomicAdd(&shs[abs_key(smp[j].x) >> 18], 1u);
+        atomicAdd(&shs[abs_key(smp[j].y) >> 18], 1u);
+        atomicAdd(&shs[abs_key(smp[j].z) >> 18], 1u);
+        atomicAdd(&shs[abs_key(smp[j].w) >> 18], 1u);
       }
       ns += sok[j] ? 4u : 0u;
     }
@@ -623,7 +628,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     (void)blk_excl_sum<uint64_t>(ns, s_sc, &S);   // (syncs: the sample histogram is complete)
     TK_D(2);
     // tau where the sample count from the top reaches t_lo = mean + 5 sigma + 4
-    // (to 1/16 octave): the k-th magnitude is >= tau unless the sample holds >=
+    // (to 1/32 octave): the k-th magnitude is >= tau unless the sample holds >=
     // t_lo values above it (a 5.6-sigma event; then the exact re-filter runs).
     // split where the count reaches mean - 4 sigma - 16: the level-0 bins cover
     // [tau, split) finely.  Same result in every CTA.
@@ -635,8 +640,8 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     find2<kSBins>(shs, t_lo, t_hi, s_sc, s_cross);
     const Cross f0 = s_cross[0], f1 = s_cross[1];
     if (EF && tid == 0) atomicAdd(&c->sampled[p], 1u);   // this CTA's sample reads are complete
-    tau = f0.ok ? (f0.bin << 19) : 0u;
-    split = f1.ok ? (uint64_t)(f1.bin + 1) << 19 : kKeyEnd;
+    tau = f0.ok ? (f0.bin << 18) : 0u;
+    split = f1.ok ? (uint64_t)(f1.bin + 1) << 18 : kKeyEnd;
     if (split <= tau) split = (uint64_t)tau + 1;
     TK_D(3);
   }

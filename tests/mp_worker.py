@@ -75,10 +75,12 @@ def main():
                       f"nnz {res.header.nnz}, status {res.header.status})", flush=True)
     fails += layerwise(comm, rank, P)
     fails += allgather(comm, rank, P)
+    fails += allgather_skewed(comm, rank, P)
     fails += algorithm1(comm, rank, P)
+    comm.close()
+    fails += failures(rank, P)
     t = torch.tensor([fails])
     dist.all_reduce(t)
-    comm.close()
     dist.destroy_process_group()
     if rank == 0:
         print(f"multigpu P={P}: {'OK' if t.item() == 0 else 'FAILED'} ({int(t.item())} mismatches)", flush=True)
@@ -175,6 +177,70 @@ def allgather(comm, rank, P):
         if not ok:
             fails += 1
             print(f"rank {rank}: allgather N={N} MISMATCH", flush=True)
+    return fails
+
+
+def allgather_skewed(comm, rank, P):
+    """Back-to-back sparse allgathers with no host sync between them while one
+    rank runs late (a spin kernel before each of its calls): a fast rank must
+    not overwrite a stream the slow one is still pulling (call-parity slots)."""
+    N, per, calls = 1 << 18, 4000, 16
+    outs, refs = [], []
+    for it in range(calls):
+        rng = np.random.default_rng(1000 + it)
+        bounds = np.linspace(0, N, P + 1).astype(np.int64)
+        order = rng.permutation(P)
+        streams = []
+        for r in range(P):
+            lo, hi = bounds[order[r]], bounds[order[r] + 1]
+            i = np.sort(rng.choice(np.arange(lo, hi), per, replace=False)).astype(np.uint32)
+            streams.append((i, rng.standard_normal(per).astype(np.float32)))
+        refs.append(oracle.sparse_allgather(N, streams)[0][rank])
+        i, v = streams[rank]
+        if rank == P - 1:
+            torch.cuda._sleep(200_000)   # ~0.1 ms late for every call
+        outs.append(comm.allgather(torch.from_numpy(i.view(np.int32)).cuda(), torch.from_numpy(v).cuda(), N))
+    torch.cuda.synchronize()
+    fails = 0
+    for it in range(calls):
+        g = S.read_result(outs[it])
+        d, ei, ev = refs[it]
+        ok = (g.header.status == 0 and not g.dense and np.array_equal(g.idx.cpu().numpy().view(np.uint32), ei)
+              and np.array_equal(g.val.cpu().numpy(), ev))
+        if not ok:
+            fails += 1
+            print(f"rank {rank}: skewed allgather call {it} MISMATCH (status {g.header.status})", flush=True)
+    return fails
+
+
+def failures(rank, P):
+    """Failure handling on the IPC world: (1) a rank that skips a collective --
+    the others' flag waits give up (header status ERR_TIMEOUT, no hang);
+    (2) ranks built with different limits -- connect reports ERR_MISMATCH."""
+    fails = 0
+    comm = S.Comm(1 << 16, 1000)
+    comm.set_timeout(300)
+    i, v = synth.uniform_streams(P, 1 << 16, 500, seed=77)[rank]
+    if rank != P - 1:   # the last rank is "dead" for this call
+        out = comm.allreduce(torch.from_numpy(i.view(np.int32)).cuda(), torch.from_numpy(v).cuda(), 1 << 16,
+                             opts=S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER))
+        st = S.read_result(out).header.status
+        if st != S.ERR_TIMEOUT:
+            fails += 1
+            print(f"rank {rank}: dead-rank call status {st}, expected ERR_TIMEOUT", flush=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    comm.close()
+    try:
+        bad = S.Comm(1 << 16 if rank != 0 else 1 << 17, 1000)
+        bad.close()
+        fails += 1
+        print(f"rank {rank}: mismatched limits were accepted", flush=True)
+    except S.SparcmlError as e:
+        if e.status != S.ERR_MISMATCH:
+            fails += 1
+            print(f"rank {rank}: mismatched limits gave status {e.status}, expected ERR_MISMATCH", flush=True)
+    dist.barrier()
     return fails
 
 

@@ -295,3 +295,25 @@ def test_in_place_rejected_where_unsafe():
     vv.fill_(2.0)
     with pytest.raises(S.SparcmlError):   # 60 > delta = 50 under forced SSAR
         w1.allreduce([(vi, vv)], 100, outs=[o], opts=S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER))
+
+
+@pytest.mark.parametrize("P,N,k", [(2, 4096, 16), (4, 4096, 64), (4, 1 << 16, 4096), (8, 1 << 20, 1000)])
+def test_auto_follows_measured_crossover(orc, P, N, k):
+    """AUTO picks recursive doubling only under the crossover measured on the box
+    (csrc/api.cu kRdMaxBytes, profiles/r02_auto_crossover_p*.log): on 2 and 4 B200
+    split-allgather won at every size, so AUTO runs split-allgather even for the
+    smallest data (the paper's small-data rule, measured, not assumed)."""
+    streams = synth.uniform_streams(P, N, k, seed=N + P)
+    w = S.LocalWorld(P, N, k)
+    outs = w.allreduce(to_cuda(streams), N, opts=S.make_opts(algo=S.ALGO_AUTO))
+    ref, _, _ = orc.split_allgather(N, streams, algo=orc.ALGO_AUTO)
+    for r in range(P):
+        g = S.read_result(outs[r])
+        assert g.header.status == 0
+        assert g.header.algo_used in (S.SSAR_SPLIT_ALLGATHER, S.DSAR_SPLIT_ALLGATHER)
+        d, ei, ev = ref[r]
+        assert g.dense == bool(d)
+        if not d:
+            np.testing.assert_array_equal(g.idx.cpu().numpy().view(np.uint32), ei)
+            np.testing.assert_array_equal(g.val.cpu().numpy(), ev)
+    w.close()
