@@ -9,6 +9,18 @@
 
 #include "sparcml.h"
 
+// Bounds checks compiled in with -DSPARCML_CHECKS (a diagnostics build: a
+// failed check traps with cudaErrorAssert; compute-sanitizer is not available
+// on this pool, so the test suite runs against this build instead).
+#ifdef SPARCML_CHECKS
+#include <cassert>
+#define SPARCML_CHECK(cond) assert(cond)
+#else
+#define SPARCML_CHECK(cond) \
+  do {                      \
+  } while (0)
+#endif
+
 namespace sparcml {
 
 constexpr int kMaxRanks = SPARCML_MAX_RANKS;

@@ -389,7 +389,9 @@ struct CandStore {
   float* sv;
   uint32_t* gi;
   float* gv;
+  uint32_t range;   // the warp's element count: the spill region's capacity
   __device__ __forceinline__ void put(uint32_t pos, uint32_t idx, float v) const {
+    SPARCML_CHECK(pos < (uint32_t)TkCfg<EF>::kCap + range);
     if (pos < (uint32_t)TkCfg<EF>::kCap) {
       si[pos] = idx;
       sv[pos] = v;
@@ -549,7 +551,8 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
   const uint64_t wbase = (uint64_t)c0 * kChunk;
   const uint32_t p = ld_relaxed_gpu_u32(&c->calls) & 1u;
   uint32_t bar_t = ld_relaxed_gpu_u32(&c->flag);
-  const CandStore<EF> cs{cidx + warp * kCap, cval + warp * kCap, a.L.sp_idx + wbase, a.L.sp_val + wbase};
+  const CandStore<EF> cs{cidx + warp * kCap, cval + warp * kCap, a.L.sp_idx + wbase, a.L.sp_val + wbase,
+                         (uint32_t)(std::min<uint64_t>(N, (uint64_t)(c0 + nch) * kChunk) - wbase)};
   tk_mark(c, 0);
   TK_C(0);
 
@@ -758,6 +761,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
       cs.get(i, &idx, &v);
       const uint32_t key = abs_key(v);
       const uint32_t at = atomicAdd(&ab[bin_of(key, tau, split, shift)], 1u);
+      SPARCML_CHECK(at < cta_n && r0 + kBins + at < r1);
       si[at] = idx;
       sv[at] = v;
     }
@@ -882,6 +886,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
               else hi_b = mid;
             }
             while (cnb[lo_b] == 0 || sof[lo_b] + cnb[lo_b] <= e) ++lo_b;   // skip empty segments
+            SPARCML_CHECK(lo_b < G && e >= sof[lo_b] && e - sof[lo_b] < cnb[lo_b]);
             lk[e] = abs_key(__ldcg(a.L.sp_val + cta_r0(lo_b) + kBins + abh[lo_b] + (e - sof[lo_b])));
             lc[e] = lo_b;
           }
@@ -1220,6 +1225,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
       const uint32_t tb = __ballot_sync(0xffffffffu, take);
       if (take) {
         const uint64_t pos = o + run + __popc(tb & lt);
+        SPARCML_CHECK(pos < k && idx < N);
         a.idx_out[pos] = idx;
         a.val_out[pos] = v;
         if (a.zero_at) a.zero_at[idx] = 0.0f;   // acc - TopK(acc)

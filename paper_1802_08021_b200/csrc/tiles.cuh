@@ -323,6 +323,7 @@ __device__ void merge_span(const uint32_t* __restrict__ A, const V* __restrict__
         }
       __syncthreads();
       for (uint32_t i = tid; i < tt; i += kThreads) {   // coalesced
+        SPARCML_CHECK(o + i < total);
         const uint32_t k = sm.ak[i];
         const V v = sm.av[i];
         out.idx[o + i] = k;

@@ -74,11 +74,8 @@ def main():
                 else:
                     a = {"ssar": oracle.ALGO_SSAR_SPLIT, "dsar": oracle.ALGO_DSAR_SPLIT, "dsar4": oracle.ALGO_DSAR_SPLIT,
                          "auto": oracle.ALGO_AUTO}[kind]
-                    if kind == "auto" and (P & (P - 1)) == 0 and 4 * N <= 256 * 1024:
-                        ref, _ = oracle.ssar_recursive_double(N, streams, dtype=dt)
-                    else:
-                        ref, _, _ = oracle.split_allgather(N, streams, algo=a, quant_bits=4 if kind == "dsar4" else 0,
-                                                           seed=seed & 0xFFFF, dtype=dt)
+                    ref, _, _ = oracle.split_allgather(N, streams, algo=a, quant_bits=4 if kind == "dsar4" else 0,
+                                                       seed=seed & 0xFFFF, dtype=dt)   # AUTO: split at every size
                 d, ei, ev = ref[rank]
                 ok = g.header.status == 0 and g.dense == d
                 if ok and d:

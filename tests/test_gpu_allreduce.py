@@ -45,10 +45,7 @@ def check_world(orc, P, N, streams, algo, bits=0, bucket=1024, seed=0, world=Non
     opts = S.make_opts(algo=algo, quant_bits=bits, quant_bucket=bucket, seed=seed)
     outs = w.allreduce(to_cuda(streams), N, opts=opts)
     torch.cuda.synchronize()
-    oalgo = algo
-    if algo == S.ALGO_AUTO and P > 1:
-        pow2 = (P & (P - 1)) == 0
-        oalgo = S.SSAR_RECURSIVE_DOUBLE if (pow2 and 4 * N <= 256 * 1024) else S.ALGO_AUTO
+    oalgo = algo   # AUTO: split-allgather at every size (the measured crossover, csrc/api.cu kRdMaxBytes)
     res, st, _ = oracle_run(orc, N, streams, oalgo if P > 1 else (S.ALGO_AUTO if algo == S.SSAR_RECURSIVE_DOUBLE else algo),
                             bits, bucket, seed)
     for r in range(P):
@@ -207,8 +204,6 @@ def test_max_min_operators(orc, op, P, algo):
         outs = w.allreduce(to_cuda(streams), N, opts=S.make_opts(algo=ALGOS[algo]), op=op)
         with orc.op_scope(op):
             oalgo = ALGOS[algo]
-            if algo == "auto" and P > 1:
-                oalgo = S.SSAR_RECURSIVE_DOUBLE if 4 * N <= 256 * 1024 else S.ALGO_AUTO
             res, st, _ = oracle_run(orc, N, streams, oalgo if P > 1 else ALGOS[algo])
         for r in range(P):
             g = S.read_result(outs[r])

@@ -32,9 +32,7 @@ def oracle_run(orc, N, streams, algo, P):
     if algo == S.SSAR_RECURSIVE_DOUBLE and P > 1:
         res, st = orc.ssar_recursive_double(N, streams, dtype=F64)
         return res, st
-    if algo == S.ALGO_AUTO and P > 1 and (P & (P - 1)) == 0 and 4 * N <= 256 * 1024:
-        res, st = orc.ssar_recursive_double(N, streams, dtype=F64)
-        return res, st
+    # AUTO runs split-allgather at every size (the crossover measured on the box, csrc/api.cu kRdMaxBytes)
     oalgo = {S.SSAR_SPLIT_ALLGATHER: orc.ALGO_SSAR_SPLIT, S.DSAR_SPLIT_ALLGATHER: orc.ALGO_DSAR_SPLIT,
              S.ALGO_AUTO: orc.ALGO_AUTO, S.SSAR_RECURSIVE_DOUBLE: orc.ALGO_AUTO}[algo]
     res, st, _ = orc.split_allgather(N, streams, algo=oalgo, dtype=F64)
