@@ -957,11 +957,22 @@ __host__ __device__ constexpr size_t dsar_smem_bytes(int P, size_t vbytes = 4) {
   return sizeof(uint32_t) * kWin + vbytes * kWin * (size_t)P;
 }
 
+// The canonical balanced rank-order tree (R-8): tree(lo, hi) = tree(lo, mid) +
+// tree(mid, hi), mid = lo + (hi - lo) / 2, unrolled at compile time for P.
+template <int OP, int LO, int HI, typename V>
+__device__ __forceinline__ V canonical_tree(const V* v) {
+  if constexpr (HI - LO == 1) {
+    return v[LO];
+  } else {
+    constexpr int MID = LO + (HI - LO) / 2;
+    return op_combine(OP, canonical_tree<OP, LO, MID>(v), canonical_tree<OP, MID, HI>(v));
+  }
+}
+
 template <int P, typename V>
 __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
-  V* vals = reinterpret_cast<V*>(smem + sizeof(uint32_t) * kWin);
+  V* vals = reinterpret_cast<V*>(smem + sizeof(uint32_t) * kWin);   // (the first kWin words: unused)
   V* const dense = static_cast<V*>(a.dense);
   __shared__ uint64_t s_ks[kMaxRanks];
   __shared__ uint32_t s_dsar, s_bmax[kWin / 8];
@@ -997,8 +1008,18 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
       if (lane == P - 1) s_pre[P] = incl;
       if (w + gridDim.x < nwin) tab_load(w + gridDim.x, n0, n1);
     }
+    // every source row starts at the operator's neutral element: an absent
+    // operand then combines to the other one (fl(x + 0) = x up to the sign of
+    // zero, which R-9 compares numerically; max(x, -inf) = x), so the tree
+    // below needs no presence bits
+    {
+      const int p0 = tid * kWinPerThread;
+      const V nv = op_neutral_v<V>(a.op);
 #pragma unroll
-    for (int q = 0; q < kWinPerThread; ++q) pres[tid + q * kThreads] = 0u;
+      for (int s = 0; s < P; ++s)
+#pragma unroll
+        for (int q = 0; q < kWinPerThread; ++q) vals[s * kWin + p0 + q] = nv;
+    }
     __syncthreads();
     // (2) scatter, every source at once, 4 element loads in flight per thread
     const uint32_t tot = s_pre[P];
@@ -1022,35 +1043,18 @@ __global__ void __launch_bounds__(kThreads) dsar_owner_kernel(OwnerArgs a) {
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (xs[q] >= 0) {
-          const uint32_t pos = xi[q] - (uint32_t)wlo;
-          vals[xs[q] * kWin + pos] = xv[q];
-          atomicOr(&pres[pos], 1u << xs[q]);
-        }
+        if (xs[q] >= 0) vals[xs[q] * kWin + (xi[q] - (uint32_t)wlo)] = xv[q];
     }
     __syncthreads();
-    // (3) combine per position in the canonical tree order
+    // (3) combine per position in the canonical tree order (R-8), in registers
     const int p0 = tid * kWinPerThread;
     V r[kWinPerThread];
 #pragma unroll
     for (int q = 0; q < kWinPerThread; ++q) {
-      const int p = p0 + q;
-      uint32_t m = (p < wn) ? pres[p] : 0u;
-      if (P > 1 && (m & (m - 1))) {
-        for (int t = 0; t < a.sched.n; ++t) {
-          const int d = a.sched.dst[t], sr = a.sched.src[t];
-          if (m & (1u << sr)) {
-            if (m & (1u << d)) vals[d * kWin + p] = op_combine(a.op, vals[d * kWin + p], vals[sr * kWin + p]);
-            else {
-              vals[d * kWin + p] = vals[sr * kWin + p];
-              m |= 1u << d;
-            }
-          }
-        }
-        r[q] = vals[p];
-      } else {
-        r[q] = m ? vals[(__ffs(m) - 1) * kWin + p] : op_neutral_v<V>(a.op);
-      }
+      V v[P];
+#pragma unroll
+      for (int s = 0; s < P; ++s) v[s] = vals[s * kWin + p0 + q];
+      r[q] = a.op == 0 ? canonical_tree<0, 0, P>(v) : (a.op == 1 ? canonical_tree<1, 0, P>(v) : canonical_tree<2, 0, P>(v));
     }
     // (4) store: QSGD codes + scales, or dense
     const uint64_t e = w * kWin + p0;   // partition-relative

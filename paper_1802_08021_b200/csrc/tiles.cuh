@@ -417,18 +417,31 @@ __device__ __forceinline__ void qsgd_encode4(const float v[4], float scale, uint
                                              uint8_t* __restrict__ codes) {
   const uint32_t s = (1u << (bits - 1)) - 1u;
   uint32_t packed = 0;
-  uint4 blk = philox4x32_10(make_uint4((uint32_t)(c0 >> 2), (uint32_t)(c0 >> 34), 0u, 0u), k0, k1);
-  uint4 blk2 = blk;
-  if ((c0 & 3) != 0) {
-    const uint64_t nb = (c0 >> 2) + 1;
-    blk2 = philox4x32_10(make_uint4((uint32_t)nb, (uint32_t)(nb >> 32), 0u, 0u), k0, k1);
-  }
+  // a zero value always codes to 0 (level = floor(0 + u) = 0 since u < 1, R-16):
+  // no random word and no division for it, and no Philox block for 4 zeros
+  bool any = false;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint64_t c = c0 + i;
-    const uint32_t w = ((c >> 2) == (c0 >> 2)) ? u4_get(blk, (int)(c & 3)) : u4_get(blk2, (int)(c & 3));
-    const uint32_t code = i < valid ? qsgd_code(v[i], scale, s, bits, w) : 0u;
-    packed |= code << (i * bits);
+  for (int i = 0; i < 4; ++i) any |= i < valid && v[i] != 0.0f;
+  if (any && scale != 0.0f) {
+    const uint4 blk = philox4x32_10(make_uint4((uint32_t)(c0 >> 2), (uint32_t)(c0 >> 34), 0u, 0u), k0, k1);
+    if ((c0 & 3) == 0) {   // the 4 counters are one Philox block: word i is element i's
+      const uint32_t wv[4] = {blk.x, blk.y, blk.z, blk.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t code = (i < valid && v[i] != 0.0f) ? qsgd_code(v[i], scale, s, bits, wv[i]) : 0u;
+        packed |= code << (i * bits);
+      }
+    } else {
+      const uint64_t nb = (c0 >> 2) + 1;
+      const uint4 blk2 = philox4x32_10(make_uint4((uint32_t)nb, (uint32_t)(nb >> 32), 0u, 0u), k0, k1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t c = c0 + i;
+        const uint32_t w = ((c >> 2) == (c0 >> 2)) ? u4_get(blk, (int)(c & 3)) : u4_get(blk2, (int)(c & 3));
+        const uint32_t code = (i < valid && v[i] != 0.0f) ? qsgd_code(v[i], scale, s, bits, w) : 0u;
+        packed |= code << (i * bits);
+      }
+    }
   }
   if (valid == 4) {
     if (bits == 2) codes[e / 4] = (uint8_t)packed;
