@@ -71,7 +71,7 @@ for _ in range(args.reps):
         tc = ws.buf[TC:TC + 2 * 1024 * 8].cpu().numpy().view(np.uint64).reshape(2, 1024)[:, :G].astype(np.float64)
         tcs.append(((tc[0] - t[0]) / 1e3, (tc[1] - t[0]) / 1e3))
         d = np.where(d > 0, (d - t[0]) / 1e3, np.nan)
-        ph.append(np.concatenate([(t[1:8] - t[0]) / 1e3, [(t[8] - t[0]) / 1e3], (t[9:15] - t[0]) / 1e3, d[:18]]))
+        ph.append(np.concatenate([(t[1:8] - t[0]) / 1e3, [(t[8] - t[0]) / 1e3], (t[9:15] - t[0]) / 1e3, d[:21]]))
 st = ws.status()
 ts = np.array(ts)
 alg = (12 if not args.plain else 4) * N + 8 * k
@@ -89,4 +89,4 @@ if ph:
     print("per-CTA start p0/p50/p100 %.2f %.2f %.2f; filter end p0/p10/p50/p90/p100 %.2f %.2f %.2f %.2f %.2f" % (
         st0.min(), np.median(st0), st0.max(), fe.min(), np.percentile(fe, 10), np.median(fe), np.percentile(fe, 90), fe.max()))
     print("CTA 0 values: tau %x split %x cta_n %d fast_ok %d crossing cnt %d bin %d fast %d kth %x" % tuple(int(v) for v in raw))
-    print("CTA 0 fine marks (TK_D 0..17): " + " ".join(f"{i}:{v:.2f}" for i, v in enumerate(p[14:])))
+    print("CTA 0 fine marks (TK_D 0..20): " + " ".join(f"{i}:{v:.2f}" for i, v in enumerate(p[14:])))
