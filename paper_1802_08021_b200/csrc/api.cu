@@ -93,6 +93,9 @@ struct Layout {
   size_t part_off, part_bytes, scales_off;
   size_t rd_off, rd_bytes, rd_val_off;  // cur[2] + recv[2 parities][L stages]
   size_t ag_off, ag_val_off, ag_bytes;  // sparse allgather: my published stream (max_nnz pairs) x 2 call parities
+  size_t rec_off;                       // fused split-allgather: owner pieces' records (P x kFzMaxG)
+  size_t fz_off, fz_bytes;              // ... and their staging, per owner
+  uint64_t fz_cap;                      // pairs per owner's staging
   size_t total;
 };
 
@@ -104,7 +107,9 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.max_N = max_N;
   L.max_nnz = max_nnz;
   L.part_cap = align_up(max_N / P + P, 64);
-  L.cap_s = align_up(std::min<uint64_t>(max_nnz, L.part_cap), 4);   // val[] 16-byte aligned (fp64 too)
+  // pairs per receive region: the fused split push keeps each element's STREAM
+  // index (up to max_nnz - 1), not its slice position; val[] 16-byte aligned
+  L.cap_s = align_up(std::max<uint64_t>(max_nnz, 1), 4);
   L.nwin = (L.part_cap + kWin - 1) / kWin;
   L.ntab = (L.part_cap + kTab - 1) / kTab;
   size_t off = align_up(sizeof(Ctrl), 256);
@@ -141,6 +146,14 @@ Layout make_layout(int P, uint64_t max_N, uint64_t max_nnz) {
   L.ag_val_off = align_up(4 * max_nnz, 256);
   L.ag_bytes = align_up(L.ag_val_off + 8 * max_nnz, 256);   // values up to 8 bytes (fp64)
   off += 2 * L.ag_bytes;
+  // fused split-allgather: owner j's pieces land at slots <= min(its inputs,
+  // its partition's positions) + 4 per CTA (split_fused_kernel)
+  L.rec_off = off;
+  off += align_up((size_t)P * kFzMaxG * 8, 256);
+  L.fz_cap = align_up(std::min<uint64_t>((uint64_t)P * L.cap_s, L.part_cap + kTab) + 4 * (uint64_t)kFzMaxG + 4, 4);
+  L.fz_off = off;
+  L.fz_bytes = P > 1 ? align_up(12 * L.fz_cap, 256) : 0;
+  off += (size_t)P * L.fz_bytes;
   L.total = align_up(off, 1 << 20);
   return L;
 }
@@ -423,6 +436,13 @@ sparcml_status run_rd(sparcml_comm* c, const std::vector<int>& R, const uint32_t
 // --------------------------------------------------------- split schedule ---
 // push (slices + window tables -> owners) ; owner reduction (waits for the P
 // slices) ; pull-concat (waits for the P owners)
+// SPARCML_FUSED=0 selects the three-kernel split path (push, owner, concat)
+// even when SSAR is known on the host (A/B runs and its tests); read per call.
+bool fused_enabled() {
+  const char* e = std::getenv("SPARCML_FUSED");
+  return !(e && e[0] == '0');
+}
+
 sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint32_t* const* idx,
                          const void* const* val, const uint64_t* nnz, char* const* out, const CallCtx& cc) {
   const Layout& L = c->L;
@@ -431,6 +451,45 @@ sparcml_status run_split(sparcml_comm* c, const std::vector<int>& R, const uint3
   uint64_t bnd[kMaxRanks + 1];
   for (int j = 0; j < P; ++j) bnd[j] = (uint64_t)j * part;
   bnd[P] = cc.N;
+  // SSAR known on the host: one fused kernel does push, owner reduction and allgather
+  const int nloc = (int)R.size();
+  const int G = cc.host_dsar == 0 && fused_enabled() ? split_fused_grid(P, cc.f64 != 0, nloc) : 0;
+  if (G > 0) {
+    FusedArgs a = {};
+    a.P = P;
+    a.nloc = nloc;
+    a.G = G;
+    a.rank0 = R[0];
+    a.N = cc.N;
+    a.delta = cc.delta;
+    a.val_offset = cc.val_offset;
+    for (int j = 0; j <= P; ++j) a.bnd[j] = bnd[j];
+    for (int j = 0; j < P; ++j) a.base[j] = c->peer[j];
+    a.recv_off = L.recv_off;
+    a.region_bytes = L.region_bytes;
+    a.cap_s = L.cap_s;
+    a.win_off = L.win_off;
+    a.win_bytes = L.win_bytes;
+    a.stage_off = L.stage_off;
+    a.rec_off = L.rec_off;
+    a.fz_off = L.fz_off;
+    a.fz_bytes = L.fz_bytes;
+    a.fz_cap = L.fz_cap;
+    for (int i = 0; i < nloc; ++i) {
+      a.idx[i] = idx[i];
+      a.val[i] = val[i];
+      a.n[i] = nnz[i];
+      a.out[i] = out[i];
+      a.sig[i] = rank_sig(c, cc.sig, R[i]);
+      if (skipped(c, R[i])) a.skip |= 1u << i;
+    }
+    a.sched = make_sched(P);
+    a.op = cc.op;
+    a.validate = cc.o.validate;
+    a.f64 = cc.f64;
+    CK(c, launch_split_fused(a, cc.s));
+    return SPARCML_OK;
+  }
   for (size_t i = 0; i < R.size(); ++i) {
     const int r = R[i];
     if (skipped(c, r)) continue;

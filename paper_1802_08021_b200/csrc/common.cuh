@@ -77,6 +77,10 @@ __device__ __forceinline__ void st_relaxed_gpu(uint64_t* p, uint64_t v) {
 // acquire-release fences: ordering without the sequentially-consistent drain
 // (__threadfence_system() is fence.sc.sys, several microseconds under load)
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// relaxed system-scope add (no return value): an arrival after a release fence
+__device__ __forceinline__ void red_add_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // streaming (read-once) vector load, no L1 allocation
@@ -426,6 +430,14 @@ struct alignas(128) Ctrl {
   uint64_t rd_sig[2][kMaxStages + 2];
   uint64_t slice_rx[2][kMaxRanks];   // split owner: pairs received from source i in call parity p
   uint64_t timeout_ns;            // flag waits give up after this long (SPARCML_ERR_TIMEOUT)
+  // fused split-allgather (split_fused_kernel): arrival counters, one 128-byte
+  // line per peer -- each of the peer's G CTAs adds 1 per call, so call c is
+  // complete at (c + 1) * G (wrap-safe compares) -- this rank's count of fused
+  // calls and its CTA ticket
+  alignas(128) uint32_t fz_push_arr[kMaxRanks * 32];   // [src * 32]: source src's CTAs whose slices are in my receive region
+  uint32_t fz_data_arr[kMaxRanks * 32];                // [j * 32]: owner j's CTAs whose pieces are in my staging area
+  alignas(128) uint32_t fz_calls;      // fused calls completed on this rank
+  uint32_t fz_ticket;                   // CTAs of this rank done with the current call
 };
 
 // ---------------------------------------------------------------------------

@@ -171,6 +171,30 @@ struct ConcatArgs {
   int pdl;                         // launch as a programmatic dependent of the owner (host_dsar known)
 };
 
+// Fused split-allgather, SSAR (split_fused_kernel): one cooperative launch per
+// rank (or one for all ranks of a loopback world) does the split push, the
+// owner reduction and the allgather.  Addresses in peer workspaces follow the
+// symmetric layout (api.cu Layout), so only the bases and offsets travel.
+constexpr int kFzMaxG = 1024;        // CTAs per rank (record slots per owner)
+struct FusedArgs {
+  int P, nloc, G;                    // ranks; ranks served by this launch (1, or P on a loopback world); CTAs per rank
+  int rank0;                         // rank of local slot 0
+  uint32_t skip;                     // loopback failure injection: local ranks whose CTAs do nothing
+  uint64_t N, delta, val_offset;
+  uint64_t bnd[kMaxRanks + 1];       // partition bounds (floor(N/P), remainder on the last)
+  char* base[kMaxRanks];             // every rank's workspace as mapped here
+  uint64_t recv_off, region_bytes, cap_s, win_off, win_bytes, stage_off;   // layout (api.cu)
+  uint64_t rec_off;                  // records {cnt, slot} of owner j's CTA b: u64 [j * kFzMaxG + b]
+  uint64_t fz_off, fz_bytes, fz_cap; // staging for owner j's pieces: idx[fz_cap], val[fz_cap] at fz_off + j * fz_bytes
+  const uint32_t* idx[kMaxRanks];    // per local rank: input stream, nnz, result buffer, call signature
+  const void* val[kMaxRanks];
+  uint64_t n[kMaxRanks];
+  char* out[kMaxRanks];
+  uint64_t sig[kMaxRanks];
+  TreeSched sched;
+  int op, validate, f64;
+};
+
 struct BarrierArgs {
   Ctrl* my;
   uint32_t* peer_flags[kMaxRanks];  // &peer_p.ctrl.flags[rank]
@@ -258,6 +282,8 @@ cudaError_t launch_rd_stage(const RdStageArgs& a, cudaStream_t s);
 cudaError_t launch_rd_unfold(const RdUnfoldArgs& a, cudaStream_t s);
 cudaError_t launch_split_push(const PushArgs& a, cudaStream_t s);
 cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s);   // host_dsar selects merge / window
+int split_fused_grid(int P, bool f64, int nloc);                  // CTAs per rank (0: cannot run)
+cudaError_t launch_split_fused(const FusedArgs& a, cudaStream_t s);
 cudaError_t launch_concat(const ConcatArgs& a, cudaStream_t s);
 cudaError_t launch_barrier(const BarrierArgs& a, cudaStream_t s);
 cudaError_t launch_p1_prep(const P1PrepArgs& a, cudaStream_t s);

@@ -8,6 +8,7 @@
 // last block stores into the consumer's control block with release semantics
 // at system scope — no barrier kernels, no host round trip, no NCCL.
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "kernels.h"
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t base = (uint64_t)blockIdx.x * kThreads * kPushItems;
   const uint64_t last = std::min<uint64_t>(a.n, base + (uint64_t)kThreads * kPushItems) - 1;
-  const uint64_t part = a.bnd[1];   // floor(N/P); owner(x) = min(x / part, P - 1)
+  const uint32_t part = (uint32_t)a.bnd[1];   // floor(N/P) (N < 2^32); owner(x) = min(x / part, P - 1)
   allow_dependents();
   // slice boundaries s_off[j] = first position with idx >= b_j: block 0 needs
   // all of them (counts, empty slices), the others only those of the owners
@@ -471,8 +472,8 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
   dbg_mark(a.ctl, 8);
   int j0 = 0, j1 = a.P;
   if (blockIdx.x != 0 && a.n > 0) {
-    j0 = (int)std::min<uint64_t>(a.idx[base] / part, a.P - 1);
-    j1 = (int)std::min<uint64_t>(a.idx[last] / part, a.P - 1) + 1;
+    j0 = (int)std::min<uint32_t>(a.idx[base] / part, a.P - 1);
+    j1 = (int)std::min<uint32_t>(a.idx[last] / part, a.P - 1) + 1;
   }
   for (int j = j0 + warp; j <= j1; j += kWarps) {
     uint64_t o;
@@ -489,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) split_push_kernel(PushArgs a) {
     if (e < a.n) {
       const uint32_t x = a.idx[e];
       const V v = static_cast<const V*>(a.val)[e];
-      const int j = (int)std::min<uint64_t>(x / part, a.P - 1);
+      const int j = (int)std::min<uint32_t>(x / part, a.P - 1);
       const uint64_t p = e - s_off[j];
       a.dst_idx[j][p] = x;
       static_cast<V*>(a.dst_val[j])[p] = v;
@@ -675,11 +676,21 @@ __device__ __forceinline__ void runs_prefix(MergeShared<P>& m, uint32_t len) {
 // most cap of them; s_c holds table entries, row = window, column = source).
 // The result (sorted, unique, canonical-tree sums) is left in xk/xv, or, if
 // oi != nullptr, written to oi/ov.  Returns its length.
-template <int P, typename V>
-__device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const uint32_t* s_c, int w0, int w1,
-                                   uint32_t* oi, V* ov_out, uint32_t* xk, V* xv, uint32_t* yk, V* yv) {
+// The P sources' slices: src.idx(s) / src.val(s) (OwnerArgs' peer arrays, or
+// pointers staged in shared memory by the fused kernel).
+struct OwnerSrc {
+  const OwnerArgs& a;
+  __device__ const uint32_t* idx(int s) const { return a.src_idx[s]; }
+  __device__ const void* val(int s) const { return a.src_val[s]; }
+};
+
+// Stage the runs of table windows [w0, w1) (s_c: table entries, row = window,
+// column = source) in shared memory, source-major (run s = slot s), all loads
+// in flight; m.off / m.len / m.ta describe the runs.  Returns the element count.
+template <int P, typename V, typename Src>
+__device__ __forceinline__ uint32_t stage_runs(const Src& src, MergeShared<P>& m, const uint32_t* s_c, int w0, int w1,
+                                               uint32_t* xk, V* xv) {
   constexpr int cap = mtile_cap(P);
-  constexpr uint32_t kTop = pow2_floor(cap);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     uint32_t len = 0;
@@ -692,8 +703,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
     runs_prefix<P>(m, len);
   }
   __syncthreads();
-  // (2) stage the runs, source-major (run s = slot s); all loads in flight
-  uint32_t n = m.off[P];
+  const uint32_t n = m.off[P];
   {
     constexpr int Q = (cap + kThreads - 1) / kThreads;
     uint32_t kk[Q];
@@ -706,8 +716,8 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
 #pragma unroll
         for (int j = 1; j < P; ++j) s += m.off[j] <= u ? 1 : 0;
         const uint32_t e = m.ta[s] + (u - m.off[s]);
-        kk[q] = __ldcg(&a.src_idx[s][e]);
-        vv[q] = __ldcg(&static_cast<const V*>(a.src_val[s])[e]);
+        kk[q] = __ldcg(&src.idx(s)[e]);
+        vv[q] = __ldcg(&static_cast<const V*>(src.val(s))[e]);
       }
     }
 #pragma unroll
@@ -720,8 +730,19 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
     }
   }
   __syncthreads();
+  return n;
+}
+
+template <int P, typename V, typename Src>
+__device__ uint32_t merge_subrange(const Src& src, int hmax_, int op, MergeShared<P>& m, const uint32_t* s_c, int w0,
+                                   int w1, uint32_t* oi, V* ov_out, uint32_t* xk, V* xv, uint32_t* yk, V* yv) {
+  constexpr int cap = mtile_cap(P);
+  constexpr uint32_t kTop = pow2_floor(cap);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // (2) stage the runs
+  uint32_t n = stage_runs<P, V>(src, m, s_c, w0, w1, xk, xv);
   // (3) canonical tree, one height per round
-  const int hmax = a.sched.hmax > 0 ? a.sched.hmax : 1;
+  const int hmax = hmax_ > 0 ? hmax_ : 1;
   uint32_t total = n;
   for (int h = 1; h <= hmax; ++h) {
     const uint8_t* role_h = m.role[h - 1];
@@ -760,7 +781,7 @@ __device__ uint32_t merge_subrange(const OwnerArgs& a, MergeShared<P>& m, const 
         V val = v[q];
         const uint32_t pos = pos0[q] + rank[q];
         if (role[q] == 1) {   // left run (lower ranks): first on ties, fl(left + right)
-          if (rank[q] < qlen[q] && xk[qoff[q] + rank[q]] == k) val = op_combine(a.op, val, xv[qoff[q] + rank[q]]);
+          if (rank[q] < qlen[q] && xk[qoff[q] + rank[q]] == k) val = op_combine(op, val, xv[qoff[q] + rank[q]]);
         } else if (role[q] == 2) {   // right run: a key the left run holds was summed there
           if (rank[q] > 0 && xk[qoff[q] + rank[q] - 1] == k) {
             k = kDead;
@@ -874,7 +895,7 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
     }
     dbg_mark(ctl, 2);
     if (tot <= (uint32_t)cap) {
-      cnt = merge_subrange<P, V>(a, m, s_c, 0, 1, nullptr, nullptr, xk, xv, yk, yv);
+      cnt = merge_subrange<P, V>(OwnerSrc{a}, a.sched.hmax, a.op, m, s_c, 0, 1, nullptr, nullptr, xk, xv, yk, yv);
     } else {
       in_smem = false;
       const uint32_t wchunk = kTabSmem / P - 1;   // windows per chunk
@@ -897,7 +918,7 @@ __global__ void __launch_bounds__(kThreads) owner_merge_kernel(OwnerArgs a) {
           uint32_t tsum;
           const uint32_t incl = block_exclusive_sum<uint32_t>(c, s_scan, &tsum) + c;
           const int take = __syncthreads_count(w < nw && incl <= (uint32_t)cap);
-          cnt += merge_subrange<P, V>(a, m, s_c, pos, pos + take, a.st_idx + ibase + cnt, st_val + ibase + cnt, xk,
+          cnt += merge_subrange<P, V>(OwnerSrc{a}, a.sched.hmax, a.op, m, s_c, pos, pos + take, a.st_idx + ibase + cnt, st_val + ibase + cnt, xk,
                                       xv, yk, yv);
           pos += take;
         }
@@ -1166,6 +1187,600 @@ cudaError_t launch_owner(const OwnerArgs& a, cudaStream_t s) {
   return cudaSuccess;
 }
 
+
+// ===========================================================================
+// fused split-allgather, SSAR (§5.3.2): ONE cooperative kernel per
+// rank runs the three phases, ordered by arrival counters instead of kernel
+// boundaries (the separate push / owner / concat kernels spent ~40% of the
+// call in launch gaps and grid-wide syncs, profiles/r01_timeline_p4.log):
+//  1. split: CTA b pushes its share of my stream, sliced by partition, into
+//     every owner's receive region (+ window-offset tables), then adds one
+//     arrival at each owner;
+//  2. owner: once all G*P source CTAs have arrived, CTA b reduces its table
+//     windows of my partition (canonical tree, R-8) into shared memory and
+//     pushes the piece straight into every reader's staging area at a slot
+//     that needs no prefix -- slot_b = ceil4(min(inputs before b, positions
+//     before b)) + 4b is monotone with room for the piece -- plus a record
+//     {count, slot}, then adds one arrival at each reader;
+//  3. allgather: once all G*P owner CTAs have arrived, CTA b reads the P*G
+//     records, and copies the pieces (j, b) of every owner j from its local
+//     staging to its exact place in out (sparse concatenation), or densifies
+//     them when K > delta; the last CTA writes the header.
+// A rank starts call s+1 only after every owner's call-s pieces reached it,
+// i.e. after every owner finished reading its receive regions: no buffer is
+// reused early, and the counters need no reset.
+// ===========================================================================
+struct SmemSrc {
+  const uint32_t* const* i;
+  const void* const* v;
+  __device__ const uint32_t* idx(int s) const { return i[s]; }
+  __device__ const void* val(int s) const { return v[s]; }
+};
+
+__device__ __forceinline__ Ctrl* fz_ctl(const FusedArgs& a, int r) { return reinterpret_cast<Ctrl*>(a.base[r]); }
+__device__ __forceinline__ uint32_t* fz_stage_idx(const FusedArgs& a, int reader, int owner) {
+  return reinterpret_cast<uint32_t*>(a.base[reader] + a.fz_off + (uint64_t)owner * a.fz_bytes);
+}
+template <typename V>
+__device__ __forceinline__ V* fz_stage_val(const FusedArgs& a, int reader, int owner) {
+  return reinterpret_cast<V*>(a.base[reader] + a.fz_off + (uint64_t)owner * a.fz_bytes + 4 * a.fz_cap);
+}
+__device__ __forceinline__ uint64_t* fz_rec(const FusedArgs& a, int reader) {
+  return reinterpret_cast<uint64_t*>(a.base[reader] + a.rec_off);
+}
+// table windows [wa, wb) of partition j reduced by CTA b (every rank computes the same split)
+__device__ __forceinline__ void fz_range(const FusedArgs& a, int j, uint32_t b, uint32_t& wa, uint32_t& wb) {
+  const uint32_t ntab = (uint32_t)ceil_div(a.bnd[j + 1] - a.bnd[j], kTab);
+  const uint32_t W = (ntab + a.G - 1) / a.G;
+  wa = std::min<uint32_t>(b * W, ntab);
+  wb = std::min<uint32_t>(wa + W, ntab);
+}
+
+// Canonical tree (R-8) over the runs that hold a key: tree(lo, hi) =
+// tree(lo, mid) (+) tree(mid, hi), a subtree without the key contributing
+// nothing (the pairwise merges of the oracle skip absent operands).
+template <int OP, int LO, int HI, typename V>
+__device__ __forceinline__ bool present_tree(const V* v, uint32_t mask, V& out) {
+  if constexpr (HI - LO == 1) {
+    out = v[LO];
+    return (mask >> LO) & 1u;
+  } else {
+    constexpr int MID = LO + (HI - LO) / 2;
+    V a, b;
+    const bool pa = present_tree<OP, LO, MID>(v, mask, a);
+    const bool pb = present_tree<OP, MID, HI>(v, mask, b);
+    out = (pa && pb) ? op_combine(OP, a, b) : (pa ? a : b);
+    return pa || pb;
+  }
+}
+
+// P-way merge of the staged runs (xk / xv, described by m) by rank, for a
+// range that fits in shared memory.  Element (k, s) LEADS key k iff no run
+// t < s holds k.  A leader's output slot is the number of leaders with a
+// smaller key: sum over runs t of lower_bound_t(k) minus the non-leaders
+// among those (a per-run prefix count, pre[]).  It combines the values of the
+// runs holding k with present_tree.  Two passes of P-way searches, one block
+// scan; no per-height merges.  Output (sorted, unique) to yk / yv; returns
+// its length.  pre[] holds n + 1 entries.
+// lower_bound of key x in each of the P runs, the P binary searches interleaved
+// step by step (independent shared-memory chains, no branches)
+template <int P, uint32_t TOP>
+__device__ __forceinline__ void runs_lower_bound(const uint32_t* xk, const uint32_t (&off)[P],
+                                                 const uint32_t (&len)[P], uint32_t x, uint32_t (&pos)[P]) {
+#pragma unroll
+  for (int t = 0; t < P; ++t) pos[t] = 0;
+#pragma unroll
+  for (uint32_t step = TOP; step; step >>= 1) {
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const uint32_t c = pos[t] + step;
+      if (c <= len[t] && xk[off[t] + c - 1] < x) pos[t] = c;
+    }
+  }
+}
+
+template <int P, typename V>
+__device__ uint32_t rank_merge(const MergeShared<P>& m, uint32_t n, const uint32_t* xk, const V* xv, uint32_t* pre,
+                               uint32_t* yk, V* yv, int op, uint32_t* s_scan, Ctrl* dbg) {
+  constexpr uint32_t kTop = pow2_floor(mtile_cap(P));
+  const int tid = threadIdx.x;
+  uint32_t off[P], len[P];
+#pragma unroll
+  for (int t = 0; t < P; ++t) {
+    off[t] = m.off[t];
+    len[t] = m.len[t];
+  }
+  // pass 1: non-leader flags
+  for (uint32_t u = tid; u < n; u += kThreads) {
+    int s = 0;
+#pragma unroll
+    for (int t = 1; t < P; ++t) s += off[t] <= u ? 1 : 0;
+    const uint32_t k = xk[u];
+    uint32_t pos[P];
+    runs_lower_bound<P, kTop>(xk, off, len, k, pos);
+    bool dup = false;
+#pragma unroll
+    for (int t = 0; t < P; ++t) dup |= t < s && pos[t] < len[t] && xk[off[t] + pos[t]] == k;
+    pre[u] = dup ? 1u : 0u;
+  }
+  __syncthreads();
+  // exclusive prefix of the flags (contiguous chunks per thread), pre[n] = total
+  {
+    const uint32_t C = (n + kThreads - 1) / kThreads;
+    const uint32_t c0 = std::min<uint32_t>(n, tid * C), c1 = std::min<uint32_t>(n, c0 + C);
+    uint32_t sum = 0;
+    for (uint32_t u = c0; u < c1; ++u) sum += pre[u];
+    uint32_t tot;
+    uint32_t run = block_exclusive_sum<uint32_t>(sum, s_scan, &tot);
+    for (uint32_t u = c0; u < c1; ++u) {
+      const uint32_t f = pre[u];
+      pre[u] = run;
+      run += f;
+    }
+    if (tid == 0) pre[n] = tot;
+  }
+  __syncthreads();
+  dbg_mark(dbg, 6);
+  // pass 2: leaders place and combine
+  for (uint32_t u = tid; u < n; u += kThreads) {
+    if (pre[u + 1] != pre[u]) continue;   // not a leader
+    int s = 0;
+#pragma unroll
+    for (int t = 1; t < P; ++t) s += off[t] <= u ? 1 : 0;
+    const uint32_t k = xk[u];
+    uint32_t pos[P];
+    runs_lower_bound<P, kTop>(xk, off, len, k, pos);
+    V v[P];
+    uint32_t mask = 0, opos = 0;
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const uint32_t p = pos[t];
+      const bool present = t >= s && p < len[t] && xk[off[t] + p] == k;   // t < s: absent (u leads)
+      opos += p - (pre[off[t] + p] - pre[off[t]]);
+      v[t] = present ? xv[off[t] + p] : V(0);
+      mask |= present ? 1u << t : 0u;
+    }
+    V r;
+    if (op == 0) present_tree<0, 0, P>(v, mask, r);
+    else if (op == 1) present_tree<1, 0, P>(v, mask, r);
+    else present_tree<2, 0, P>(v, mask, r);
+    yk[opos] = k;
+    yv[opos] = r;
+  }
+  __syncthreads();
+  return n - pre[n];
+}
+
+__host__ __device__ constexpr size_t split_fused_smem_bytes(int P, size_t vbytes) {
+  // xk, yk, pre (cap + 4) as u32; xv, yv as values
+  return 4 * (size_t)mtile_cap(P) * 3 + 16 + 2 * vbytes * (size_t)mtile_cap(P);
+}
+
+template <int P, typename V>
+__global__ void __launch_bounds__(kThreads) split_fused_kernel(FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int cap = mtile_cap(P);
+  uint32_t* xk = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* yk = xk + cap;
+  uint32_t* pre = yk + cap;                                 // cap + 4 entries
+  V* xv = reinterpret_cast<V*>(pre + cap + 4);              // 16-byte aligned: cap % 4 == 0
+  V* yv = xv + cap;
+  __shared__ MergeShared<P> m;
+  __shared__ uint64_t s_off[kMaxRanks + 1];
+  __shared__ uint32_t s_c[kTabSmem];
+  __shared__ uint32_t s_scan[kWarps + 1];
+  __shared__ const uint32_t* s_sidx[P];
+  __shared__ const void* s_sval[P];
+  __shared__ uint32_t s_ok, s_last;
+  __shared__ uint32_t s_tot[P], s_before[P], s_pu[P + 1], s_pc[P];
+  __shared__ uint64_t s_pslot[P], s_po[P];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t G = (uint32_t)a.G;
+  const int l = (int)(blockIdx.x / G);
+  const uint32_t b = blockIdx.x - (uint32_t)l * G;
+  if ((a.skip >> l) & 1u) return;
+  const int r = a.rank0 + l;
+  Ctrl* ctl = fz_ctl(a, r);
+  const uint32_t calls = *(volatile uint32_t*)&ctl->fz_calls;
+  const uint32_t target = (calls + 1u) * G;   // per counter: G arrivals per call (u32, wraps consistently)
+  const uint32_t part = (uint32_t)a.bnd[1];   // N < 2^32: 32-bit owner arithmetic
+  dbg_mark(ctl, 8);
+
+  // ---- 1. split push: CTA b pushes elements [e0, e1) of my stream.  An
+  // element keeps its STREAM index e in the owner's receive region, and the
+  // window-offset tables hold stream indices (table[0] = the slice's first
+  // element, table[ntab] = one past its last), so no CTA searches for the
+  // partition boundaries: first / last elements of a slice are recognised
+  // from their neighbours' owners, and so are empty slices.
+  {
+    const uint32_t* idx = a.idx[l];
+    const V* val = static_cast<const V*>(a.val[l]);
+    const uint64_t n = a.n[l];
+    const uint64_t E = ceil_div(n, G);
+    const uint64_t e0 = std::min<uint64_t>(n, (uint64_t)b * E), e1 = std::min<uint64_t>(n, e0 + E);
+    if (tid == 0) s_ok = (b == 0 && n == 0) ? (1u << P) - 1u : 0u;   // owners with an empty slice
+    __syncthreads();
+    dbg_mark(ctl, 9);
+    constexpr int kPI = 4;   // elements per thread per round, all loads in flight
+    for (uint64_t eb = e0; eb < e1; eb += (uint64_t)kThreads * kPI) {
+      uint32_t xs[kPI], xq[kPI], xn[kPI];
+      V vs[kPI];
+#pragma unroll
+      for (int i = 0; i < kPI; ++i) {
+        const uint64_t e = eb + (uint64_t)i * kThreads + tid;
+        if (e < e1) {
+          xs[i] = idx[e];
+          vs[i] = val[e];
+          xq[i] = e > 0 ? idx[e - 1] : 0u;
+          xn[i] = e + 1 < n ? idx[e + 1] : 0u;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kPI; ++i) {
+        const uint64_t e = eb + (uint64_t)i * kThreads + tid;
+        if (e >= e1) continue;
+        const uint32_t x = xs[i];
+        const int j = (int)std::min<uint32_t>(x / part, P - 1);
+        const int jq = e > 0 ? (int)std::min<uint32_t>(xq[i] / part, P - 1) : -1;
+        const int jn = e + 1 < n ? (int)std::min<uint32_t>(xn[i] / part, P - 1) : P;
+        char* pb = a.base[j];
+        uint32_t* di = reinterpret_cast<uint32_t*>(pb + a.recv_off + (uint64_t)r * a.region_bytes);
+        di[e] = x;
+        reinterpret_cast<V*>(di + a.cap_s)[e] = vs[i];
+        // window-offset table: dw[w] = first stream index of the slice whose table window >= w
+        uint32_t* dw = reinterpret_cast<uint32_t*>(pb + a.win_off + (uint64_t)r * a.win_bytes);
+        const uint32_t lo = (uint32_t)a.bnd[j];
+        const int64_t w = (int64_t)((x - lo) / kTab);
+        const int64_t wprev = jq == j ? (int64_t)((xq[i] - lo) / kTab) : -1;
+        for (int64_t q = wprev + 1; q <= w; ++q) dw[q] = (uint32_t)e;
+        if (jn != j) {   // last element of the slice
+          const int64_t nwin = (int64_t)ceil_div(a.bnd[j + 1] - lo, kTab);
+          for (int64_t q = w + 1; q <= nwin; ++q) dw[q] = (uint32_t)(e + 1);
+        }
+        // owners strictly between my neighbours' and mine get nothing from me
+        const uint32_t gap = ((jq + 1 < j) ? ((1u << j) - (1u << (jq + 1))) : 0u) |
+                             ((jn > j + 1) ? ((1u << jn) - (1u << (j + 1))) : 0u);
+        if (gap) atomicOr(&s_ok, gap);
+        if (a.validate) check_input(idx, e, n, a.N, x, vs[i], &ctl->status);
+      }
+    }
+    __syncthreads();
+    const uint32_t empty = s_ok;
+    for (int j = 0; j < P; ++j) {   // empty slices: a constant table (zero)
+      if (!((empty >> j) & 1u)) continue;
+      uint32_t* dw = reinterpret_cast<uint32_t*>(a.base[j] + a.win_off + (uint64_t)r * a.win_bytes);
+      const uint64_t ntab = ceil_div(a.bnd[j + 1] - a.bnd[j], kTab);
+      for (uint64_t q = tid; q <= ntab; q += kThreads) dw[q] = 0;
+    }
+    if (b == 0 && tid < P) {
+      Ctrl* pc = fz_ctl(a, tid);
+      pc->k_in[r] = n;
+      pc->sig_in[r] = sig_out(ctl, a.sig[l]);
+    }
+    __syncthreads();
+    dbg_mark(ctl, 11);
+    if (tid < P) {   // release my stores, then arrive at owner tid (its counter for source r)
+      fence_acq_rel_sys();
+      red_add_sys(&fz_ctl(a, tid)->fz_push_arr[r * 32], 1u);
+    }
+    dbg_mark(ctl, 10);
+  }
+
+  // ---- 2. owner: reduce my table windows [wa, wb) once every source CTA arrived
+  for (int q = tid; q < kMaxTreeH * P; q += kThreads) {
+    const int hh = q / P, sl = q - hh * P;
+    m.role[hh][sl] = a.sched.role[hh][sl];
+    m.part[hh][sl] = a.sched.part[hh][sl];
+  }
+  if (tid < P) {
+    s_sidx[tid] = reinterpret_cast<const uint32_t*>(a.base[r] + a.recv_off + (uint64_t)tid * a.region_bytes);
+    s_sval[tid] = a.base[r] + a.recv_off + (uint64_t)tid * a.region_bytes + 4 * a.cap_s;
+  }
+  if (tid == 0) s_ok = 1;
+  __syncthreads();
+  if (tid < P && !wait_flag_geq(&ctl->fz_push_arr[tid * 32], target, ctl)) s_ok = 0;
+  __syncthreads();
+  const bool ok1 = s_ok != 0;
+  dbg_mark(ctl, 1);
+  const uint32_t* win0 = reinterpret_cast<const uint32_t*>(a.base[r] + a.win_off);
+  const uint32_t ntab_r = (uint32_t)ceil_div(a.bnd[r + 1] - a.bnd[r], kTab);
+  if (tid < P && ok1) {
+    check_sig(ctl, *(volatile uint64_t*)&ctl->sig_in[tid], a.sig[l]);
+    if (b == 0) {   // pairs received from source tid (the header's traffic)
+      const uint32_t* wt = win0 + (uint64_t)tid * (a.win_bytes / 4);
+      ctl->slice_rx[calls & 1u][tid] = __ldcg(&wt[ntab_r]) - __ldcg(&wt[0]);
+    }
+  }
+  if (b == 0 && warp == 0) {
+    uint64_t ks = (tid < P && ok1) ? *(volatile uint64_t*)&ctl->k_in[tid] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ks += __shfl_xor_sync(0xffffffffu, ks, o);
+    if (lane == 0) {
+      ctl->k_sum = ks;
+      ctl->dsar = 0;
+    }
+  }
+  uint32_t* const st_idx = reinterpret_cast<uint32_t*>(a.base[r] + a.stage_off);
+  V* const st_val = reinterpret_cast<V*>(a.base[r] + a.stage_off + 4 * (uint64_t)P * a.cap_s);
+  uint32_t wa, wb;
+  fz_range(a, r, b, wa, wb);
+  bool in_smem = true;
+  uint32_t cnt = 0;
+  uint64_t ibase = 0;
+  if (ok1 && wa < wb) {
+    if (tid < P) {   // (and the slice's first stream index: ibase counts elements)
+      const uint32_t* wt = win0 + (uint64_t)tid * (a.win_bytes / 4);
+      s_c[tid] = __ldcg(&wt[wa]);
+      s_c[P + tid] = __ldcg(&wt[wb]);
+      s_c[2 * P + tid] = __ldcg(&wt[0]);
+    }
+    __syncthreads();
+    dbg_mark(ctl, 2);
+    uint32_t tot = 0;
+#pragma unroll
+    for (int src = 0; src < P; ++src) {
+      tot += s_c[P + src] - s_c[src];
+      ibase += s_c[src] - s_c[2 * P + src];
+    }
+    const SmemSrc srcs{s_sidx, s_sval};
+    if (tot <= (uint32_t)cap) {
+      const uint32_t n = stage_runs<P, V>(srcs, m, s_c, 0, 1, xk, xv);
+      dbg_mark(ctl, 0);
+      cnt = rank_merge<P, V>(m, n, xk, xv, pre, yk, yv, a.op, s_scan, ctl);
+    } else {
+      in_smem = false;
+      const uint32_t wchunk = kTabSmem / P - 1;   // windows per chunk
+      for (uint32_t cw = wa; cw < wb; cw += wchunk) {
+        const int nw = (int)std::min<uint32_t>(wchunk, wb - cw);
+        __syncthreads();
+        for (int q = tid; q < (nw + 1) * P; q += kThreads) {
+          const int w = q / P, src = q - w * P;
+          s_c[q] = __ldcg(&win0[(uint64_t)src * (a.win_bytes / 4) + cw + w]);
+        }
+        __syncthreads();
+        for (int pos = 0; pos < nw;) {   // greedy maximal pieces of at most cap elements
+          const int w = pos + tid;
+          uint32_t c = 0;
+          if (w < nw) {
+#pragma unroll
+            for (int src = 0; src < P; ++src) c += s_c[(w + 1) * P + src] - s_c[w * P + src];
+          }
+          uint32_t tsum;
+          const uint32_t incl = block_exclusive_sum<uint32_t>(c, s_scan, &tsum) + c;
+          const int take = __syncthreads_count(w < nw && incl <= (uint32_t)cap);
+          cnt += merge_subrange<P, V>(srcs, a.sched.hmax, a.op, m, s_c, pos, pos + take, st_idx + ibase + cnt,
+                                      st_val + ibase + cnt, xk, xv, yk, yv);
+          pos += take;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  dbg_mark(ctl, 3);
+  // push the piece into every reader's staging area (mine last), then arrive
+  {
+    const uint64_t xb = std::min<uint64_t>(ibase, (uint64_t)wa * kTab);
+    const uint64_t slot = ((xb + 3) & ~3ull) + 4ull * b;
+    for (int i = 1; i <= P; ++i) {
+      const int d = (r + i) % P;
+      uint32_t* di = fz_stage_idx(a, d, r) + slot;
+      V* dv = fz_stage_val<V>(a, d, r) + slot;
+      if (in_smem) {   // 16-byte stores; the tail beyond cnt stays inside the slot
+        for (uint32_t u = tid; 4 * u < cnt; u += kThreads) {
+          reinterpret_cast<uint4*>(di)[u] = reinterpret_cast<const uint4*>(yk)[u];
+          if constexpr (sizeof(V) == 4) {
+            reinterpret_cast<float4*>(dv)[u] = reinterpret_cast<const float4*>(yv)[u];
+          } else {
+            reinterpret_cast<double2*>(dv)[2 * u] = reinterpret_cast<const double2*>(yv)[2 * u];
+            reinterpret_cast<double2*>(dv)[2 * u + 1] = reinterpret_cast<const double2*>(yv)[2 * u + 1];
+          }
+        }
+      } else {
+        for (uint32_t u = tid; u < cnt; u += kThreads) {
+          di[u] = __ldcg(st_idx + ibase + u);
+          dv[u] = __ldcg(st_val + ibase + u);
+        }
+      }
+      if (tid == 0) fz_rec(a, d)[(uint64_t)r * kFzMaxG + b] = (uint64_t)cnt | (slot << 32);
+    }
+    __syncthreads();
+    dbg_mark(ctl, 4);
+    if (tid < P) {   // arrive at reader tid (its counter for owner r)
+      fence_acq_rel_sys();
+      red_add_sys(&fz_ctl(a, tid)->fz_data_arr[r * 32], 1u);
+    }
+    dbg_mark(ctl, 5);
+  }
+
+  // ---- 3. allgather: pieces (j, b) of every owner j from my staging into out
+  if (tid == 0) s_ok = 1;
+  if (tid < P) {
+    s_tot[tid] = 0;
+    s_before[tid] = 0;
+  }
+  __syncthreads();
+  if (tid < P && !wait_flag_geq(&ctl->fz_data_arr[tid * 32], target, ctl)) s_ok = 0;
+  __syncthreads();
+  const bool ok2 = s_ok != 0;
+  dbg_mark(ctl, 14);
+  const uint64_t* rec = fz_rec(a, r);
+  if (ok2) {   // every owner's piece counts: all loads in flight, then one reduction per owner
+    uint32_t t[P], bf[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) t[j] = bf[j] = 0;
+    for (uint32_t q = tid; q < G; q += kThreads) {
+      uint32_t c[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) c[j] = (uint32_t)__ldcg(rec + (uint64_t)j * kFzMaxG + q);
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        t[j] += c[j];
+        bf[j] += q < b ? c[j] : 0u;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const uint32_t tt = __reduce_add_sync(0xffffffffu, t[j]);
+      const uint32_t bb = __reduce_add_sync(0xffffffffu, bf[j]);
+      if (lane == 0) {
+        atomicAdd(&s_tot[j], tt);
+        atomicAdd(&s_before[j], bb);
+      }
+    }
+  }
+  __syncthreads();
+  dbg_mark(ctl, 12);
+  uint64_t K = 0;
+  for (int j = 0; j < P; ++j) K += s_tot[j];
+  const bool dense = K > a.delta;
+  char* out = a.out[l];
+  // CTA 0 writes the header now (its own phases produced k_sum and the slice
+  // counts; every status bit but a late timeout is set by now)
+  auto header_status = [&]() { return *(volatile uint32_t*)&ctl->status; };
+  if (b == 0 && tid == 0) {
+    uint64_t sent = 0, recv = 0;
+    for (int j = 0; j < P; ++j) {
+      if (j == r) continue;
+      recv += pair_bytes<V>() * ctl->slice_rx[calls & 1u][j];
+      recv += pair_bytes<V>() * s_tot[j];
+    }
+    sent += pair_bytes<V>() * (a.n[l] - ctl->slice_rx[calls & 1u][r]);   // my stream minus my own slice
+    sent += (uint64_t)(P - 1) * pair_bytes<V>() * s_tot[r];
+    write_header(reinterpret_cast<sparcml_header*>(out), dense ? SPARCML_REPR_DENSE : SPARCML_REPR_SPARSE,
+                 dense ? a.N : K, a.N, ctl->k_sum, sent, recv, SPARCML_SSAR_SPLIT_ALLGATHER, header_status(),
+                 dense ? (uint64_t)SPARCML_HEADER_BYTES : a.val_offset, hdr_magic<V>());
+  }
+  if (ok2 && !dense) {
+    // my pieces (j, b): count, staging slot, output offset; units of 4 pairs
+    if (tid == 0) {
+      uint64_t pre_k = 0;
+      s_pu[0] = 0;
+      for (int j = 0; j < P; ++j) {
+        const uint64_t rj = __ldcg(rec + (uint64_t)j * kFzMaxG + b);
+        s_pslot[j] = rj >> 32;
+        s_pc[j] = (uint32_t)rj;
+        s_po[j] = pre_k + s_before[j];
+        s_pu[j + 1] = s_pu[j] + (((uint32_t)rj + 3) >> 2);
+        pre_k += s_tot[j];
+      }
+    }
+    __syncthreads();
+    uint32_t* oi = reinterpret_cast<uint32_t*>(out + SPARCML_HEADER_BYTES);
+    V* ov = reinterpret_cast<V*>(out + a.val_offset);
+    const uint32_t U = s_pu[P];
+    constexpr int kU = 8;   // units per thread per round, all loads in flight
+    for (uint32_t u0 = tid; u0 < U; u0 += kThreads * kU) {
+      uint4 k4[kU];
+      V v4[kU][4];
+      int jj[kU];
+#pragma unroll
+      for (int x = 0; x < kU; ++x) {
+        const uint32_t u = u0 + x * kThreads;
+        jj[x] = -1;
+        if (u >= U) continue;
+        int j = 0;
+        while (u >= s_pu[j + 1]) ++j;
+        jj[x] = j;
+        const uint64_t e = s_pslot[j] + 4ull * (u - s_pu[j]);
+        k4[x] = __ldcg(reinterpret_cast<const uint4*>(fz_stage_idx(a, r, j) + e));
+        load4(fz_stage_val<V>(a, r, j) + e, 4, v4[x]);
+      }
+#pragma unroll
+      for (int x = 0; x < kU; ++x) {
+        const int j = jj[x];
+        if (j < 0) continue;
+        const uint32_t u = u0 + x * kThreads;
+        const uint32_t q = 4 * (u - s_pu[j]);
+        const uint32_t c = std::min<uint32_t>(4u, s_pc[j] - q);
+        const uint64_t o = s_po[j] + q;
+        const uint32_t kk[4] = {k4[x].x, k4[x].y, k4[x].z, k4[x].w};
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i)
+          if (i < c) {
+            oi[o + i] = kk[i];
+            ov[o + i] = v4[x][i];
+          }
+      }
+    }
+  } else if (ok2) {   // K > delta: owner j's positions of piece b, neutral where absent
+    V* od = reinterpret_cast<V*>(out + SPARCML_HEADER_BYTES);
+    const V nv = op_neutral_v<V>(a.op);
+    for (int j = 0; j < P; ++j) {
+      const uint64_t rj = __ldcg(rec + (uint64_t)j * kFzMaxG + b);
+      const uint32_t c = (uint32_t)rj;
+      const uint32_t* si = fz_stage_idx(a, r, j) + (rj >> 32);
+      const V* sv = fz_stage_val<V>(a, r, j) + (rj >> 32);
+      uint32_t pa, pz;
+      fz_range(a, j, b, pa, pz);
+      const uint64_t p0 = a.bnd[j] + (uint64_t)pa * kTab;
+      const uint64_t p1 = std::min<uint64_t>(a.bnd[j + 1], a.bnd[j] + (uint64_t)pz * kTab);
+      for (uint64_t p = p0 + tid; p < p1; p += kThreads) od[p] = nv;
+      __syncthreads();
+      for (uint32_t u = tid; u < c; u += kThreads) od[__ldcg(si + u)] = __ldcg(sv + u);
+    }
+  }
+  // CTA 0 closes the call on this rank once its own copies are done: every
+  // CTA of mine has read `calls` (their owner phases all arrived before my
+  // data wait passed), and every status bit of the call but a late timeout is
+  // in the header.  No ticket, so no CTA waits for the others' stores to drain.
+  dbg_mark(ctl, 15);
+  if (b == 0 && tid == 0) {
+    ctl->status = 0;
+    ctl->fz_calls = calls + 1;
+    ctl->seq = ctl->seq + 1;   // the call is complete on this rank when the kernel is
+  }
+  dbg_mark(ctl, 13);
+}
+
+using FusedFn = void (*)(FusedArgs);
+template <typename V, int... Ps>
+struct FusedTable {
+  static FusedFn get(int P) {
+    FusedFn f = nullptr;
+    ((P == Ps ? (f = split_fused_kernel<Ps, V>, 0) : 0), ...);
+    return f;
+  }
+};
+static FusedFn fused_fn(int P, bool f64) {
+  return f64 ? FusedTable<double, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P)
+             : FusedTable<float, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>::get(P);
+}
+
+// CTAs per rank: every CTA of the launch must be co-resident (they wait on
+// each other's arrivals); one rank per GPU takes SPARCML_FUSED_BPSM (default
+// 2) per SM, a loopback world splits the GPU's resident CTAs between its ranks.
+int split_fused_grid(int P, bool f64, int nloc) {
+  static int bpsm = -1;
+  if (bpsm < 0) {
+    const char* e = std::getenv("SPARCML_FUSED_BPSM");
+    bpsm = e ? std::max(1, std::atoi(e)) : 1;   // A/B at P = 4 (cfg2): 1 per SM beats 2 and 3
+  }
+  if (P < 2 || P > kMaxRanks) return 0;
+  static int occ[2][kMaxRanks + 1] = {{0}};
+  if (!occ[f64][P]) {
+    const FusedFn f = fused_fn(P, f64);
+    const size_t smem = split_fused_smem_bytes(P, f64 ? 8 : 4);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, kThreads, smem);
+    occ[f64][P] = std::max(per, 0) + 1;   // +1: 0 means "not computed"
+  }
+  const int per = occ[f64][P] - 1;
+  int g = nloc == 1 ? std::min(per, bpsm) * device_sm_count() : per * device_sm_count() / nloc;
+  return std::min(g, kFzMaxG);
+}
+
+cudaError_t launch_split_fused(const FusedArgs& a, cudaStream_t s) {
+  const bool f64 = a.f64 != 0;
+  FusedArgs ac = a;
+  void* args[] = {(void*)&ac};
+  SPARCML_PROF("split_fused", s);
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)fused_fn(a.P, f64), dim3((unsigned)(a.G * a.nloc)),
+                                                    dim3(kThreads), args, split_fused_smem_bytes(a.P, f64 ? 8 : 4), s);
+  ++g_launches;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
 // ===========================================================================
 // allgather phase (§5.3.2 P:757-758 / §5.3.3): pull every owner's

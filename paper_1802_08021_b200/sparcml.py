@@ -174,7 +174,7 @@ def profile_read(name: str):
     return int(n.value), float(ms.value)
 
 
-PROFILED_KERNELS = ["topk", "topk_all", "topk_bucketed", "split_push", "owner", "owner_dsar", "ag_publish", "ag_gather",
+PROFILED_KERNELS = ["topk", "topk_all", "topk_bucketed", "split_push", "split_fused", "owner", "owner_dsar", "ag_publish", "ag_gather",
                     "barrier", "merge", "concat", "rd_push", "rd_stage", "p1_prep", "p1_sparse", "quantize",
                     "dequantize"]
 

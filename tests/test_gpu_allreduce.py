@@ -312,3 +312,29 @@ def test_auto_follows_measured_crossover(orc, P, N, k):
             np.testing.assert_array_equal(g.idx.cpu().numpy().view(np.uint32), ei)
             np.testing.assert_array_equal(g.val.cpu().numpy(), ev)
     w.close()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("algo", ["ssar", "auto"])
+def test_split_three_kernel_path(orc, P, algo, monkeypatch):
+    """SSAR known on the host runs the fused split-allgather kernel; the
+    three-kernel path (push, owner, concat: what runs when the device decides
+    SSAR/DSAR) stays bit-exact too (SPARCML_FUSED=0 selects it)."""
+    monkeypatch.setenv("SPARCML_FUSED", "0")
+    N = 70_001
+    streams = synth.uniform_streams(P, N, 3000, seed=P + 50, kind="normal")
+    check_world(orc, P, N, streams, ALGOS[algo])
+    streams = synth.uniform_streams(P, N, 20_000, seed=P + 51, kind="normal")   # dense block ranges
+    check_world(orc, P, N, streams, S.SSAR_SPLIT_ALLGATHER)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8, 16])
+def test_fused_split_back_to_back(orc, P):
+    """Many fused calls on one world with changing sizes and densities: the
+    arrival counters carry over between calls without a reset."""
+    N = 90_000
+    w = S.LocalWorld(P, N, 30_000)
+    for it, k in enumerate([10, 3000, 30_000, 0, 1, 12_000, 500]):
+        streams = synth.uniform_streams(P, N, k, seed=100 * P + it, kind="normal")
+        check_world(orc, P, N, streams, S.SSAR_SPLIT_ALLGATHER, world=w)
+    w.close()
