@@ -522,10 +522,10 @@ class Bench:
                      "config": self.config_dict(k, kk, bucket, algo)})
         # ---------------- extras: in-run baselines and merge rooflines ----------------
         if not self.args.no_extra:
-            line["baselines"] = self.baselines(grads[0], k, out_k=k, idx=idx, val=val)
+            line["baselines"] = self.extra(lambda: self.baselines(grads[0], k, out_k=k, idx=idx, val=val))
             if P == 1:
-                line["merge_roofline"] = self.merge_roofline(hbm_peak, peak_src)
-                line["owner_roofline"] = self.owner_roofline(hbm_peak, peak_src)
+                line["merge_roofline"] = self.extra(lambda: self.merge_roofline(hbm_peak, peak_src))
+                line["owner_roofline"] = self.extra(lambda: self.owner_roofline(hbm_peak, peak_src))
         line["e2e"] = None if self.args.no_e2e else self.e2e_topk(grads[0], topk, allreduce, out)
         line["cpu_baseline"] = self.cpu_baseline()
         return line
@@ -682,6 +682,14 @@ class Bench:
             out["naive_note"] = "NCCL all_gather of every rank's unmerged k pairs (exchange only, no merge)"
         return out
 
+    @staticmethod
+    def extra(fn):
+        """An optional extra measurement: a failure is reported in the line, never fatal to it."""
+        try:
+            return fn()
+        except Exception as e:   # noqa: BLE001
+            return {"error": f"{type(e).__name__}: {e}"}
+
     def merge_roofline(self, hbm_peak, peak_src):
         """The union-merge-with-sum (§5.1) at config 4's sizes: two uniform streams of
         k = 10% of 2^24 each (the recursive-doubling stage merge, merge_tile), stand-alone."""
@@ -726,6 +734,10 @@ class Bench:
         w = S.LocalWorld(Pw, N, k)
         outs = [S.new_out(N, self.dev) for _ in range(Pw)]
         opts = S.make_opts(algo=S.SSAR_SPLIT_ALLGATHER)
+        # the three-kernel split path (push, owner, concat): SSAR known on the host otherwise
+        # runs the fused kernel, which has no separate owner launch (read per call)
+        fused_env = os.environ.get("SPARCML_FUSED")
+        os.environ["SPARCML_FUSED"] = "0"
         for _ in range(3):
             w.allreduce(streams, N, outs=outs, opts=opts)
         self.barrier()
@@ -741,8 +753,14 @@ class Bench:
         n, ms = S.profile_read("owner")
         S.profile_only(None)
         S.profile_reset()
+        if fused_env is None:
+            os.environ.pop("SPARCML_FUSED", None)
+        else:
+            os.environ["SPARCML_FUSED"] = fused_env
         K = int(S.read_result(outs[0]).header.nnz)
         w.close()
+        if n == 0:
+            return {"kernel": "owner_merge_kernel<4>", "unavailable": "no owner launch was profiled"}
         t = ms / 1e3 / n
         alg = 8 * (Pw * k + K) / Pw   # per owner: its slices of every rank in, its partition result out
         return {"kernel": "owner_merge_kernel<4> (canonical-tree P-way merge in shared memory)", "bound": "hbm",
