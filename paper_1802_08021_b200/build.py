@@ -39,19 +39,31 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    # an object is reused when it is newer than its source, every header and this
+    # script, and was compiled with the same flags (stamp file)
+    hdr_t = max(os.path.getmtime(d) for d in deps() if not d.endswith(".cu"))
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
-        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
+        stamp = obj + ".cmd"
+        if (not force and os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == " ".join(cmd)
+                and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t)):
+            continue
+        if os.path.exists(stamp):
+            os.remove(stamp)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), stamp,
+                      " ".join(cmd)))
     logs = []
-    for src, p in procs:
+    for src, p, stamp, cmdline in procs:
         out, _ = p.communicate()
         logs.append(out.decode())
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError(f"nvcc failed on {src}")
-    with open(os.path.join(objdir, "ptxas.log"), "w") as f:
+        with open(stamp, "w") as f:
+            f.write(cmdline)
+    with open(os.path.join(objdir, "ptxas.log"), "a" if not procs else "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))

@@ -236,6 +236,62 @@ __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t 
   return excl;
 }
 
+// Called by the WHOLE block (kThreads).  Like warp_tile_lookback, but every
+// thread inspects one predecessor, so a step covers kThreads tiles: tiles taken
+// in one wave resolve in one round trip instead of (tile / 32) chained ones.
+// Returns the exclusive prefix to every thread.
+__device__ __forceinline__ uint64_t block_tile_lookback(TileStatus* st, uint32_t tile, uint32_t first, uint64_t agg,
+                                                        uint32_t gen, uint64_t* s_red /* kWarps */,
+                                                        int* s_near) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tag = gen << 2;
+  if (tid == 0) {
+    st[tile].agg = agg;
+    __threadfence();
+    st_release_gpu(&st[tile].flag, tag | 1u);
+  }
+  uint64_t excl = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = base - tid;
+    uint32_t state = 2;   // before the job's first tile: an inclusive prefix of 0
+    uint64_t v = 0;
+    if (t >= (int64_t)first) {
+      uint32_t f = ld_acquire_gpu(&st[t].flag);
+      if ((f & ~3u) != tag || (f & 3u) == 0) {
+        do {
+          f = ld_relaxed_gpu_u32(&st[t].flag);
+        } while ((f & ~3u) != tag || (f & 3u) == 0);
+        f = ld_acquire_gpu(&st[t].flag);
+      }
+      state = f & 3u;
+      v = state == 2u ? ld_relaxed_gpu(&st[t].incl) : ld_relaxed_gpu(&st[t].agg);
+    }
+    // the nearest predecessor holding an inclusive prefix (smallest thread id with state 2)
+    if (tid == 0) *s_near = kThreads;
+    __syncthreads();
+    if (state == 2u) atomicMin(s_near, tid);
+    __syncthreads();
+    const int j = *s_near;
+    const uint64_t w = warp_sum<uint64_t>(tid <= j ? v : 0ull);
+    if (lane == 0) s_red[warp] = w;
+    __syncthreads();
+    uint64_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) sum += s_red[i];
+    excl += sum;
+    __syncthreads();   // s_red / s_near are reused by the next step
+    if (j < kThreads) break;
+    base -= kThreads;
+  }
+  if (tid == 0) {
+    st[tile].incl = excl + agg;
+    __threadfence();
+    st_release_gpu(&st[tile].flag, tag | 2u);
+  }
+  return excl;
+}
+
 // End-of-kernel protocol for ticketed kernels: the last block to finish
 // resets the ticket/done counters and bumps the generation.
 __device__ __forceinline__ void scan_block_exit(ScanCounters* c) {

@@ -168,6 +168,7 @@ __device__ __forceinline__ void load4(const double* src, int cnt, double v[4]) {
 __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   MergeSmem<float>& sm = *reinterpret_cast<MergeSmem<float>*>(smem);
+  constexpr int kC = SpanCfg<float>::kChunk;
   __shared__ uint64_t s_na[kMaxJobs], s_nb[kMaxJobs];
   __shared__ uint32_t s_base[kMaxJobs + 1];
   __shared__ uint32_t s_ticket, s_gen;
@@ -180,8 +181,7 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
   __syncthreads();
   if (tid == 0) {
     s_base[0] = 0;
-    for (int j = 0; j < a.njobs; ++j)
-      s_base[j + 1] = s_base[j] + (uint32_t)ceil_div(s_na[j] + s_nb[j], kMergeTile);
+    for (int j = 0; j < a.njobs; ++j) s_base[j + 1] = s_base[j] + (uint32_t)ceil_div(s_na[j] + s_nb[j], kC);
     s_gen = a.ctr->gen;
   }
   __syncthreads();
@@ -190,13 +190,20 @@ __global__ void __launch_bounds__(kThreads) merge_jobs_kernel(MergeJobsArgs a) {
     if (o.n) *o.n = 0;
     if (o.n2) *o.n2 = 0;
   }
-  (void)s_ticket;
-  // jobs one after another, each a merge span over the whole grid (the block
-  // counts of job j live at status[j * gridDim.x ..])
-  for (int j = 0; j < a.njobs; ++j) {
+  // one ticket space over every job's chunks: ticket t is chunk t - base[j] of
+  // job j, its status entry is t, and its look-back stops at base[j]
+  uint64_t* mk = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(a.ctr) + 64);   // (diagnostics)
+  bool mfirst = true;
+  while (true) {
+    const uint32_t t = next_ticket(a.ctr, &s_ticket);
+    __syncthreads();
+    if (t >= s_base[a.njobs]) break;
+    int j = 0;
+    while (t >= s_base[j + 1]) ++j;
     const MergeJob& jb = a.job[j];
-    merge_span(jb.a_idx, jb.a_val, s_na[j], jb.b_idx, jb.b_val, s_nb[j], sm, a.status + (size_t)j * gridDim.x, s_gen,
-               jb.out);
+    merge_chunk(jb.a_idx, jb.a_val, s_na[j], jb.b_idx, jb.b_val, s_nb[j], (uint64_t)(t - s_base[j]) * kC, sm,
+                a.status, t, s_base[j], s_gen, jb.out, mk, mfirst);
+    mfirst = false;
   }
   scan_block_exit_last(a.ctr);
 }
@@ -208,7 +215,7 @@ cudaError_t launch_merge_jobs(const MergeJobsArgs& a, int grid_cap, cudaStream_t
     cudaFuncSetAttribute(merge_jobs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const int grid = std::max(1, std::min(grid_cap, device_sm_count() * 4));
+  const int grid = std::max(1, std::min(grid_cap, device_sm_count() * 3));
   SPARCML_PROF("merge", s);
   merge_jobs_kernel<<<grid, kThreads, smem, s>>>(a);
   ++g_launches;
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) rd_stage_kernel(RdStageArgs a) {
     mo.val2 = m.base ? reinterpret_cast<V*>(m.base + m.val_off) : nullptr;
     mo.n2 = nullptr;
     __syncthreads();
-    merge_span(a_idx, a_val, an, b_idx, b_val, bn, sm, a.status, s_gen, mo);
+    merge_span(a_idx, a_val, an, b_idx, b_val, bn, sm, a.status, s_gen, mo, a.ctr, &s_ticket);
   } else {
     // densify: window over [0, N) with the two streams (sparse or dense)
     if (tid == 0) {

@@ -53,6 +53,15 @@ constexpr int kChunk = 256;                   // elements per pipeline chunk (1 
 #ifndef SPARCML_TOPK_FENCE
 #define SPARCML_TOPK_FENCE 0                 // 1: proxy fence before every ring refill (A/B diagnostics)
 #endif
+#ifndef SPARCML_TOPK_ROLES
+#define SPARCML_TOPK_ROLES 1                 // 1: warps 0-7 issue the sample loads first, warps 8-15 set up the rings
+#endif
+#ifndef SPARCML_TOPK_BITSEL
+#define SPARCML_TOPK_BITSEL 0                // 1: sample quantiles by a bitwise block search (no sample histogram)
+#endif
+#ifndef SPARCML_TOPK_COOP
+#define SPARCML_TOPK_COOP 1                  // 0: plain launch (one CTA per SM fits; A/B diagnostics)
+#endif
 constexpr int kBins = 4096;                   // bins per histogram level (last one: overflow [split, hi))
 constexpr int kLevels = 6;                    // histogram slots per call (filter, re-filter, refinements)
 constexpr int kListCap = 4096;                // crossing-bin candidates resolved in shared memory
@@ -556,58 +565,87 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
   tk_mark(c, 0);
   TK_C(0);
 
-  // ---- ring set-up and prologue: the first kStages chunks of every warp ---------
-  // (issued before the sample's loads: a fence after outstanding loads would
-  // wait for them, and the ring is what the filter needs first)
+  // ---- ring set-up, prologue and the shared sample ---------------------------------
+  // ROLES: warps [0, 8) issue the sample's loads at once (ahead of the ring's bulk
+  // copies in the memory queues: the threshold is what every warp waits for),
+  // while lanes 0-1 of warps [8, 16) each set up one warp's ring (mbarrier init,
+  // fences, the first kStages chunks).  A fence only orders its own thread's
+  // accesses, so the ring warps' fences do not wait for the sample's loads.
+  // Otherwise every warp's lane 0 sets up its own ring before the sample.
   uint64_t* wbar = mbar + warp * kStages;
   float* wring = ring + (size_t)warp * kStages * Cfg::kArr * kChunk;
   const uint64_t pol = l2_evict_first_policy();
-  auto issue = [&](uint32_t cc, int s) {
+  auto issue_w = [&](uint32_t w, uint32_t cc, int s) {
     if ((uint64_t)(cc + 1) * kChunk > N) return;   // the ragged final chunk is read directly
-    float* d = wring + (size_t)s * Cfg::kArr * kChunk;
-    mbar_expect_tx(&wbar[s], Cfg::kArr * kChunk * 4);
-    bulk_g2s(d, a.x + (uint64_t)cc * kChunk, kChunk * 4, &wbar[s], pol);
-    if (EF) bulk_g2s(d + kChunk, a.g + (uint64_t)cc * kChunk, kChunk * 4, &wbar[s], pol);
+    float* d = ring + ((size_t)w * kStages + s) * Cfg::kArr * kChunk;
+    uint64_t* bar = mbar + w * kStages + s;
+    mbar_expect_tx(bar, Cfg::kArr * kChunk * 4);
+    bulk_g2s(d, a.x + (uint64_t)cc * kChunk, kChunk * 4, bar, pol);
+    if (EF) bulk_g2s(d + kChunk, a.g + (uint64_t)cc * kChunk, kChunk * 4, bar, pol);
   };
-  if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&wbar[s], 1);
+  auto setup_ring = [&](uint32_t w) {   // one thread: warp w's mbarriers and prologue
+    for (int s = 0; s < kStages; ++s) mbar_init(mbar + w * kStages + s, 1);
     fence_mbar_init();
     fence_proxy_async_smem();
-    TK_D(18);
-    if (!SPARCML_TOPK_LATE_PRO)
-      for (int s = 0; s < kStages && (uint32_t)s < nch; ++s) issue(c0 + s, s);
-    TK_D(19);
-  }
-  __syncwarp();
-
+    if (!SPARCML_TOPK_LATE_PRO) {
+      const uint32_t gw_ = b * kTkWarps + w;
+      const uint32_t c0_ = wstart(sp, gw_), n_ = wcount(sp, gw_);
+      for (int s = 0; s < kStages && (uint32_t)s < n_; ++s) issue_w(w, c0_ + s, s);
+    }
+  };
+  auto issue = [&](uint32_t cc, int s) { issue_w((uint32_t)warp, cc, s); };
   const bool sampling = N >= kSampleMinN;
+  constexpr int kSThreads = SPARCML_TOPK_ROLES ? kTkThreads / 2 : kTkThreads;   // sampling threads
+  constexpr int kSPer = kSampleGran / kSThreads;                                  // granules per sampling thread
+  float4 smp[kSPer], smg[kSPer];
+  bool sok[kSPer];
+#pragma unroll
+  for (int j = 0; j < kSPer; ++j) {   // threads without samples (the ring warps) hold none
+    sok[j] = false;
+    smp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    smg[j] = smp[j];
+  }
+  auto sample_loads = [&]() {
+#pragma unroll
+    for (int j = 0; j < kSPer; ++j) {
+      uint64_t pos = 0;
+      sok[j] = sampling && tid < kSThreads && sample_pos((uint32_t)(tid + j * kSThreads), N, C, W, sp, &pos);
+      smp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      smg[j] = smp[j];
+      if (sok[j]) {
+        smp[j] = __ldcg(reinterpret_cast<const float4*>(a.x + pos));
+        if (EF) smg[j] = __ldcg(reinterpret_cast<const float4*>(a.g + pos));
+      }
+    }
+  };
+  if (SPARCML_TOPK_ROLES) {
+    static_assert(kTkWarps == 16, "two ring warps per set-up warp");
+    if (warp < kTkWarps / 2) {
+      sample_loads();
+    } else if (lane < 2) {
+      setup_ring((uint32_t)(2 * (warp - kTkWarps / 2) + lane));
+    }
+    __syncwarp();
+    TK_D(18);
+  } else {
+    if (lane == 0) setup_ring((uint32_t)warp);
+    __syncwarp();
+    TK_D(18);
+  }
+
   constexpr int kSBins = 8192;    // sample histogram: key >> 18 (1/32 octave), in the candidate area
   static_assert(kSBins * 4 <= kTkWarps * kCap * 8, "sample histogram fits the candidate area");
   uint32_t* shs = cidx;
   for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
-  if (sampling)
+  if (sampling && !SPARCML_TOPK_BITSEL)
     for (int i = tid; i < kSBins / 4; i += kTkThreads) reinterpret_cast<uint4*>(shs)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (tid == 0) {
     s_bad = 0;
     s_spill = 0;
   }
-  __syncthreads();
+  __syncthreads();   // (also: every ring's mbarriers are initialised before any warp waits on them)
   TK_D(0);
-  // ---- S: the shared sample (its loads in flight with the ring's) ----------------------
-  constexpr int kSPer = kSampleGran / kTkThreads;   // granules per thread
-  float4 smp[kSPer], smg[kSPer];
-  bool sok[kSPer];
-#pragma unroll
-  for (int j = 0; j < kSPer; ++j) {
-    uint64_t pos = 0;
-    sok[j] = sampling && sample_pos((uint32_t)(tid + j * kTkThreads), N, C, W, sp, &pos);
-    smp[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    smg[j] = smp[j];
-    if (sok[j]) {
-      smp[j] = __ldcg(reinterpret_cast<const float4*>(a.x + pos));
-      if (EF) smg[j] = __ldcg(reinterpret_cast<const float4*>(a.g + pos));
-    }
-  }
+  if (!SPARCML_TOPK_ROLES) sample_loads();   // behind the rings' prologue in the memory queues
 
   uint32_t tau = 0;
   uint64_t split = kKeyEnd;
@@ -618,33 +656,72 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
       if (EF)   // acc = fmaf(alpha, g, eps) at the sampled positions
         smp[j] = make_float4(__fmaf_rn(a.alpha, smg[j].x, smp[j].x), __fmaf_rn(a.alpha, smg[j].y, smp[j].y),
                              __fmaf_rn(a.alpha, smg[j].z, smp[j].z), __fmaf_rn(a.alpha, smg[j].w, smp[j].w));
-      if (sok[j]) {
-        atomicAdd(&shs[abs_key(smp[j].x) >> 18], 1u);
-        atomicAdd(&shs[abs_key(smp[j].y) >> 18], 1u);
-        atomicAdd(&shs[abs_key(smp[j].z) >> 18], 1u);
-        atomicAdd(&shs[abs_key(smp[j].w) >> 18], 1u);
-      }
       ns += sok[j] ? 4u : 0u;
     }
     TK_D(1);
-    uint64_t S;
-    (void)blk_excl_sum<uint64_t>(ns, s_sc, &S);   // (syncs: the sample histogram is complete)
-    TK_D(2);
     // tau where the sample count from the top reaches t_lo = mean + 5 sigma + 4
     // (to 1/32 octave): the k-th magnitude is >= tau unless the sample holds >=
     // t_lo values above it (a 5.6-sigma event; then the exact re-filter runs).
     // split where the count reaches mean - 4 sigma - 16: the level-0 bins cover
     // [tau, split) finely.  Same result in every CTA.
+    uint64_t S;
+    (void)blk_excl_sum<uint64_t>(ns, s_sc, &S);
+    TK_D(2);
     const float mean = (float)((double)k * (double)S / (double)N);
     const float sd = sqrtf(mean);
     const uint64_t t_lo = (uint64_t)ceilf(mean + 5.0f * sd + 4.0f);
     const float th = mean - 4.0f * sd - 16.0f;
     const uint64_t t_hi = th > 1.0f ? (uint64_t)th : 1;
-    find2<kSBins>(shs, t_lo, t_hi, s_sc, s_cross);
-    const Cross f0 = s_cross[0], f1 = s_cross[1];
+    if (SPARCML_TOPK_BITSEL) {
+      // the 1/32-octave bin holding the t-th largest sample key, bit by bit from
+      // the top (bits 30..18): the largest T = m * 2^18 with #(keys >= T) >= t.
+      // Both targets per round, counts packed in 16-bit halves (S <= 4096).
+      uint32_t key[4 * kSPer];
+#pragma unroll
+      for (int j = 0; j < kSPer; ++j) {
+        key[4 * j] = sok[j] ? abs_key(smp[j].x) : 0u;
+        key[4 * j + 1] = sok[j] ? abs_key(smp[j].y) : 0u;
+        key[4 * j + 2] = sok[j] ? abs_key(smp[j].z) : 0u;
+        key[4 * j + 3] = sok[j] ? abs_key(smp[j].w) : 0u;
+      }
+      uint32_t* s_red = reinterpret_cast<uint32_t*>(shs);   // 2 x kTkWarps round counts (candidate area, unused yet)
+      uint32_t Tlo = 0, Thi = 0;
+#pragma unroll 1
+      for (int bit = 30; bit >= 18; --bit) {
+        const uint32_t cl = Tlo | (1u << bit), ch = Thi | (1u << bit);
+        uint32_t cnt = 0;
+        if (tid < kSThreads) {
+#pragma unroll
+          for (int j = 0; j < 4 * kSPer; ++j) cnt += (key[j] >= cl ? 1u : 0u) + (key[j] >= ch ? 0x10000u : 0u);
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) s_red[(bit & 1) * kTkWarps + warp] = cnt;
+        __syncthreads();
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kTkWarps; ++w) tot += s_red[(bit & 1) * kTkWarps + w];
+        if ((tot & 0xFFFFu) >= t_lo) Tlo = cl;
+        if ((tot >> 16) >= t_hi) Thi = ch;
+      }
+      tau = S >= t_lo ? Tlo : 0u;
+      split = S >= t_hi ? (uint64_t)Thi + (1u << 18) : kKeyEnd;
+      __syncthreads();   // s_red (the candidate area) is free again
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSPer; ++j)
+        if (sok[j]) {
+          atomicAdd(&shs[abs_key(smp[j].x) >> 18], 1u);
+          atomicAdd(&shs[abs_key(smp[j].y) >> 18], 1u);
+          atomicAdd(&shs[abs_key(smp[j].z) >> 18], 1u);
+          atomicAdd(&shs[abs_key(smp[j].w) >> 18], 1u);
+        }
+      __syncthreads();
+      find2<kSBins>(shs, t_lo, t_hi, s_sc, s_cross);
+      const Cross f0 = s_cross[0], f1 = s_cross[1];
+      tau = f0.ok ? (f0.bin << 18) : 0u;
+      split = f1.ok ? (uint64_t)(f1.bin + 1) << 18 : kKeyEnd;
+    }
     if (EF && tid == 0) atomicAdd(&c->sampled[p], 1u);   // this CTA's sample reads are complete
-    tau = f0.ok ? (f0.bin << 18) : 0u;
-    split = f1.ok ? (uint64_t)(f1.bin + 1) << 18 : kKeyEnd;
     if (split <= tau) split = (uint64_t)tau + 1;
     TK_D(3);
   }
@@ -755,6 +832,12 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     TK_D(12);
     uint32_t* si = a.L.sp_idx + r0 + kBins;
     float* sv = a.L.sp_val + r0 + kBins;
+    // sorted into shared memory behind the cursors (the drained ring), then
+    // copied out coalesced: scattered 4-byte global stores cost a sector each
+    constexpr uint32_t kStageCap = (uint32_t)((Cfg::kRing - (size_t)kBins * 4) / 8);
+    const bool staged = cta_n <= kStageCap;
+    uint32_t* qi = ab + kBins;
+    float* qv = reinterpret_cast<float*>(qi + kStageCap);
     for (uint32_t i = lane; i < nw; i += 32) {
       uint32_t idx;
       float v;
@@ -762,8 +845,20 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
       const uint32_t key = abs_key(v);
       const uint32_t at = atomicAdd(&ab[bin_of(key, tau, split, shift)], 1u);
       SPARCML_CHECK(at < cta_n && r0 + kBins + at < r1);
-      si[at] = idx;
-      sv[at] = v;
+      if (staged) {
+        qi[at] = idx;
+        qv[at] = v;
+      } else {
+        si[at] = idx;
+        sv[at] = v;
+      }
+    }
+    if (staged) {
+      __syncthreads();
+      for (uint32_t i = tid; i < cta_n; i += kTkThreads) {
+        si[i] = qi[i];
+        sv[i] = qv[i];
+      }
     }
     TK_D(13);
   }
@@ -1521,6 +1616,10 @@ static cudaError_t launch_stream(const TkArgs& a, cudaStream_t s) {
   }
   TkArgs ac = a;
   void* args[] = {(void*)&ac};
+  if (!SPARCML_TOPK_COOP) {   // one CTA per SM and a grid <= the SM count: co-resident once the SMs drain
+    topk_stream_kernel<EF, STORE><<<dim3((unsigned)topk_grid(a.N)), dim3(kTkThreads), TkCfg<EF>::kSmem, s>>>(ac);
+    return cudaGetLastError();
+  }
   return cudaLaunchCooperativeKernel((const void*)topk_stream_kernel<EF, STORE>, dim3((unsigned)topk_grid(a.N)),
                                      dim3(kTkThreads), args, TkCfg<EF>::kSmem, s);
 }

@@ -15,46 +15,110 @@
 namespace sparcml {
 
 // ---------------------------------------------------------------------------
-// merge tile
+// merge chunk: the union-merge-with-sum of two sorted sparse streams (§5.1
+// "Efficient Summation", both sparse, overlapping indices), one
+// pass over the inputs.  The merged sequence is cut into chunks of kSpanItems
+// * kThreads diagonal positions; a block takes chunks by ticket (so every
+// predecessor of a chunk is held by a running or finished block).  Per chunk:
+// two warps locate its ends on the merge path in global memory (33-ary
+// searches), the A and B windows are staged into shared memory with 16-byte
+// loads (one round trip), every thread merges kSpanItems consecutive outputs
+// from its own diagonal, a block scan compacts the emitted pairs in place,
+// warp 0 publishes the chunk's count and looks back for its offset (decoupled
+// look-back), and the block writes the run coalesced.
 // ---------------------------------------------------------------------------
+#ifndef SPARCML_SPAN_ITEMS
+#define SPARCML_SPAN_ITEMS 16   // outputs per thread for 4-byte values (8-byte: half)
+#endif
+template <typename V>
+struct SpanCfg {
+  static constexpr int kItems = sizeof(V) == 4 ? SPARCML_SPAN_ITEMS : SPARCML_SPAN_ITEMS / 2;   // outputs per thread
+  static constexpr int kChunk = kItems * kThreads;          // diagonal positions per chunk
+};
+
 template <typename V = float>
 struct MergeSmem {
-  uint32_t ak[kMergeTile + 1];   // ak[0] = A[a0-1] (look-behind), ak[1+i] = A[a0+i]
-  uint32_t bk[kMergeTile + 1];   // bk[i] = B[b0+i], bk[lb] = B[b1] (look-ahead)
-  V av[kMergeTile + 1];
-  V bv[kMergeTile + 1];
+  static constexpr int kC = SpanCfg<V>::kChunk;
+  alignas(16) uint32_t ak[kC + 4];   // ak[0] = A[a0-1] (look-behind), ak[1+i] = A[a0+i]
+  alignas(16) uint32_t bk[kC + 4];   // bk[i] = B[b0+i], bk[lb] = B[b1] (look-ahead)
+  alignas(16) V av[kC + 4];
+  alignas(16) V bv[kC + 4];
   uint64_t split[2];
   uint32_t scan[kWarps + 1];
-  uint64_t excl;
-  int has_prev_a, has_next_b;
+  uint64_t red[kWarps];
+  int near;
 };
 
 template <typename V = float>
 struct MergeOutput {
   uint32_t* idx;
   V* val;
-  uint64_t* n;          // receives the output count (written by the last tile)
+  uint64_t* n;          // receives the output count (written by the last chunk)
   uint32_t* idx2;       // optional mirror (a peer's receive buffer over NVLink)
   V* val2;
   uint64_t* n2;
   int op;               // reduction operator (R-30)
 };
 
-// Merges diagonal range [d0, d0 + kMergeTile) of merge(A, B).  Returns nothing;
-// writes its outputs at the exclusive prefix found by look-back.  Must be
-// called by all kThreads threads.  gtile/gfirst: global tile ids for the
-// look-back chain of this job.
+__device__ __forceinline__ uint64_t umin64(uint64_t x, uint64_t y) { return x < y ? x : y; }
+
+// n consecutive elements src[s0 ..) -> dst[0 ..), the whole block: 16-byte
+// loads of the aligned quads inside [s0, s0+n) (src 16-byte aligned), scalar
+// loads at the ragged ends.
+template <typename T>
+__device__ __forceinline__ void stage_run(T* dst, const T* __restrict__ src, uint64_t s0, int n) {
+  constexpr int kPer = 16 / sizeof(T);
+  const int tid = threadIdx.x;
+  if (n <= 0) return;
+  if ((reinterpret_cast<uintptr_t>(src) & 15u) != 0) {
+    for (int i = tid; i < n; i += kThreads) dst[i] = __ldcg(src + s0 + i);
+    return;
+  }
+  const uint64_t q0 = (s0 + kPer - 1) / kPer, q1 = (s0 + (uint64_t)n) / kPer;   // whole quads [q0, q1)
+  const int head = (int)umin64((uint64_t)n, q0 * kPer - s0);
+  if (tid < head) dst[tid] = __ldcg(src + s0 + tid);
+  const int nq = q1 > q0 ? (int)(q1 - q0) : 0;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src) + q0;
+  T* d = dst + head;
+#pragma unroll 4
+  for (int q = tid; q < nq; q += kThreads) {
+    const uint4 u = __ldcg(s4 + q);
+    const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) d[q * kPer + j] = e[j];
+  }
+  const int tail0 = head + nq * kPer;
+  if (tid < n - tail0) dst[tail0 + tid] = __ldcg(src + s0 + tail0 + tid);
+}
+
+// diagnostics (-DSPARCML_DEBUG_MARKS): mk[0][i] = block 0's first chunk reaching
+// point i, mk[1][i] = the latest chunk (%globaltimer ns)
+__device__ __forceinline__ void merge_mark(uint64_t* mk, int i, bool first) {
+#ifdef SPARCML_DEBUG_MARKS
+  if (mk && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (first && blockIdx.x == 0) mk[i] = t;
+    atomicMax(reinterpret_cast<unsigned long long*>(&mk[12 + i]), (unsigned long long)t);
+  }
+#else
+  (void)mk;
+  (void)i;
+  (void)first;
+#endif
+}
+
 template <typename V>
-__device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
-                                           const V* __restrict__ Av, uint64_t na,
-                                           const uint32_t* __restrict__ B,
-                                           const V* __restrict__ Bv, uint64_t nb,
-                                           uint64_t d0, MergeSmem<V>& sm, TileStatus* st,
-                                           uint32_t gtile, uint32_t gfirst, uint32_t gen,
-                                           const MergeOutput<V>& out) {
+__device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, const V* __restrict__ Av, uint64_t na,
+                                            const uint32_t* __restrict__ B, const V* __restrict__ Bv, uint64_t nb,
+                                            uint64_t d0, MergeSmem<V>& sm, TileStatus* st, uint32_t tile,
+                                            uint32_t first, uint32_t gen, const MergeOutput<V>& out,
+                                            uint64_t* mk = nullptr, bool mfirst = false) {
+  constexpr int kItems = SpanCfg<V>::kItems;
+  merge_mark(mk, 0, mfirst);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t total_in = na + nb;
-  const uint64_t d1 = (d0 + kMergeTile < total_in) ? d0 + kMergeTile : total_in;
+  const uint64_t total = na + nb;
+  const uint64_t d1 = umin64(d0 + SpanCfg<V>::kChunk, total);
   if (warp == 0) {
     const uint64_t s = warp_merge_path(A, na, B, nb, d0);
     if (lane == 0) sm.split[0] = s;
@@ -63,60 +127,52 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
     if (lane == 0) sm.split[1] = s;
   }
   __syncthreads();
+  merge_mark(mk, 1, mfirst);
   const uint64_t a0 = sm.split[0], a1 = sm.split[1];
   const uint64_t b0 = d0 - a0, b1 = d1 - a1;
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
-  for (int i = tid; i < la; i += kThreads) {
-    sm.ak[i + 1] = A[a0 + i];
-    sm.av[i + 1] = Av[a0 + i];
-  }
-  for (int i = tid; i < lb; i += kThreads) {
-    sm.bk[i] = B[b0 + i];
-    sm.bv[i] = Bv[b0 + i];
-  }
-  if (tid == 0) {
-    sm.has_prev_a = a0 > 0;
-    if (a0 > 0) sm.ak[0] = A[a0 - 1];
-    sm.has_next_b = b1 < nb;
-    if (b1 < nb) {
-      sm.bk[lb] = B[b1];
-      sm.bv[lb] = Bv[b1];
-    }
-  }
+  const bool has_prev_a = a0 > 0;
+  const int wb = lb + (b1 < nb ? 1 : 0);   // + the look-ahead B[b1]
+  stage_run(sm.ak + 1, A, a0, la);
+  stage_run(sm.av + 1, Av, a0, la);
+  stage_run(sm.bk, B, b0, wb);
+  stage_run(sm.bv, Bv, b0, wb);
+  if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
   __syncthreads();
+  merge_mark(mk, 2, mfirst);
+  // this thread's outputs: diagonal dt of the chunk
   const int L = la + lb;
-  const int dt = min(tid * kMergeItems, L);
+  const int dt = min(tid * kItems, L);
   int lo = max(0, dt - lb), hi = min(dt, la);
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (sm.ak[mid + 1] <= sm.bk[dt - 1 - mid]) lo = mid + 1; else hi = mid;
   }
   int ia = lo, ib = dt - lo;
-  const bool has_prev_a = sm.has_prev_a, has_next_b = sm.has_next_b;
-  uint32_t ok[kMergeItems];
-  V ov[kMergeItems];
+  uint32_t ok[kItems];
+  V ov[kItems];
   uint32_t emit = 0;
 #pragma unroll
-  for (int s = 0; s < kMergeItems; ++s) {
+  for (int s = 0; s < kItems; ++s) {
     ok[s] = 0;
-    ov[s] = 0;
+    ov[s] = V(0);
     if (dt + s < L) {
-      const bool takeA = ib >= lb || (ia < la && sm.ak[ia + 1] <= sm.bk[ib]);
+      const uint32_t ka = ia < la ? sm.ak[ia + 1] : 0xFFFFFFFFu;
+      const uint32_t kb = ib < wb ? sm.bk[ib] : 0xFFFFFFFFu;
+      const bool takeA = ib >= lb || (ia < la && ka <= kb);
       if (takeA) {
-        const uint32_t key = sm.ak[ia + 1];
         V v = sm.av[ia + 1];
-        // the element following A[ia] in merged order is B[ib] (or the look-ahead)
-        if ((ib < lb || has_next_b) && sm.bk[ib] == key) v = op_combine(out.op, v, sm.bv[ib]);
-        ok[s] = key;
+        // the element following A[ia] in merged order is B[ib] (in the window or the look-ahead)
+        if (ib < wb && kb == ka) v = op_combine(out.op, v, sm.bv[ib]);
+        ok[s] = ka;
         ov[s] = v;
         emit |= 1u << s;
         ++ia;
       } else {
-        const uint32_t key = sm.bk[ib];
-        // a B element equal to the preceding A element was already summed into it
-        const bool dup = (ia > 0 || has_prev_a) && sm.ak[ia] == key;
+        // a B element equal to the preceding A element was already combined into it
+        const bool dup = (ia > 0 || has_prev_a) && sm.ak[ia] == kb;
         if (!dup) {
-          ok[s] = key;
+          ok[s] = kb;
           ov[s] = sm.bv[ib];
           emit |= 1u << s;
         }
@@ -126,221 +182,58 @@ __device__ __forceinline__ void merge_tile(const uint32_t* __restrict__ A,
   }
   uint32_t tile_total;
   const uint32_t my_off = block_exclusive_sum<uint32_t>(__popc(emit), sm.scan, &tile_total);
-  // block_exclusive_sum ended with __syncthreads: ak/av are free for staging
-  if (warp == 0) {
-    const uint64_t e = warp_tile_lookback(st, gtile, gfirst, tile_total, gen);
-    if (lane == 0) sm.excl = e;
-  }
+  // (the scan ended with __syncthreads: the staged windows are consumed)
+  merge_mark(mk, 3, mfirst);
+  const uint64_t o = block_tile_lookback(st, tile, first, tile_total, gen, sm.red, &sm.near);
+  merge_mark(mk, 4, mfirst);
+  uint32_t pos = my_off;
 #pragma unroll
-  for (int s = 0; s < kMergeItems; ++s) {
+  for (int s = 0; s < kItems; ++s)
     if (emit & (1u << s)) {
-      const uint32_t pos = my_off + __popc(emit & ((1u << s) - 1u));
       sm.ak[pos] = ok[s];
       sm.av[pos] = ov[s];
+      ++pos;
     }
-  }
   __syncthreads();
-  const uint64_t base = sm.excl;
-  for (uint32_t i = tid; i < tile_total; i += kThreads) {
-    out.idx[base + i] = sm.ak[i];
-    out.val[base + i] = sm.av[i];
+  for (uint32_t i = tid; i < tile_total; i += kThreads) {   // coalesced
+    SPARCML_CHECK(o + i < total);
+    const uint32_t k = sm.ak[i];
+    const V v = sm.av[i];
+    out.idx[o + i] = k;
+    out.val[o + i] = v;
     if (out.idx2) {
-      out.idx2[base + i] = sm.ak[i];
-      out.val2[base + i] = sm.av[i];
+      out.idx2[o + i] = k;
+      out.val2[o + i] = v;
     }
   }
-  if (tid == 0 && d1 == total_in) {
-    if (out.n) *out.n = base + tile_total;
-    if (out.n2) *out.n2 = base + tile_total;
+  if (tid == 0 && d1 == total) {
+    if (out.n) *out.n = o + tile_total;
+    if (out.n2) *out.n2 = o + tile_total;
   }
-  __syncthreads();
+  __syncthreads();   // sm is reused by the block's next chunk
+  merge_mark(mk, 5, mfirst);
 }
 
-// ---------------------------------------------------------------------------
-// merge span: the whole union-merge-with-sum on the grid without a per-tile
-// look-back chain.  Block b owns the contiguous diagonal range of tiles
-// [T*b/G, T*(b+1)/G); two global merge-path searches locate its ends, after
-// which every tile boundary inside the range follows from the previous tile's
-// merge (each tile stages the next kMergeTile elements of A and B from where
-// the previous one stopped -- a superset window -- and its local merge path
-// says how many of each it consumed).  Pass 1 counts the block's output;
-// the block publishes the count and adds up its predecessors' (one load per
-// predecessor, all in flight: no serial look-back); pass 2 re-merges the same
-// tiles (their inputs now hit L2) and writes at the final offsets.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t umin64(uint64_t x, uint64_t y) { return x < y ? x : y; }
-
-template <typename V>
-struct SpanTile {
-  uint32_t ok[kMergeItems];
-  V ov[kMergeItems];
-  uint32_t emit;
-  uint32_t la;   // A elements the tile consumed
-};
-
-// Stage the windows at (a, b) and merge the tile's first L outputs.  All kThreads threads.
-template <typename V>
-__device__ __forceinline__ void span_tile(const uint32_t* __restrict__ A, const V* __restrict__ Av, uint64_t na,
-                                          const uint32_t* __restrict__ B, const V* __restrict__ Bv, uint64_t nb,
-                                          uint64_t a, uint64_t b, int L, int op, MergeSmem<V>& sm, SpanTile<V>& t) {
-  const int tid = threadIdx.x;
-  const int wa = (int)umin64((uint64_t)L, na - a);          // A window
-  const int wbL = (int)umin64((uint64_t)L, nb - b);         // B window for the merge
-  const int wb = (int)umin64((uint64_t)L + 1, nb - b);      // + the look-ahead element
-  __syncthreads();   // the previous tile's readers are done with sm
-#pragma unroll 4
-  for (int i = tid; i < wa; i += kThreads) {
-    sm.ak[i + 1] = __ldcg(&A[a + i]);
-    sm.av[i + 1] = __ldcg(&Av[a + i]);
-  }
-#pragma unroll 4
-  for (int i = tid; i < wb; i += kThreads) {
-    sm.bk[i] = __ldcg(&B[b + i]);
-    sm.bv[i] = __ldcg(&Bv[b + i]);
-  }
-  if (tid == 0) {
-    sm.has_prev_a = a > 0;
-    if (a > 0) sm.ak[0] = __ldcg(&A[a - 1]);
-  }
-  __syncthreads();
-  // the tile's consumption: merge path of the windows at diagonal L (warp 0, lane 0)
-  if (tid == 0) {
-    int lo = max(0, L - wbL), hi = min(L, wa);
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sm.ak[mid + 1] <= sm.bk[L - 1 - mid]) lo = mid + 1; else hi = mid;
-    }
-    sm.split[0] = (uint64_t)lo;
-  }
-  const int dt = min(tid * kMergeItems, L);
-  int lo = max(0, dt - wbL), hi = min(dt, wa);
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (sm.ak[mid + 1] <= sm.bk[dt - 1 - mid]) lo = mid + 1; else hi = mid;
-  }
-  int ia = lo, ib = dt - lo;
-  const bool has_prev_a = sm.has_prev_a;
-  t.emit = 0;
-#pragma unroll
-  for (int s = 0; s < kMergeItems; ++s) {
-    t.ok[s] = 0;
-    t.ov[s] = V(0);
-    if (dt + s < L) {
-      const bool takeA = ib >= wbL || (ia < wa && sm.ak[ia + 1] <= sm.bk[ib]);
-      if (takeA) {
-        const uint32_t key = sm.ak[ia + 1];
-        V v = sm.av[ia + 1];
-        // the element following A[ia] in merged order is B[ib] (in the window or the look-ahead)
-        if (ib < wb && sm.bk[ib] == key) v = op_combine(op, v, sm.bv[ib]);
-        t.ok[s] = key;
-        t.ov[s] = v;
-        t.emit |= 1u << s;
-        ++ia;
-      } else {
-        const uint32_t key = sm.bk[ib];
-        // a B element equal to the preceding A element was already summed into it
-        const bool dup = (ia > 0 || has_prev_a) && sm.ak[ia] == key;
-        if (!dup) {
-          t.ok[s] = key;
-          t.ov[s] = sm.bv[ib];
-          t.emit |= 1u << s;
-        }
-        ++ib;
-      }
-    }
-  }
-  __syncthreads();
-  t.la = (uint32_t)sm.split[0];
-}
-
+// The whole merge on the grid: chunks by ticket from `ctr` (tickets [t0, t0 +
+// nchunks) belong to this merge; status entries are indexed by ticket).
 template <typename V>
 __device__ void merge_span(const uint32_t* __restrict__ A, const V* __restrict__ Av, uint64_t na,
                            const uint32_t* __restrict__ B, const V* __restrict__ Bv, uint64_t nb, MergeSmem<V>& sm,
-                           TileStatus* st, uint32_t gen, const MergeOutput<V>& out) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t G = gridDim.x, blk = blockIdx.x;
+                           TileStatus* st, uint32_t gen, const MergeOutput<V>& out, ScanCounters* ctr,
+                           uint32_t* s_ticket) {
   const uint64_t total = na + nb;
-  const uint64_t T = (total + kMergeTile - 1) / kMergeTile;
-  const uint64_t D0 = umin64(T * blk / G * kMergeTile, total);
-  const uint64_t D1 = umin64(T * (blk + 1) / G * kMergeTile, total);
-  __shared__ uint64_t s_a0, s_off;
-  if (warp == 0 && D0 < D1) {
-    const uint64_t s0 = warp_merge_path(A, na, B, nb, D0);
-    if (lane == 0) s_a0 = s0;
+  const uint32_t nchunks = (uint32_t)((total + SpanCfg<V>::kChunk - 1) / SpanCfg<V>::kChunk);
+  while (true) {
+    if (threadIdx.x == 0) *s_ticket = atomicAdd(&ctr->ticket, 1u);
+    __syncthreads();
+    const uint32_t t = *s_ticket;
+    __syncthreads();
+    if (t >= nchunks) break;
+    merge_chunk(A, Av, na, B, Bv, nb, (uint64_t)t * SpanCfg<V>::kChunk, sm, st, t, 0u, gen, out);
   }
-  __syncthreads();
-  SpanTile<V> t;
-  // pass 1: count
-  uint32_t cnt = 0;
-  if (D0 < D1) {
-    uint64_t a = s_a0, b = D0 - s_a0;
-    for (uint64_t d = D0; d < D1; d += kMergeTile) {
-      const int L = (int)umin64(kMergeTile, D1 - d);
-      span_tile(A, Av, na, B, Bv, nb, a, b, L, out.op, sm, t);
-      cnt += __popc(t.emit);
-      a += t.la;
-      b += (uint64_t)L - t.la;
-    }
-  }
-  uint32_t ctot;
-  (void)block_exclusive_sum<uint32_t>(cnt, sm.scan, &ctot);
-  // publish this block's count, then add up the predecessors' (all loads in flight)
-  if (tid == 0) {
-    st[blk].agg = ctot;
-    __threadfence();
-    st_release_gpu(&st[blk].flag, (gen << 2) | 1u);
-  }
-  uint64_t before = 0;
-  for (uint32_t j = tid; j < blk; j += kThreads) {
-    uint32_t f = ld_acquire_gpu(&st[j].flag);
-    while (f != ((gen << 2) | 1u)) {
-      __nanosleep(20);
-      f = ld_acquire_gpu(&st[j].flag);
-    }
-    before += ld_relaxed_gpu(&st[j].agg);
-  }
-  uint64_t btot;
-  __shared__ uint64_t s_red[kWarps + 1];
-  (void)block_exclusive_sum<uint64_t>(before, s_red, &btot);
-  if (tid == 0) s_off = btot;
-  __syncthreads();
-  // pass 2: the same tiles, written at the final offsets
-  uint64_t o = s_off;
-  if (D0 < D1) {
-    uint64_t a = s_a0, b = D0 - s_a0;
-    for (uint64_t d = D0; d < D1; d += kMergeTile) {
-      const int L = (int)umin64(kMergeTile, D1 - d);
-      span_tile(A, Av, na, B, Bv, nb, a, b, L, out.op, sm, t);
-      uint32_t tt;
-      const uint32_t my = block_exclusive_sum<uint32_t>(__popc(t.emit), sm.scan, &tt);
-      uint32_t pos = my;
-#pragma unroll
-      for (int s = 0; s < kMergeItems; ++s)   // compact through shared memory (the windows are consumed)
-        if (t.emit & (1u << s)) {
-          sm.ak[pos] = t.ok[s];
-          sm.av[pos] = t.ov[s];
-          ++pos;
-        }
-      __syncthreads();
-      for (uint32_t i = tid; i < tt; i += kThreads) {   // coalesced
-        SPARCML_CHECK(o + i < total);
-        const uint32_t k = sm.ak[i];
-        const V v = sm.av[i];
-        out.idx[o + i] = k;
-        out.val[o + i] = v;
-        if (out.idx2) {
-          out.idx2[o + i] = k;
-          out.val2[o + i] = v;
-        }
-      }
-      o += tt;
-      a += t.la;
-      b += (uint64_t)L - t.la;
-    }
-  }
-  if (blk == G - 1 && tid == 0) {
-    if (out.n) *out.n = o;
-    if (out.n2) *out.n2 = o;
+  if (total == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (out.n) *out.n = 0;
+    if (out.n2) *out.n2 = 0;
   }
 }
 

@@ -31,6 +31,7 @@ def host_idx(t):
 MERGE_CASES = [
     (0, 0, 100), (0, 5, 100), (7, 0, 100), (1, 1, 2), (2047, 1, 5000), (2048, 2048, 10_000),
     (3000, 5000, 9000), (10_000, 10_000, 10_000), (100_000, 30_000, 1 << 20), (70_001, 70_003, 1 << 18),
+    (4095, 1, 9000), (4096, 4096, 20_000), (12_289, 4099, 30_000), (1_677_721, 1_677_721, 1 << 24),
 ]
 
 
@@ -39,6 +40,19 @@ def test_merge_sum_parity(orc, na, nb, N):
     (ia, va), (ib, vb) = synth.uniform_streams(2, N, [na, nb], seed=na + nb, kind="normal")
     io, vo = S.merge_sum(cu_idx(ia), cu(va, torch.float32), cu_idx(ib), cu(vb, torch.float32))
     eo, ev = orc.merge_sum(ia, va, ib, vb)
+    np.testing.assert_array_equal(host_idx(io), eo)
+    np.testing.assert_array_equal(vo.cpu().numpy().view(np.uint32), ev.view(np.uint32))
+
+
+@pytest.mark.parametrize("off_a,off_b", [(1, 0), (0, 3), (2, 1), (4, 4)])
+def test_merge_sum_unaligned_inputs(orc, off_a, off_b):
+    """Streams starting at any 4-byte offset: the 16-byte staging loads apply only to aligned quads."""
+    N = 1 << 17
+    (ia, va), (ib, vb) = synth.uniform_streams(2, N, [9001 + off_a, 7003 + off_b], seed=5, kind="normal")
+    ta, tva = cu_idx(ia), cu(va, torch.float32)
+    tb, tvb = cu_idx(ib), cu(vb, torch.float32)
+    io, vo = S.merge_sum(ta[off_a:], tva[off_a:], tb[off_b:], tvb[off_b:])
+    eo, ev = orc.merge_sum(ia[off_a:], va[off_a:], ib[off_b:], vb[off_b:])
     np.testing.assert_array_equal(host_idx(io), eo)
     np.testing.assert_array_equal(vo.cpu().numpy().view(np.uint32), ev.view(np.uint32))
 
@@ -144,6 +158,35 @@ def test_ef_topk_fallback_when_sample_underestimates(orc):
     np.testing.assert_array_equal(vo.cpu().numpy(), ev)
     np.testing.assert_array_equal(et.cpu().numpy(), ee)
     assert ws.status() == (0, 2)
+
+
+@pytest.mark.parametrize("ef,k", [(False, 1048), (True, 1048), (False, 100_000), (True, 300_000)])
+def test_topk_sample_far_below_the_data(orc, ef, k):
+    """Adversarial the other way: the sampled granules hold tiny values, every
+    other value is normal, so the sampled threshold and histogram range sit far
+    below the data -- every value is a candidate (spilled past the shared
+    lists), all land in the overflow bin, and the refine levels of the slow path
+    must still find the exact selection."""
+    N = 1 << 20
+    rng = np.random.default_rng(12)
+    x, _ = _defeat_sample(N, rng, lambda n: rng.standard_normal(n).astype(np.float32),
+                          lambda n: (rng.random(n, dtype=np.float32) * np.float32(1e-30)).astype(np.float32))
+    ws = S.TopkWorkspace(N, k)
+    if ef:
+        g, _ = _defeat_sample(N, rng, lambda n: rng.standard_normal(n).astype(np.float32),
+                              lambda n: (rng.random(n, dtype=np.float32) * np.float32(1e-30)).astype(np.float32))
+        et = cu(x, torch.float32)
+        io, vo = S.ef_topk(et, cu(g, torch.float32), 0.5, k, ws=ws)
+        ei, ev, ee = orc.ef_topk(x, g, 0.5, k)
+        np.testing.assert_array_equal(et.cpu().numpy(), ee)
+    else:
+        res = torch.empty(N, device="cuda")
+        io, vo = S.topk_sparsify(cu(x, torch.float32), k, residual=res, ws=ws)
+        ei, ev, er = orc.topk(x, k, residual=True)
+        np.testing.assert_array_equal(res.cpu().numpy(), er)
+    np.testing.assert_array_equal(host_idx(io), ei)
+    np.testing.assert_array_equal(vo.cpu().numpy(), ev)
+    assert ws.status()[0] == 0
 
 
 def test_topk_workspace_reused_across_sizes(orc):
