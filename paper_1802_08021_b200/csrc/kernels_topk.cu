@@ -59,6 +59,9 @@ constexpr int kChunk = 256;                   // elements per pipeline chunk (1 
 #ifndef SPARCML_TOPK_BITSEL
 #define SPARCML_TOPK_BITSEL 0                // 1: sample quantiles by a bitwise block search (no sample histogram)
 #endif
+#ifndef SPARCML_TOPK_WARM
+#define SPARCML_TOPK_WARM 1                  // 1: tau / split from the previous call's k-th magnitude (no sample)
+#endif
 #ifndef SPARCML_TOPK_COOP
 #define SPARCML_TOPK_COOP 1                  // 0: plain launch (one CTA per SM fits; A/B diagnostics)
 #endif
@@ -85,7 +88,7 @@ struct TopkCtl {
   uint32_t arrive;          // arrivals at the current grid barrier (reset by the last arriver)
   uint32_t flag;            // grid barriers released so far (wrapping)
   uint32_t calls;           // completed calls; parity p = calls & 1 selects the per-call slots below
-  uint32_t status, passes;  // last call: non-finite input seen, filter passes (1, or 2 after a re-filter)
+  uint32_t status, passes;  // last call: non-finite input seen, filter passes (1; +1 per re-filter)
   uint32_t bad[2];          // per call parity: a non-finite value was seen
   uint32_t sampled[2];      // per call parity: CTAs done sampling (EF write guard)
   uint32_t list_n[2];       // per call parity: length of the crossing-bin list
@@ -97,6 +100,9 @@ struct TopkCtl {
   uint32_t cta_a[kMaxGrid];  // per CTA: candidates with key >= hi of the final range
   uint32_t cta_e[kMaxGrid];  // per CTA: candidates in [lo, hi) of the final range
   uint64_t t_cta[2][kMaxGrid];   // per CTA: %globaltimer at start and filter end (SPARCML_DEBUG_MARKS)
+  uint32_t warm_kth;        // last call's k-th magnitude key (0: none, or that call missed; sample instead)
+  uint32_t warm_ef;         // ... of an EF call (1) or a plain sparsify (0)
+  uint64_t warm_N, warm_k;  // ... for this (N, k)
 };
 
 struct TopkLayout {
@@ -594,7 +600,16 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     }
   };
   auto issue = [&](uint32_t cc, int s) { issue_w((uint32_t)warp, cc, s); };
-  const bool sampling = N >= kSampleMinN;
+  // Warm start: a previous call on this workspace with the same (N, k) found the
+  // k-th magnitude m without a miss; take tau = m (1 - 1/64), split = m (1 + 1/8)
+  // and skip the sample.  Under error feedback m drifts by < 1% per step once the
+  // accumulator's distribution settles; a miss is still exact
+  // (m < tau: the tau = 0 re-filter; m >= split: the overflow bin's refinement)
+  // and makes the next call sample again.
+  const uint32_t wk = SPARCML_TOPK_WARM ? c->warm_kth : 0u;
+  const bool warm = SPARCML_TOPK_WARM && N >= kSampleMinN && wk > 0u && wk < 0x7F800000u && c->warm_N == N &&
+                    c->warm_k == k && c->warm_ef == (EF ? 1u : 0u);
+  const bool sampling = N >= kSampleMinN && !warm;
   constexpr int kSThreads = SPARCML_TOPK_ROLES ? kTkThreads / 2 : kTkThreads;   // sampling threads
   constexpr int kSPer = kSampleGran / kSThreads;                                  // granules per sampling thread
   float4 smp[kSPer], smg[kSPer];
@@ -618,7 +633,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
       }
     }
   };
-  if (SPARCML_TOPK_ROLES) {
+  if (SPARCML_TOPK_ROLES && sampling) {
     static_assert(kTkWarps == 16, "two ring warps per set-up warp");
     if (warp < kTkWarps / 2) {
       sample_loads();
@@ -724,6 +739,10 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     if (EF && tid == 0) atomicAdd(&c->sampled[p], 1u);   // this CTA's sample reads are complete
     if (split <= tau) split = (uint64_t)tau + 1;
     TK_D(3);
+  } else if (warm) {
+    const float m = __uint_as_float(wk);
+    tau = abs_key(m * (1.0f - 1.0f / 64.0f));
+    split = (uint64_t)abs_key(m * 1.125f) + 1u;   // <= Inf's key + 1 < kKeyEnd
   }
   uint32_t shift = shift_for(split - tau, kBins - 1);
   if (SPARCML_TOPK_LATE_PRO && lane == 0)
@@ -896,7 +915,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
   uint32_t lo = tau;
   uint64_t spl = split, hi = kKeyEnd, above = 0;
   uint32_t passes = 1;
-  bool exact = false, fast = false;
+  bool exact = false, fast = false, resampled = false;
   uint32_t kth = 0;
   uint64_t need = 0;
   {
@@ -1049,17 +1068,53 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
       for (int i = tid; i < kBins; i += kTkThreads) sh[i] = 0;
       __syncthreads();
       if (!f.ok) {
-        // fewer than k candidates: the sample over-estimated tau.  Exact re-filter
-        // of every value (tau = 0) from the current vector (EF: acc, now in eps).
-        passes = 2;
+        // fewer than k candidates: tau over-estimated the k-th magnitude.  Re-filter
+        // the current vector (EF: acc, now in eps).  After a warm-start miss the
+        // threshold comes from the sample of that vector (one more streaming pass);
+        // otherwise -- or if that misses too -- exactly, with tau = 0 (every value
+        // a candidate: far slower, a 5.6-sigma event for the sample).
+        ++passes;
         ++slot;
         lo = 0;
         spl = kKeyEnd;
         hi = kKeyEnd;
         above = 0;
-        shift = shift_for(kKeyEnd, kBins - 1);
         nw = 0;
         const float* src = EF ? a.dst : a.x;
+        if (warm && !resampled) {
+          resampled = true;
+          uint32_t* shs = cidx;   // the sample histogram, in the (discarded) candidate area
+          constexpr int kSBins2 = 8192;
+          for (int i = tid; i < kSBins2 / 4; i += kTkThreads)
+            reinterpret_cast<uint4*>(shs)[i] = make_uint4(0u, 0u, 0u, 0u);
+          __syncthreads();
+          uint32_t ns = 0;
+          for (uint32_t q = tid; q < (uint32_t)kSampleGran; q += kTkThreads) {
+            uint64_t pos = 0;
+            if (!sample_pos(q, N, C, W, sp, &pos)) continue;
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(src + pos));
+            atomicAdd(&shs[abs_key(v.x) >> 18], 1u);
+            atomicAdd(&shs[abs_key(v.y) >> 18], 1u);
+            atomicAdd(&shs[abs_key(v.z) >> 18], 1u);
+            atomicAdd(&shs[abs_key(v.w) >> 18], 1u);
+            ns += 4;
+          }
+          uint64_t S;
+          (void)blk_excl_sum<uint64_t>(ns, s_sc, &S);   // (ends with a block barrier)
+          const float mean = (float)((double)k * (double)S / (double)N);
+          const float sd = sqrtf(mean);
+          const uint64_t t_lo = (uint64_t)ceilf(mean + 5.0f * sd + 4.0f);
+          const float th = mean - 4.0f * sd - 16.0f;
+          const uint64_t t_hi = th > 1.0f ? (uint64_t)th : 1;
+          find2<kSBins2>(shs, t_lo, t_hi, s_sc, s_cross);
+          const Cross f0 = s_cross[0], f1 = s_cross[1];
+          __syncthreads();   // every thread has its crossings; the candidate area is free again
+          lo = f0.ok ? (f0.bin << 18) : 0u;
+          if (lo > 0x7F800000u) lo = 0x7F800000u;
+          spl = f1.ok ? (uint64_t)(f1.bin + 1) << 18 : kKeyEnd;
+          if (spl <= lo) spl = (uint64_t)lo + 1;
+        }
+        shift = shift_for(spl - lo, kBins - 1);
         for (uint32_t i = 0; i < nch; ++i) {
           const uint64_t cc = c0 + i;
           const bool full = (cc + 1) * kChunk <= N;
@@ -1075,7 +1130,7 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
               for (int j = 0; j < 4; ++j) v[j] = gp + j < N ? __ldcg(src + gp + j) : 0.0f;
             }
             uint32_t dummy = 0;
-            consume_row<EF, false>(v, gp, full, N, nullptr, 0u, spl, shift, sh, cs, nw, dummy);
+            consume_row<EF, false>(v, gp, full, N, nullptr, lo, spl, shift, sh, cs, nw, dummy);
           }
         }
         __syncthreads();
@@ -1265,6 +1320,12 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
   if (b == 0 && tid == 0) {
     c->passes = passes;
     c->calls = c->calls + 1u;
+    // warm start for the next call: only when the k-th magnitude fell inside this
+    // call's level-0 range [tau, split) (a miss samples next time)
+    c->warm_kth = (passes == 1u && kth >= tau && (uint64_t)kth < split) ? kth : 0u;
+    c->warm_ef = EF ? 1u : 0u;
+    c->warm_N = N;
+    c->warm_k = k;
   }
   // ---- placement: per warp, pass 1 counts (> kth, == kth), every warp scans the
   // 16 pairs (offsets, tie quotas), pass 2 writes in index order.  Compact loops:

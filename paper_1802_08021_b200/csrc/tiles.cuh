@@ -91,6 +91,28 @@ __device__ __forceinline__ void stage_run(T* dst, const T* __restrict__ src, uin
   if (tid < n - tail0) dst[tail0 + tid] = __ldcg(src + s0 + tail0 + tid);
 }
 
+#ifndef SPARCML_MERGE_ASYNC
+#define SPARCML_MERGE_ASYNC 1   // 1: stage the four windows with cp.async (every load in flight at once)
+#endif
+// n consecutive elements src[s0 ..) -> dst[0 ..) with 4- or 8-byte cp.async
+// (LDGSTS, consecutive lanes on consecutive words: coalesced, no alignment
+// needed); the caller commits and waits once for all four windows, so the
+// block has a single load round trip instead of one per window.
+template <typename T>
+__device__ __forceinline__ void stage_run_async(T* dst, const T* __restrict__ src, uint64_t s0, int n) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte elements");
+  for (int i = threadIdx.x; i < n; i += kThreads) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + i);
+    if (sizeof(T) == 4)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + s0 + i) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + s0 + i) : "memory");
+  }
+}
+__device__ __forceinline__ void stage_async_wait() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // diagnostics (-DSPARCML_DEBUG_MARKS): mk[0][i] = block 0's first chunk reaching
 // point i, mk[1][i] = the latest chunk (%globaltimer ns)
 __device__ __forceinline__ void merge_mark(uint64_t* mk, int i, bool first) {
@@ -133,11 +155,20 @@ __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, cons
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
   const bool has_prev_a = a0 > 0;
   const int wb = lb + (b1 < nb ? 1 : 0);   // + the look-ahead B[b1]
-  stage_run(sm.ak + 1, A, a0, la);
-  stage_run(sm.av + 1, Av, a0, la);
-  stage_run(sm.bk, B, b0, wb);
-  stage_run(sm.bv, Bv, b0, wb);
-  if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
+  if (SPARCML_MERGE_ASYNC) {
+    stage_run_async(sm.ak + 1, A, a0, la);
+    stage_run_async(sm.bk, B, b0, wb);
+    stage_run_async(sm.av + 1, Av, a0, la);
+    stage_run_async(sm.bv, Bv, b0, wb);
+    if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
+    stage_async_wait();
+  } else {
+    stage_run(sm.ak + 1, A, a0, la);
+    stage_run(sm.av + 1, Av, a0, la);
+    stage_run(sm.bk, B, b0, wb);
+    stage_run(sm.bv, Bv, b0, wb);
+    if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
+  }
   __syncthreads();
   merge_mark(mk, 2, mfirst);
   // this thread's outputs: diagonal dt of the chunk

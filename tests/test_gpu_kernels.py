@@ -212,6 +212,57 @@ def test_topk_workspace_reused_across_sizes(orc):
         assert ws.status() == (0, 1)
 
 
+@pytest.mark.parametrize("ef", [False, True])
+def test_topk_warm_start_hits_and_misses_are_exact(orc, ef):
+    """A call on a workspace whose previous call had the same (N, k) takes tau
+    and the histogram range from that call's k-th magnitude instead of sampling.
+    Same distribution: a hit (one pass).  Data scaled by 1e-3: every value is
+    below the warm tau, so the exact re-filter runs (passes == 2, which a
+    sampled tau would not need -- the warm start was taken).  The next call
+    samples again.  Data scaled by 1e3: the k-th magnitude lies above the
+    histogram range (the overflow bin's refinement).  All bit-exact."""
+    N, k = 1 << 20, 10_000
+    ws = S.TopkWorkspace(N, k)
+    rng = np.random.default_rng(21)
+    expect_passes = [1, 1, 2, 1, 1, 1, 1]
+    for it, (scale, want) in enumerate(zip([1.0, 1.0, 1e-3, 1.0, 1.0, 1e3, 1.0], expect_passes)):
+        x = (rng.standard_normal(N) * scale).astype(np.float32)
+        if ef:
+            g = (rng.standard_normal(N) * scale).astype(np.float32)
+            et = cu(x, torch.float32)
+            io, vo = S.ef_topk(et, cu(g, torch.float32), 0.5, k, ws=ws)
+            ei, ev, ee = orc.ef_topk(x, g, 0.5, k)
+            np.testing.assert_array_equal(et.cpu().numpy(), ee, err_msg=f"call {it}")
+        else:
+            res = torch.empty(N, device="cuda")
+            io, vo = S.topk_sparsify(cu(x, torch.float32), k, residual=res, ws=ws)
+            ei, ev, er = orc.topk(x, k, residual=True)
+            np.testing.assert_array_equal(res.cpu().numpy(), er, err_msg=f"call {it}")
+        np.testing.assert_array_equal(host_idx(io), ei, err_msg=f"call {it}")
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev, err_msg=f"call {it}")
+        assert ws.status() == (0, want), f"call {it}"
+
+
+def test_ef_topk_warm_start_over_many_steps(orc):
+    """Algorithm 1's loop for 12 steps on one workspace: from the
+    second step on tau comes from the previous step's k-th magnitude, which
+    drifts upward while the accumulator fills (the early steps can land in the
+    overflow bin).  Every step bit-exact, eps included."""
+    N, k = 1 << 19, 5243
+    eps = np.zeros(N, np.float32)
+    grads = [synth.gaussian_vector(N, seed=40 + s) for s in range(3)]
+    et = torch.zeros(N, device="cuda")
+    gts = [cu(g, torch.float32) for g in grads]
+    ws = S.TopkWorkspace(N, k)
+    for step in range(12):
+        io, vo = S.ef_topk(et, gts[step % 3], 0.01, k, ws=ws)
+        ei, ev, eps = orc.ef_topk(eps, grads[step % 3], 0.01, k)
+        np.testing.assert_array_equal(host_idx(io), ei, err_msg=f"step {step}")
+        np.testing.assert_array_equal(vo.cpu().numpy(), ev, err_msg=f"step {step}")
+        np.testing.assert_array_equal(et.cpu().numpy(), eps, err_msg=f"step {step}")
+        assert ws.status()[0] == 0
+
+
 def test_topk_heavy_ties_refine_levels(orc):
     """Half-integer values (config 5's gradients) give crossing bins of one
     magnitude with far more than the list capacity: exact-bin and refine paths."""
