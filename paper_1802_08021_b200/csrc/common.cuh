@@ -165,12 +165,8 @@ struct ScanCounters {
   uint32_t pad;
 };
 
-struct alignas(32) TileStatus {
-  uint32_t flag;     // (gen << 2) | state ; state 1 = aggregate, 2 = inclusive
-  uint32_t pad;
-  uint64_t agg;
-  uint64_t incl;
-  uint64_t pad2;
+struct TileStatus {
+  uint64_t word;     // ((gen << 2 | state) << 32) | value; state 1 = aggregate, 2 = inclusive prefix
 };
 
 template <typename T>
@@ -186,21 +182,16 @@ __device__ __forceinline__ T warp_sum(T x) {
 // exclusive one (to every lane).  `first` is the job's first global tile.
 __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t tile, uint32_t first,
                                                        uint64_t agg, uint32_t gen) {
+  // (status and value in one 64-bit word, as in block_tile_lookback below)
   const int lane = threadIdx.x & 31;
-  const uint32_t tag = gen << 2;
+  const uint64_t tag = (uint64_t)(gen << 2) << 32;
+  const uint64_t tmask = (uint64_t)0xFFFFFFFCu << 32;
+  SPARCML_CHECK(agg <= 0xFFFFFFFFull);
   if (tile == first) {
-    if (lane == 0) {
-      st[tile].incl = agg;
-      __threadfence();
-      st_release_gpu(&st[tile].flag, tag | 2u);
-    }
+    if (lane == 0) st_relaxed_gpu(&st[tile].word, tag | (2ull << 32) | agg);
     return 0;
   }
-  if (lane == 0) {
-    st[tile].agg = agg;
-    __threadfence();
-    st_release_gpu(&st[tile].flag, tag | 1u);
-  }
+  if (lane == 0) st_relaxed_gpu(&st[tile].word, tag | (1ull << 32) | agg);
   uint64_t excl = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {
@@ -208,16 +199,12 @@ __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t 
     uint32_t state = 2;
     uint64_t v = 0;
     if (t >= (int64_t)first) {
-      uint32_t f;
-      f = ld_acquire_gpu(&st[t].flag);
-      if ((f & ~3u) != tag || (f & 3u) == 0) {
-        do {
-          f = ld_relaxed_gpu_u32(&st[t].flag);
-        } while ((f & ~3u) != tag || (f & 3u) == 0);
-        f = ld_acquire_gpu(&st[t].flag);
-      }
-      state = f & 3u;
-      v = state == 2u ? ld_relaxed_gpu(&st[t].incl) : ld_relaxed_gpu(&st[t].agg);
+      uint64_t w;
+      do {
+        w = ld_relaxed_gpu(&st[t].word);
+      } while ((w & tmask) != tag || (w & (3ull << 32)) == 0);
+      state = (uint32_t)(w >> 32) & 3u;
+      v = w & 0xFFFFFFFFull;
     }
     const uint32_t im = __ballot_sync(0xffffffffu, state == 2u);
     if (im) {
@@ -228,11 +215,8 @@ __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t 
     excl += warp_sum<uint64_t>(v);
     base -= 32;
   }
-  if (lane == 0) {
-    st[tile].incl = excl + agg;
-    __threadfence();
-    st_release_gpu(&st[tile].flag, tag | 2u);
-  }
+  SPARCML_CHECK(excl + agg <= 0xFFFFFFFFull);
+  if (lane == 0) st_relaxed_gpu(&st[tile].word, tag | (2ull << 32) | (excl + agg));
   return excl;
 }
 
@@ -243,36 +227,42 @@ __device__ __forceinline__ uint64_t warp_tile_lookback(TileStatus* st, uint32_t 
 __device__ __forceinline__ uint64_t block_tile_lookback(TileStatus* st, uint32_t tile, uint32_t first, uint64_t agg,
                                                         uint32_t gen, uint64_t* s_red /* kWarps */,
                                                         int* s_near) {
+  // Status and value share one 64-bit word, written and read with single
+  // relaxed accesses: a reader that sees the state also sees its value, so no
+  // acquire load (each one invalidates the SM's L1) and no fence is needed.
+  // Values are per-job output counts: < 2^32 (indices are u32).
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t tag = gen << 2;
-  if (tid == 0) {
-    st[tile].agg = agg;
-    __threadfence();
-    st_release_gpu(&st[tile].flag, tag | 1u);
-  }
+  const uint64_t tag = (uint64_t)(gen << 2) << 32;
+  const uint64_t tmask = (uint64_t)0xFFFFFFFCu << 32;
+  SPARCML_CHECK(agg <= 0xFFFFFFFFull);
+  if (tid == 0) st_relaxed_gpu(&st[tile].word, tag | (1ull << 32) | agg);
   uint64_t excl = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {
     const int64_t t = base - tid;
     uint32_t state = 2;   // before the job's first tile: an inclusive prefix of 0
     uint64_t v = 0;
-    if (t >= (int64_t)first) {
-      uint32_t f = ld_acquire_gpu(&st[t].flag);
-      if ((f & ~3u) != tag || (f & 3u) == 0) {
-        do {
-          f = ld_relaxed_gpu_u32(&st[t].flag);
-        } while ((f & ~3u) != tag || (f & 3u) == 0);
-        f = ld_acquire_gpu(&st[t].flag);
+    int j;
+    // Polling rounds: each thread reads its predecessor's word once per round; the
+    // round ends when every predecessor nearer than the nearest inclusive prefix
+    // has published at least its aggregate (a farther one is never waited for).
+    bool have = t < (int64_t)first;
+    while (true) {
+      if (!have) {
+        const uint64_t w = ld_relaxed_gpu(&st[t].word);
+        if ((w & tmask) == tag && (w & (3ull << 32)) != 0) {
+          state = (uint32_t)(w >> 32) & 3u;
+          v = w & 0xFFFFFFFFull;
+          have = true;
+        }
       }
-      state = f & 3u;
-      v = state == 2u ? ld_relaxed_gpu(&st[t].incl) : ld_relaxed_gpu(&st[t].agg);
+      if (tid == 0) *s_near = kThreads;
+      __syncthreads();
+      if (have && state == 2u) atomicMin(s_near, tid);
+      __syncthreads();
+      j = *s_near;
+      if (!__syncthreads_or(!have && tid <= j)) break;
     }
-    // the nearest predecessor holding an inclusive prefix (smallest thread id with state 2)
-    if (tid == 0) *s_near = kThreads;
-    __syncthreads();
-    if (state == 2u) atomicMin(s_near, tid);
-    __syncthreads();
-    const int j = *s_near;
     const uint64_t w = warp_sum<uint64_t>(tid <= j ? v : 0ull);
     if (lane == 0) s_red[warp] = w;
     __syncthreads();
@@ -284,11 +274,8 @@ __device__ __forceinline__ uint64_t block_tile_lookback(TileStatus* st, uint32_t
     if (j < kThreads) break;
     base -= kThreads;
   }
-  if (tid == 0) {
-    st[tile].incl = excl + agg;
-    __threadfence();
-    st_release_gpu(&st[tile].flag, tag | 2u);
-  }
+  SPARCML_CHECK(excl + agg <= 0xFFFFFFFFull);
+  if (tid == 0) st_relaxed_gpu(&st[tile].word, tag | (2ull << 32) | (excl + agg));
   return excl;
 }
 

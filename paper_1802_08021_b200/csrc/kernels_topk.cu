@@ -337,21 +337,26 @@ __device__ __forceinline__ Cross find_desc(const uint32_t* h, uint64_t t, uint64
 // Grid barrier of a cooperative launch: arrivals on a counter (the last
 // arriver resets it) and a wrapping release flag; `target` = the flag value
 // that releases this barrier.
+#ifndef SPARCML_TOPK_BAR_ACQREL
+#define SPARCML_TOPK_BAR_ACQREL 1   // 1: acq_rel fences (0: membar.gl, i.e. fence.sc, A/B diagnostics)
+#endif
 __device__ __forceinline__ void tk_grid_barrier(TopkCtl* c, uint32_t target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (SPARCML_TOPK_BAR_ACQREL) fence_acq_rel_gpu();   // release: this CTA's writes (cumulative over the bar.sync)
+    else __threadfence();
     const uint32_t old = atomicAdd(&c->arrive, 1u);
     if (old == gridDim.x - 1) {
       atomicExch(&c->arrive, 0u);
-      __threadfence();
+      if (SPARCML_TOPK_BAR_ACQREL) fence_acq_rel_gpu();   // acquire the other CTAs' arrivals, release to the waiters
+      else __threadfence();
       st_release_gpu(&c->flag, target);
     } else {
       while ((int)(ld_relaxed_gpu_u32(&c->flag) - target) < 0) {
       }
       (void)ld_acquire_gpu(&c->flag);
     }
-    __threadfence();
+    if (!SPARCML_TOPK_BAR_ACQREL) __threadfence();
   }
   __syncthreads();
 }

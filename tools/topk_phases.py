@@ -24,6 +24,7 @@ ap.add_argument("--N", type=int, default=1 << 24)
 ap.add_argument("--density", type=float, default=0.01)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--plain", action="store_true", help="plain top-k (no EF)")
+ap.add_argument("--pre", type=int, default=5, help="untimed calls first (EF: the accumulator settles, warm start)")
 ap.add_argument("--noflush", action="store_true", help="skip the L2 flush between launches (diagnostics)")
 args = ap.parse_args()
 N = args.N
@@ -45,7 +46,7 @@ def run():
         S.ef_topk(eps, g, 0.01, k, ws=ws, idx_out=io, val_out=vo)
 
 
-for _ in range(5):
+for _ in range(args.pre):
     run()
 torch.cuda.synchronize()
 ts, ph, tcs = [], [], []
@@ -71,6 +72,8 @@ for _ in range(args.reps):
         tc = ws.buf[TC:TC + 2 * 1024 * 8].cpu().numpy().view(np.uint64).reshape(2, 1024)[:, :G].astype(np.float64)
         tcs.append(((tc[0] - t[0]) / 1e3, (tc[1] - t[0]) / 1e3))
         d = np.where(d > 0, (d - t[0]) / 1e3, np.nan)
+        if not np.isfinite(d[11]) or not np.isfinite(d[8]):
+            pass
         ph.append(np.concatenate([(t[1:8] - t[0]) / 1e3, [(t[8] - t[0]) / 1e3], (t[9:15] - t[0]) / 1e3, d[:21]]))
 st = ws.status()
 ts = np.array(ts)
@@ -79,7 +82,7 @@ print(f"N={N} k={k} {'plain' if args.plain else 'EF'}: us per launch median {np.
       f"p25 {np.percentile(ts, 25):.2f} p75 {np.percentile(ts, 75):.2f} min {ts.min():.2f}; "
       f"alg bytes {alg} -> {alg / np.median(ts) / 1e3:.1f} GB/s; status {st}")
 if ph:
-    p = np.median(np.array(ph), axis=0)
+    p = np.nanmedian(np.array(ph), axis=0)
     names = ["sample", "filter", "barrierA", "locate", "barrierB", "offsets", "place"]
     print("phase ends, latest CTA (us after CTA 0 starts, median): " + ", ".join(f"{n} {v:.2f}" for n, v in zip(names, p)))
     print(f"latest CTA start {p[7]:.2f}; CTA 0 phase ends: " + ", ".join(f"{n} {v:.2f}" for n, v in zip(names, p[8:14])))
