@@ -165,8 +165,9 @@ struct ScanCounters {
   uint32_t pad;
 };
 
-struct TileStatus {
+struct alignas(32) TileStatus {   // one 32-byte sector each: neighbours' writes never share a sector
   uint64_t word;     // ((gen << 2 | state) << 32) | value; state 1 = aggregate, 2 = inclusive prefix
+  uint64_t pad[3];
 };
 
 template <typename T>

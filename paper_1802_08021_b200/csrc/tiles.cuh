@@ -36,13 +36,22 @@ struct SpanCfg {
   static constexpr int kChunk = kItems * kThreads;          // diagonal positions per chunk
 };
 
+#ifndef SPARCML_MERGE_PAD
+#define SPARCML_MERGE_PAD 0   // 1: one pad word per 8 in the staged windows (A/B: 44 vs 42 us unpadded, not kept)
+#endif
+// Logical index i of a staged window lives at mpad(i): every thread walks its
+// own run of ~kItems/2 elements of each window, so lane t reads near 8t -- with
+// a pad word per 8 the lanes fall into distinct banks instead of 4.
+__device__ __forceinline__ int mpad(int i) { return SPARCML_MERGE_PAD ? i + (i >> 3) : i; }
+
 template <typename V = float>
 struct MergeSmem {
   static constexpr int kC = SpanCfg<V>::kChunk;
-  alignas(16) uint32_t ak[kC + 4];   // ak[0] = A[a0-1] (look-behind), ak[1+i] = A[a0+i]
-  alignas(16) uint32_t bk[kC + 4];   // bk[i] = B[b0+i], bk[lb] = B[b1] (look-ahead)
-  alignas(16) V av[kC + 4];
-  alignas(16) V bv[kC + 4];
+  static constexpr int kN = SPARCML_MERGE_PAD ? kC + 4 + (kC + 4) / 8 + 1 : kC + 4;   // padded length
+  alignas(16) uint32_t ak[kN];   // ak[0] = A[a0-1] (look-behind), ak[1+i] = A[a0+i] (at mpad)
+  alignas(16) uint32_t bk[kN];   // bk[i] = B[b0+i], bk[lb] = B[b1] (look-ahead)
+  alignas(16) V av[kN];
+  alignas(16) V bv[kN];
   uint64_t split[2];
   uint32_t scan[kWarps + 1];
   uint64_t red[kWarps];
@@ -62,47 +71,16 @@ struct MergeOutput {
 
 __device__ __forceinline__ uint64_t umin64(uint64_t x, uint64_t y) { return x < y ? x : y; }
 
-// n consecutive elements src[s0 ..) -> dst[0 ..), the whole block: 16-byte
-// loads of the aligned quads inside [s0, s0+n) (src 16-byte aligned), scalar
-// loads at the ragged ends.
-template <typename T>
-__device__ __forceinline__ void stage_run(T* dst, const T* __restrict__ src, uint64_t s0, int n) {
-  constexpr int kPer = 16 / sizeof(T);
-  const int tid = threadIdx.x;
-  if (n <= 0) return;
-  if ((reinterpret_cast<uintptr_t>(src) & 15u) != 0) {
-    for (int i = tid; i < n; i += kThreads) dst[i] = __ldcg(src + s0 + i);
-    return;
-  }
-  const uint64_t q0 = (s0 + kPer - 1) / kPer, q1 = (s0 + (uint64_t)n) / kPer;   // whole quads [q0, q1)
-  const int head = (int)umin64((uint64_t)n, q0 * kPer - s0);
-  if (tid < head) dst[tid] = __ldcg(src + s0 + tid);
-  const int nq = q1 > q0 ? (int)(q1 - q0) : 0;
-  const uint4* s4 = reinterpret_cast<const uint4*>(src) + q0;
-  T* d = dst + head;
-#pragma unroll 4
-  for (int q = tid; q < nq; q += kThreads) {
-    const uint4 u = __ldcg(s4 + q);
-    const T* e = reinterpret_cast<const T*>(&u);
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) d[q * kPer + j] = e[j];
-  }
-  const int tail0 = head + nq * kPer;
-  if (tid < n - tail0) dst[tail0 + tid] = __ldcg(src + s0 + tail0 + tid);
-}
 
-#ifndef SPARCML_MERGE_ASYNC
-#define SPARCML_MERGE_ASYNC 1   // 1: stage the four windows with cp.async (every load in flight at once)
-#endif
 // n consecutive elements src[s0 ..) -> dst[0 ..) with 4- or 8-byte cp.async
 // (LDGSTS, consecutive lanes on consecutive words: coalesced, no alignment
 // needed); the caller commits and waits once for all four windows, so the
 // block has a single load round trip instead of one per window.
 template <typename T>
-__device__ __forceinline__ void stage_run_async(T* dst, const T* __restrict__ src, uint64_t s0, int n) {
+__device__ __forceinline__ void stage_run_async(T* dst, int dst0, const T* __restrict__ src, uint64_t s0, int n) {
   static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte elements");
   for (int i = threadIdx.x; i < n; i += kThreads) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + i);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + mpad(dst0 + i));
     if (sizeof(T) == 4)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + s0 + i) : "memory");
     else
@@ -155,20 +133,12 @@ __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, cons
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
   const bool has_prev_a = a0 > 0;
   const int wb = lb + (b1 < nb ? 1 : 0);   // + the look-ahead B[b1]
-  if (SPARCML_MERGE_ASYNC) {
-    stage_run_async(sm.ak + 1, A, a0, la);
-    stage_run_async(sm.bk, B, b0, wb);
-    stage_run_async(sm.av + 1, Av, a0, la);
-    stage_run_async(sm.bv, Bv, b0, wb);
-    if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
-    stage_async_wait();
-  } else {
-    stage_run(sm.ak + 1, A, a0, la);
-    stage_run(sm.av + 1, Av, a0, la);
-    stage_run(sm.bk, B, b0, wb);
-    stage_run(sm.bv, Bv, b0, wb);
-    if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
-  }
+  stage_run_async(sm.ak, 1, A, a0, la);
+  stage_run_async(sm.bk, 0, B, b0, wb);
+  stage_run_async(sm.av, 1, Av, a0, la);
+  stage_run_async(sm.bv, 0, Bv, b0, wb);
+  if (tid == 0 && has_prev_a) sm.ak[0] = __ldcg(&A[a0 - 1]);
+  stage_async_wait();
   __syncthreads();
   merge_mark(mk, 2, mfirst);
   // this thread's outputs: diagonal dt of the chunk
@@ -177,7 +147,7 @@ __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, cons
   int lo = max(0, dt - lb), hi = min(dt, la);
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (sm.ak[mid + 1] <= sm.bk[dt - 1 - mid]) lo = mid + 1; else hi = mid;
+    if (sm.ak[mpad(mid + 1)] <= sm.bk[mpad(dt - 1 - mid)]) lo = mid + 1; else hi = mid;
   }
   int ia = lo, ib = dt - lo;
   uint32_t ok[kItems];
@@ -188,23 +158,23 @@ __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, cons
     ok[s] = 0;
     ov[s] = V(0);
     if (dt + s < L) {
-      const uint32_t ka = ia < la ? sm.ak[ia + 1] : 0xFFFFFFFFu;
-      const uint32_t kb = ib < wb ? sm.bk[ib] : 0xFFFFFFFFu;
+      const uint32_t ka = ia < la ? sm.ak[mpad(ia + 1)] : 0xFFFFFFFFu;
+      const uint32_t kb = ib < wb ? sm.bk[mpad(ib)] : 0xFFFFFFFFu;
       const bool takeA = ib >= lb || (ia < la && ka <= kb);
       if (takeA) {
-        V v = sm.av[ia + 1];
+        V v = sm.av[mpad(ia + 1)];
         // the element following A[ia] in merged order is B[ib] (in the window or the look-ahead)
-        if (ib < wb && kb == ka) v = op_combine(out.op, v, sm.bv[ib]);
+        if (ib < wb && kb == ka) v = op_combine(out.op, v, sm.bv[mpad(ib)]);
         ok[s] = ka;
         ov[s] = v;
         emit |= 1u << s;
         ++ia;
       } else {
         // a B element equal to the preceding A element was already combined into it
-        const bool dup = (ia > 0 || has_prev_a) && sm.ak[ia] == kb;
+        const bool dup = (ia > 0 || has_prev_a) && sm.ak[mpad(ia)] == kb;
         if (!dup) {
           ok[s] = kb;
-          ov[s] = sm.bv[ib];
+          ov[s] = sm.bv[mpad(ib)];
           emit |= 1u << s;
         }
         ++ib;
@@ -221,15 +191,15 @@ __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, cons
 #pragma unroll
   for (int s = 0; s < kItems; ++s)
     if (emit & (1u << s)) {
-      sm.ak[pos] = ok[s];
-      sm.av[pos] = ov[s];
+      sm.ak[mpad(pos)] = ok[s];
+      sm.av[mpad(pos)] = ov[s];
       ++pos;
     }
   __syncthreads();
   for (uint32_t i = tid; i < tile_total; i += kThreads) {   // coalesced
     SPARCML_CHECK(o + i < total);
-    const uint32_t k = sm.ak[i];
-    const V v = sm.av[i];
+    const uint32_t k = sm.ak[mpad(i)];
+    const V v = sm.av[mpad(i)];
     out.idx[o + i] = k;
     out.val[o + i] = v;
     if (out.idx2) {
