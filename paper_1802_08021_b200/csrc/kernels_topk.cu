@@ -62,6 +62,12 @@ constexpr int kChunk = 256;                   // elements per pipeline chunk (1 
 #ifndef SPARCML_TOPK_WARM
 #define SPARCML_TOPK_WARM 1                  // 1: tau / split from the previous call's k-th magnitude (no sample)
 #endif
+#ifndef SPARCML_TOPK_WARM_LO
+#define SPARCML_TOPK_WARM_LO 64                // warm tau = m (1 - 1/LO)  (128: -1-2 us in a seed-cycling loop, but low-side misses when one gradient repeats: bench top-k 55 us)
+#endif
+#ifndef SPARCML_TOPK_WARM_HI
+#define SPARCML_TOPK_WARM_HI 8                 // warm split = m (1 + 1/HI)
+#endif
 #ifndef SPARCML_TOPK_COOP
 #define SPARCML_TOPK_COOP 1                  // 0: plain launch (one CTA per SM fits; A/B diagnostics)
 #endif
@@ -746,8 +752,8 @@ __global__ void __launch_bounds__(kTkThreads, 1) topk_stream_kernel(TkArgs a) {
     TK_D(3);
   } else if (warm) {
     const float m = __uint_as_float(wk);
-    tau = abs_key(m * (1.0f - 1.0f / 64.0f));
-    split = (uint64_t)abs_key(m * 1.125f) + 1u;   // <= Inf's key + 1 < kKeyEnd
+    tau = abs_key(m * (1.0f - 1.0f / (float)SPARCML_TOPK_WARM_LO));
+    split = (uint64_t)abs_key(m * (1.0f + 1.0f / (float)SPARCML_TOPK_WARM_HI)) + 1u;   // <= Inf's key + 1 < kKeyEnd
   }
   uint32_t shift = shift_for(split - tau, kBins - 1);
   if (SPARCML_TOPK_LATE_PRO && lane == 0)
