@@ -350,7 +350,14 @@ sparcml_status sparcml_merge_sum(const uint32_t* ia, const float* va, uint64_t n
  * entries, buckets in order (sorted overall); ws may then be NULL (it only
  * receives the status).  Requires finite x (NaN/Inf are reported through
  * sparcml_topk_status).  ws from sparcml_topk_workspace_bytes, zero-initialised
- * once with sparcml_ops_workspace_init. */
+ * once with sparcml_ops_workspace_init; one workspace serves any N up to the
+ * size it was made for.  The workspace carries state between calls: the
+ * global top-k remembers the k-th magnitude m it found, and the next call with
+ * the same (N, k, EF or not) starts its candidate threshold at m(1 - 1/64)
+ * instead of sampling (the warm start).  The result never
+ * depends on it -- a wrong guess costs one more filter pass (passes == 2) --
+ * so use one workspace per vector (e.g. per layer's eps) to keep the guesses
+ * good.  Calls on one workspace must be stream-ordered (not concurrent). */
 size_t sparcml_topk_workspace_bytes(uint64_t N, uint64_t k);
 sparcml_status sparcml_topk_sparsify(const float* x, uint64_t N, uint64_t k, uint64_t bucket,
                                      uint32_t* idx_out, float* val_out, float* residual,
@@ -368,11 +375,14 @@ sparcml_status sparcml_ef_topk(float* eps, const float* grad, float alpha, uint6
  * vector of N values; writes min(count, cap) of them to pos_host and returns
  * the count (0 when N < 65536: no sampling).  The selection never depends on
  * them for correctness -- an input that defeats the sample takes the exact
- * re-filter path (passes == 2); tests use this to build such an input. */
+ * re-filter path (passes == 2); tests use this to build such an input.  (A
+ * call that starts warm samples only when its warm threshold misses.) */
 size_t sparcml_topk_sample_positions(uint64_t N, uint64_t* pos_host, size_t cap);
 
 /* Synchronous: device status of the last top-k run on `ws` (0 or
- * SPARCML_ERR_NONFINITE) and how many filter passes it needed. */
+ * SPARCML_ERR_NONFINITE) and how many filter passes it needed (1; +1 for each
+ * re-filter: a warm-start miss re-filters from a sample, a sample miss with
+ * threshold 0). */
 sparcml_status sparcml_topk_status(const void* ws, uint32_t* status_host, uint32_t* passes_host,
                                    void* stream);
 
