@@ -108,6 +108,48 @@ __device__ __forceinline__ void merge_mark(uint64_t* mk, int i, bool first) {
 #endif
 }
 
+#ifndef SPARCML_MERGE_BSEARCH
+#define SPARCML_MERGE_BSEARCH 0   // 1: both chunk ends searched by the whole block, 129-ary (A/B: 47 vs 42 us, not kept)
+#endif
+// Both ends of a chunk on the merge path at once, the whole block: warps 0-3
+// search diagonal d0, warps 4-7 diagonal d1, 128 probes per round (129-ary:
+// 4 dependent load rounds for 2 x 1.68M pairs instead of 6).  The probe
+// predicate A[p] <= B[d-1-p] is monotone in p; c true probes put the split in
+// (p_c, p_c+1].  out[g] = the split of diagonal g (A elements before it).
+__device__ __forceinline__ void block_merge_path2(const uint32_t* __restrict__ A, uint64_t na,
+                                                  const uint32_t* __restrict__ B, uint64_t nb, uint64_t d0,
+                                                  uint64_t d1, uint32_t* s_cnt /* kWarps */, uint64_t* out) {
+  static_assert(kWarps == 8, "two groups of four warps");
+  const int tid = threadIdx.x, warp = tid >> 5, g = warp >> 2, l = tid & 127;
+  const uint64_t d = g ? d1 : d0;
+  uint64_t lo = d > nb ? d - nb : 0;
+  uint64_t hi = d < na ? d : na;
+  while (__syncthreads_or(hi - lo > 128)) {   // (also orders s_cnt's reads before the next writes)
+    const uint64_t span = hi - lo;
+    bool pred = false;
+    if (span > 128) {
+      const uint64_t p = lo + (span * (uint64_t)(l + 1)) / 129;
+      pred = A[p] <= B[d - 1 - p];
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, pred);
+    if ((tid & 31) == 0) s_cnt[warp] = __popc(b);
+    __syncthreads();
+    if (span > 128) {
+      const int c = (int)(s_cnt[4 * g] + s_cnt[4 * g + 1] + s_cnt[4 * g + 2] + s_cnt[4 * g + 3]);
+      const uint64_t plo = lo + (span * (uint64_t)c) / 129;
+      const uint64_t phi = lo + (span * (uint64_t)(c + 1)) / 129;
+      lo = c > 0 ? plo + 1 : lo;
+      hi = c < 128 ? phi : hi;
+    }
+  }
+  const uint64_t p = lo + (uint64_t)l;
+  const bool pred = p < hi && A[p] <= B[d - 1 - p];
+  const uint32_t b = __ballot_sync(0xffffffffu, pred);
+  if ((tid & 31) == 0) s_cnt[warp] = __popc(b);
+  __syncthreads();
+  if (l == 0) out[g] = lo + s_cnt[4 * g] + s_cnt[4 * g + 1] + s_cnt[4 * g + 2] + s_cnt[4 * g + 3];
+}
+
 template <typename V>
 __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, const V* __restrict__ Av, uint64_t na,
                                             const uint32_t* __restrict__ B, const V* __restrict__ Bv, uint64_t nb,
@@ -119,7 +161,9 @@ __device__ __forceinline__ void merge_chunk(const uint32_t* __restrict__ A, cons
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t total = na + nb;
   const uint64_t d1 = umin64(d0 + SpanCfg<V>::kChunk, total);
-  if (warp == 0) {
+  if (SPARCML_MERGE_BSEARCH) {
+    block_merge_path2(A, na, B, nb, d0, d1, sm.scan, sm.split);
+  } else if (warp == 0) {
     const uint64_t s = warp_merge_path(A, na, B, nb, d0);
     if (lane == 0) sm.split[0] = s;
   } else if (warp == 1) {
